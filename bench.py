@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 P-CG iterations/s (+ SpMV GFLOP/s, % of the HBM roofline) on the
+SURVEY §8(d) C3 workload — 3D 7-point Laplacian on a 400^3 grid (64M rows, 447M nnz),
+Jacobi-preconditioned CG, CSR, FP64, b = 1, x0 = 0, tol 1e-6.
+
+  python bench.py [--gpus N --steps K --warmup W]           # our arm (one JSON line)
+  python bench.py --impl reference [--steps K --warmup W]   # the reference's CPU path
+
+A step is one P-CG iteration.  Ours: the device-resident FAST iteration (3 kernels, CUDA
+graph) timed with CUDA events on the solver stream; `e2e` is a full solve through the
+C-ABI with HOST (pinned) CSR arrays (upload + convert + solve + download inside the timed
+call).  The reference arm runs the reference library (oracle/_ref, built from
+/root/reference) on the box's host cores.  Under torchrun each rank drives one GPU; the
+row-partitioned multi-GPU solver is not in this round, so N>1 runs replicas (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 CG iterations/sec and SpMV GFLOP/s (+% HBM roofline) at 1/2/4/8 B200"
+GOLDEN_ITERS, GOLDEN_MEASURE = 733, 9.650895609e-07  # SURVEY §6 / §8(a12), oracle at 400^3
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=400, help="grid side (C3 = 400)")
+    ap.add_argument("--format", default="csr", choices=["csr", "ell", "hyb"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=20)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed plumbing
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo", rank=self.rank, world_size=self.world)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [line.split(",") for line in open(self.f.name).read().strip().splitlines() if line.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, name in enumerate(names):
+                if r[5 + k].strip() == "Active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- roofline constants
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def spmv_bytes(n_rows, n_cols, nnz):
+    # int32-index CSR + one read of x + one write of y
+    return 12 * nnz + 4 * (n_rows + 1) + 8 * n_cols + 8 * n_rows
+
+
+def iter_bytes(n_rows, n_cols, nnz):
+    # P-CG: k_spmv = 1, V = 11 vector streams
+    return spmv_bytes(n_rows, n_cols, nnz) + 8 * n_rows * 11
+
+
+def ncu_traffic():
+    """dram bytes per launch of the SpMV kernel from the committed `ncu --set full` summary."""
+    p = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ----------------------------------------------------------------------------- CPU arms
+def cpu_reference_rate(m, iters: int, warm: int, bs: int, tw: int):
+    """Reference solve_pcg on the host cores: per-iteration time from two solves of
+    max_iterations = warm and warm + iters (setup cancels)."""
+    from oracle.oracle import REF_SO, Port, Ref
+    b = np.ones(m.n_rows)
+    if os.path.exists(REF_SO):
+        R = Ref()
+        rm = R.from_csr(m)
+        t0 = time.perf_counter()
+        o1 = R.solve(rm, "pcg", b, max_it=warm, bs=bs, tw=tw, hist_cap=1)
+        t1 = time.perf_counter()
+        o2 = R.solve(rm, "pcg", b, max_it=warm + iters, bs=bs, tw=tw, hist_cap=1)
+        t2 = time.perf_counter()
+        done = o2["iterations"] - o1["iterations"]
+        dt = (t2 - t1) - (t1 - t0)
+        return dict(value=done / dt if dt > 0 else None, cores=R.default_workers(), kind="reference",
+                    seconds=t2 - t0, iterations=done)
+    P = Port()
+    t0 = time.perf_counter()
+    o1 = P.solve(m, "pcg", b, max_it=warm, bs=bs, tw=tw)
+    t1 = time.perf_counter()
+    o2 = P.solve(m, "pcg", b, max_it=warm + iters, bs=bs, tw=tw)
+    t2 = time.perf_counter()
+    done = o2["iterations"] - o1["iterations"]
+    dt = (t2 - t1) - (t1 - t0)
+    return dict(value=done / dt if dt > 0 else None, cores=1, kind="port", seconds=t2 - t0, iterations=done)
+
+
+def oracle_csr(n):
+    from oracle.oracle import Port
+    return Port().generate("lap3d7", n)
+
+
+def config_block(args, dist, extra=None):
+    c = {"workload": f"C3: P-CG + Jacobi, 3D 7-point Laplacian {args.n}^3 "
+                     f"({args.n ** 3:,} rows), {args.format.upper()}, FP64, b=1, x0=0, tol 1e-6",
+         "matrix": f"lap3d7 n={args.n}", "format": args.format, "solver": "pcg", "preconditioner": "jacobi",
+         "parallelism": f"replicas{dist.world}" if dist.world > 1 else "single-gpu",
+         "l2": "inputs larger than L2 (12.3 GB touched per iteration vs 126 MB L2)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+def run_reference(args, dist):
+    if dist.rank != 0:
+        return None
+    m = oracle_csr(args.n)
+    ncores = os.cpu_count()
+    os.environ["KRYSP_WORKERS"] = str(ncores)
+    r = cpu_reference_rate(m, args.steps, max(args.warmup, 1), 1024, 1)
+    line = {"metric": METRIC, "value": r["value"], "unit": "iterations/s", "impl": "reference", "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / r["value"] if r["value"] else None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic 3D 7-point Laplacian)",
+            "config": config_block(args, dist, {"policy": "<1024,1> (reference tuned winner, SURVEY §6)"}),
+            "cpu_baseline": {"value": r["value"], "unit": "iterations/s", "cores": r["cores"], "kind": r["kind"],
+                             "sample": f"{r['iterations']} P-CG iterations of the full 400^3 problem "
+                                       f"(solve_pcg max_iterations {args.warmup}+{args.steps} minus "
+                                       f"{args.warmup}), KRYSP_WORKERS={r['cores']}"},
+            "e2e": {"value": r["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    return line
+
+
+def run_ours(args, dist):
+    import paper_2108_13162_b200 as kg
+
+    ctx = kg.Context(dist.local)
+    A = ctx.generate("lap3d7", args.n)
+    if args.format != "csr":
+        A = A.convert(args.format, slot_cap=1 << 40)
+    info = A.info
+    n, nnz = info["n_rows"], info["nnz"]
+    b = ctx.to_device(np.ones(n))
+    x0 = ctx.to_device(np.zeros(n))
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), tolerance=1e-6, max_iterations=30000)
+    solver = kg.PcgSolver(A, b, x0, cfg)
+    solver.time(args.warmup)
+    clocks = Clocks(dist.local)
+    dist.barrier()
+    ctx.sync()
+    clocks.start()
+    t = solver.time(args.steps)  # CUDA events on the solver stream, synchronous
+    ck = clocks.stop()
+    dist.barrier()
+    t_max = dist.max(t)
+    rep = solver.report()
+    ran = rep.iterations
+    assert ran == args.warmup + args.steps, f"solve converged inside the timed region ({ran} iterations)"
+    prof_n = min(20, max(1, GOLDEN_ITERS - ran - 5))
+    t_spmv, t_upd, t_dir = solver.profile(prof_n)
+    kpi = solver.kernels_per_iteration
+    solver.close()
+
+    bw_peak, peak_kind = peaks()
+    B_spmv = spmv_bytes(n, info["n_cols"], nnz)
+    B_iter = iter_bytes(n, info["n_cols"], nnz)
+    it_per_s = dist.world * args.steps / t_max
+    ms_step = 1e3 * t_max / args.steps
+    achieved = B_spmv / t_spmv / 1e9
+    line = {"metric": METRIC, "value": it_per_s, "unit": "iterations/s", "n_gpus": dist.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic 3D 7-point Laplacian, generated on device)",
+            "config": config_block(args, dist, {"policy": "auto (FAST mode)", "mode": "fast",
+                                                "nnz": nnz, "rows": n}),
+            "roofline": {"bound": "hbm", "kernel": f"spmv_{args.format} + fused <p,Ap>",
+                         "achieved": achieved, "peak": bw_peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / bw_peak, "traffic": ncu_traffic(),
+                         "algorithmic_bytes_per_launch": B_spmv,
+                         "launch_ms": t_spmv * 1e3, "update_ms": t_upd * 1e3, "direction_ms": t_dir * 1e3},
+            "spmv_gflops": 2 * nnz / t_spmv / 1e9,
+            "iteration_roofline": {"bytes": B_iter, "achieved_gbs": B_iter / (t_max / args.steps) / 1e9,
+                                   "frac": B_iter / (t_max / args.steps) / 1e9 / bw_peak},
+            "gpu_launches": kpi * args.steps,
+            "clocks": ck}
+    # ---- e2e: full solve through the C-ABI with host buffers -------------------------------
+    if not args.no_e2e:
+        hm = kg.generate_csr("lap3d7", args.n, pinned=True)
+        import torch
+        hb = torch.ones(n, dtype=torch.float64, pin_memory=True).numpy()
+        hx0 = torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
+        e2e_cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0))
+        its, secs, rep2 = 0, 0.0, None
+        dist.barrier()
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            rep2 = kg.solve_csr_host(ctx, hm, "pcg", hb, hx0, e2e_cfg, fmt=args.format)
+            secs += time.perf_counter() - t0
+            its += rep2.iterations
+        secs = dist.max(secs)
+        h2d = (hm.row_ptr.nbytes + hm.col_idx.nbytes + hm.values.nbytes + hb.nbytes + hx0.nbytes)
+        line["e2e"] = {"value": dist.world * its / secs, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": 8 * n + 8 * rep2.iterations,
+                       "what": "krysp_gpu_solve_csr_host: pinned int64 CSR + b + x0 upload, device CSR build, "
+                               "FAST P-CG to convergence, solution download",
+                       "seconds_per_step": secs / args.e2e_steps}
+        line["parity"] = {"iterations": rep2.iterations, "golden_iterations": GOLDEN_ITERS,
+                          "final_residual_measure": rep2.final_residual_measure,
+                          "golden_final_measure": GOLDEN_MEASURE,
+                          "iterations_within_1": abs(rep2.iterations - GOLDEN_ITERS) <= 1,
+                          "measure_abs_diff": abs(rep2.final_residual_measure - GOLDEN_MEASURE)}
+    # ---- CPU baseline (rank 0, N = 1) --------------------------------------------------------
+    if dist.world == 1 and dist.rank == 0 and not args.no_cpu:
+        hm = oracle_csr(args.n)
+        os.environ["KRYSP_WORKERS"] = str(os.cpu_count())
+        r = cpu_reference_rate(hm, args.cpu_iters, 2, 1024, 1)
+        line["cpu_baseline"] = {"value": r["value"], "unit": "iterations/s", "cores": r["cores"], "kind": r["kind"],
+                                "sample": f"{r['iterations']} P-CG iterations of the same 400^3 problem, policy "
+                                          f"<1024,1> (difference of max_iterations 2+{args.cpu_iters} and 2)"}
+    return line
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    try:
+        line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
+        if dist.rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

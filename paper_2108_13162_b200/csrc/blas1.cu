@@ -1,0 +1,278 @@
+// BLAS-1 kernels (reference kernels.cpp:41-127) and the Jacobi diagonal (solvers.cpp:72-113).
+//
+// Element-wise kernels compute exactly the reference's expression with IEEE roundings
+// (__dmul_rn / __dadd_rn, never FMA):
+//   daxpy  y = fl(fl(a*x) + y)            kernels.cpp:49
+//   axpby  y = fl(fl(a*x) + fl(b*y))      :116
+//   scale  x = fl(a*x)                    :105
+//   scal_elementwise a = fl(a*b)          :61
+// Dots:
+//   EXACT  partial[c] = sequential sum over chunk c of block_size elements (from 0.0), then
+//          a strict left-to-right fold of the partials (kernels.cpp:66-84) — bit-identical.
+//   FAST   fixed-grid, fixed-tree reduction (deterministic run to run, not bit-equal to CPU).
+#include "internal.cuh"
+
+namespace kg {
+
+namespace {
+
+constexpr int kNT = 256;
+
+unsigned ew_grid(krysp_gpu_ctx* c, int64_t n) { return grid_for((n + 1) / 2, kNT, (int64_t)c->sm_count * 16); }
+
+#define GRID_STRIDE(i, n) \
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void daxpy_kernel(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    GRID_STRIDE(i, n) y[i] = __dadd_rn(__dmul_rn(a, x[i]), y[i]);
+}
+__global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
+    GRID_STRIDE(i, n) y[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
+}
+__global__ void scale_kernel(int64_t n, double a, double* __restrict__ x) {
+    GRID_STRIDE(i, n) x[i] = __dmul_rn(a, x[i]);
+}
+__global__ void copy_kernel(int64_t n, const double* __restrict__ s, double* __restrict__ d) {
+    GRID_STRIDE(i, n) d[i] = s[i];
+}
+__global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
+    GRID_STRIDE(i, n) x[i] = v;
+}
+__global__ void scal_ew_kernel(int64_t n, double* __restrict__ a, const double* __restrict__ b) {
+    GRID_STRIDE(i, n) a[i] = __dmul_rn(a[i], b[i]);
+}
+__global__ void mul_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ o) {
+    GRID_STRIDE(i, n) o[i] = __dmul_rn(a[i], b[i]);
+}
+
+// ---------------------------------------------------------------- FAST dot
+template <int NT>
+__global__ void __launch_bounds__(NT) dot_fast_kernel(int64_t n, const double* __restrict__ x,
+                                                      const double* __restrict__ y, double* partials,
+                                                      unsigned* counter, double* out) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    const int64_t n2 = n / 2;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const double2* y2 = reinterpret_cast<const double2*>(y);
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+    if (aligned) {
+        GRID_STRIDE(i, n2) {
+            double2 a = x2[i], b = y2[i];
+            acc = fma(a.x, b.x, acc);
+            acc = fma(a.y, b.y, acc);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) acc = fma(x[n - 1], y[n - 1], acc);
+    } else {
+        GRID_STRIDE(i, n) acc = fma(x[i], y[i], acc);
+    }
+    double b = block_sum<NT>(acc, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = b;
+    if (last_block(counter)) {
+        double t = reduce_partials<NT>(partials, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            *out = t;
+            *counter = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- EXACT dot
+// 4 warps per block; warp w owns 32 consecutive chunks, lane l accumulates chunk c0+l in
+// order.  Each step the warp reads 32 contiguous elements of each of its 32 chunks
+// (coalesced), transposes the products through shared memory, and every lane adds its
+// chunk's 32 products sequentially.  The last block folds all partials left to right.
+constexpr int kExactWarps = 4;
+
+__global__ void __launch_bounds__(32 * kExactWarps)
+    dot_exact_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ y, int bs,
+                     int64_t n_chunks, double* partials, unsigned* counter, double* out) {
+    __shared__ double tile[kExactWarps][32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t c0 = ((int64_t)blockIdx.x * kExactWarps + w) * 32;
+    double acc = 0.0;
+    for (int j0 = 0; j0 < bs; j0 += 32) {
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+            const int64_t c = c0 + q;
+            const int64_t i = c * bs + j0 + lane;
+            double p = 0.0;  // absent elements add +0.0: a no-op on a sum that starts at +0.0
+            if (c < n_chunks && i < n) p = __dmul_rn(x[i], y[i]);
+            tile[w][q][lane] = p;
+        }
+        __syncwarp();
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) acc = __dadd_rn(acc, tile[w][lane][q]);
+        __syncwarp();
+    }
+    if (c0 + lane < n_chunks) partials[c0 + lane] = acc;
+    if (last_block(counter)) {
+        if (w == 0) {
+            // strict left-to-right fold (kernels.cpp:80-83)
+            double total = 0.0;
+            for (int64_t b = 0; b < n_chunks; b += 32) {
+                const double v = (b + lane < n_chunks) ? __ldcg(partials + b + lane) : 0.0;
+                const int cnt = (int)(n_chunks - b < 32 ? n_chunks - b : 32);
+                for (int q = 0; q < cnt; ++q) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, q));
+            }
+            if (lane == 0) {
+                *out = total;
+                *counter = 0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- diagonal / Jacobi
+__global__ void diag_csr(CsrView A, double* d, int64_t n) {
+    GRID_STRIDE(r, n) {
+        double v = 0.0;
+        if (r < A.n_rows)
+            for (int32_t k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k)
+                if (A.col[k] == r) v = A.val[k];
+        d[r] = v;
+    }
+}
+__global__ void diag_ell(EllView E, double* d, int64_t n) {
+    GRID_STRIDE(r, n) {
+        double v = 0.0;
+        if (r < E.n_rows)
+            for (int32_t s = 0; s < E.width; ++s) {
+                const int64_t slot = (int64_t)s * E.n_rows + r;
+                if (E.jcoef[slot] == r) v = E.coef[slot];
+            }
+        d[r] = v;
+    }
+}
+// HYB: diag = ell_diag + coo_diag (solvers.cpp:93-98); COO: diag[r] += v (:75-78)
+__global__ void diag_coo_add(CooView O, double* d, int64_t n, int hyb) {
+    GRID_STRIDE(k, O.nnz) {
+        const int32_t r = O.row[k];
+        if (k > 0 && O.row[k - 1] == r) continue;
+        double acc = 0.0;
+        for (int64_t j = k; j < O.nnz && O.row[j] == r; ++j)
+            if (O.col[j] == r) acc = __dadd_rn(acc, O.val[j]);
+        if (r < n) d[r] = hyb ? __dadd_rn(d[r], acc) : acc;
+    }
+}
+__global__ void invert_kernel(int64_t n, double* d, int* zero_row) {
+    GRID_STRIDE(i, n) {
+        if (d[i] == 0.0) atomicMin(zero_row, (int)i);
+        else d[i] = __ddiv_rn(1.0, d[i]);
+    }
+}
+
+}  // namespace
+
+void k_daxpy(krysp_gpu_ctx* c, int64_t n, double a, const double* x, double* y) {
+    if (n <= 0) return;
+    daxpy_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, a, x, y);
+    KG_LAUNCH(c);
+}
+void k_axpby(krysp_gpu_ctx* c, int64_t n, double a, const double* x, double b, double* y) {
+    if (n <= 0) return;
+    axpby_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, a, x, b, y);
+    KG_LAUNCH(c);
+}
+void k_scale(krysp_gpu_ctx* c, int64_t n, double a, double* x) {
+    if (n <= 0) return;
+    scale_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, a, x);
+    KG_LAUNCH(c);
+}
+void k_copy(krysp_gpu_ctx* c, int64_t n, const double* s, double* d) {
+    if (n <= 0 || s == d) return;
+    copy_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, s, d);
+    KG_LAUNCH(c);
+}
+void k_fill(krysp_gpu_ctx* c, int64_t n, double v, double* x) {
+    if (n <= 0) return;
+    fill_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, v, x);
+    KG_LAUNCH(c);
+}
+void k_scal_elementwise(krysp_gpu_ctx* c, int64_t n, double* a, const double* b) {
+    if (n <= 0) return;
+    scal_ew_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, a, b);
+    KG_LAUNCH(c);
+}
+void k_mul(krysp_gpu_ctx* c, int64_t n, const double* a, const double* b, double* o) {
+    if (n <= 0) return;
+    mul_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, a, b, o);
+    KG_LAUNCH(c);
+}
+
+void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode, double* d_out) {
+    if (n <= 0) {
+        KG_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), c->stream));
+        return;
+    }
+    if (mode == KRYSP_MODE_EXACT) {
+        if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
+        const int64_t n_chunks = (n + bs - 1) / bs;
+        const int64_t per_block = 32 * kExactWarps;
+        const int64_t blocks = (n_chunks + per_block - 1) / per_block;
+        // partial storage: use the slot area when it fits, else a temporary
+        double* partials = c->d_partials + kPartialCap;  // slot 1
+        double* tmp = nullptr;
+        if (n_chunks + per_block > (int64_t)kPartialCap * (kSlots - 1)) {
+            tmp = dev_alloc<double>(n_chunks + per_block, false);
+            partials = tmp;
+        }
+        dot_exact_kernel<<<(unsigned)blocks, 32 * kExactWarps, 0, c->stream>>>(n, x, y, (int)bs, n_chunks, partials,
+                                                                              c->d_counters + 1, d_out);
+        KG_LAUNCH(c);
+        if (tmp) {
+            KG_CUDA(cudaStreamSynchronize(c->stream));
+            dev_free(tmp);
+        }
+    } else {
+        const unsigned g = grid_for((n + 1) / 2, kNT, (int64_t)c->sm_count * 4);
+        dot_fast_kernel<kNT><<<g, kNT, 0, c->stream>>>(n, x, y, c->d_partials, c->d_counters, d_out);
+        KG_LAUNCH(c);
+    }
+}
+
+double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode) {
+    k_dot(c, n, x, y, bs, mode, c->d_scalars);
+    KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    return c->h_pinned[0];
+}
+
+void k_diagonal(const krysp_gpu_mat* m, double* d) {
+    krysp_gpu_ctx* c = m->ctx;
+    const int64_t n = std::min(m->n_rows, m->n_cols);
+    if (n <= 0) return;
+    const unsigned g = grid_for(n, kNT, (int64_t)c->sm_count * 16);
+    switch (m->format) {
+        case KRYSP_FMT_CSR:
+            diag_csr<<<g, kNT, 0, c->stream>>>(m->csr(), d, n);
+            KG_LAUNCH(c);
+            break;
+        case KRYSP_FMT_ELL:
+        case KRYSP_FMT_HYB:
+            diag_ell<<<g, kNT, 0, c->stream>>>(m->ell(), d, n);
+            KG_LAUNCH(c);
+            if (m->format == KRYSP_FMT_HYB && m->coo_nnz) {
+                diag_coo_add<<<grid_for(m->coo_nnz, kNT, (int64_t)c->sm_count * 16), kNT, 0, c->stream>>>(m->coo(), d, n, 1);
+                KG_LAUNCH(c);
+            }
+            break;
+        case KRYSP_FMT_COO:
+            k_fill(c, n, 0.0, d);
+            if (m->coo_nnz) {
+                diag_coo_add<<<grid_for(m->coo_nnz, kNT, (int64_t)c->sm_count * 16), kNT, 0, c->stream>>>(m->coo(), d, n, 0);
+                KG_LAUNCH(c);
+            }
+            break;
+    }
+}
+
+// make_jacobi solvers.cpp:102-113: zero -> Breakdown("zero diagonal entry at row i")
+void k_invert_diag(krysp_gpu_ctx* c, int64_t n, double* d, int* d_zero_row) {
+    if (n <= 0) return;
+    invert_kernel<<<ew_grid(c, n), kNT, 0, c->stream>>>(n, d, d_zero_row);
+    KG_LAUNCH(c);
+}
+
+}  // namespace kg

@@ -1,0 +1,291 @@
+// Internal header of libkrysp_gpu.so (sm_100a).  Not installed; the public surface is
+// include/krysp_gpu.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/krysp_gpu.h"
+
+namespace kg {
+
+// ---------------------------------------------------------------- errors
+struct Status : std::exception {
+    krysp_status code;
+    std::string msg;
+    Status(krysp_status c, std::string m) : code(c), msg(std::move(m)) {}
+    const char* what() const noexcept override { return msg.c_str(); }
+};
+
+[[noreturn]] void fail(krysp_status code, const char* fmt, ...);
+
+#define KG_CUDA(call)                                                                      \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            ::kg::fail(KRYSP_CUDA_ERROR, "%s:%d %s: %s", __FILE__, __LINE__, #call,        \
+                       cudaGetErrorString(e_));                                            \
+    } while (0)
+
+#define KG_LAUNCH(ctx)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess)                                                             \
+            ::kg::fail(KRYSP_CUDA_ERROR, "%s:%d launch: %s", __FILE__, __LINE__,          \
+                       cudaGetErrorString(e_));                                            \
+        (ctx)->launches++;                                                                 \
+    } while (0)
+
+// ---------------------------------------------------------------- context
+}  // namespace kg
+
+struct krysp_gpu_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    int64_t launches = 0;
+    // reduction scratch: partial sums (kPartialCap doubles per slot), one arrival counter
+    // per slot, device scalars, and pinned host scalars for D2H of reduction results
+    double* d_partials = nullptr;
+    unsigned* d_counters = nullptr;
+    double* d_scalars = nullptr;
+    double* h_pinned = nullptr;
+};
+
+namespace kg {
+
+constexpr int kPartialCap = 1 << 16;  // per reduction slot (>= any fast-mode grid)
+constexpr int kSlots = 8;
+constexpr int kScalarCap = 256;
+
+// ---------------------------------------------------------------- matrices
+// Device storage: int32 indices, f64 values.  Index / value arrays carry kPad trailing
+// zero elements so 16-byte vector loads may run past the last entry.
+constexpr int64_t kPad = 8;
+
+struct CsrView {
+    int32_t n_rows, n_cols;
+    int64_t nnz;
+    const int32_t* __restrict__ row_ptr;
+    const int32_t* __restrict__ col;
+    const double* __restrict__ val;
+};
+struct EllView {
+    int32_t n_rows, n_cols;
+    int32_t width;
+    const int32_t* __restrict__ jcoef;  // column-major, sentinel = n_cols
+    const double* __restrict__ coef;
+};
+struct CooView {
+    int32_t n_rows, n_cols;
+    int64_t nnz;
+    const int32_t* __restrict__ row;
+    const int32_t* __restrict__ col;
+    const double* __restrict__ val;
+};
+
+}  // namespace kg
+
+struct krysp_gpu_mat {
+    krysp_gpu_ctx* ctx = nullptr;
+    int32_t format = KRYSP_FMT_CSR;
+    int64_t n_rows = 0, n_cols = 0, nnz = 0;
+    // CSR
+    int32_t* rp = nullptr;
+    int32_t* ci = nullptr;
+    double* cv = nullptr;
+    // ELL (also the ELL part of HYB)
+    int64_t width = 0;
+    int32_t* jcoef = nullptr;
+    double* coef = nullptr;
+    // COO (also the overflow part of HYB)
+    int64_t coo_nnz = 0;
+    int32_t* co_r = nullptr;
+    int32_t* co_c = nullptr;
+    double* co_v = nullptr;
+    // cached row statistics (CSR): max row length, max nnz per 256-row tile
+    int64_t max_row = -1;
+    int64_t max_tile_nnz = -1;
+    int64_t bytes = 0;
+
+    kg::CsrView csr() const {
+        return {(int32_t)n_rows, (int32_t)n_cols, nnz, rp, ci, cv};
+    }
+    kg::EllView ell() const { return {(int32_t)n_rows, (int32_t)n_cols, (int32_t)width, jcoef, coef}; }
+    kg::CooView coo() const { return {(int32_t)n_rows, (int32_t)n_cols, coo_nnz, co_r, co_c, co_v}; }
+};
+
+namespace kg {
+
+// ---------------------------------------------------------------- memory helpers
+template <typename T>
+T* dev_alloc(int64_t count, bool zero = true, cudaStream_t s = nullptr) {
+    T* p = nullptr;
+    size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
+    KG_CUDA(cudaMalloc(&p, bytes));
+    if (zero) KG_CUDA(cudaMemsetAsync(p, 0, bytes, s));
+    return p;
+}
+void dev_free(void* p);
+
+// RAII device vector of doubles
+struct DVec {
+    double* p = nullptr;
+    int64_t n = 0;
+    DVec() = default;
+    explicit DVec(int64_t n_, cudaStream_t s = nullptr) : n(n_) { p = dev_alloc<double>(n_ + 2, true, s); }
+    DVec(const DVec&) = delete;
+    DVec& operator=(const DVec&) = delete;
+    DVec(DVec&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; }
+    DVec& operator=(DVec&& o) noexcept {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        return *this;
+    }
+    ~DVec() { dev_free(p); }
+    operator double*() const { return p; }
+};
+
+inline unsigned grid_for(int64_t work, int threads, int64_t cap) {
+    int64_t g = (work + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+// ---------------------------------------------------------------- device reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum (fixed tree); result valid in every thread.  Uses `sh` with at
+// least NT/32 doubles.  Must be called by all threads of the block.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double t = (threadIdx.x < NT / 32) ? sh[threadIdx.x] : 0.0;
+    if (w == 0) t = warp_sum(t);
+    if (threadIdx.x == 0) sh[0] = t;
+    __syncthreads();
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// Arrival on a grid-wide counter; returns true in every thread of the block that arrives
+// last.  Partials written before the call are visible to that block.
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = atomicAdd(counter, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
+// Same as block_sum for a runtime block size (multiple of 32, <= 1024).
+__device__ __forceinline__ double block_sum_dyn(double v, double* sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double t = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+    if (w == 0) t = warp_sum(t);
+    if (threadIdx.x == 0) sh[0] = t;
+    __syncthreads();
+    double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ double reduce_partials_dyn(const double* partials, int count, double* sh) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) acc += __ldcg(partials + i);
+    return block_sum_dyn(acc, sh);
+}
+
+// Deterministic reduction of `count` partials (fixed order) by one block.
+template <int NT>
+__device__ __forceinline__ double reduce_partials(const double* partials, int count, double* sh) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < count; i += NT) acc += __ldcg(partials + i);
+    return block_sum<NT>(acc, sh);
+}
+
+// ---------------------------------------------------------------- C-ABI guard
+extern thread_local std::string g_last_error;
+
+template <typename F>
+krysp_status guard(F&& f) {
+    try {
+        f();
+        return KRYSP_OK;
+    } catch (const Status& s) {
+        g_last_error = s.msg;
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return KRYSP_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return KRYSP_ERROR;
+    }
+}
+
+// ---------------------------------------------------------------- host-side internals
+void ctx_check_device(krysp_gpu_ctx* ctx);
+int64_t kernel_launches(krysp_gpu_ctx* ctx);
+
+// formats.cu
+void mat_free_arrays(krysp_gpu_mat* m);
+krysp_gpu_mat* mat_new(krysp_gpu_ctx* ctx, int32_t fmt, int64_t n_rows, int64_t n_cols);
+void mat_row_stats(krysp_gpu_mat* m);  // fills max_row / max_tile_nnz for CSR
+krysp_gpu_mat* convert_to_csr(const krysp_gpu_mat* m);
+
+// spmv.cu
+enum SpmvVariant : int32_t {
+    kVarCsrVector = 0,  // paper's CSR-vector kernel, tw lanes per row, exact policy order
+    kVarCsrTile = 1,    // smem-staged thread-per-row CSR (tw == 1 order)
+    kVarEll = 2,
+    kVarHyb = 3,
+    kVarCoo = 4,
+};
+int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const krysp_policy& pol,
+                    int32_t mode, cudaStream_t s);
+void check_policy(const krysp_policy& pol);
+
+// blas1.cu
+void k_daxpy(krysp_gpu_ctx* c, int64_t n, double a, const double* x, double* y);
+void k_axpby(krysp_gpu_ctx* c, int64_t n, double a, const double* x, double b, double* y);
+void k_scale(krysp_gpu_ctx* c, int64_t n, double a, double* x);
+void k_copy(krysp_gpu_ctx* c, int64_t n, const double* s, double* d);
+void k_fill(krysp_gpu_ctx* c, int64_t n, double v, double* x);
+void k_scal_elementwise(krysp_gpu_ctx* c, int64_t n, double* a, const double* b);
+void k_mul(krysp_gpu_ctx* c, int64_t n, const double* a, const double* b, double* out);  // out = a*b
+// Device-side dot into d_out (no sync).  EXACT: chunk + fold (policy.block_size).
+void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode,
+           double* d_out);
+double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs,
+                int32_t mode);
+void k_diagonal(const krysp_gpu_mat* m, double* d);
+void k_invert_diag(krysp_gpu_ctx* c, int64_t n, double* d, int* d_zero_row);
+
+}  // namespace kg

@@ -1,0 +1,1042 @@
+// Preconditioned Krylov solvers on the device (reference solvers.cpp:119-787).
+//
+// Two execution paths share the same kernels:
+//  * Engine-driven ("host-driven"): the recurrence of each reference solver restated with
+//    device vectors; every reference kernel call becomes one device kernel with identical
+//    rounding, every scalar the reference computes on the host is computed on the host from
+//    the device reduction.  In KRYSP_MODE_EXACT this replays the reference bit for bit
+//    (SpMV lane order, chunked dots, no FMA); in FAST mode only the dot order differs.
+//  * Device-resident fused P-CG (FAST): one iteration = 3 kernels (SpMV + <p,Ap>; update of
+//    x, r with the Jacobi-scaled <r,z>; direction), scalars and the convergence test stay
+//    on the device, iterations are CUDA-graph captured in chunks and kernels of a converged
+//    solve exit on entry — so the iteration count is exact without per-iteration host syncs.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+
+#include "spmv_kernels.cuh"
+
+namespace kg {
+
+namespace {
+
+constexpr double kBreakdownEps = 1e-300;  // solvers.cpp:14
+
+bool vanishes(double v) { return std::fabs(v) < kBreakdownEps; }
+
+void check_finite(double v, const char* what) {
+    if (!std::isfinite(v)) fail(KRYSP_NON_FINITE, "%s became non-finite", what);
+}
+
+// ------------------------------------------------------------------ engine
+struct Engine {
+    krysp_gpu_ctx* c;
+    const krysp_gpu_mat* A;
+    const krysp_gpu_mat* At = nullptr;  // bicgcr
+    krysp_policy pol;
+    int32_t mode;
+    int64_t n;
+    DVec inv;  // Jacobi inverse diagonal (empty when unpreconditioned)
+    bool jacobi = false;
+    DVec tmp;
+
+    Engine(const krysp_gpu_mat* A_, const krysp_solver_cfg& cfg)
+        : c(A_->ctx), A(A_), pol(cfg.policy), mode(cfg.mode), n(A_->n_rows), tmp(A_->n_rows, A_->ctx->stream) {
+        if (pol.block_size == 0) {
+            if (mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "auto policy (block_size 0) requires FAST mode");
+            krysp_gpu_autotune_policy(A, &pol);
+        }
+        check_policy(pol);
+        if (cfg.preconditioner) make_jacobi();
+    }
+
+    DVec vec() { return DVec(n, c->stream); }
+
+    // maybe_jacobi / make_jacobi, solvers.cpp:54-59, 102-113
+    void make_jacobi() {
+        jacobi = true;
+        inv = DVec(n, c->stream);
+        k_diagonal(A, inv);
+        int* zr = dev_alloc<int>(1, false);
+        int big = INT32_MAX;
+        KG_CUDA(cudaMemcpyAsync(zr, &big, sizeof big, cudaMemcpyHostToDevice, c->stream));
+        k_invert_diag(c, n, inv, zr);
+        int hz;
+        KG_CUDA(cudaMemcpyAsync(&hz, zr, sizeof hz, cudaMemcpyDeviceToHost, c->stream));
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+        dev_free(zr);
+        if (hz != INT32_MAX) fail(KRYSP_BREAKDOWN, "zero diagonal entry at row %d; Jacobi preconditioner undefined", hz);
+    }
+
+    void spmv(const krysp_gpu_mat* M, const double* x, double* y) { spmv_launch(M, x, y, pol, mode, c->stream); }
+    void spmv(const double* x, double* y) { spmv(A, x, y); }
+    // apply_precond solvers.cpp:46-52: z = copy(r), then z *= inv
+    void precond(const double* r, double* z) {
+        if (jacobi) k_mul(c, n, r, inv, z);  // fl(r*inv): the same single rounding as copy + scal
+        else k_copy(c, n, r, z);
+    }
+    void op(const double* in, double* out) {
+        spmv(in, tmp);
+        precond(tmp, out);
+    }
+    void op_t(const double* in, double* out) {
+        spmv(At, in, tmp);
+        precond(tmp, out);
+    }
+    // initial_residual solvers.cpp:62-68
+    void residual(const double* b, const double* x, double* r) {
+        spmv(x, r);
+        k_scale(c, n, -1.0, r);
+        k_daxpy(c, n, 1.0, b, r);
+    }
+    double dot(const double* x, const double* y) { return host_dot(c, n, x, y, pol.block_size, mode); }
+    double norm2(const double* x) { return std::sqrt(dot(x, x)); }
+    void daxpy(double a, const double* x, double* y) { k_daxpy(c, n, a, x, y); }
+    void axpby(double a, const double* x, double b, double* y) { k_axpby(c, n, a, x, b, y); }
+    void copy(const double* s, double* d) { k_copy(c, n, s, d); }
+};
+
+struct Report {
+    bool converged = false;
+    int64_t iterations = 0;
+    double final_measure = 0.0;
+    std::vector<double> history;
+    std::vector<double> trace;  // 4 per iteration (pcg)
+    void push(double m) {
+        history.push_back(m);
+        ++iterations;
+    }
+};
+
+// ------------------------------------------------------------------ host-driven solvers
+// solve_pcg solvers.cpp:119-187
+void pcg(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep, bool trace) {
+    DVec r = e.vec(), z = e.vec(), p = e.vec(), ap = e.vec();
+    e.residual(b, x, r);
+    double norm_r0 = e.norm2(r);
+    if (norm_r0 == 0.0) norm_r0 = 1.0;
+    e.precond(r, z);
+    double rho = e.dot(r, z), rho_1 = 0.0;
+    double norm_r = rho / norm_r0;
+    if (norm_r <= cfg.tolerance) {
+        rep.converged = true;
+        rep.final_measure = norm_r;
+        return;
+    }
+    bool first = true;
+    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+        double beta = 0.0;
+        if (first) first = false;
+        else {
+            beta = rho / rho_1;
+            e.daxpy(beta, p, z);
+        }
+        std::swap(z, p);
+        e.spmv(p, ap);
+        double sigma = e.dot(p, ap);
+        check_finite(sigma, "sigma");
+        if (vanishes(sigma)) fail(KRYSP_BREAKDOWN, "pcg: <p, Ap> vanished before convergence");
+        double alpha = rho / sigma;
+        check_finite(alpha, "alpha");
+        e.daxpy(alpha, p, x);
+        e.daxpy(-alpha, ap, r);
+        rho_1 = rho;
+        if (trace) rep.trace.insert(rep.trace.end(), {rho, beta, sigma, alpha});
+        e.precond(r, z);
+        rho = e.dot(r, z);
+        check_finite(rho, "rho");
+        norm_r = rho / norm_r0;
+        rep.push(norm_r);
+        if (norm_r <= cfg.tolerance) rep.converged = true;
+    }
+    rep.final_measure = norm_r;
+}
+
+// solve_cg_classic solvers.cpp:193-250
+void cg_classic(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    DVec g = e.vec(), z = e.vec(), w = e.vec(), kw = e.vec();
+    e.spmv(x, g);
+    e.daxpy(-1.0, b, g);
+    double norm_g0 = e.norm2(g);
+    if (norm_g0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    e.precond(g, z);
+    e.copy(z, w);
+    double measure = 1.0;
+    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+        e.spmv(w, kw);
+        double denom = e.dot(kw, w);
+        check_finite(denom, "descent denominator");
+        if (vanishes(denom)) fail(KRYSP_BREAKDOWN, "cg: <Kw, w> vanished before convergence");
+        double rho = -e.dot(g, w) / denom;
+        check_finite(rho, "rho");
+        e.daxpy(rho, w, x);
+        e.daxpy(rho, kw, g);
+        e.precond(g, z);
+        double gamma = -e.dot(z, kw) / denom;
+        check_finite(gamma, "gamma");
+        e.axpby(1.0, z, gamma, w);
+        measure = e.norm2(g) / norm_g0;
+        check_finite(measure, "residual measure");
+        rep.push(measure);
+        if (measure <= cfg.tolerance) rep.converged = true;
+    }
+    rep.final_measure = measure;
+}
+
+// solve_gcr solvers.cpp:256-338
+void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    const int64_t m = cfg.restart;
+    DVec raw = e.vec(), r = e.vec(), w = e.vec();
+    e.residual(b, x, raw);
+    e.precond(raw, r);
+    double norm_r0 = e.norm2(r);
+    if (norm_r0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    std::vector<DVec> dirs, op_dirs;
+    double measure = 1.0;
+    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+        // the basis storage is reused across restarts (dirs.clear() in the reference)
+        int64_t kept = 0;
+        auto slot = [&](std::vector<DVec>& v, int64_t j) -> DVec& {
+            while ((int64_t)v.size() <= j) v.emplace_back(e.vec());
+            return v[(size_t)j];
+        };
+        e.copy(r, slot(dirs, 0));
+        e.op(slot(dirs, 0), slot(op_dirs, 0));
+        kept = 1;
+        for (int64_t j = 0; j < m; ++j) {
+            const double* p = dirs[(size_t)j];
+            const double* ap = op_dirs[(size_t)j];
+            double d = e.dot(ap, ap);
+            check_finite(d, "direction norm");
+            if (vanishes(d)) fail(KRYSP_BREAKDOWN, "gcr: direction norm vanished");
+            double alpha = e.dot(r, ap) / d;
+            check_finite(alpha, "alpha");
+            e.daxpy(alpha, p, x);
+            e.daxpy(-alpha, ap, r);
+            measure = e.norm2(r) / norm_r0;
+            check_finite(measure, "residual measure");
+            rep.push(measure);
+            if (measure <= cfg.tolerance) {
+                rep.converged = true;
+                break;
+            }
+            if (rep.iterations >= cfg.max_iterations) break;
+            if (j + 1 == m) break;
+            e.op(r, w);
+            DVec& pn = slot(dirs, j + 1);
+            DVec& apn = slot(op_dirs, j + 1);
+            e.copy(r, pn);
+            e.copy(w, apn);
+            for (int64_t i = 0; i <= j; ++i) {
+                double beta = e.dot(w, op_dirs[(size_t)i]) / e.dot(op_dirs[(size_t)i], op_dirs[(size_t)i]);
+                e.daxpy(-beta, dirs[(size_t)i], pn);
+                e.daxpy(-beta, op_dirs[(size_t)i], apn);
+            }
+            kept = j + 2;
+        }
+        (void)kept;
+    }
+    rep.final_measure = measure;
+}
+
+// solve_bicgstab solvers.cpp:344-438
+void bicgstab(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    DVec raw = e.vec(), r = e.vec(), rh = e.vec(), p = e.vec(), v = e.vec(), s = e.vec(), t = e.vec();
+    e.residual(b, x, raw);
+    e.precond(raw, r);
+    double norm_r0 = e.norm2(r);
+    if (norm_r0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    e.copy(r, rh);
+    e.copy(r, p);
+    double rho = e.dot(rh, r);
+    double measure = 1.0;
+    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+        e.op(p, v);
+        double denom = e.dot(rh, v);
+        check_finite(denom, "<r_hat, v>");
+        if (vanishes(denom)) fail(KRYSP_BREAKDOWN, "bicgstab: <r_hat, v> vanished");
+        double alpha = rho / denom;
+        check_finite(alpha, "alpha");
+        e.copy(r, s);
+        e.daxpy(-alpha, v, s);
+        measure = e.norm2(s) / norm_r0;
+        check_finite(measure, "residual measure");
+        if (measure <= cfg.tolerance) {
+            e.daxpy(alpha, p, x);
+            rep.push(measure);
+            rep.converged = true;
+            break;
+        }
+        e.op(s, t);
+        double tt = e.dot(t, t);
+        if (vanishes(tt)) fail(KRYSP_BREAKDOWN, "bicgstab: <t, t> vanished");
+        double omega = e.dot(t, s) / tt;
+        check_finite(omega, "omega");
+        if (vanishes(omega)) fail(KRYSP_BREAKDOWN, "bicgstab: omega vanished");
+        e.daxpy(alpha, p, x);
+        e.daxpy(omega, s, x);
+        e.copy(s, r);
+        e.daxpy(-omega, t, r);
+        measure = e.norm2(r) / norm_r0;
+        check_finite(measure, "residual measure");
+        rep.push(measure);
+        if (measure <= cfg.tolerance) {
+            rep.converged = true;
+            break;
+        }
+        double rho_new = e.dot(rh, r);
+        if (vanishes(rho_new)) fail(KRYSP_BREAKDOWN, "bicgstab: <r_hat, r> vanished");
+        double beta = (rho_new / rho) * (alpha / omega);
+        check_finite(beta, "beta");
+        e.daxpy(-omega, v, p);
+        e.axpby(1.0, r, beta, p);
+        rho = rho_new;
+    }
+    rep.final_measure = measure;
+}
+
+// solve_bicgstab_l solvers.cpp:444-572
+void bicgstab_l(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    const int64_t L = cfg.stab_l;
+    DVec raw = e.vec(), rs = e.vec();
+    std::vector<DVec> rr, uu;
+    for (int64_t j = 0; j <= L; ++j) {
+        rr.emplace_back(e.vec());
+        uu.emplace_back(e.vec());  // zero-initialised (std::vector<double>(n, 0.0))
+    }
+    e.residual(b, x, raw);
+    e.precond(raw, rr[0]);
+    double norm_r0 = e.norm2(rr[0]);
+    if (norm_r0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    e.copy(rr[0], rs);
+    double rho0 = 1.0, alpha = 0.0, omega = 1.0, measure = 1.0;
+    std::vector<double> sigma(L + 1), gp(L + 1), g(L + 1), gpp(L + 1);
+    std::vector<double> tau((size_t)((L + 1) * (L + 1)), 0.0);
+    auto TAU = [&](int64_t i, int64_t j) -> double& { return tau[(size_t)(i * (L + 1) + j)]; };
+    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+        rho0 = -omega * rho0;
+        for (int64_t j = 0; j < L && !rep.converged; ++j) {
+            double rho1 = e.dot(rr[j], rs);
+            check_finite(rho1, "rho");
+            if (vanishes(rho0)) fail(KRYSP_BREAKDOWN, "bicgstab(l): rho vanished");
+            double beta = alpha * rho1 / rho0;
+            check_finite(beta, "beta");
+            rho0 = rho1;
+            for (int64_t i = 0; i <= j; ++i) e.axpby(1.0, rr[i], -beta, uu[i]);
+            e.op(uu[j], uu[j + 1]);
+            double gg = e.dot(uu[j + 1], rs);
+            if (vanishes(gg)) fail(KRYSP_BREAKDOWN, "bicgstab(l): <u, r_shadow> vanished");
+            alpha = rho0 / gg;
+            check_finite(alpha, "alpha");
+            for (int64_t i = 0; i <= j; ++i) e.daxpy(-alpha, uu[i + 1], rr[i]);
+            e.op(rr[j], rr[j + 1]);
+            e.daxpy(alpha, uu[0], x);
+            measure = e.norm2(rr[0]) / norm_r0;
+            check_finite(measure, "residual measure");
+            if (measure <= cfg.tolerance) rep.converged = true;
+        }
+        if (rep.converged) {
+            rep.push(measure);
+            break;
+        }
+        for (int64_t j = 1; j <= L; ++j) {
+            for (int64_t i = 1; i < j; ++i) {
+                TAU(i, j) = e.dot(rr[j], rr[i]) / sigma[i];
+                e.daxpy(-TAU(i, j), rr[i], rr[j]);
+            }
+            sigma[j] = e.dot(rr[j], rr[j]);
+            if (vanishes(sigma[j])) fail(KRYSP_BREAKDOWN, "bicgstab(l): minimal-residual system singular");
+            gp[j] = e.dot(rr[0], rr[j]) / sigma[j];
+        }
+        g[L] = gp[L];
+        omega = g[L];
+        for (int64_t j = L - 1; j >= 1; --j) {
+            double s = 0.0;
+            for (int64_t i = j + 1; i <= L; ++i) s += TAU(j, i) * g[i];
+            g[j] = gp[j] - s;
+        }
+        for (int64_t j = 1; j < L; ++j) {
+            double s = 0.0;
+            for (int64_t i = j + 1; i < L; ++i) s += TAU(j, i) * g[i + 1];
+            gpp[j] = g[j + 1] + s;
+        }
+        e.daxpy(g[1], rr[0], x);
+        e.daxpy(-gp[L], rr[L], rr[0]);
+        e.daxpy(-g[L], uu[L], uu[0]);
+        for (int64_t j = 1; j < L; ++j) {
+            e.daxpy(-g[j], uu[j], uu[0]);
+            e.daxpy(gpp[j], rr[j], x);
+            e.daxpy(-gp[j], rr[j], rr[0]);
+        }
+        measure = e.norm2(rr[0]) / norm_r0;
+        check_finite(measure, "residual measure");
+        rep.push(measure);
+        if (measure <= cfg.tolerance) rep.converged = true;
+    }
+    rep.final_measure = measure;
+}
+
+// solve_tfqmr solvers.cpp:578-696
+void tfqmr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    DVec raw = e.vec(), r0 = e.vec(), w = e.vec(), u = e.vec(), un = e.vec(), v = e.vec(), d = e.vec();
+    DVec bu = e.vec(), bun = e.vec(), res = e.vec(), tmp2 = e.vec();
+    e.residual(b, x, raw);
+    e.precond(raw, r0);
+    double norm_r0 = e.norm2(r0);
+    if (norm_r0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    // true_measure lambda :607-613
+    auto true_measure = [&]() {
+        e.spmv(x, tmp2);
+        k_scale(e.c, e.n, -1.0, tmp2);
+        e.daxpy(1.0, b, tmp2);
+        e.precond(tmp2, res);
+        return e.norm2(res) / norm_r0;
+    };
+    e.copy(r0, w);
+    e.copy(r0, u);
+    e.op(u, v);
+    e.copy(v, bu);
+    double tau = norm_r0, theta = 0.0, eta = 0.0;
+    double rho = e.dot(r0, r0), alpha = 0.0, measure = 1.0;
+    for (int64_t m = 0; rep.iterations < cfg.max_iterations && !rep.converged; ++m) {
+        const bool even = (m % 2 == 0);
+        if (even) {
+            double denom = e.dot(v, r0);
+            if (vanishes(denom)) fail(KRYSP_BREAKDOWN, "tfqmr: <v, r_shadow> vanished");
+            alpha = rho / denom;
+            check_finite(alpha, "alpha");
+            e.copy(u, un);
+            e.daxpy(-alpha, v, un);
+        } else {
+            e.op(u, bu);
+        }
+        e.daxpy(-alpha, bu, w);
+        double scale = (theta * theta * eta) / alpha;
+        check_finite(scale, "direction scale");
+        e.axpby(1.0, u, scale, d);
+        theta = e.norm2(w) / tau;
+        double cc = 1.0 / std::sqrt(1.0 + theta * theta);
+        tau = tau * theta * cc;
+        eta = cc * cc * alpha;
+        check_finite(tau, "tau");
+        e.daxpy(eta, d, x);
+        double bound = tau * std::sqrt((double)(m + 2)) / norm_r0;
+        if (bound <= cfg.tolerance) {
+            measure = true_measure();
+            if (measure <= cfg.tolerance) {
+                rep.push(measure);
+                rep.converged = true;
+                break;
+            }
+        }
+        if (!even) {
+            double rho_new = e.dot(w, r0);
+            if (vanishes(rho_new)) fail(KRYSP_BREAKDOWN, "tfqmr: rho vanished");
+            double beta = rho_new / rho;
+            check_finite(beta, "beta");
+            rho = rho_new;
+            e.copy(w, un);
+            e.daxpy(beta, u, un);
+            e.op(un, bun);
+            e.axpby(beta, bu, beta * beta, v);
+            e.daxpy(1.0, bun, v);
+            std::swap(bu, bun);
+            measure = true_measure();
+            check_finite(measure, "residual measure");
+            rep.push(measure);
+            if (measure <= cfg.tolerance) rep.converged = true;
+        }
+        std::swap(u, un);
+    }
+    rep.final_measure = measure;
+}
+
+// solve_bicgcr solvers.cpp:702-787 (transpose built on device, formats.cpp:312-334)
+void bicgcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    DVec raw = e.vec(), z = e.vec(), zt = e.vec(), p = e.vec(), pt = e.vec(), bz = e.vec(), bp = e.vec(),
+         btpt = e.vec();
+    e.residual(b, x, raw);
+    e.precond(raw, z);
+    double norm_z0 = e.norm2(z);
+    if (norm_z0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    e.copy(z, zt);
+    e.copy(z, p);
+    e.copy(z, pt);
+    e.op(z, bz);
+    e.copy(bz, bp);
+    double num = e.dot(zt, bz), measure = 1.0;
+    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+        e.op_t(pt, btpt);
+        double denom = e.dot(btpt, bp);
+        check_finite(denom, "<B'p', Bp>");
+        if (vanishes(denom)) fail(KRYSP_BREAKDOWN, "bicgcr: direction denominator vanished");
+        double alpha = num / denom;
+        check_finite(alpha, "alpha");
+        e.daxpy(alpha, p, x);
+        e.daxpy(-alpha, bp, z);
+        e.daxpy(-alpha, btpt, zt);
+        measure = e.norm2(z) / norm_z0;
+        check_finite(measure, "residual measure");
+        rep.push(measure);
+        if (measure <= cfg.tolerance) {
+            rep.converged = true;
+            break;
+        }
+        e.op(z, bz);
+        double num_new = e.dot(zt, bz);
+        check_finite(num_new, "<z', Bz>");
+        if (vanishes(num)) fail(KRYSP_BREAKDOWN, "bicgcr: <z', Bz> vanished");
+        double beta = num_new / num;
+        check_finite(beta, "beta");
+        e.axpby(1.0, z, beta, p);
+        e.axpby(1.0, zt, beta, pt);
+        e.axpby(1.0, bz, beta, bp);
+        num = num_new;
+    }
+    rep.final_measure = measure;
+}
+
+// ------------------------------------------------------------------ device-resident P-CG
+struct CgState {
+    double rho, rho_1, sigma, alpha, beta, norm_r0, tol;
+    long long iter, max_it;
+    int done, status;
+};
+
+enum : int { kStRunning = 0, kStBreakdownSigma = 1, kStNonFiniteSigma = 2, kStNonFiniteAlpha = 3, kStNonFiniteRho = 4 };
+
+constexpr int kFusedNT = 256;
+
+// Epilogue of the SpMV: Ap[r] = (A p)[r], partial <p, Ap>; the last block forms sigma and
+// alpha = rho / sigma with the reference's checks (solvers.cpp:160-166).
+struct EpiCgSigma {
+    double* __restrict__ ap;
+    const double* __restrict__ p;
+    double* partials;
+    unsigned* counter;
+    CgState* st;
+    double acc;
+    __device__ __forceinline__ bool active() const { return *(volatile int*)&st->done == 0; }
+    __device__ __forceinline__ void row(int64_t r, double v) {
+        ap[r] = v;
+        acc = fma(p[r], v, acc);
+    }
+    __device__ __forceinline__ void finish() {
+        __shared__ double sh[32];
+        const double b = block_sum_dyn(acc, sh);
+        if (threadIdx.x == 0) partials[blockIdx.x] = b;
+        if (last_block(counter)) {
+            const double sigma = reduce_partials_dyn(partials, gridDim.x, sh);
+            if (threadIdx.x == 0) {
+                *counter = 0;
+                st->sigma = sigma;
+                if (!isfinite(sigma)) {
+                    st->status = kStNonFiniteSigma;
+                    st->done = 1;
+                } else if (fabs(sigma) < kBreakdownEps) {
+                    st->status = kStBreakdownSigma;
+                    st->done = 1;
+                } else {
+                    const double alpha = st->rho / sigma;
+                    st->alpha = alpha;
+                    if (!isfinite(alpha)) {
+                        st->status = kStNonFiniteAlpha;
+                        st->done = 1;
+                    }
+                }
+            }
+        }
+    }
+};
+
+// x += alpha p; r -= alpha Ap; <r, D^-1 r> (solvers.cpp:167-181), convergence on device.
+template <bool kJacobi>
+__global__ void __launch_bounds__(kFusedNT) cg_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                              const double* __restrict__ p, const double* __restrict__ ap,
+                                                              const double* __restrict__ inv, CgState* st,
+                                                              double* partials, unsigned* counter,
+                                                              double* history, double* trace) {
+    if (*(volatile int*)&st->done) return;
+    __shared__ double sh[32];
+    const double alpha = st->alpha, malpha = -alpha;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kFusedNT) {
+        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        const double ri = __dadd_rn(__dmul_rn(malpha, ap[i]), r[i]);
+        r[i] = ri;
+        const double zi = kJacobi ? __dmul_rn(ri, inv[i]) : ri;
+        acc = fma(ri, zi, acc);
+    }
+    const double b = block_sum<kFusedNT>(acc, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = b;
+    if (last_block(counter)) {
+        const double rho_new = reduce_partials<kFusedNT>(partials, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            *counter = 0;
+            const long long it = st->iter;
+            if (trace) {
+                double* t = trace + 4 * it;
+                t[0] = st->rho;
+                t[1] = st->beta;
+                t[2] = st->sigma;
+                t[3] = st->alpha;
+            }
+            if (!isfinite(rho_new)) {
+                st->status = kStNonFiniteRho;
+                st->done = 1;
+                return;
+            }
+            const double measure = rho_new / st->norm_r0;
+            history[it] = measure;
+            st->iter = it + 1;
+            st->rho_1 = st->rho;
+            st->beta = rho_new / st->rho;
+            st->rho = rho_new;
+            if (measure <= st->tol || it + 1 >= st->max_it) st->done = 1;
+        }
+    }
+}
+
+// p = D^-1 r + beta p (solvers.cpp:154-157: z += beta p, then p <- z)
+template <bool kJacobi>
+__global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, double* __restrict__ p,
+                                                                 const double* __restrict__ r,
+                                                                 const double* __restrict__ inv, const CgState* st) {
+    if (*(volatile const int*)&st->done) return;
+    const double beta = st->beta;
+    for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kFusedNT) {
+        const double zi = kJacobi ? __dmul_rn(r[i], inv[i]) : r[i];
+        p[i] = __dadd_rn(__dmul_rn(beta, p[i]), zi);
+    }
+}
+
+// generic epilogue pass for formats whose row values are not final inside one kernel
+template <class Epi>
+__global__ void __launch_bounds__(1024) vec_epi_kernel(int64_t n, const double* __restrict__ y, Epi epi) {
+    if (!epi.active()) return;
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r < n) epi.row(r, y[r]);
+    epi.finish();
+}
+
+template <class Epi>
+void spmv_fused(Engine& e, const double* x, double* y, Epi epi) {
+    const krysp_gpu_mat* m = e.A;
+    cudaStream_t s = e.c->stream;
+    if (m->format == KRYSP_FMT_CSR) {
+        if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, x, epi, s);
+        else launch_csr_vector(m, x, epi, e.pol.block_size, e.pol.workers_per_row, s);
+    } else if (m->format == KRYSP_FMT_ELL || (m->format == KRYSP_FMT_HYB && m->coo_nnz == 0)) {
+        launch_ell(m, x, epi, e.pol.block_size, s);
+    } else {
+        spmv_launch(m, x, y, e.pol, e.mode, s);
+        vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, INT32_MAX), 1024, 0, s>>>(m->n_rows, y, epi);
+        KG_LAUNCH(e.c);
+    }
+}
+
+}  // namespace
+
+// Device-resident FAST P-CG session: setup once, then iterations are enqueued as CUDA-graph
+// launches (chunks of kChunk iterations + single-iteration graphs for remainders).  Also
+// backs the krysp_gpu_solver_* C-ABI (bench / profiling / multi-step drivers).
+struct PcgSession {
+    static constexpr int kChunk = 16;
+    Engine e;
+    krysp_solver_cfg cfg;
+    int64_t n;
+    DVec x, r, p, ap;
+    CgState* st = nullptr;
+    double* hist = nullptr;
+    double* d_trace = nullptr;
+    double measure0 = 0.0;
+    bool done_at_setup = false;
+    cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr, exec_prof = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int kernels_per_iteration = 0;
+
+    PcgSession(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg_, const double* b, const double* x0, bool trace)
+        : e(A, cfg_), cfg(cfg_), n(A->n_rows), x(A->n_rows, A->ctx->stream), r(A->n_rows, A->ctx->stream),
+          p(A->n_rows, A->ctx->stream), ap(A->n_rows, A->ctx->stream) {
+        krysp_gpu_ctx* c = e.c;
+        try {
+            if (n) KG_CUDA(cudaMemcpyAsync(x, x0, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+            // solve_pcg setup, solvers.cpp:131-146
+            e.residual(b, x, r);
+            double norm_r0 = e.norm2(r);
+            if (norm_r0 == 0.0) norm_r0 = 1.0;
+            e.precond(r, p);  // z, which the first iteration takes as p (swap, no beta term)
+            const double rho = e.dot(r, p);
+            measure0 = rho / norm_r0;
+            CgState h{};
+            h.rho = rho;
+            h.norm_r0 = norm_r0;
+            h.tol = cfg.tolerance;
+            h.max_it = cfg.max_iterations;
+            if (measure0 <= cfg.tolerance) {
+                done_at_setup = true;
+                h.done = 1;
+            }
+            st = dev_alloc<CgState>(1, false);
+            hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
+            if (trace) d_trace = dev_alloc<double>(4 * cfg.max_iterations, true, c->stream);
+            KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+            KG_CUDA(cudaStreamSynchronize(c->stream));
+            for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
+            exec_chunk = capture(kChunk, false);
+            exec_one = capture(1, false);
+            exec_prof = capture(1, true);
+        } catch (...) {
+            release();
+            throw;
+        }
+    }
+    ~PcgSession() { release(); }
+
+    void release() {
+        if (exec_chunk) cudaGraphExecDestroy(exec_chunk);
+        if (exec_one) cudaGraphExecDestroy(exec_one);
+        if (exec_prof) cudaGraphExecDestroy(exec_prof);
+        exec_chunk = exec_one = exec_prof = nullptr;
+        for (auto& v : ev)
+            if (v) cudaEventDestroy(v), v = nullptr;
+        dev_free(st);
+        dev_free(hist);
+        dev_free(d_trace);
+        st = nullptr;
+        hist = d_trace = nullptr;
+    }
+
+    void iteration(bool events) {
+        krysp_gpu_ctx* c = e.c;
+        double* part_a = c->d_partials + 2 * kPartialCap;
+        double* part_b = c->d_partials + 3 * kPartialCap;
+        unsigned* cnt_a = c->d_counters + 2;
+        unsigned* cnt_b = c->d_counters + 3;
+        const unsigned g_vec = grid_for(n, kFusedNT, (int64_t)c->sm_count * 8);
+        const int64_t before = c->launches;
+        if (events) KG_CUDA(cudaEventRecord(ev[0], c->stream));
+        EpiCgSigma epi{ap, p, part_a, cnt_a, st, 0.0};
+        spmv_fused(e, p, ap, epi);
+        if (events) KG_CUDA(cudaEventRecord(ev[1], c->stream));
+        if (e.jacobi)
+            cg_update_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, x, r, p, ap, e.inv, st, part_b, cnt_b, hist, d_trace);
+        else
+            cg_update_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, x, r, p, ap, nullptr, st, part_b, cnt_b, hist, d_trace);
+        KG_LAUNCH(c);
+        if (events) KG_CUDA(cudaEventRecord(ev[2], c->stream));
+        if (e.jacobi) cg_direction_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, e.inv, st);
+        else cg_direction_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, nullptr, st);
+        KG_LAUNCH(c);
+        if (events) KG_CUDA(cudaEventRecord(ev[3], c->stream));
+        kernels_per_iteration = (int)(c->launches - before);
+    }
+
+    cudaGraphExec_t capture(int iters, bool events) {
+        krysp_gpu_ctx* c = e.c;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        KG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            for (int i = 0; i < iters; ++i) iteration(events);
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        KG_CUDA(cudaStreamEndCapture(c->stream, &graph));
+        KG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        return exec;
+    }
+
+    // enqueue n iterations (kernels of a finished solve exit on entry)
+    void enqueue(int64_t iters) {
+        krysp_gpu_ctx* c = e.c;
+        for (int64_t i = 0; i + kChunk <= iters; i += kChunk) KG_CUDA(cudaGraphLaunch(exec_chunk, c->stream));
+        for (int64_t i = 0; i < iters % kChunk; ++i) KG_CUDA(cudaGraphLaunch(exec_one, c->stream));
+    }
+
+    bool finished() {
+        krysp_gpu_ctx* c = e.c;
+        int* h_done = reinterpret_cast<int*>(c->h_pinned + 8);
+        KG_CUDA(cudaMemcpyAsync(h_done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+        return *h_done != 0;
+    }
+
+    double run_to_convergence() {
+        krysp_gpu_ctx* c = e.c;
+        cudaEvent_t a, b;
+        KG_CUDA(cudaEventCreate(&a));
+        KG_CUDA(cudaEventCreate(&b));
+        KG_CUDA(cudaEventRecord(a, c->stream));
+        while (!finished()) enqueue(kChunk);
+        KG_CUDA(cudaEventRecord(b, c->stream));
+        KG_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        KG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        return ms * 1e-3;
+    }
+
+    // n single-iteration graphs with event nodes: mean seconds of [spmv, update, direction]
+    void profile(int64_t iters, double out[3]) {
+        krysp_gpu_ctx* c = e.c;
+        out[0] = out[1] = out[2] = 0.0;
+        for (int64_t i = 0; i < iters; ++i) {
+            KG_CUDA(cudaGraphLaunch(exec_prof, c->stream));
+            KG_CUDA(cudaEventSynchronize(ev[3]));
+            for (int k = 0; k < 3; ++k) {
+                float ms = 0.f;
+                KG_CUDA(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+                out[k] += ms * 1e-3;
+            }
+        }
+        for (int k = 0; k < 3; ++k) out[k] /= (double)(iters > 0 ? iters : 1);
+    }
+
+    CgState state() {
+        CgState h{};
+        KG_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, e.c->stream));
+        KG_CUDA(cudaStreamSynchronize(e.c->stream));
+        return h;
+    }
+
+    // fill rep; throws the reference's exception for a device-detected breakdown
+    void finish(Report& rep, bool trace) {
+        CgState h = state();
+        rep.history.resize((size_t)h.iter);
+        if (h.iter) KG_CUDA(cudaMemcpy(rep.history.data(), hist, sizeof(double) * h.iter, cudaMemcpyDeviceToHost));
+        if (trace && h.iter) {
+            rep.trace.resize((size_t)(4 * h.iter));
+            KG_CUDA(cudaMemcpy(rep.trace.data(), d_trace, sizeof(double) * 4 * h.iter, cudaMemcpyDeviceToHost));
+        }
+        rep.iterations = h.iter;
+        rep.final_measure = h.iter ? rep.history.back() : measure0;
+        rep.converged = rep.final_measure <= cfg.tolerance;
+        switch (h.status) {
+            case kStBreakdownSigma: fail(KRYSP_BREAKDOWN, "pcg: <p, Ap> vanished before convergence");
+            case kStNonFiniteSigma: fail(KRYSP_NON_FINITE, "sigma became non-finite");
+            case kStNonFiniteAlpha: fail(KRYSP_NON_FINITE, "alpha became non-finite");
+            case kStNonFiniteRho: fail(KRYSP_NON_FINITE, "rho became non-finite");
+            default: break;
+        }
+    }
+};
+
+namespace {
+
+void pcg_fused(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep,
+               bool trace, double* device_seconds) {
+    PcgSession s(A, cfg, b, x, trace);
+    if (!s.done_at_setup) *device_seconds = s.run_to_convergence();
+    if (A->n_rows) KG_CUDA(cudaMemcpyAsync(x, s.x, 8 * A->n_rows, cudaMemcpyDeviceToDevice, A->ctx->stream));
+    s.finish(rep, trace);
+}
+
+}  // namespace
+
+krysp_gpu_mat* transpose(const krysp_gpu_mat* m);
+
+// check_system solvers.cpp:16-28, then dispatch.  x (device, n) holds x0 on entry and the
+// solution on return.
+void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, const krysp_solver_cfg& cfg,
+           krysp_report* out, double* h_history, double* h_trace) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (A->n_rows != A->n_cols) fail(KRYSP_DIMENSION_MISMATCH, "solver expects a square matrix");
+    if (!(cfg.tolerance > 0.0) || cfg.max_iterations < 1 || cfg.restart < 1 || cfg.stab_l < 1)
+        fail(KRYSP_ERROR,
+             "solver config requires tolerance > 0, max_iterations >= 1, restart >= 1, stab_l >= 1");
+    if (cfg.mode != KRYSP_MODE_EXACT && cfg.mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "unknown mode %d", cfg.mode);
+    if (method < KRYSP_PCG || method > KRYSP_BICGCR) fail(KRYSP_ERROR, "unknown method %d", method);
+    std::unique_ptr<krysp_gpu_mat, void (*)(krysp_gpu_mat*)> at(nullptr, [](krysp_gpu_mat* m) {
+        if (m) {
+            mat_free_arrays(m);
+            delete m;
+        }
+    });
+    cudaStream_t stream = A->ctx->stream;
+    const bool fused = method == KRYSP_PCG && cfg.mode == KRYSP_MODE_FAST;
+    Report rep;
+    double dev_s = 0.0;
+    std::exception_ptr err;
+    cudaEvent_t ev0, ev1;
+    KG_CUDA(cudaEventCreate(&ev0));
+    KG_CUDA(cudaEventCreate(&ev1));
+    KG_CUDA(cudaEventRecord(ev0, stream));
+    try {
+        if (fused) {
+            pcg_fused(A, cfg, b, x, rep, h_trace != nullptr, &dev_s);
+        } else {
+            Engine e(A, cfg);
+            switch (method) {
+                case KRYSP_PCG: pcg(e, cfg, b, x, rep, h_trace != nullptr); break;
+                case KRYSP_CG_CLASSIC: cg_classic(e, cfg, b, x, rep); break;
+                case KRYSP_GCR: gcr(e, cfg, b, x, rep); break;
+                case KRYSP_BICGSTAB: bicgstab(e, cfg, b, x, rep); break;
+                case KRYSP_BICGSTAB_L: bicgstab_l(e, cfg, b, x, rep); break;
+                case KRYSP_TFQMR: tfqmr(e, cfg, b, x, rep); break;
+                case KRYSP_BICGCR:
+                    at.reset(transpose(A));
+                    e.At = at.get();
+                    bicgcr(e, cfg, b, x, rep);
+                    break;
+            }
+        }
+    } catch (...) {
+        err = std::current_exception();
+    }
+    KG_CUDA(cudaEventRecord(ev1, stream));
+    KG_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    KG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    out->converged = rep.converged ? 1 : 0;
+    out->iterations = rep.iterations;
+    out->final_residual_measure = rep.final_measure;
+    out->device_time = fused ? dev_s : ms * 1e-3;
+    if (h_history && !rep.history.empty())
+        std::memcpy(h_history, rep.history.data(), sizeof(double) * std::min<size_t>(rep.history.size(), (size_t)cfg.max_iterations));
+    if (h_trace && !rep.trace.empty()) std::memcpy(h_trace, rep.trace.data(), sizeof(double) * rep.trace.size());
+    out->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (err) std::rethrow_exception(err);
+}
+
+}  // namespace kg
+
+// ------------------------------------------------------------------ stepwise solver C-ABI
+struct krysp_gpu_solver {
+    kg::PcgSession* s = nullptr;
+};
+
+using kg::guard;
+
+extern "C" {
+
+krysp_status krysp_gpu_solver_create(const krysp_gpu_mat* m, int32_t method, const double* b, const double* x0,
+                                     const krysp_solver_cfg* cfg, krysp_gpu_solver** out) {
+    return guard([&] {
+        if (!m || !cfg || !out || !b || !x0) kg::fail(KRYSP_ERROR, "solver_create: NULL argument");
+        if (method != KRYSP_PCG || cfg->mode != KRYSP_MODE_FAST)
+            kg::fail(KRYSP_ERROR, "stepwise solver supports method KRYSP_PCG in KRYSP_MODE_FAST");
+        if (m->n_rows != m->n_cols) kg::fail(KRYSP_DIMENSION_MISMATCH, "solver expects a square matrix");
+        if (!(cfg->tolerance > 0.0) || cfg->max_iterations < 1)
+            kg::fail(KRYSP_ERROR, "solver config requires tolerance > 0, max_iterations >= 1");
+        KG_CUDA(cudaSetDevice(m->ctx->device));
+        auto* h = new krysp_gpu_solver;
+        try {
+            h->s = new kg::PcgSession(m, *cfg, b, x0, false);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+krysp_status krysp_gpu_solver_iterate(krysp_gpu_solver* h, int64_t n) {
+    return guard([&] {
+        if (!h) kg::fail(KRYSP_ERROR, "NULL solver");
+        h->s->enqueue(n);
+    });
+}
+
+krysp_status krysp_gpu_solver_time(krysp_gpu_solver* h, int64_t n, double* seconds) {
+    return guard([&] {
+        if (!h || !seconds) kg::fail(KRYSP_ERROR, "NULL argument");
+        cudaStream_t st = h->s->e.c->stream;
+        cudaEvent_t a, b;
+        KG_CUDA(cudaEventCreate(&a));
+        KG_CUDA(cudaEventCreate(&b));
+        KG_CUDA(cudaEventRecord(a, st));
+        h->s->enqueue(n);
+        KG_CUDA(cudaEventRecord(b, st));
+        KG_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        KG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *seconds = ms * 1e-3;
+    });
+}
+
+krysp_status krysp_gpu_solver_profile(krysp_gpu_solver* h, int64_t n, double seconds[3]) {
+    return guard([&] {
+        if (!h || !seconds) kg::fail(KRYSP_ERROR, "NULL argument");
+        h->s->profile(n, seconds);
+    });
+}
+
+krysp_status krysp_gpu_solver_run(krysp_gpu_solver* h, double* seconds) {
+    return guard([&] {
+        if (!h) kg::fail(KRYSP_ERROR, "NULL solver");
+        double t = h->s->run_to_convergence();
+        if (seconds) *seconds = t;
+    });
+}
+
+krysp_status krysp_gpu_solver_report(krysp_gpu_solver* h, krysp_report* rep, double* h_hist) {
+    return guard([&] {
+        if (!h || !rep) kg::fail(KRYSP_ERROR, "NULL argument");
+        std::memset(rep, 0, sizeof *rep);
+        kg::Report r;
+        std::exception_ptr err;
+        try {
+            h->s->finish(r, false);
+        } catch (...) {
+            err = std::current_exception();
+        }
+        rep->converged = r.converged;
+        rep->iterations = r.iterations;
+        rep->final_residual_measure = r.final_measure;
+        if (h_hist && !r.history.empty()) std::memcpy(h_hist, r.history.data(), 8 * r.history.size());
+        if (err) std::rethrow_exception(err);
+    });
+}
+
+krysp_status krysp_gpu_solver_solution(krysp_gpu_solver* h, double* x) {
+    return guard([&] {
+        if (!h || !x) kg::fail(KRYSP_ERROR, "NULL argument");
+        auto* s = h->s;
+        if (s->n) KG_CUDA(cudaMemcpyAsync(x, s->x, 8 * s->n, cudaMemcpyDeviceToDevice, s->e.c->stream));
+        KG_CUDA(cudaStreamSynchronize(s->e.c->stream));
+    });
+}
+
+int32_t krysp_gpu_solver_kernels_per_iteration(const krysp_gpu_solver* h) {
+    return h && h->s ? h->s->kernels_per_iteration : 0;
+}
+
+krysp_status krysp_gpu_solver_destroy(krysp_gpu_solver* h) {
+    return guard([&] {
+        if (!h) return;
+        if (h->s) cudaStreamSynchronize(h->s->e.c->stream);
+        delete h->s;
+        delete h;
+    });
+}
+
+}  // extern "C"
