@@ -47,32 +47,87 @@ __global__ void mul_kernel(int64_t n, const double* __restrict__ a, const double
 }
 
 // ---------------------------------------------------------------- FAST dot
+// Compensated (Ogita-Rump-Oishi Dot2) with a fixed grid and a fixed combination tree:
+// deterministic run to run and accurate as if summed in twice the working precision.  The
+// kernel is HBM-bound, so the extra FP64 work is free; it keeps order-sensitive recurrences
+// (BiCGStab under heavy cancellation) from seeing rounding-noise zeros.
+struct D2 {
+    double s, c;
+};
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+__device__ __forceinline__ void d2_add_prod(D2& acc, double a, double b) {
+    const double p = __dmul_rn(a, b);
+    const double ep = __fma_rn(a, b, -p);
+    double s, es;
+    two_sum(acc.s, p, s, es);
+    acc.s = s;
+    acc.c = __dadd_rn(acc.c, __dadd_rn(ep, es));
+}
+__device__ __forceinline__ D2 d2_merge(D2 a, D2 b) {
+    double s, e;
+    two_sum(a.s, b.s, s, e);
+    return {s, __dadd_rn(__dadd_rn(a.c, b.c), e)};
+}
+__device__ __forceinline__ D2 warp_d2(D2 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        D2 w{__shfl_xor_sync(0xffffffffu, v.s, o), __shfl_xor_sync(0xffffffffu, v.c, o)};
+        v = d2_merge(v, w);
+    }
+    return v;
+}
+template <int NT>
+__device__ __forceinline__ D2 block_d2(D2 v, D2* sh) {
+    v = warp_d2(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    D2 t = (threadIdx.x < NT / 32) ? sh[threadIdx.x] : D2{0.0, 0.0};
+    if (w == 0) t = warp_d2(t);
+    if (threadIdx.x == 0) sh[0] = t;
+    __syncthreads();
+    D2 r = sh[0];
+    __syncthreads();
+    return r;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) dot_fast_kernel(int64_t n, const double* __restrict__ x,
                                                       const double* __restrict__ y, double* partials,
                                                       unsigned* counter, double* out) {
-    __shared__ double sh[32];
-    double acc = 0.0;
+    __shared__ D2 sh[32];
+    D2 acc{0.0, 0.0};
     const int64_t n2 = n / 2;
     const double2* x2 = reinterpret_cast<const double2*>(x);
     const double2* y2 = reinterpret_cast<const double2*>(y);
     const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
     if (aligned) {
         GRID_STRIDE(i, n2) {
-            double2 a = x2[i], b = y2[i];
-            acc = fma(a.x, b.x, acc);
-            acc = fma(a.y, b.y, acc);
+            const double2 a = x2[i], b = y2[i];
+            d2_add_prod(acc, a.x, b.x);
+            d2_add_prod(acc, a.y, b.y);
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) acc = fma(x[n - 1], y[n - 1], acc);
+        if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) d2_add_prod(acc, x[n - 1], y[n - 1]);
     } else {
-        GRID_STRIDE(i, n) acc = fma(x[i], y[i], acc);
+        GRID_STRIDE(i, n) d2_add_prod(acc, x[i], y[i]);
     }
-    double b = block_sum<NT>(acc, sh);
-    if (threadIdx.x == 0) partials[blockIdx.x] = b;
+    const D2 b = block_d2<NT>(acc, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = b.s;
+        partials[2 * blockIdx.x + 1] = b.c;
+    }
     if (last_block(counter)) {
-        double t = reduce_partials<NT>(partials, gridDim.x, sh);
+        D2 t{0.0, 0.0};
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += NT)
+            t = d2_merge(t, D2{__ldcg(partials + 2 * i), __ldcg(partials + 2 * i + 1)});
+        t = block_d2<NT>(t, sh);
         if (threadIdx.x == 0) {
-            *out = t;
+            *out = __dadd_rn(t.s, t.c);
             *counter = 0;
         }
     }

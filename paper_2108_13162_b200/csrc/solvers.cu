@@ -735,20 +735,20 @@ struct PcgSession {
         unsigned* cnt_b = c->d_counters + 3;
         const unsigned g_vec = grid_for(n, kFusedNT, (int64_t)c->sm_count * 8);
         const int64_t before = c->launches;
-        if (events) KG_CUDA(cudaEventRecord(ev[0], c->stream));
+        if (events) KG_CUDA(cudaEventRecordWithFlags(ev[0], c->stream, cudaEventRecordExternal));
         EpiCgSigma epi{ap, p, part_a, cnt_a, st, 0.0};
         spmv_fused(e, p, ap, epi);
-        if (events) KG_CUDA(cudaEventRecord(ev[1], c->stream));
+        if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
         if (e.jacobi)
             cg_update_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, x, r, p, ap, e.inv, st, part_b, cnt_b, hist, d_trace);
         else
             cg_update_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, x, r, p, ap, nullptr, st, part_b, cnt_b, hist, d_trace);
         KG_LAUNCH(c);
-        if (events) KG_CUDA(cudaEventRecord(ev[2], c->stream));
+        if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
         if (e.jacobi) cg_direction_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, e.inv, st);
         else cg_direction_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, nullptr, st);
         KG_LAUNCH(c);
-        if (events) KG_CUDA(cudaEventRecord(ev[3], c->stream));
+        if (events) KG_CUDA(cudaEventRecordWithFlags(ev[3], c->stream, cudaEventRecordExternal));
         kernels_per_iteration = (int)(c->launches - before);
     }
 
