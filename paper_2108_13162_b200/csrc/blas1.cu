@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(32 * kExactWarps)
         __syncwarp();
     }
     if (c0 + lane < n_chunks) partials[c0 + lane] = acc;
+    __threadfence();  // every lane wrote a partial (last_block fences thread 0 only)
     if (last_block(counter)) {
         if (w == 0) {
             // strict left-to-right fold (kernels.cpp:80-83)

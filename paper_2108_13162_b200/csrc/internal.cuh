@@ -187,11 +187,13 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 
 // Arrival on a grid-wide counter; returns true in every thread of the block that arrives
 // last.  Partials written before the call are visible to that block.
+// Only thread 0 may have written the block's partials (the callers' convention), so only
+// it needs the release fence before arriving.
 __device__ __forceinline__ bool last_block(unsigned* counter) {
     __shared__ bool s_last;
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         unsigned t = atomicAdd(counter, 1u);
         s_last = (t == gridDim.x - 1);
     }

@@ -634,8 +634,8 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
 template <class Epi>
 __global__ void __launch_bounds__(1024) vec_epi_kernel(int64_t n, const double* __restrict__ y, Epi epi) {
     if (!epi.active()) return;
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r < n) epi.row(r, y[r]);
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        epi.row(r, y[r]);
     epi.finish();
 }
 
@@ -650,7 +650,7 @@ void spmv_fused(Engine& e, const double* x, double* y, Epi epi) {
         launch_ell(m, x, epi, e.pol.block_size, s);
     } else {
         spmv_launch(m, x, y, e.pol, e.mode, s);
-        vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, INT32_MAX), 1024, 0, s>>>(m->n_rows, y, epi);
+        vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y, epi);
         KG_LAUNCH(e.c);
     }
 }

@@ -9,11 +9,18 @@
 // Products and sums are __dmul_rn / __dadd_rn (never contracted to FMA), so y is
 // bit-identical to the reference for the same workers_per_row.
 //
+// Grids are bounded (a few resident CTAs per SM) and every kernel loops over "virtual
+// blocks" — the paper's blocks of block_size threads (exec.cpp:38-46) — so a fused
+// reduction epilogue arrives on its grid-wide counter once per CTA, not once per 256 rows
+// (same-address atomics serialise in the L2 slice).
+//
 // The epilogue (Epi) receives each finished row value: a plain store, or a store fused with
 // a preconditioner scale and dot-product partials (solvers.cu).  Epi::finish() is called
 // by every thread of every block exactly once (block reductions live there); Epi::active()
 // is read once at entry and lets a converged solver's queued iterations exit immediately.
 #pragma once
+#include <unordered_map>
+
 #include "internal.cuh"
 
 namespace kg {
@@ -30,71 +37,85 @@ struct EpiStore {
 };
 
 // ------------------------------------------------------------------ CSR vector (paper)
-// One segment of TW lanes per row; block = policy.block_size threads; grid =
-// grid_spmv_blocks (exec.cpp:38-41).  Every lane participates in the shuffles.
+// One segment of TW lanes per row; virtual blocks of blockDim.x threads cover
+// blockDim.x / TW rows each.  Every lane participates in the shuffles.
 template <int TW, class Epi>
-__global__ void csr_vector_kernel(CsrView A, const double* __restrict__ x, Epi epi) {
+__global__ void csr_vector_kernel(CsrView A, const double* __restrict__ x, Epi epi, int64_t n_vblocks) {
     if (!epi.active()) return;
-    const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t row = gid / TW;
     const int lane = threadIdx.x & (TW - 1);
-    double sum = 0.0;
-    if (row < A.n_rows) {
-        const int32_t b = A.row_ptr[row], e = A.row_ptr[row + 1];
+    for (int64_t vb = blockIdx.x; vb < n_vblocks; vb += gridDim.x) {
+        const int64_t row = (vb * blockDim.x + threadIdx.x) / TW;
+        double sum = 0.0;
+        if (row < A.n_rows) {
+            const int32_t b = A.row_ptr[row], e = A.row_ptr[row + 1];
 #pragma unroll 4
-        for (int32_t k = b + lane; k < e; k += TW) sum = madd(sum, __ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)));
-    }
+            for (int32_t k = b + lane; k < e; k += TW) sum = madd(sum, __ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)));
+        }
 #pragma unroll
-    for (int off = TW / 2; off >= 1; off >>= 1) sum = __dadd_rn(sum, __shfl_down_sync(0xffffffffu, sum, off, TW));
-    if (row < A.n_rows && lane == 0) epi.row(row, sum);
+        for (int off = TW / 2; off >= 1; off >>= 1) sum = __dadd_rn(sum, __shfl_down_sync(0xffffffffu, sum, off, TW));
+        if (row < A.n_rows && lane == 0) epi.row(row, sum);
+    }
     epi.finish();
 }
 
 // ------------------------------------------------------------------ CSR tile (tw == 1 order)
-// A block owns 256 consecutive rows.  Their contiguous nnz range is staged in shared memory
-// with coalesced 16-byte streaming loads (the matrix is read once: evict-first keeps x in
-// L2), then each thread sums its own row sequentially — the tw == 1 reference order.
-// Tiles larger than `cap` entries fall back to direct global loads for that block.
+// A tile is 256 consecutive rows.  Their contiguous nnz range is staged in shared memory with
+// coalesced 16-byte streaming loads (the matrix is read once: evict-first keeps x in L2),
+// then each thread sums its own row sequentially — the tw == 1 reference order.  Tiles
+// larger than `cap` entries fall back to direct global loads for that tile.
 constexpr int kTileRows = 256;
 
 template <class Epi>
-__global__ void __launch_bounds__(kTileRows) csr_tile_kernel(CsrView A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kTileRows, 4) csr_tile_kernel(CsrView A, const double* __restrict__ x,
                                                              Epi epi, int cap) {
     if (!epi.active()) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* s_val = reinterpret_cast<double*>(smem_raw);
     int32_t* s_col = reinterpret_cast<int32_t*>(s_val + cap + 8);
-    const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
-    const int64_t r = r0 + threadIdx.x;
-    const int64_t r1 = (r0 + kTileRows < A.n_rows) ? r0 + kTileRows : (int64_t)A.n_rows;
-    const int32_t k0 = __ldg(A.row_ptr + r0), k1 = __ldg(A.row_ptr + r1);
-    const int32_t k0a = k0 & ~3;
-    int32_t rb = 0, re = 0;
-    if (r < A.n_rows) {
-        rb = __ldg(A.row_ptr + r);
-        re = __ldg(A.row_ptr + r + 1);
-    }
-    double sum = 0.0;
-    if (k1 - k0a <= cap) {
-        const int groups = (k1 - k0a + 3) >> 2;
-        for (int g = threadIdx.x; g < groups; g += kTileRows) {
-            const int64_t e = (int64_t)k0a + 4 * g;
-            const double2 v0 = __ldcs(reinterpret_cast<const double2*>(A.val + e));
-            const double2 v1 = __ldcs(reinterpret_cast<const double2*>(A.val + e + 2));
-            const int4 c = __ldcs(reinterpret_cast<const int4*>(A.col + e));
-            reinterpret_cast<double2*>(s_val)[2 * g] = v0;
-            reinterpret_cast<double2*>(s_val)[2 * g + 1] = v1;
-            reinterpret_cast<int4*>(s_col)[g] = c;
+    const int64_t n_tiles = ((int64_t)A.n_rows + kTileRows - 1) / kTileRows;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int64_t r0 = tile * kTileRows;
+        const int64_t r = r0 + threadIdx.x;
+        const int64_t r1 = (r0 + kTileRows < A.n_rows) ? r0 + kTileRows : (int64_t)A.n_rows;
+        const int32_t k0 = __ldg(A.row_ptr + r0), k1 = __ldg(A.row_ptr + r1);
+        const int32_t k0a = k0 & ~3;
+        int32_t rb = 0, re = 0;
+        if (r < A.n_rows) {
+            rb = __ldg(A.row_ptr + r);
+            re = __ldg(A.row_ptr + r + 1);
         }
-        __syncthreads();
-        const int a = rb - k0a, b = re - k0a;
+        double sum = 0.0;
+        if (k1 - k0a <= cap) {
+            // coalesced, bank-conflict-free staging: consecutive threads move consecutive 16 B
+            const int groups = (k1 - k0a + 3) >> 2;
+            const double2* gv = reinterpret_cast<const double2*>(A.val + k0a);
+            const int4* gc = reinterpret_cast<const int4*>(A.col + k0a);
+            double2* sv = reinterpret_cast<double2*>(s_val);
+            int4* sc = reinterpret_cast<int4*>(s_col);
+            for (int q = threadIdx.x; q < 2 * groups; q += kTileRows) sv[q] = __ldcs(gv + q);
+            for (int g = threadIdx.x; g < groups; g += kTileRows) sc[g] = __ldcs(gc + g);
+            __syncthreads();
+            const int a = rb - k0a, len = re - rb;
+            if (len <= 8) {
+                // short rows (stencils): all gathers in flight at once, then the ordered sum
+                double xv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < len) xv[j] = __ldg(x + s_col[a + j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < len) sum = madd(sum, s_val[a + j], xv[j]);
+            } else {
 #pragma unroll 8
-        for (int k = a; k < b; ++k) sum = madd(sum, s_val[k], __ldg(x + s_col[k]));
-    } else {
+                for (int k = a; k < a + len; ++k) sum = madd(sum, s_val[k], __ldg(x + s_col[k]));
+            }
+            __syncthreads();  // the next tile overwrites the staging buffers
+        } else {
 #pragma unroll 4
-        for (int32_t k = rb; k < re; ++k) sum = madd(sum, __ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)));
+            for (int32_t k = rb; k < re; ++k) sum = madd(sum, __ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)));
+        }
+        if (r < A.n_rows) epi.row(r, sum);
     }
-    if (r < A.n_rows) epi.row(r, sum);
     epi.finish();
 }
 
@@ -105,34 +126,36 @@ inline int tile_smem_bytes(int cap) { return (cap + 8) * 8 + (cap + 8) * 4; }
 template <class Epi>
 __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
     if (!epi.active()) return;
-    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    double sum = 0.0;
-    if (r < E.n_rows) {
-        const int64_t n = E.n_rows;
-        const int32_t* jc = E.jcoef + r;
-        const double* cf = E.coef + r;
-        int s = 0;
-        for (; s + 4 <= E.width; s += 4) {
-            int32_t c[4];
-            double v[4];
+    const int64_t n = E.n_rows;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r - threadIdx.x < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        double sum = 0.0;
+        if (r < n) {
+            const int32_t* jc = E.jcoef + r;
+            const double* cf = E.coef + r;
+            int s = 0;
+            for (; s + 4 <= E.width; s += 4) {
+                int32_t c[4];
+                double v[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                c[j] = __ldcs(jc + (int64_t)(s + j) * n);
-                v[j] = __ldcs(cf + (int64_t)(s + j) * n);
+                for (int j = 0; j < 4; ++j) {
+                    c[j] = __ldcs(jc + (int64_t)(s + j) * n);
+                    v[j] = __ldcs(cf + (int64_t)(s + j) * n);
+                }
+                double xv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
             }
-            double xv[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
-        }
-        for (; s < E.width; ++s) {
-            const int32_t c = __ldcs(jc + (int64_t)s * n);
-            if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * n), __ldg(x + c));
+            for (; s < E.width; ++s) {
+                const int32_t c = __ldcs(jc + (int64_t)s * n);
+                if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * n), __ldg(x + c));
+            }
+            epi.row(r, sum);
         }
     }
-    if (r < E.n_rows) epi.row(r, sum);
     epi.finish();
 }
 
@@ -144,44 +167,70 @@ __global__ void coo_accumulate_kernel(CooView O, const double* __restrict__ x, d
 // Largest shared-memory tile the CSR tile kernel will stage (entries).
 constexpr int kTileCapMax = 8192;
 
+// Resident CTAs per SM for (kernel, block, smem), cached.
+template <typename K>
+inline int resident_blocks(K kernel, int threads, int smem) {
+    static std::unordered_map<uint64_t, int> cache;
+    const uint64_t key = ((uint64_t)threads << 32) | (uint32_t)smem;
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem));
+    if (nb < 1) nb = 1;
+    cache[key] = nb;
+    return nb;
+}
+
+inline int64_t bounded_grid(krysp_gpu_ctx* c, int per_sm, int64_t work_blocks) {
+    const int64_t cap = (int64_t)c->sm_count * per_sm;
+    return work_blocks < cap ? work_blocks : cap;
+}
+
+template <int TW, class Epi>
+inline void launch_csr_vector_tw(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
+    const int64_t nvb = (TW * m->n_rows + bs - 1) / bs;  // grid_spmv_blocks
+    if (nvb == 0) return;
+    auto k = csr_vector_kernel<TW, Epi>;
+    const int64_t g = bounded_grid(m->ctx, resident_blocks(k, (int)bs, 0), nvb);
+    k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), x, epi, nvb);
+    KG_LAUNCH(m->ctx);
+}
+
 template <class Epi>
 inline void launch_csr_vector(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, int64_t tw, cudaStream_t s) {
-    krysp_gpu_ctx* c = m->ctx;
-    const int64_t blocks = (tw * m->n_rows + bs - 1) / bs;  // grid_spmv_blocks
-    if (blocks == 0) return;
-    const CsrView A = m->csr();
     switch (tw) {
-        case 1: csr_vector_kernel<1, Epi><<<(unsigned)blocks, (unsigned)bs, 0, s>>>(A, x, epi); break;
-        case 2: csr_vector_kernel<2, Epi><<<(unsigned)blocks, (unsigned)bs, 0, s>>>(A, x, epi); break;
-        case 4: csr_vector_kernel<4, Epi><<<(unsigned)blocks, (unsigned)bs, 0, s>>>(A, x, epi); break;
-        case 8: csr_vector_kernel<8, Epi><<<(unsigned)blocks, (unsigned)bs, 0, s>>>(A, x, epi); break;
-        case 16: csr_vector_kernel<16, Epi><<<(unsigned)blocks, (unsigned)bs, 0, s>>>(A, x, epi); break;
-        case 32: csr_vector_kernel<32, Epi><<<(unsigned)blocks, (unsigned)bs, 0, s>>>(A, x, epi); break;
+        case 1: launch_csr_vector_tw<1>(m, x, epi, bs, s); break;
+        case 2: launch_csr_vector_tw<2>(m, x, epi, bs, s); break;
+        case 4: launch_csr_vector_tw<4>(m, x, epi, bs, s); break;
+        case 8: launch_csr_vector_tw<8>(m, x, epi, bs, s); break;
+        case 16: launch_csr_vector_tw<16>(m, x, epi, bs, s); break;
+        case 32: launch_csr_vector_tw<32>(m, x, epi, bs, s); break;
         default: fail(KRYSP_ERROR, "workers_per_row %lld not in {1,2,4,8,16,32}", (long long)tw);
     }
-    KG_LAUNCH(c);
 }
 
 template <class Epi>
 inline void launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s) {
     krysp_gpu_ctx* c = m->ctx;
-    const int64_t blocks = (m->n_rows + kTileRows - 1) / kTileRows;
-    if (blocks == 0) return;
+    const int64_t tiles = (m->n_rows + kTileRows - 1) / kTileRows;
+    if (tiles == 0) return;
     int cap = (int)std::min<int64_t>(std::max<int64_t>(m->max_tile_nnz + 8, 64), kTileCapMax);
     cap = (cap + 3) & ~3;
     const int smem = tile_smem_bytes(cap);
     if (smem > 48 * 1024)
         KG_CUDA(cudaFuncSetAttribute(csr_tile_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    csr_tile_kernel<Epi><<<(unsigned)blocks, kTileRows, smem, s>>>(m->csr(), x, epi, cap);
+    const int64_t g = bounded_grid(c, resident_blocks(csr_tile_kernel<Epi>, kTileRows, smem), tiles);
+    csr_tile_kernel<Epi><<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, cap);
     KG_LAUNCH(c);
 }
 
 template <class Epi>
 inline void launch_ell(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
     krysp_gpu_ctx* c = m->ctx;
-    const int64_t blocks = (m->n_rows + bs - 1) / bs;
-    if (blocks == 0) return;
-    ell_kernel<Epi><<<(unsigned)blocks, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+    const int64_t nvb = (m->n_rows + bs - 1) / bs;
+    if (nvb == 0) return;
+    const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi>, (int)bs, 0), nvb);
+    ell_kernel<Epi><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
     KG_LAUNCH(c);
 }
 
