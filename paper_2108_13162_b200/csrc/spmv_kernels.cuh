@@ -121,6 +121,124 @@ __global__ void __launch_bounds__(kTileRows, 4) csr_tile_kernel(CsrView A, const
 
 inline int tile_smem_bytes(int cap) { return (cap + 8) * 8 + (cap + 8) * 4; }
 
+// ------------------------------------------------------------------ CSR tile, TMA pipeline
+// Same tw == 1 order, but tiles are moved by the Tensor Memory Accelerator: one elected
+// thread issues 1-D bulk copies (cp.async.bulk, L2 evict-first) of the next tile's row
+// pointers, column indices and values into the other shared-memory stage while the block
+// gathers x and sums the current tile — the HBM stream never waits for the compute.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+struct TmaTileLayout {
+    int cap;  // entries per stage (>= max tile nnz + 8, multiple of 4)
+    __host__ __device__ int val_bytes() const { return (cap + 8) * 8; }
+    __host__ __device__ int col_bytes() const { return (cap + 8) * 4; }
+    __host__ __device__ int rp_bytes() const { return (kTileRows + 8) * 4; }
+    __host__ __device__ int stage_bytes() const { return val_bytes() + col_bytes() + rp_bytes(); }
+    __host__ __device__ int total_bytes() const { return 2 * stage_bytes() + 64; }
+};
+
+template <class Epi>
+__global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const double* __restrict__ x, Epi epi,
+                                                            TmaTileLayout L) {
+    if (!epi.active()) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // 2 mbarriers
+    unsigned char* stage_base = smem_raw + 64;
+    const int64_t n_tiles = ((int64_t)A.n_rows + kTileRows - 1) / kTileRows;
+    const uint64_t pol = evict_first_policy();
+
+    auto stage_ptr = [&](int s, int part) -> unsigned char* {
+        unsigned char* b = stage_base + s * L.stage_bytes();
+        return part == 0 ? b : part == 1 ? b + L.val_bytes() : b + L.val_bytes() + L.col_bytes();
+    };
+    // thread 0: bulk-copy tile `t` into stage `s`
+    auto issue = [&](int64_t t, int s) {
+        const int64_t r0 = t * kTileRows;
+        const int64_t r1 = (r0 + kTileRows < A.n_rows) ? r0 + kTileRows : (int64_t)A.n_rows;
+        const int32_t k0 = __ldg(A.row_ptr + r0), k1 = __ldg(A.row_ptr + r1);
+        const int32_t va = k0 & ~1, vb = (k1 + 1) & ~1;
+        const int32_t ca = k0 & ~3, cb = (k1 + 3) & ~3;
+        const uint32_t bv = (uint32_t)(vb - va) * 8u, bc = (uint32_t)(cb - ca) * 4u;
+        const uint32_t brp = (uint32_t)(((r1 - r0 + 1) + 3) & ~3) * 4u;
+        mbar_arrive_expect_tx(&bars[s], bv + bc + brp);
+        bulk_g2s(stage_ptr(s, 2), A.row_ptr + r0, brp, &bars[s], pol);
+        if (bv) bulk_g2s(stage_ptr(s, 0), A.val + va, bv, &bars[s], pol);
+        if (bc) bulk_g2s(stage_ptr(s, 1), A.col + ca, bc, &bars[s], pol);
+    };
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+    uint32_t parity = 0;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        const int s = it & 1;
+        const int64_t next = tile + gridDim.x;
+        if (threadIdx.x == 0 && next < n_tiles) issue(next, s ^ 1);  // stage s^1 freed last iteration
+        mbar_wait(&bars[s], (parity >> s) & 1u);
+        parity ^= 1u << s;
+        const double* s_val = reinterpret_cast<const double*>(stage_ptr(s, 0));
+        const int32_t* s_col = reinterpret_cast<const int32_t*>(stage_ptr(s, 1));
+        const int32_t* s_rp = reinterpret_cast<const int32_t*>(stage_ptr(s, 2));
+        const int64_t r = tile * kTileRows + threadIdx.x;
+        double sum = 0.0;
+        if (r < A.n_rows) {
+            const int32_t k0 = s_rp[0];
+            const int32_t rb = s_rp[threadIdx.x], re = s_rp[threadIdx.x + 1];
+            const int av = rb - (k0 & ~1), ac = rb - (k0 & ~3), len = re - rb;
+            if (len <= 8) {
+                double xv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < len) xv[j] = __ldg(x + s_col[ac + j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < len) sum = madd(sum, s_val[av + j], xv[j]);
+            } else {
+#pragma unroll 8
+                for (int j = 0; j < len; ++j) sum = madd(sum, s_val[av + j], __ldg(x + s_col[ac + j]));
+            }
+            epi.row(r, sum);
+        }
+        __syncthreads();  // stage s is re-filled in the next-but-one iteration
+    }
+    epi.finish();
+}
+
 // ------------------------------------------------------------------ ELL
 // Thread per row, column-major slab => every slot load is a coalesced 32-lane stream.
 template <class Epi>
@@ -170,8 +288,16 @@ constexpr int kTileCapMax = 8192;
 // Resident CTAs per SM for (kernel, block, smem), cached.
 template <typename K>
 inline int resident_blocks(K kernel, int threads, int smem) {
-    static std::unordered_map<uint64_t, int> cache;
-    const uint64_t key = ((uint64_t)threads << 32) | (uint32_t)smem;
+    struct Key {
+        const void* k;
+        int t, s;
+        bool operator==(const Key& o) const { return k == o.k && t == o.t && s == o.s; }
+    };
+    struct H {
+        size_t operator()(const Key& a) const { return std::hash<const void*>()(a.k) ^ ((size_t)a.t << 20) ^ a.s; }
+    };
+    static std::unordered_map<Key, int, H> cache;
+    const Key key{reinterpret_cast<const void*>(kernel), threads, smem};
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     int nb = 0;
@@ -216,11 +342,12 @@ inline void launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cu
     if (tiles == 0) return;
     int cap = (int)std::min<int64_t>(std::max<int64_t>(m->max_tile_nnz + 8, 64), kTileCapMax);
     cap = (cap + 3) & ~3;
-    const int smem = tile_smem_bytes(cap);
+    const TmaTileLayout L{cap};
+    const int smem = L.total_bytes();
     if (smem > 48 * 1024)
-        KG_CUDA(cudaFuncSetAttribute(csr_tile_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t g = bounded_grid(c, resident_blocks(csr_tile_kernel<Epi>, kTileRows, smem), tiles);
-    csr_tile_kernel<Epi><<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, cap);
+        KG_CUDA(cudaFuncSetAttribute(csr_tma_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t g = bounded_grid(c, resident_blocks(csr_tma_kernel<Epi>, kTileRows, smem), tiles);
+    csr_tma_kernel<Epi><<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, L);
     KG_LAUNCH(c);
 }
 
