@@ -10,8 +10,9 @@ A step is one P-CG iteration.  Ours: the device-resident FAST iteration (3 kerne
 graph) timed with CUDA events on the solver stream; `e2e` is a full solve through the
 C-ABI with HOST (pinned) CSR arrays (upload + convert + solve + download inside the timed
 call).  The reference arm runs the reference library (oracle/_ref, built from
-/root/reference) on the box's host cores.  Under torchrun each rank drives one GPU; the
-row-partitioned multi-GPU solver is not in this round, so N>1 runs replicas (weak scaling).
+/root/reference) on the box's host cores.  Under torchrun (N > 1) the same 400^3 problem is
+row-partitioned over the N GPUs (strong scaling): band rows, NCCL x-halo overlapped with
+the interior-row SpMV, NCCL-allreduced scalars, graph-captured iterations.
 """
 from __future__ import annotations
 
@@ -45,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=20)
+    ap.add_argument("--dist", action="store_true", help="use the partitioned (NCCL) path even at N = 1")
     return ap.parse_args()
 
 
@@ -306,11 +308,92 @@ def run_ours(args, dist):
     return line
 
 
+def run_ours_dist(args, dist):
+    """N > 1: one C3 problem row-partitioned over the N GPUs (strong scaling), NCCL halo +
+    allreduce inside the library (krysp_gpu_dist_*)."""
+    import paper_2108_13162_b200 as kg
+    from paper_2108_13162_b200.dist import DistSystem, band_rows
+
+    if args.format != "csr":
+        raise SystemExit("the partitioned path runs CSR")
+    ctx = kg.Context(dist.local)
+    D = DistSystem.nccl(ctx, dist.rank, dist.world)
+    D.generate("lap3d7", args.n)
+    D.setup()
+    info = D.part_info(dist.rank)
+    n_loc = info["n_local"]
+    N = args.n ** 3
+    b = ctx.to_device(np.ones(n_loc))
+    x0 = ctx.to_device(np.zeros(n_loc))
+    D.pcg_create([b], [x0], kg.SolverConfig(mode="fast", tolerance=1e-6, max_iterations=30000))
+    D.pcg_time(args.warmup)
+    clocks = Clocks(dist.local)
+    dist.barrier()
+    ctx.sync()
+    clocks.start()
+    t = D.pcg_time(args.steps)
+    ck = clocks.stop()
+    dist.barrier()
+    t_max = dist.max(t)
+    rep = D.pcg_report()
+    assert rep.iterations == args.warmup + args.steps, f"converged inside the timed region ({rep.iterations})"
+    kpi = D.kernels_per_iteration
+    # finish the solve for the parity check (same problem as the single-GPU golden)
+    D.pcg_run()
+    fin = D.pcg_report()
+    # e2e: a whole partitioned solve from pinned host b / x0 to the host solution
+    import torch
+    hb = torch.ones(n_loc, dtype=torch.float64, pin_memory=True).numpy()
+    hx0 = torch.zeros(n_loc, dtype=torch.float64, pin_memory=True).numpy()
+    dist.barrier()
+    t0 = time.perf_counter()
+    db, dx0 = ctx.to_device(hb), ctx.to_device(hx0)
+    D.pcg_create([db], [dx0], kg.SolverConfig(mode="fast", tolerance=1e-6, max_iterations=30000))
+    D.pcg_run()
+    e2e_rep = D.pcg_report()
+    sol = D.pcg_solution(dist.rank)
+    e2e_s = dist.max(time.perf_counter() - t0)
+    D.close()
+    nnz_total = 7 * N - 6 * args.n ** 2
+    bw_peak, peak_kind = peaks()
+    B_iter_gpu = iter_bytes(N, N, nnz_total) / dist.world
+    t_it = t_max / args.steps
+    line = {"metric": METRIC, "value": args.steps / t_max, "unit": "iterations/s", "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_it, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic 3D 7-point Laplacian, each band generated on its GPU)",
+            "config": {"workload": f"C3: P-CG + Jacobi, 3D 7-point Laplacian {args.n}^3 ({N:,} rows) row-partitioned "
+                                   f"over {dist.world} GPUs, CSR, FP64, b=1, x0=0, tol 1e-6",
+                       "matrix": f"lap3d7 n={args.n}", "format": "csr", "solver": "pcg", "mode": "fast",
+                       "parallelism": f"band-rows{dist.world} (NCCL x-halo overlapped with interior SpMV, "
+                                      "NCCL allreduce of the 2 scalars)",
+                       "l2": "inputs larger than L2", "rows_per_gpu": n_loc},
+            "roofline": {"bound": "hbm", "kernel": "whole P-CG iteration per GPU (B_iter / N)",
+                         "achieved": B_iter_gpu / t_it / 1e9, "peak": bw_peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": B_iter_gpu / t_it / 1e9 / bw_peak, "traffic": None},
+            "gpu_launches": kpi * args.steps, "clocks": ck,
+            "e2e": {"value": e2e_rep.iterations / e2e_s, "unit": "iterations/s",
+                    "h2d_bytes_per_step": int(hb.nbytes + hx0.nbytes), "d2h_bytes_per_step": int(sol.nbytes),
+                    "what": "krysp_gpu_dist_pcg_create/run/solution from pinned host b, x0 to the host solution "
+                            "(per rank; the band matrix stays device-resident, generated on its GPU)",
+                    "seconds_per_step": e2e_s},
+            "parity": {"iterations": fin.iterations, "golden_iterations": GOLDEN_ITERS if args.n == 400 else None,
+                       "final_residual_measure": fin.final_residual_measure,
+                       "golden_final_measure": GOLDEN_MEASURE if args.n == 400 else None,
+                       "iterations_within_1": abs(fin.iterations - GOLDEN_ITERS) <= 1 if args.n == 400 else None}}
+    return line
+
+
 def main():
     args = parse()
     dist = Dist()
     try:
-        line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
+        if args.impl == "reference":
+            line = run_reference(args, dist)
+        elif dist.world > 1 or args.dist:
+            line = run_ours_dist(args, dist)
+        else:
+            line = run_ours(args, dist)
         if dist.rank == 0 and line is not None:
             print(json.dumps(line), flush=True)
     finally:

@@ -264,6 +264,43 @@ krysp_status krysp_gpu_solver_solution(krysp_gpu_solver* s, double* d_x);
 int32_t krysp_gpu_solver_kernels_per_iteration(const krysp_gpu_solver* s);
 krysp_status krysp_gpu_solver_destroy(krysp_gpu_solver* s);
 
+/* ------------------------------------------------------------------ multi-GPU
+ * Band-row partition (band_row_assignment, substructure.cpp:20-31), x-halo over NCCL
+ * (send/recv, overlapped with the interior-row SpMV) and NCCL-allreduced P-CG scalars, the
+ * paper's band-row scheme.  One process per GPU: rank >= 0 with an NCCL
+ * unique id from krysp_gpu_dist_unique_id on rank 0; rank = -1 holds all nparts parts in
+ * this process on one device (in-process emulation used by the tests).  Array arguments
+ * (d_x, d_y, d_b, d_x0) hold one device pointer per part held by this process, in part order. */
+typedef struct krysp_gpu_dist krysp_gpu_dist;
+krysp_status krysp_gpu_band_rows(int64_t n, int32_t nparts, int32_t part, int64_t* lo, int64_t* hi);
+/* host-side halo plan of band `part` (rows' CSR with global columns): sorted ghost columns
+ * and per-owner segments owner_seg[q]..owner_seg[q+1] (nparts + 1 entries); ghosts may be NULL */
+krysp_status krysp_gpu_halo_plan_host(int64_t n_global, int32_t nparts, int32_t part, const int64_t* row_ptr,
+                                      const int64_t* col_idx, int64_t* n_ghost, int64_t* ghosts,
+                                      int64_t* owner_seg);
+krysp_status krysp_gpu_dist_unique_id(uint8_t id[128]);
+krysp_status krysp_gpu_dist_create(krysp_gpu_ctx* ctx, int32_t nparts, int32_t rank, const uint8_t* id,
+                                   krysp_gpu_dist** out);
+/* this process's bands of a synthetic matrix (device generator), or of a host CSR (rows
+ * [lo, hi) with GLOBAL column ids; [lo, hi) must be the band of `part`) */
+krysp_status krysp_gpu_dist_generate(krysp_gpu_dist* d, const char* kind, int64_t n, double pe);
+krysp_status krysp_gpu_dist_set_csr(krysp_gpu_dist* d, int32_t part, int64_t n_global, int64_t lo, int64_t hi,
+                                    const int64_t* row_ptr, const int64_t* col_idx, const double* values);
+/* collective: ghost columns, local renumbering, halo plans, interior row range */
+krysp_status krysp_gpu_dist_setup(krysp_gpu_dist* d);
+/* info: [lo, hi, n_local, n_ghost, nnz, n_recv_neighbours, n_send, interior_lo, interior_hi] */
+krysp_status krysp_gpu_dist_part_info(krysp_gpu_dist* d, int32_t part, int64_t info[9]);
+krysp_status krysp_gpu_dist_spmv(krysp_gpu_dist* d, const double* const* d_x, double* const* d_y);
+krysp_status krysp_gpu_dist_pcg_create(krysp_gpu_dist* d, const double* const* d_b, const double* const* d_x0,
+                                       const krysp_solver_cfg* cfg);
+krysp_status krysp_gpu_dist_pcg_iterate(krysp_gpu_dist* d, int64_t n_iterations);
+krysp_status krysp_gpu_dist_pcg_time(krysp_gpu_dist* d, int64_t n_iterations, double* seconds);
+krysp_status krysp_gpu_dist_pcg_run(krysp_gpu_dist* d, double* seconds);
+krysp_status krysp_gpu_dist_pcg_report(krysp_gpu_dist* d, krysp_report* report, double* h_history);
+krysp_status krysp_gpu_dist_pcg_solution(krysp_gpu_dist* d, int32_t part, double* d_x);
+int32_t krysp_gpu_dist_kernels_per_iteration(const krysp_gpu_dist* d);
+krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d);
+
 /* ------------------------------------------------------------------ autotune.hpp:40-64 */
 /* tune_spmv autotune.cpp:136-177 with CUDA-event timing under the same protocol
  * (:37-87) and tie-break (:118-134).  grid may be NULL (= default_policy_grid, 72).

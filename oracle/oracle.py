@@ -373,3 +373,8 @@ class Ref:
 
     def default_workers(self):
         return int(self.L.kref_default_workers())
+
+    def band_row_assignment(self, n, parts):
+        out = np.zeros(n, np.int64)
+        self._chk(self.L.kref_band_row_assignment(_I(n), _I(parts), _ptr(out)))
+        return out

@@ -28,6 +28,7 @@
 #include "krysp/kernels.hpp"
 #include "krysp/solvers.hpp"
 #include "krysp/stats.hpp"
+#include "krysp/substructure.hpp"
 
 using namespace krysp;
 
@@ -343,5 +344,13 @@ int kref_generate(const char* kind, int64_t n, double pe, kref_mat** out) {
 }
 
 int64_t kref_default_workers() { return default_worker_count(); }
+
+// band_row_assignment (substructure.cpp:20-31): assignment[e] for e in [0, n)
+int kref_band_row_assignment(int64_t n, int64_t parts, int64_t* out) {
+    return guard([&] {
+        auto a = band_row_assignment(n, parts);
+        std::memcpy(out, a.data(), a.size() * sizeof(int64_t));
+    });
+}
 
 }  // extern "C"

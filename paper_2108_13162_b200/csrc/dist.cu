@@ -1,0 +1,1078 @@
+// Row-partitioned multi-GPU P-CG.
+//
+// Partition: band rows, band_row_assignment (reference substructure.cpp:20-31: base = n/P,
+// the last band takes the remainder).  Each part keeps its rows as a local CSR whose columns
+// are renumbered: owned columns -> [0, n_local), ghost columns (owned by other bands) ->
+// n_local + rank of the column in the sorted ghost list.  Entries keep their order inside a
+// row, so every local row sum is bit-identical to the single-domain SpMV.
+//
+// Per SpMV the ghost values of x arrive from their owners (halo exchange: pack kernel +
+// NCCL send/recv over NVLink, on a second stream) while the interior rows — the longest run
+// of rows without ghost columns, a full band minus one i-plane per side for a 3-D stencil —
+// are multiplied; the boundary rows follow once the halo has landed.  The two P-CG scalars
+// are NCCL-allreduced on device; the convergence test runs on device from the reduced values,
+// so every rank stops at the same iteration.  Iterations are CUDA-graph captured.
+//
+// Transport: NCCL (one process per GPU, `rank` >= 0; libnccl.so.2 is loaded at run time), or
+// in-process emulation (`rank` = -1: all parts on one device, halo = device memcpy, allreduce
+// = an ordered sum kernel) used to test the partitioned path on a single GPU.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <numeric>
+
+#include "spmv_kernels.cuh"
+
+namespace kg {
+
+krysp_gpu_mat* generate_rows(krysp_gpu_ctx*, const char*, int64_t, double, int64_t, int64_t);
+int64_t generator_dim(const char*, int64_t);
+krysp_gpu_mat* upload_csr(krysp_gpu_ctx*, int64_t, int64_t, const int64_t*, const int64_t*, const double*);
+
+// ------------------------------------------------------------------ NCCL (run-time loaded)
+struct NcclApi {
+    bool ok = false;
+    std::string err;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+
+    static NcclApi& get() {
+        static NcclApi a;
+        static bool tried = false;
+        if (!tried) {
+            tried = true;
+            a.load();
+        }
+        if (!a.ok) fail(KRYSP_NCCL_ERROR, "NCCL unavailable: %s", a.err.c_str());
+        return a;
+    }
+    void load() {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            err = e ? e : "dlopen failed";
+            return;
+        }
+#define KG_SYM(name)                                                   \
+    name = reinterpret_cast<decltype(name)>(dlsym(h, "nccl" #name));   \
+    if (!name) {                                                       \
+        err = "libnccl.so.2 lacks nccl" #name;                         \
+        return;                                                        \
+    }
+        KG_SYM(GetUniqueId)
+        KG_SYM(CommInitRank)
+        KG_SYM(CommDestroy)
+        KG_SYM(AllReduce)
+        KG_SYM(AllGather)
+        KG_SYM(Send)
+        KG_SYM(Recv)
+        KG_SYM(GroupStart)
+        KG_SYM(GroupEnd)
+        KG_SYM(GetErrorString)
+#undef KG_SYM
+        ok = true;
+    }
+};
+
+#define KG_NCCL(call)                                                                                 \
+    do {                                                                                              \
+        ncclResult_t r_ = (call);                                                                     \
+        if (r_ != ncclSuccess)                                                                        \
+            ::kg::fail(KRYSP_NCCL_ERROR, "%s:%d %s: %s", __FILE__, __LINE__, #call,                 \
+                       ::kg::NcclApi::get().GetErrorString(r_));                                      \
+    } while (0)
+
+// band_row_assignment (substructure.cpp:20-31)
+void band_rows(int64_t n, int64_t parts, int64_t part, int64_t* lo, int64_t* hi) {
+    if (parts < 1 || parts > n) fail(KRYSP_ERROR, "band-row split needs 1 <= parts <= n");
+    if (part < 0 || part >= parts) fail(KRYSP_ERROR, "part %lld outside [0, %lld)", (long long)part, (long long)parts);
+    const int64_t base = n / parts;
+    *lo = part * base;
+    *hi = part == parts - 1 ? n : (part + 1) * base;
+}
+
+int64_t band_owner(int64_t n, int64_t parts, int64_t c) {
+    const int64_t base = n / parts;
+    const int64_t s = base > 0 ? c / base : parts - 1;
+    return s < parts - 1 ? s : parts - 1;
+}
+
+struct DistCgState {
+    double rho, rho_1, sigma_loc, sigma, alpha, beta, norm_r0, tol, rho_loc, rho_new;
+    long long iter, max_it;
+    int done, status;
+};
+enum : int { kDsBreakdownSigma = 1, kDsNonFiniteSigma = 2, kDsNonFiniteAlpha = 3, kDsNonFiniteRho = 4 };
+
+struct DistPart {
+    int id = 0;
+    int64_t n_global = 0, lo = 0, hi = 0, n_local = 0, n_ghost = 0;
+    krysp_gpu_mat* A = nullptr;  // band rows; after setup: local column numbering
+    std::vector<int64_t> ghosts;
+    std::vector<int> recv_from;
+    std::vector<int64_t> roff, rcnt;
+    std::vector<int> send_to;
+    std::vector<int64_t> soff, scnt;
+    int32_t* send_idx = nullptr;
+    double* sendbuf = nullptr;
+    int64_t n_send = 0;
+    int64_t clean_a = 0, clean_b = 0;
+    // P-CG state
+    DVec x, r, p, ap, inv;  // p has n_local + n_ghost entries
+    DistCgState* st = nullptr;
+    double* hist = nullptr;
+    double* part_slot = nullptr;  // 3 x kPartialCap partials (interior, lower, upper boundary)
+    void release() {
+        if (A) {
+            mat_free_arrays(A);
+            delete A;
+            A = nullptr;
+        }
+        dev_free(send_idx);
+        dev_free(sendbuf);
+        dev_free(st);
+        dev_free(hist);
+        dev_free(part_slot);
+        send_idx = nullptr;
+        sendbuf = hist = part_slot = nullptr;
+        st = nullptr;
+    }
+};
+
+namespace {
+
+constexpr int kNT = 256;
+const double kZero = 0.0, kOne = 1.0;
+
+__global__ void count_ghosts(CsrView A, int64_t lo, int64_t hi, unsigned long long* cnt) {
+    unsigned long long local = 0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < A.nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = A.col[k];
+        local += (c < lo || c >= hi);
+    }
+    if (local) atomicAdd(cnt, local);
+}
+
+__global__ void collect_ghosts(CsrView A, int64_t lo, int64_t hi, int32_t* out, unsigned long long* pos) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < A.nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = A.col[k];
+        if (c < lo || c >= hi) out[atomicAdd(pos, 1ull)] = (int32_t)c;
+    }
+}
+
+__global__ void remap_cols(int32_t* col, int64_t nnz, int64_t lo, int64_t hi, int64_t n_local,
+                           const int32_t* __restrict__ ghosts, int64_t n_ghost) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = col[k];
+        if (c >= lo && c < hi) {
+            col[k] = (int32_t)(c - lo);
+        } else {
+            int64_t a = 0, b = n_ghost;  // lower_bound
+            while (a < b) {
+                const int64_t m = (a + b) >> 1;
+                if (ghosts[m] < c) a = m + 1;
+                else b = m;
+            }
+            col[k] = (int32_t)(n_local + a);
+        }
+    }
+}
+
+__global__ void row_touches_ghost(const int32_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t n_local,
+                                  unsigned char* flag) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_local; r += (int64_t)gridDim.x * blockDim.x) {
+        unsigned char f = 0;
+        for (int32_t k = rp[r]; k < rp[r + 1]; ++k) f |= (col[k] >= n_local);
+        flag[r] = f;
+    }
+}
+
+__global__ void pack_kernel(const double* __restrict__ x, const int32_t* __restrict__ idx, double* __restrict__ buf,
+                            int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = x[idx[i]];
+}
+
+__global__ void to_local_idx(const int64_t* __restrict__ g, int32_t* __restrict__ l, int64_t n, int64_t lo) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        l[i] = (int32_t)(g[i] - lo);
+}
+
+// SpMV epilogue writing per-CTA partials of <w, y> (no grid-wide finalize)
+struct EpiDotPartial {
+    double* __restrict__ y;
+    const double* __restrict__ w;
+    double* partials;
+    const DistCgState* st;
+    double acc;
+    __device__ __forceinline__ bool active() const { return *(volatile const int*)&st->done == 0; }
+    __device__ __forceinline__ void row(int64_t r, double v) {
+        y[r] = v;
+        acc = fma(w[r], v, acc);
+    }
+    __device__ __forceinline__ void finish() {
+        __shared__ double sh[32];
+        const double b = block_sum_dyn(acc, sh);
+        if (threadIdx.x == 0) partials[blockIdx.x] = b;
+    }
+};
+
+// sigma_loc = ordered sum of up to 3 partial arrays
+__global__ void sum_partials(DistCgState* st, const double* a, int na, const double* b, int nb, const double* c,
+                             int nc) {
+    if (*(volatile int*)&st->done) return;
+    __shared__ double sh[32];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < na; i += blockDim.x) acc += a[i];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += b[i];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) acc += c[i];
+    const double t = block_sum<kNT>(acc, sh);
+    if (threadIdx.x == 0) st->sigma_loc = t;
+}
+
+__global__ void alpha_kernel(DistCgState* st) {
+    if (st->done) return;
+    const double sigma = st->sigma;
+    if (!isfinite(sigma)) {
+        st->status = kDsNonFiniteSigma;
+        st->done = 1;
+    } else if (fabs(sigma) < 1e-300) {
+        st->status = kDsBreakdownSigma;
+        st->done = 1;
+    } else {
+        st->alpha = st->rho / sigma;
+        if (!isfinite(st->alpha)) {
+            st->status = kDsNonFiniteAlpha;
+            st->done = 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kNT) dist_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                           const double* __restrict__ p, const double* __restrict__ ap,
+                                                           const double* __restrict__ inv, DistCgState* st,
+                                                           double* partials, unsigned* counter) {
+    if (*(volatile int*)&st->done) return;
+    __shared__ double sh[32];
+    const double alpha = st->alpha, malpha = -alpha;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        const double ri = __dadd_rn(__dmul_rn(malpha, ap[i]), r[i]);
+        r[i] = ri;
+        const double zi = inv ? __dmul_rn(ri, inv[i]) : ri;
+        acc = fma(ri, zi, acc);
+    }
+    const double b = block_sum<kNT>(acc, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = b;
+    if (last_block(counter)) {
+        const double t = reduce_partials<kNT>(partials, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            st->rho_loc = t;
+            *counter = 0;
+        }
+    }
+}
+
+// convergence test on the reduced rho (solvers.cpp:174-181)
+__global__ void converge_kernel(DistCgState* st, double* history) {
+    if (st->done) return;
+    const double rho_new = st->rho_new;
+    if (!isfinite(rho_new)) {
+        st->status = kDsNonFiniteRho;
+        st->done = 1;
+        return;
+    }
+    const long long it = st->iter;
+    const double measure = rho_new / st->norm_r0;
+    if (history) history[it] = measure;
+    st->iter = it + 1;
+    st->rho_1 = st->rho;
+    st->beta = rho_new / st->rho;
+    st->rho = rho_new;
+    if (measure <= st->tol || it + 1 >= st->max_it) st->done = 1;
+}
+
+__global__ void __launch_bounds__(kNT) dist_direction_kernel(int64_t n, double* __restrict__ p,
+                                                              const double* __restrict__ r,
+                                                              const double* __restrict__ inv, const DistCgState* st) {
+    if (*(volatile const int*)&st->done) return;
+    const double beta = st->beta;
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+        const double zi = inv ? __dmul_rn(r[i], inv[i]) : r[i];
+        p[i] = __dadd_rn(__dmul_rn(beta, p[i]), zi);
+    }
+}
+
+// in-process "allreduce": ordered sum over parts of the field at byte offset `src`
+__global__ void emu_allreduce(DistCgState** sts, int nparts, int src, int dst) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += *reinterpret_cast<const double*>(reinterpret_cast<const char*>(sts[p]) + src);
+    for (int p = 0; p < nparts; ++p) *reinterpret_cast<double*>(reinterpret_cast<char*>(sts[p]) + dst) = s;
+}
+
+}  // namespace
+}  // namespace kg
+
+// ------------------------------------------------------------------ the distributed object
+struct krysp_gpu_dist {
+    krysp_gpu_ctx* ctx = nullptr;
+    int nparts = 1;
+    int rank = -1;  // -1: in-process emulation of all parts
+    ncclComm_t comm = nullptr;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
+    std::vector<kg::DistPart> parts;
+    bool ready = false;
+    // P-CG
+    bool pcg = false;
+    krysp_solver_cfg cfg{};
+    kg::DistCgState** d_sts = nullptr;
+    cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr;
+    int kernels_per_iteration = 0;
+    double measure0 = 0.0;
+    bool done_at_setup = false;
+    static constexpr int kChunk = 16;
+
+    bool emulated() const { return rank < 0; }
+    kg::DistPart& part(int p) {
+        for (auto& q : parts)
+            if (q.id == p) return q;
+        kg::fail(KRYSP_ERROR, "part %d is not held by this process", p);
+    }
+};
+
+namespace kg {
+namespace {
+
+void set_matrix(krysp_gpu_dist* d, DistPart& P, krysp_gpu_mat* band, int64_t n_global, int64_t lo, int64_t hi) {
+    if (P.A) {
+        mat_free_arrays(P.A);
+        delete P.A;
+    }
+    P.A = band;
+    P.n_global = n_global;
+    P.lo = lo;
+    P.hi = hi;
+    P.n_local = hi - lo;
+    d->ready = false;
+}
+
+// ghosts, local renumbering, interior range
+void localize(krysp_gpu_dist* d, DistPart& P) {
+    krysp_gpu_ctx* c = d->ctx;
+    krysp_gpu_mat* A = P.A;
+    if (!A) fail(KRYSP_ERROR, "part %d has no matrix", P.id);
+    unsigned long long* cnt = dev_alloc<unsigned long long>(2, true, c->stream);
+    const unsigned g = grid_for(A->nnz, kNT, (int64_t)c->sm_count * 16);
+    if (A->nnz) {
+        count_ghosts<<<g, kNT, 0, c->stream>>>(A->csr(), P.lo, P.hi, cnt);
+        KG_LAUNCH(c);
+    }
+    unsigned long long h_cnt = 0;
+    KG_CUDA(cudaMemcpyAsync(&h_cnt, cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    P.ghosts.clear();
+    int32_t* d_ghost = nullptr;
+    if (h_cnt) {
+        int32_t* raw = dev_alloc<int32_t>((int64_t)h_cnt, false);
+        int32_t* sorted = dev_alloc<int32_t>((int64_t)h_cnt, false);
+        d_ghost = dev_alloc<int32_t>((int64_t)h_cnt, false);
+        int* n_unique = dev_alloc<int>(1, true, c->stream);
+        collect_ghosts<<<g, kNT, 0, c->stream>>>(A->csr(), P.lo, P.hi, raw, cnt + 1);
+        KG_LAUNCH(c);
+        size_t t1 = 0, t2 = 0;
+        KG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t1, raw, sorted, (int)h_cnt, 0, 32, c->stream));
+        KG_CUDA(cub::DeviceSelect::Unique(nullptr, t2, sorted, d_ghost, n_unique, (int)h_cnt, c->stream));
+        void* tmp = dev_alloc<char>((int64_t)std::max(t1, t2), false);
+        KG_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t1, raw, sorted, (int)h_cnt, 0, 32, c->stream));
+        KG_CUDA(cub::DeviceSelect::Unique(tmp, t2, sorted, d_ghost, n_unique, (int)h_cnt, c->stream));
+        KG_LAUNCH(c);
+        int nu = 0;
+        KG_CUDA(cudaMemcpyAsync(&nu, n_unique, 4, cudaMemcpyDeviceToHost, c->stream));
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+        std::vector<int32_t> hg((size_t)nu);
+        KG_CUDA(cudaMemcpy(hg.data(), d_ghost, 4 * (size_t)nu, cudaMemcpyDeviceToHost));
+        P.ghosts.assign(hg.begin(), hg.end());
+        for (void* q : {(void*)raw, (void*)sorted, tmp, (void*)n_unique}) dev_free(q);
+    }
+    dev_free(cnt);
+    P.n_ghost = (int64_t)P.ghosts.size();
+    if (P.n_local + P.n_ghost >= INT32_MAX) fail(KRYSP_ERROR, "local column space exceeds int32");
+    if (A->nnz) {
+        remap_cols<<<g, kNT, 0, c->stream>>>(A->ci, A->nnz, P.lo, P.hi, P.n_local, d_ghost, P.n_ghost);
+        KG_LAUNCH(c);
+    }
+    A->n_cols = P.n_local + P.n_ghost;
+    // receive segments: ghosts are sorted by global id, hence grouped by owner ascending
+    P.recv_from.clear();
+    P.roff.clear();
+    P.rcnt.clear();
+    for (int64_t i = 0; i < P.n_ghost; ++i) {
+        const int owner = (int)band_owner(P.n_global, d->nparts, P.ghosts[(size_t)i]);
+        if (P.recv_from.empty() || P.recv_from.back() != owner) {
+            P.recv_from.push_back(owner);
+            P.roff.push_back(i);
+            P.rcnt.push_back(0);
+        }
+        P.rcnt.back()++;
+    }
+    // interior rows: longest run of rows without ghost columns, aligned to 256-row tiles
+    P.clean_a = 0;
+    P.clean_b = P.n_local;
+    if (P.n_ghost) {
+        unsigned char* fl = dev_alloc<unsigned char>(P.n_local + 1, true, c->stream);
+        if (P.n_local) {
+            row_touches_ghost<<<grid_for(P.n_local, kNT, (int64_t)c->sm_count * 16), kNT, 0, c->stream>>>(
+                A->rp, A->ci, P.n_local, fl);
+            KG_LAUNCH(c);
+        }
+        std::vector<unsigned char> h((size_t)P.n_local);
+        KG_CUDA(cudaMemcpyAsync(h.data(), fl, (size_t)P.n_local, cudaMemcpyDeviceToHost, c->stream));
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+        dev_free(fl);
+        int64_t best_a = 0, best_len = 0, run_a = 0;
+        for (int64_t r = 0; r <= P.n_local; ++r) {
+            if (r == P.n_local || h[(size_t)r]) {
+                if (r - run_a > best_len) {
+                    best_len = r - run_a;
+                    best_a = run_a;
+                }
+                run_a = r + 1;
+            }
+        }
+        int64_t a = (best_a + kTileRows - 1) / kTileRows * kTileRows;
+        int64_t b = (best_a + best_len) / kTileRows * kTileRows;
+        if (b <= a) a = b = 0;
+        P.clean_a = a;
+        P.clean_b = b;
+    }
+    dev_free(d_ghost);
+}
+
+// exchange need lists -> send lists
+void build_send_plans(krysp_gpu_dist* d) {
+    krysp_gpu_ctx* c = d->ctx;
+    const int P = d->nparts;
+    if (d->emulated()) {
+        for (auto& Q : d->parts) {  // Q = owner, sends to parts that need its rows
+            Q.send_to.clear();
+            Q.soff.clear();
+            Q.scnt.clear();
+            std::vector<int32_t> idx;
+            for (auto& R : d->parts) {
+                for (size_t k = 0; k < R.recv_from.size(); ++k) {
+                    if (R.recv_from[k] != Q.id) continue;
+                    Q.send_to.push_back(R.id);
+                    Q.soff.push_back((int64_t)idx.size());
+                    Q.scnt.push_back(R.rcnt[k]);
+                    for (int64_t i = 0; i < R.rcnt[k]; ++i)
+                        idx.push_back((int32_t)(R.ghosts[(size_t)(R.roff[k] + i)] - Q.lo));
+                }
+            }
+            dev_free(Q.send_idx);
+            dev_free(Q.sendbuf);
+            Q.n_send = (int64_t)idx.size();
+            Q.send_idx = dev_alloc<int32_t>(Q.n_send + 1, false);
+            Q.sendbuf = dev_alloc<double>(Q.n_send + 1, false);
+            if (Q.n_send) KG_CUDA(cudaMemcpy(Q.send_idx, idx.data(), 4 * idx.size(), cudaMemcpyHostToDevice));
+        }
+        return;
+    }
+    // NCCL: all-gather the P x P need-count matrix, then exchange the global-id lists
+    NcclApi& N = NcclApi::get();
+    DistPart& Me = d->parts[0];
+    std::vector<int64_t> row((size_t)P, 0);
+    for (size_t k = 0; k < Me.recv_from.size(); ++k) row[(size_t)Me.recv_from[k]] = Me.rcnt[k];
+    int64_t* d_row = dev_alloc<int64_t>(P, false);
+    int64_t* d_all = dev_alloc<int64_t>((int64_t)P * P, false);
+    KG_CUDA(cudaMemcpy(d_row, row.data(), 8 * (size_t)P, cudaMemcpyHostToDevice));
+    KG_NCCL(N.AllGather(d_row, d_all, (size_t)P, ncclInt64, d->comm, c->stream));
+    std::vector<int64_t> all((size_t)P * P);
+    KG_CUDA(cudaMemcpyAsync(all.data(), d_all, 8 * all.size(), cudaMemcpyDeviceToHost, c->stream));
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    // my ghost ids (int64) on device, grouped by owner
+    int64_t* d_need = dev_alloc<int64_t>(Me.n_ghost + 1, false);
+    if (Me.n_ghost) KG_CUDA(cudaMemcpy(d_need, Me.ghosts.data(), 8 * (size_t)Me.n_ghost, cudaMemcpyHostToDevice));
+    Me.send_to.clear();
+    Me.soff.clear();
+    Me.scnt.clear();
+    int64_t total = 0;
+    for (int q = 0; q < P; ++q) {
+        const int64_t k = all[(size_t)q * P + d->rank];  // q needs k of my rows
+        if (q != d->rank && k > 0) {
+            Me.send_to.push_back(q);
+            Me.soff.push_back(total);
+            Me.scnt.push_back(k);
+            total += k;
+        }
+    }
+    int64_t* d_req = dev_alloc<int64_t>(total + 1, false);
+    KG_NCCL(N.GroupStart());
+    for (size_t k = 0; k < Me.recv_from.size(); ++k)
+        KG_NCCL(N.Send(d_need + Me.roff[k], (size_t)Me.rcnt[k], ncclInt64, Me.recv_from[k], d->comm, c->stream));
+    for (size_t k = 0; k < Me.send_to.size(); ++k)
+        KG_NCCL(N.Recv(d_req + Me.soff[k], (size_t)Me.scnt[k], ncclInt64, Me.send_to[k], d->comm, c->stream));
+    KG_NCCL(N.GroupEnd());
+    dev_free(Me.send_idx);
+    dev_free(Me.sendbuf);
+    Me.n_send = total;
+    Me.send_idx = dev_alloc<int32_t>(total + 1, false);
+    Me.sendbuf = dev_alloc<double>(total + 1, false);
+    if (total) {
+        to_local_idx<<<grid_for(total, kNT, 4096), kNT, 0, c->stream>>>(d_req, Me.send_idx, total, Me.lo);
+        KG_LAUNCH(c);
+    }
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    for (void* q : {(void*)d_row, (void*)d_all, (void*)d_need, (void*)d_req}) dev_free(q);
+}
+
+// x_ext of every held part gets its ghost values.  NCCL mode: on stream s.
+void halo(krysp_gpu_dist* d, const std::vector<double*>& xs, cudaStream_t s) {
+    krysp_gpu_ctx* c = d->ctx;
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+        DistPart& P = d->parts[i];
+        if (P.n_send) {
+            pack_kernel<<<grid_for(P.n_send, kNT, 2048), kNT, 0, s>>>(xs[i], P.send_idx, P.sendbuf, P.n_send);
+            KG_LAUNCH(c);
+        }
+    }
+    if (d->emulated()) {
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            DistPart& R = d->parts[i];
+            for (size_t k = 0; k < R.recv_from.size(); ++k) {
+                DistPart& Q = d->part(R.recv_from[k]);
+                size_t j = std::find(Q.send_to.begin(), Q.send_to.end(), R.id) - Q.send_to.begin();
+                KG_CUDA(cudaMemcpyAsync(xs[i] + R.n_local + R.roff[k], Q.sendbuf + Q.soff[j], 8 * (size_t)R.rcnt[k],
+                                        cudaMemcpyDeviceToDevice, s));
+            }
+        }
+        return;
+    }
+    NcclApi& N = NcclApi::get();
+    DistPart& Me = d->parts[0];
+    if (Me.send_to.empty() && Me.recv_from.empty()) return;
+    KG_NCCL(N.GroupStart());
+    for (size_t k = 0; k < Me.send_to.size(); ++k)
+        KG_NCCL(N.Send(Me.sendbuf + Me.soff[k], (size_t)Me.scnt[k], ncclDouble, Me.send_to[k], d->comm, s));
+    for (size_t k = 0; k < Me.recv_from.size(); ++k)
+        KG_NCCL(N.Recv(xs[0] + Me.n_local + Me.roff[k], (size_t)Me.rcnt[k], ncclDouble, Me.recv_from[k], d->comm, s));
+    KG_NCCL(N.GroupEnd());
+}
+
+// shallow view of rows [a, b) of a local CSR
+krysp_gpu_mat row_view(const krysp_gpu_mat* A, int64_t a, int64_t b) {
+    krysp_gpu_mat v = *A;
+    v.rp = A->rp + a;
+    v.n_rows = b - a;
+    return v;
+}
+
+template <class Epi>
+int64_t launch_rows(const krysp_gpu_mat& v, const double* x, Epi epi, cudaStream_t s) {
+    if (v.n_rows <= 0) return 0;
+    if (csr_use_tile(&v, 1)) return launch_csr_tile(&v, x, epi, s);
+    return launch_csr_vector_tw<1>(&v, x, epi, 256, s);
+}
+
+// host-side allreduce of one double per held part (setup only)
+double allreduce_host(krysp_gpu_dist* d, const std::vector<double*>& d_vals) {
+    krysp_gpu_ctx* c = d->ctx;
+    if (d->emulated()) {
+        double s = 0.0;
+        for (double* p : d_vals) {
+            double v;
+            KG_CUDA(cudaMemcpyAsync(&v, p, 8, cudaMemcpyDeviceToHost, c->stream));
+            KG_CUDA(cudaStreamSynchronize(c->stream));
+            s += v;
+        }
+        return s;
+    }
+    KG_NCCL(NcclApi::get().AllReduce(d_vals[0], d_vals[0], 1, ncclDouble, ncclSum, d->comm, c->stream));
+    double v;
+    KG_CUDA(cudaMemcpyAsync(&v, d_vals[0], 8, cudaMemcpyDeviceToHost, c->stream));
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    return v;
+}
+
+void device_allreduce(krysp_gpu_dist* d, size_t src, size_t dst, cudaStream_t s) {
+    if (d->emulated()) {
+        emu_allreduce<<<1, 32, 0, s>>>(d->d_sts, d->nparts, (int)src, (int)dst);
+        KG_LAUNCH(d->ctx);
+        return;
+    }
+    DistCgState* st = d->parts[0].st;
+    KG_NCCL(NcclApi::get().AllReduce(reinterpret_cast<char*>(st) + src, reinterpret_cast<char*>(st) + dst, 1,
+                                     ncclDouble, ncclSum, d->comm, s));
+}
+
+// one distributed P-CG iteration (all held parts), enqueued on ctx->stream
+void dist_iteration(krysp_gpu_dist* d) {
+    krysp_gpu_ctx* c = d->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t before = c->launches;
+    std::vector<double*> ps;
+    for (auto& P : d->parts) ps.push_back(P.p);
+    const bool overlap = !d->emulated();
+    if (overlap) {
+        KG_CUDA(cudaEventRecord(d->ev_fork, s));
+        KG_CUDA(cudaStreamWaitEvent(d->cstream, d->ev_fork, 0));
+        halo(d, ps, d->cstream);
+        KG_CUDA(cudaEventRecord(d->ev_halo, d->cstream));
+    } else {
+        halo(d, ps, s);
+    }
+    std::vector<int64_t> ga(d->parts.size()), gb(d->parts.size()), gc(d->parts.size());
+    for (size_t i = 0; i < d->parts.size(); ++i) {  // interior rows (no ghosts): overlap the halo
+        DistPart& P = d->parts[i];
+        krysp_gpu_mat v = row_view(P.A, P.clean_a, P.clean_b);
+        EpiDotPartial e{P.ap + P.clean_a, P.p + P.clean_a, P.part_slot, P.st, 0.0};
+        ga[i] = launch_rows(v, P.p, e, s);
+    }
+    if (overlap) KG_CUDA(cudaStreamWaitEvent(s, d->ev_halo, 0));
+    for (size_t i = 0; i < d->parts.size(); ++i) {  // boundary rows
+        DistPart& P = d->parts[i];
+        krysp_gpu_mat lo_v = row_view(P.A, 0, P.clean_a), hi_v = row_view(P.A, P.clean_b, P.n_local);
+        EpiDotPartial e1{P.ap, P.p, P.part_slot + kPartialCap, P.st, 0.0};
+        EpiDotPartial e2{P.ap + P.clean_b, P.p + P.clean_b, P.part_slot + 2 * kPartialCap, P.st, 0.0};
+        gb[i] = launch_rows(lo_v, P.p, e1, s);
+        gc[i] = launch_rows(hi_v, P.p, e2, s);
+        sum_partials<<<1, kNT, 0, s>>>(P.st, P.part_slot, (int)ga[i], P.part_slot + kPartialCap, (int)gb[i],
+                                       P.part_slot + 2 * kPartialCap, (int)gc[i]);
+        KG_LAUNCH(c);
+    }
+    device_allreduce(d, offsetof(DistCgState, sigma_loc), offsetof(DistCgState, sigma), s);
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+        DistPart& P = d->parts[i];
+        alpha_kernel<<<1, 1, 0, s>>>(P.st);
+        KG_LAUNCH(c);
+        const unsigned g = grid_for(P.n_local, kNT, (int64_t)c->sm_count * 8);
+        dist_update_kernel<<<g, kNT, 0, s>>>(P.n_local, P.x, P.r, P.p, P.ap, d->cfg.preconditioner ? (const double*)P.inv : nullptr,
+                                              P.st, c->d_partials + (4 + (i % 4)) * kPartialCap, c->d_counters + 4 + (i % 4));
+        KG_LAUNCH(c);
+    }
+    device_allreduce(d, offsetof(DistCgState, rho_loc), offsetof(DistCgState, rho_new), s);
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+        DistPart& P = d->parts[i];
+        converge_kernel<<<1, 1, 0, s>>>(P.st, P.hist);
+        KG_LAUNCH(c);
+        const unsigned g = grid_for(P.n_local, kNT, (int64_t)c->sm_count * 8);
+        dist_direction_kernel<<<g, kNT, 0, s>>>(P.n_local, P.p, P.r, d->cfg.preconditioner ? (const double*)P.inv : nullptr,
+                                                 P.st);
+        KG_LAUNCH(c);
+    }
+    d->kernels_per_iteration = (int)(c->launches - before);
+}
+
+cudaGraphExec_t capture(krysp_gpu_dist* d, int iters) {
+    krysp_gpu_ctx* c = d->ctx;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    KG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        for (int i = 0; i < iters; ++i) dist_iteration(d);
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    KG_CUDA(cudaStreamEndCapture(c->stream, &graph));
+    KG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    return exec;
+}
+
+void pcg_release(krysp_gpu_dist* d) {
+    if (d->exec_chunk) cudaGraphExecDestroy(d->exec_chunk);
+    if (d->exec_one) cudaGraphExecDestroy(d->exec_one);
+    d->exec_chunk = d->exec_one = nullptr;
+    dev_free(d->d_sts);
+    d->d_sts = nullptr;
+    for (auto& P : d->parts) {
+        dev_free(P.st);
+        dev_free(P.hist);
+        dev_free(P.part_slot);
+        P.st = nullptr;
+        P.hist = P.part_slot = nullptr;
+        P.x = DVec();
+        P.r = DVec();
+        P.p = DVec();
+        P.ap = DVec();
+        P.inv = DVec();
+    }
+    d->pcg = false;
+}
+
+// setup of solve_pcg (solvers.cpp:131-146) on the partitioned system
+void pcg_create(krysp_gpu_dist* d, const double* const* bs, const double* const* x0s, const krysp_solver_cfg& cfg) {
+    if (!d->ready) fail(KRYSP_ERROR, "krysp_gpu_dist_setup must run before the solver");
+    if (cfg.mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "the partitioned P-CG runs in KRYSP_MODE_FAST");
+    if (!(cfg.tolerance > 0.0) || cfg.max_iterations < 1) fail(KRYSP_ERROR, "solver config requires tolerance > 0, max_iterations >= 1");
+    pcg_release(d);
+    krysp_gpu_ctx* c = d->ctx;
+    cudaStream_t s = c->stream;
+    d->cfg = cfg;
+    std::vector<double*> xs, rs, dots;
+    double* d_dot = dev_alloc<double>((int64_t)d->parts.size() * 2, true, s);
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+        DistPart& P = d->parts[i];
+        P.x = DVec(P.n_local, s);
+        P.r = DVec(P.n_local, s);
+        P.p = DVec(P.n_local + P.n_ghost, s);
+        P.ap = DVec(P.n_local, s);
+        P.part_slot = dev_alloc<double>(3 * (int64_t)kPartialCap, true, s);
+        P.hist = dev_alloc<double>(cfg.max_iterations, true, s);
+        P.st = dev_alloc<DistCgState>(1, true, s);
+        if (P.n_local) KG_CUDA(cudaMemcpyAsync(P.p, x0s[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, s));
+        if (P.n_local) KG_CUDA(cudaMemcpyAsync(P.x, x0s[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, s));
+        xs.push_back(P.p);
+    }
+    // r = b - A x0 (spmv, scale(-1), daxpy(1, b)) with a halo of x0
+    halo(d, xs, s);
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+        DistPart& P = d->parts[i];
+        krysp_policy pol{256, 1, 0, 0};
+        spmv_launch(P.A, P.p, P.r, pol, KRYSP_MODE_FAST, s);
+        k_scale(c, P.n_local, -1.0, P.r);
+        k_daxpy(c, P.n_local, 1.0, bs[i], P.r);
+        k_dot(c, P.n_local, P.r, P.r, 256, KRYSP_MODE_FAST, d_dot + 2 * i);
+    }
+    dots.clear();
+    for (size_t i = 0; i < d->parts.size(); ++i) dots.push_back(d_dot + 2 * i);
+    double norm_r0 = std::sqrt(allreduce_host(d, dots));
+    if (norm_r0 == 0.0) norm_r0 = 1.0;
+    // Jacobi (zero diagonal anywhere -> Breakdown on every rank)
+    std::vector<double*> zeros;
+    int* zr = dev_alloc<int>((int64_t)d->parts.size(), false);
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+        DistPart& P = d->parts[i];
+        if (cfg.preconditioner) {
+            P.inv = DVec(P.n_local, s);
+            krysp_gpu_mat v = *P.A;
+            v.n_cols = P.n_local;  // diagonal of the owned block
+            k_diagonal(&v, P.inv);
+            int big = INT32_MAX;
+            KG_CUDA(cudaMemcpyAsync(zr + i, &big, 4, cudaMemcpyHostToDevice, s));
+            k_invert_diag(c, P.n_local, P.inv, zr + i);
+        }
+    }
+    std::vector<int> hz(d->parts.size(), INT32_MAX);
+    if (cfg.preconditioner) {
+        KG_CUDA(cudaMemcpyAsync(hz.data(), zr, 4 * hz.size(), cudaMemcpyDeviceToHost, s));
+        KG_CUDA(cudaStreamSynchronize(s));
+    }
+    for (size_t i = 0; i < d->parts.size(); ++i)
+        KG_CUDA(cudaMemcpyAsync(d_dot + 2 * i + 1, hz[i] == INT32_MAX ? &kZero : &kOne, 8, cudaMemcpyHostToDevice, s));
+    std::vector<double*> zflags;
+    for (size_t i = 0; i < d->parts.size(); ++i) zflags.push_back(d_dot + 2 * i + 1);
+    const double n_zero = allreduce_host(d, zflags);
+    dev_free(zr);
+    if (n_zero > 0.0) {
+        dev_free(d_dot);
+        fail(KRYSP_BREAKDOWN, "zero diagonal entry; Jacobi preconditioner undefined");
+    }
+    // z = D^-1 r -> p, rho = <r, z>
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+        DistPart& P = d->parts[i];
+        if (cfg.preconditioner) k_mul(c, P.n_local, P.r, P.inv, P.p);
+        else k_copy(c, P.n_local, P.r, P.p);
+        k_dot(c, P.n_local, P.r, P.p, 256, KRYSP_MODE_FAST, d_dot + 2 * i);
+    }
+    const double rho = allreduce_host(d, dots);
+    dev_free(d_dot);
+    d->measure0 = rho / norm_r0;
+    DistCgState h{};
+    h.rho = rho;
+    h.norm_r0 = norm_r0;
+    h.tol = cfg.tolerance;
+    h.max_it = cfg.max_iterations;
+    d->done_at_setup = d->measure0 <= cfg.tolerance;
+    h.done = d->done_at_setup ? 1 : 0;
+    std::vector<DistCgState*> sts;
+    for (auto& P : d->parts) {
+        KG_CUDA(cudaMemcpyAsync(P.st, &h, sizeof h, cudaMemcpyHostToDevice, s));
+        sts.push_back(P.st);
+    }
+    d->d_sts = reinterpret_cast<DistCgState**>(dev_alloc<char>(8 * (int64_t)sts.size(), false));
+    KG_CUDA(cudaMemcpyAsync(d->d_sts, sts.data(), 8 * sts.size(), cudaMemcpyHostToDevice, s));
+    KG_CUDA(cudaStreamSynchronize(s));
+    d->exec_chunk = capture(d, krysp_gpu_dist::kChunk);
+    d->exec_one = capture(d, 1);
+    d->pcg = true;
+}
+
+void pcg_enqueue(krysp_gpu_dist* d, int64_t n) {
+    if (!d->pcg) fail(KRYSP_ERROR, "no distributed solver (krysp_gpu_dist_pcg_create)");
+    cudaStream_t s = d->ctx->stream;
+    for (int64_t i = 0; i + krysp_gpu_dist::kChunk <= n; i += krysp_gpu_dist::kChunk) KG_CUDA(cudaGraphLaunch(d->exec_chunk, s));
+    for (int64_t i = 0; i < n % krysp_gpu_dist::kChunk; ++i) KG_CUDA(cudaGraphLaunch(d->exec_one, s));
+}
+
+bool pcg_done(krysp_gpu_dist* d) {
+    int v = 0;
+    KG_CUDA(cudaMemcpyAsync(&v, &d->parts[0].st->done, 4, cudaMemcpyDeviceToHost, d->ctx->stream));
+    KG_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    return v != 0;
+}
+
+}  // namespace
+}  // namespace kg
+
+// ------------------------------------------------------------------ C-ABI
+using kg::guard;
+
+extern "C" {
+
+krysp_status krysp_gpu_band_rows(int64_t n, int32_t nparts, int32_t part, int64_t* lo, int64_t* hi) {
+    return guard([&] {
+        if (!lo || !hi) kg::fail(KRYSP_ERROR, "NULL argument");
+        kg::band_rows(n, nparts, part, lo, hi);
+    });
+}
+
+// Host-side halo plan of one band (the same ownership rule as the device setup): the sorted
+// ghost columns of rows [lo, hi) and, per owner part, the [begin, end) segment of that list.
+krysp_status krysp_gpu_halo_plan_host(int64_t n_global, int32_t nparts, int32_t part, const int64_t* row_ptr,
+                                      const int64_t* col_idx, int64_t* n_ghost, int64_t* ghosts,
+                                      int64_t* owner_seg /* nparts + 1 */) {
+    return guard([&] {
+        if (!row_ptr || !n_ghost) kg::fail(KRYSP_ERROR, "NULL argument");
+        int64_t lo, hi;
+        kg::band_rows(n_global, nparts, part, &lo, &hi);
+        std::vector<int64_t> g;
+        for (int64_t k = row_ptr[0]; k < row_ptr[hi - lo]; ++k)
+            if (col_idx[k] < lo || col_idx[k] >= hi) g.push_back(col_idx[k]);
+        std::sort(g.begin(), g.end());
+        g.erase(std::unique(g.begin(), g.end()), g.end());
+        *n_ghost = (int64_t)g.size();
+        if (ghosts) std::copy(g.begin(), g.end(), ghosts);
+        if (owner_seg) {
+            size_t k = 0;
+            for (int32_t q = 0; q < nparts; ++q) {
+                owner_seg[q] = (int64_t)k;
+                while (k < g.size() && kg::band_owner(n_global, nparts, g[k]) == q) ++k;
+            }
+            owner_seg[nparts] = (int64_t)k;
+        }
+    });
+}
+
+krysp_status krysp_gpu_dist_unique_id(uint8_t id[128]) {
+    return guard([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId u;
+        KG_NCCL(kg::NcclApi::get().GetUniqueId(&u));
+        std::memcpy(id, &u, 128);
+    });
+}
+
+krysp_status krysp_gpu_dist_create(krysp_gpu_ctx* ctx, int32_t nparts, int32_t rank, const uint8_t* id,
+                                   krysp_gpu_dist** out) {
+    return guard([&] {
+        if (!ctx || !out) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (nparts < 1) kg::fail(KRYSP_ERROR, "nparts must be >= 1");
+        KG_CUDA(cudaSetDevice(ctx->device));
+        auto* d = new krysp_gpu_dist;
+        d->ctx = ctx;
+        d->nparts = nparts;
+        d->rank = rank;
+        try {
+            if (rank < 0) {
+                for (int p = 0; p < nparts; ++p) {
+                    d->parts.emplace_back();
+                    d->parts.back().id = p;
+                }
+            } else {
+                if (rank >= nparts || !id) kg::fail(KRYSP_ERROR, "rank %d / id invalid", rank);
+                ncclUniqueId u;
+                std::memcpy(&u, id, 128);
+                KG_NCCL(kg::NcclApi::get().CommInitRank(&d->comm, nparts, u, rank));
+                d->parts.emplace_back();
+                d->parts.back().id = rank;
+                KG_CUDA(cudaStreamCreateWithFlags(&d->cstream, cudaStreamNonBlocking));
+                KG_CUDA(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
+                KG_CUDA(cudaEventCreateWithFlags(&d->ev_halo, cudaEventDisableTiming));
+            }
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
+krysp_status krysp_gpu_dist_generate(krysp_gpu_dist* d, const char* kind, int64_t n, double pe) {
+    return guard([&] {
+        if (!d || !kind) kg::fail(KRYSP_ERROR, "NULL argument");
+        const int64_t dim = kg::generator_dim(kind, n);
+        for (auto& P : d->parts) {
+            int64_t lo, hi;
+            kg::band_rows(dim, d->nparts, P.id, &lo, &hi);
+            kg::set_matrix(d, P, kg::generate_rows(d->ctx, kind, n, pe, lo, hi), dim, lo, hi);
+        }
+    });
+}
+
+krysp_status krysp_gpu_dist_set_csr(krysp_gpu_dist* d, int32_t part, int64_t n_global, int64_t lo, int64_t hi,
+                                    const int64_t* rp, const int64_t* ci, const double* cv) {
+    return guard([&] {
+        if (!d || !rp) kg::fail(KRYSP_ERROR, "NULL argument");
+        int64_t elo, ehi;
+        kg::band_rows(n_global, d->nparts, part, &elo, &ehi);
+        if (elo != lo || ehi != hi)
+            kg::fail(KRYSP_DIMENSION_MISMATCH, "part %d owns rows [%lld, %lld) (band_row_assignment)", part,
+                     (long long)elo, (long long)ehi);
+        kg::DistPart& P = d->part(part);
+        kg::set_matrix(d, P, kg::upload_csr(d->ctx, hi - lo, n_global, rp, ci, cv), n_global, lo, hi);
+    });
+}
+
+krysp_status krysp_gpu_dist_setup(krysp_gpu_dist* d) {
+    return guard([&] {
+        if (!d) kg::fail(KRYSP_ERROR, "NULL argument");
+        kg::pcg_release(d);
+        for (auto& P : d->parts) kg::localize(d, P);
+        kg::build_send_plans(d);
+        d->ready = true;
+    });
+}
+
+krysp_status krysp_gpu_dist_part_info(krysp_gpu_dist* d, int32_t part, int64_t info[9]) {
+    return guard([&] {
+        kg::DistPart& P = d->part(part);
+        info[0] = P.lo;
+        info[1] = P.hi;
+        info[2] = P.n_local;
+        info[3] = P.n_ghost;
+        info[4] = P.A ? P.A->nnz : 0;
+        info[5] = (int64_t)P.recv_from.size();
+        info[6] = P.n_send;
+        info[7] = P.clean_a;
+        info[8] = P.clean_b;
+    });
+}
+
+// y = A x for every held part (x, y: local vectors of n_local)
+krysp_status krysp_gpu_dist_spmv(krysp_gpu_dist* d, const double* const* d_x, double* const* d_y) {
+    return guard([&] {
+        if (!d || !d->ready) kg::fail(KRYSP_ERROR, "krysp_gpu_dist_setup must run first");
+        krysp_gpu_ctx* c = d->ctx;
+        std::vector<kg::DVec> ext;
+        std::vector<double*> xs;
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            kg::DistPart& P = d->parts[i];
+            ext.emplace_back(P.n_local + P.n_ghost, c->stream);
+            if (P.n_local) KG_CUDA(cudaMemcpyAsync(ext.back(), d_x[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, c->stream));
+            xs.push_back(ext.back());
+        }
+        kg::halo(d, xs, c->stream);
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            krysp_policy pol{256, 1, 0, 0};
+            kg::spmv_launch(d->parts[i].A, xs[i], d_y[i], pol, KRYSP_MODE_EXACT, c->stream);
+        }
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+krysp_status krysp_gpu_dist_pcg_create(krysp_gpu_dist* d, const double* const* d_b, const double* const* d_x0,
+                                       const krysp_solver_cfg* cfg) {
+    return guard([&] {
+        if (!d || !d_b || !d_x0 || !cfg) kg::fail(KRYSP_ERROR, "NULL argument");
+        kg::pcg_create(d, d_b, d_x0, *cfg);
+    });
+}
+
+krysp_status krysp_gpu_dist_pcg_iterate(krysp_gpu_dist* d, int64_t n) {
+    return guard([&] { kg::pcg_enqueue(d, n); });
+}
+
+krysp_status krysp_gpu_dist_pcg_time(krysp_gpu_dist* d, int64_t n, double* seconds) {
+    return guard([&] {
+        cudaStream_t s = d->ctx->stream;
+        cudaEvent_t a, b;
+        KG_CUDA(cudaEventCreate(&a));
+        KG_CUDA(cudaEventCreate(&b));
+        KG_CUDA(cudaEventRecord(a, s));
+        kg::pcg_enqueue(d, n);
+        KG_CUDA(cudaEventRecord(b, s));
+        KG_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        KG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        if (seconds) *seconds = ms * 1e-3;
+    });
+}
+
+krysp_status krysp_gpu_dist_pcg_run(krysp_gpu_dist* d, double* seconds) {
+    return guard([&] {
+        auto t0 = std::chrono::steady_clock::now();
+        if (!d->done_at_setup)
+            while (!kg::pcg_done(d)) kg::pcg_enqueue(d, krysp_gpu_dist::kChunk);
+        if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+krysp_status krysp_gpu_dist_pcg_report(krysp_gpu_dist* d, krysp_report* rep, double* h_hist) {
+    return guard([&] {
+        if (!d || !rep || !d->pcg) kg::fail(KRYSP_ERROR, "no distributed solver");
+        std::memset(rep, 0, sizeof *rep);
+        kg::DistCgState h{};
+        KG_CUDA(cudaMemcpy(&h, d->parts[0].st, sizeof h, cudaMemcpyDeviceToHost));
+        std::vector<double> hist((size_t)h.iter);
+        if (h.iter) KG_CUDA(cudaMemcpy(hist.data(), d->parts[0].hist, 8 * (size_t)h.iter, cudaMemcpyDeviceToHost));
+        rep->iterations = h.iter;
+        rep->final_residual_measure = h.iter ? hist.back() : d->measure0;
+        rep->converged = rep->final_residual_measure <= d->cfg.tolerance;
+        if (h_hist && h.iter) std::memcpy(h_hist, hist.data(), 8 * (size_t)h.iter);
+        switch (h.status) {
+            case kg::kDsBreakdownSigma: kg::fail(KRYSP_BREAKDOWN, "pcg: <p, Ap> vanished before convergence");
+            case kg::kDsNonFiniteSigma: kg::fail(KRYSP_NON_FINITE, "sigma became non-finite");
+            case kg::kDsNonFiniteAlpha: kg::fail(KRYSP_NON_FINITE, "alpha became non-finite");
+            case kg::kDsNonFiniteRho: kg::fail(KRYSP_NON_FINITE, "rho became non-finite");
+            default: break;
+        }
+    });
+}
+
+krysp_status krysp_gpu_dist_pcg_solution(krysp_gpu_dist* d, int32_t part, double* d_x) {
+    return guard([&] {
+        kg::DistPart& P = d->part(part);
+        if (!P.x.p) kg::fail(KRYSP_ERROR, "no distributed solver");
+        if (P.n_local) KG_CUDA(cudaMemcpyAsync(d_x, P.x, 8 * P.n_local, cudaMemcpyDeviceToDevice, d->ctx->stream));
+        KG_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    });
+}
+
+int32_t krysp_gpu_dist_kernels_per_iteration(const krysp_gpu_dist* d) { return d ? d->kernels_per_iteration : 0; }
+
+krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d) {
+    return guard([&] {
+        if (!d) return;
+        cudaSetDevice(d->ctx->device);
+        cudaStreamSynchronize(d->ctx->stream);
+        kg::pcg_release(d);
+        for (auto& P : d->parts) P.release();
+        if (d->comm) kg::NcclApi::get().CommDestroy(d->comm);
+        if (d->cstream) cudaStreamDestroy(d->cstream);
+        if (d->ev_fork) cudaEventDestroy(d->ev_fork);
+        if (d->ev_halo) cudaEventDestroy(d->ev_halo);
+        delete d;
+    });
+}
+
+}  // extern "C"

@@ -346,17 +346,18 @@ __device__ __forceinline__ int gen_row_dev(int kind, int64_t n, double pe, int64
     return k;
 }
 
-__global__ void gen_count(int kind, int64_t n, double pe, int64_t dim, int64_t* cnt) {
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < dim;
+// rows [row0, row0 + rows) of the global matrix (global column ids)
+__global__ void gen_count(int kind, int64_t n, double pe, int64_t row0, int64_t rows, int64_t* cnt) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
          r += (int64_t)gridDim.x * blockDim.x)
-        cnt[r] = gen_row_dev(kind, n, pe, r, nullptr, nullptr);
+        cnt[r] = gen_row_dev(kind, n, pe, row0 + r, nullptr, nullptr);
 }
 
-__global__ void gen_fill(int kind, int64_t n, double pe, int64_t dim, const int64_t* off,
+__global__ void gen_fill(int kind, int64_t n, double pe, int64_t row0, int64_t rows, const int64_t* off,
                          int32_t* ci, double* cv) {
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < dim;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows;
          r += (int64_t)gridDim.x * blockDim.x)
-        gen_row_dev(kind, n, pe, r, ci + off[r], cv + off[r]);
+        gen_row_dev(kind, n, pe, row0 + r, ci + off[r], cv + off[r]);
 }
 
 int kind_id(const char* kind) {
@@ -498,6 +499,51 @@ krysp_gpu_mat* upload_coo(krysp_gpu_ctx* c, int64_t n_rows, int64_t n_cols, int6
     return m;
 }
 
+int64_t generator_dim(const char* kind, int64_t n) { return kind_dim(kind_id(kind), n); }
+
+// Rows [lo, hi) of a synthetic matrix as device CSR with GLOBAL column ids
+// (hi - lo rows x dim columns); generate() is the whole matrix.
+krysp_gpu_mat* generate_rows(krysp_gpu_ctx* c, const char* kind, int64_t n, double pe, int64_t lo, int64_t hi) {
+    int k = kind_id(kind);
+    if (k == 5) fail(KRYSP_ERROR, "powerlaw is generated on the host (krysp_gpu_gen_csr_host)");
+    if (n < 2) fail(KRYSP_ERROR, "generator needs n >= 2");
+    const int64_t full = kind_dim(k, n);
+    if (lo < 0 || hi > full || lo > hi) fail(KRYSP_ERROR, "row range [%lld, %lld) outside %lld rows", (long long)lo,
+                                             (long long)hi, (long long)full);
+    const int64_t dim = hi - lo;
+    krysp_gpu_mat* m = mat_new(c, KRYSP_FMT_CSR, dim, full);
+    int64_t* cnt = dev_alloc<int64_t>(dim + 1, false, c->stream);
+    int64_t* off = dev_alloc<int64_t>(dim + 2, false, c->stream);
+    if (dim) {
+        gen_count<<<grid_for(dim, kNT, cap_grid(c)), kNT, 0, c->stream>>>(k, n, pe, lo, dim, cnt);
+        KG_LAUNCH(c);
+    }
+    exclusive_scan(c, cnt, off, dim);
+    int64_t nnz = d2h_i64(c, off + dim);
+    if (nnz >= INT32_MAX) {
+        dev_free(cnt);
+        dev_free(off);
+        delete m;
+        fail(KRYSP_ERROR, "nnz %lld exceeds the int32 device index range", (long long)nnz);
+    }
+    m->nnz = nnz;
+    m->rp = dev_alloc<int32_t>(dim + 1 + kPad, true, c->stream);
+    m->ci = dev_alloc<int32_t>(nnz + kPad, true, c->stream);
+    m->cv = dev_alloc<double>(nnz + kPad, true, c->stream);
+    narrow_offsets<<<grid_for(dim + 1, kNT, cap_grid(c)), kNT, 0, c->stream>>>(off, m->rp, dim + 1);
+    KG_LAUNCH(c);
+    if (dim) {
+        gen_fill<<<grid_for(dim, kNT, cap_grid(c)), kNT, 0, c->stream>>>(k, n, pe, lo, dim, off, m->ci, m->cv);
+        KG_LAUNCH(c);
+    }
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    dev_free(cnt);
+    dev_free(off);
+    m->bytes = (dim + 1) * 4 + nnz * 12;
+    mat_row_stats(m);
+    return m;
+}
+
 krysp_gpu_mat* generate(krysp_gpu_ctx* c, const char* kind, int64_t n, double pe) {
     int k = kind_id(kind);
     if (k == 5) fail(KRYSP_ERROR, "powerlaw is generated on the host (krysp_gpu_gen_csr_host)");
@@ -506,7 +552,7 @@ krysp_gpu_mat* generate(krysp_gpu_ctx* c, const char* kind, int64_t n, double pe
     krysp_gpu_mat* m = mat_new(c, KRYSP_FMT_CSR, dim, dim);
     int64_t* cnt = dev_alloc<int64_t>(dim + 1, false, c->stream);
     int64_t* off = dev_alloc<int64_t>(dim + 2, false, c->stream);
-    gen_count<<<grid_for(dim, kNT, cap_grid(c)), kNT, 0, c->stream>>>(k, n, pe, dim, cnt);
+    gen_count<<<grid_for(dim, kNT, cap_grid(c)), kNT, 0, c->stream>>>(k, n, pe, 0, dim, cnt);
     KG_LAUNCH(c);
     exclusive_scan(c, cnt, off, dim);
     int64_t nnz = d2h_i64(c, off + dim);
@@ -522,7 +568,7 @@ krysp_gpu_mat* generate(krysp_gpu_ctx* c, const char* kind, int64_t n, double pe
     m->cv = dev_alloc<double>(nnz + kPad, true, c->stream);
     narrow_offsets<<<grid_for(dim + 1, kNT, cap_grid(c)), kNT, 0, c->stream>>>(off, m->rp, dim + 1);
     KG_LAUNCH(c);
-    gen_fill<<<grid_for(dim, kNT, cap_grid(c)), kNT, 0, c->stream>>>(k, n, pe, dim, off, m->ci, m->cv);
+    gen_fill<<<grid_for(dim, kNT, cap_grid(c)), kNT, 0, c->stream>>>(k, n, pe, 0, dim, off, m->ci, m->cv);
     KG_LAUNCH(c);
     KG_CUDA(cudaStreamSynchronize(c->stream));
     dev_free(cnt);

@@ -203,14 +203,12 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
     double measure = 1.0;
     while (rep.iterations < cfg.max_iterations && !rep.converged) {
         // the basis storage is reused across restarts (dirs.clear() in the reference)
-        int64_t kept = 0;
         auto slot = [&](std::vector<DVec>& v, int64_t j) -> DVec& {
             while ((int64_t)v.size() <= j) v.emplace_back(e.vec());
             return v[(size_t)j];
         };
         e.copy(r, slot(dirs, 0));
         e.op(slot(dirs, 0), slot(op_dirs, 0));
-        kept = 1;
         for (int64_t j = 0; j < m; ++j) {
             const double* p = dirs[(size_t)j];
             const double* ap = op_dirs[(size_t)j];
@@ -240,9 +238,7 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
                 e.daxpy(-beta, dirs[(size_t)i], pn);
                 e.daxpy(-beta, op_dirs[(size_t)i], apn);
             }
-            kept = j + 2;
         }
-        (void)kept;
     }
     rep.final_measure = measure;
 }

@@ -59,65 +59,7 @@ __global__ void csr_vector_kernel(CsrView A, const double* __restrict__ x, Epi e
 }
 
 // ------------------------------------------------------------------ CSR tile (tw == 1 order)
-// A tile is 256 consecutive rows.  Their contiguous nnz range is staged in shared memory with
-// coalesced 16-byte streaming loads (the matrix is read once: evict-first keeps x in L2),
-// then each thread sums its own row sequentially — the tw == 1 reference order.  Tiles
-// larger than `cap` entries fall back to direct global loads for that tile.
 constexpr int kTileRows = 256;
-
-template <class Epi>
-__global__ void __launch_bounds__(kTileRows, 4) csr_tile_kernel(CsrView A, const double* __restrict__ x,
-                                                             Epi epi, int cap) {
-    if (!epi.active()) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* s_val = reinterpret_cast<double*>(smem_raw);
-    int32_t* s_col = reinterpret_cast<int32_t*>(s_val + cap + 8);
-    const int64_t n_tiles = ((int64_t)A.n_rows + kTileRows - 1) / kTileRows;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t r0 = tile * kTileRows;
-        const int64_t r = r0 + threadIdx.x;
-        const int64_t r1 = (r0 + kTileRows < A.n_rows) ? r0 + kTileRows : (int64_t)A.n_rows;
-        const int32_t k0 = __ldg(A.row_ptr + r0), k1 = __ldg(A.row_ptr + r1);
-        const int32_t k0a = k0 & ~3;
-        int32_t rb = 0, re = 0;
-        if (r < A.n_rows) {
-            rb = __ldg(A.row_ptr + r);
-            re = __ldg(A.row_ptr + r + 1);
-        }
-        double sum = 0.0;
-        if (k1 - k0a <= cap) {
-            // coalesced, bank-conflict-free staging: consecutive threads move consecutive 16 B
-            const int groups = (k1 - k0a + 3) >> 2;
-            const double2* gv = reinterpret_cast<const double2*>(A.val + k0a);
-            const int4* gc = reinterpret_cast<const int4*>(A.col + k0a);
-            double2* sv = reinterpret_cast<double2*>(s_val);
-            int4* sc = reinterpret_cast<int4*>(s_col);
-            for (int q = threadIdx.x; q < 2 * groups; q += kTileRows) sv[q] = __ldcs(gv + q);
-            for (int g = threadIdx.x; g < groups; g += kTileRows) sc[g] = __ldcs(gc + g);
-            __syncthreads();
-            const int a = rb - k0a, len = re - rb;
-            if (len <= 8) {
-                // short rows (stencils): all gathers in flight at once, then the ordered sum
-                double xv[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < len) xv[j] = __ldg(x + s_col[a + j]);
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < len) sum = madd(sum, s_val[a + j], xv[j]);
-            } else {
-#pragma unroll 8
-                for (int k = a; k < a + len; ++k) sum = madd(sum, s_val[k], __ldg(x + s_col[k]));
-            }
-            __syncthreads();  // the next tile overwrites the staging buffers
-        } else {
-#pragma unroll 4
-            for (int32_t k = rb; k < re; ++k) sum = madd(sum, __ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)));
-        }
-        if (r < A.n_rows) epi.row(r, sum);
-    }
-    epi.finish();
-}
 
 inline int tile_smem_bytes(int cap) { return (cap + 8) * 8 + (cap + 8) * 4; }
 
@@ -171,9 +113,9 @@ template <class Epi>
 __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const double* __restrict__ x, Epi epi,
                                                             TmaTileLayout L) {
     if (!epi.active()) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // 2 mbarriers
-    unsigned char* stage_base = smem_raw + 64;
+    extern __shared__ __align__(128) unsigned char smem_tma[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma);  // 2 mbarriers
+    unsigned char* stage_base = smem_tma + 64;
     const int64_t n_tiles = ((int64_t)A.n_rows + kTileRows - 1) / kTileRows;
     const uint64_t pol = evict_first_policy();
 
@@ -313,13 +255,14 @@ inline int64_t bounded_grid(krysp_gpu_ctx* c, int per_sm, int64_t work_blocks) {
 }
 
 template <int TW, class Epi>
-inline void launch_csr_vector_tw(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
+inline int64_t launch_csr_vector_tw(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
     const int64_t nvb = (TW * m->n_rows + bs - 1) / bs;  // grid_spmv_blocks
-    if (nvb == 0) return;
+    if (nvb == 0) return 0;
     auto k = csr_vector_kernel<TW, Epi>;
     const int64_t g = bounded_grid(m->ctx, resident_blocks(k, (int)bs, 0), nvb);
     k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), x, epi, nvb);
     KG_LAUNCH(m->ctx);
+    return g;
 }
 
 template <class Epi>
@@ -335,11 +278,12 @@ inline void launch_csr_vector(const krysp_gpu_mat* m, const double* x, Epi epi, 
     }
 }
 
+// returns the grid size (number of per-CTA partials an epilogue writes)
 template <class Epi>
-inline void launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s) {
+inline int64_t launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s) {
     krysp_gpu_ctx* c = m->ctx;
     const int64_t tiles = (m->n_rows + kTileRows - 1) / kTileRows;
-    if (tiles == 0) return;
+    if (tiles == 0) return 0;
     int cap = (int)std::min<int64_t>(std::max<int64_t>(m->max_tile_nnz + 8, 64), kTileCapMax);
     cap = (cap + 3) & ~3;
     const TmaTileLayout L{cap};
@@ -349,6 +293,7 @@ inline void launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cu
     const int64_t g = bounded_grid(c, resident_blocks(csr_tma_kernel<Epi>, kTileRows, smem), tiles);
     csr_tma_kernel<Epi><<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, L);
     KG_LAUNCH(c);
+    return g;
 }
 
 template <class Epi>

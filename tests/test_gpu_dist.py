@@ -1,0 +1,100 @@
+"""GPU: the row-partitioned path (krysp_gpu_dist_*) on one B200.
+
+* in-process emulation with P = 1..8 bands: distributed SpMV bit-identical to the
+  single-domain SpMV; partitioned FAST P-CG within +-1 iteration / 1e-10 of the oracle;
+* NCCL transport with one rank: the real communicator / graph-captured NCCL path.
+"""
+import numpy as np
+import pytest
+
+import paper_2108_13162_b200 as kg
+from paper_2108_13162_b200.dist import DistSystem, band_rows, halo_plan, nccl_unique_id
+
+pytestmark = pytest.mark.gpu
+
+
+def split(x, N, P):
+    return [x[slice(*band_rows(N, P, p))] for p in range(P)]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_dist_spmv_bitexact(ctx, port, P):
+    n = 24
+    g = port.generate("lap3d7", n)
+    N = g.n_rows
+    D = DistSystem.emulated(ctx, P)
+    D.generate("lap3d7", n)
+    D.setup()
+    x = np.random.default_rng(P).uniform(-1, 1, N)
+    ys = D.spmv([ctx.to_device(v) for v in split(x, N, P)])
+    got = np.concatenate([y.to_host() for y in ys])
+    np.testing.assert_array_equal(got, port.spmv(g, x, "csr", 256, 1))
+    for p in range(P):
+        info = D.part_info(p)
+        lo, hi = band_rows(N, P, p)
+        assert (info["lo"], info["hi"]) == (lo, hi)
+        nbrs = (p > 0) + (p < P - 1)
+        assert info["n_ghost"] == nbrs * n * n and info["n_recv_neighbours"] == nbrs
+        if nbrs:
+            assert info["interior_hi"] > info["interior_lo"]  # overlap window exists
+
+
+def test_dist_host_csr_and_plan(ctx, port):
+    P, kind = 3, "fem27"
+    m = port.generate(kind, 9, pe=0.5)
+    N = m.n_rows
+    D = DistSystem.emulated(ctx, P)
+    for p in range(P):
+        lo, hi = band_rows(N, P, p)
+        rp = m.row_ptr[lo:hi + 1] - m.row_ptr[lo]
+        sl = slice(m.row_ptr[lo], m.row_ptr[hi])
+        band = kg.CsrMatrix(hi - lo, N, rp, m.col_idx[sl], m.values[sl])
+        D.set_csr(p, N, band)
+        ghosts, seg = halo_plan(N, P, p, band)
+        assert seg[p + 1] == seg[p]  # never a ghost of itself
+    D.setup()
+    for p in range(P):
+        lo, hi = band_rows(N, P, p)
+        rp = m.row_ptr[lo:hi + 1] - m.row_ptr[lo]
+        sl = slice(m.row_ptr[lo], m.row_ptr[hi])
+        ghosts, _ = halo_plan(N, P, p, kg.CsrMatrix(hi - lo, N, rp, m.col_idx[sl], m.values[sl]))
+        assert D.part_info(p)["n_ghost"] == len(ghosts)
+    x = np.random.default_rng(3).uniform(-1, 1, N)
+    got = np.concatenate([y.to_host() for y in D.spmv([ctx.to_device(v) for v in split(x, N, P)])])
+    np.testing.assert_array_equal(got, port.spmv(m, x, "csr", 256, 1))
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("key", ["lap3d7_30_pcg", "lap3d7_100_pcg", "poisson2d_100_pcg"])
+def test_dist_pcg_parity(ctx, golden, P, key):
+    c = golden["configs"][key]
+    D = DistSystem.emulated(ctx, P)
+    D.generate(c["kind"], c["n"], 0.5)
+    D.setup()
+    N = D.part_info(P - 1)["hi"]
+    bs = [ctx.to_device(np.ones(len(v))) for v in split(np.ones(N), N, P)]
+    x0 = [ctx.to_device(np.zeros(len(v))) for v in split(np.ones(N), N, P)]
+    D.pcg_create(bs, x0, kg.SolverConfig(mode="fast"))
+    D.pcg_run()
+    rep = D.pcg_report()
+    assert rep.converged
+    assert abs(rep.iterations - c["iterations"]) <= 1
+    assert abs(rep.final_residual_measure - c["final_residual_measure"]) <= 1e-10
+    # the partitioned solution matches the single-GPU FAST solve
+    single = kg.solve_pcg(ctx.generate(c["kind"], c["n"], 0.5), np.ones(N), cfg=kg.SolverConfig(mode="fast"))
+    x = np.concatenate([D.pcg_solution(p) for p in range(P)])
+    assert np.max(np.abs(x - single.solution)) <= 1e-6 * np.max(np.abs(single.solution))
+
+
+def test_nccl_single_rank(ctx, golden):
+    c = golden["configs"]["lap3d7_30_pcg"]
+    D = DistSystem(ctx, 1, 0, nccl_unique_id())
+    D.generate("lap3d7", 30)
+    D.setup()
+    N = 30 ** 3
+    D.pcg_create([ctx.to_device(np.ones(N))], [ctx.to_device(np.zeros(N))], kg.SolverConfig(mode="fast"))
+    D.pcg_run()
+    rep = D.pcg_report()
+    assert abs(rep.iterations - c["iterations"]) <= 1
+    assert abs(rep.final_residual_measure - c["final_residual_measure"]) <= 1e-10
+    D.close()
