@@ -536,14 +536,14 @@ def solve_bicgcr(A, b, x0=None, cfg=None) -> SolveReport:
     return solve(A, "bicgcr", b, x0, cfg)
 
 
-class PcgSolver:
-    """Stepwise device-resident FAST P-CG (krysp_gpu_solver_*): setup once, then enqueue /
-    time / profile iterations.  b, x0: DeviceArray or numpy."""
+class DeviceSolver:
+    """Stepwise device-resident FAST P-CG / BiCGStab (krysp_gpu_solver_*): setup once, then
+    enqueue / time / profile iterations.  b, x0: DeviceArray or numpy."""
 
-    def __init__(self, A: DeviceMatrix, b, x0=None, cfg: Optional[SolverConfig] = None):
+    def __init__(self, A: DeviceMatrix, b, x0=None, cfg: Optional[SolverConfig] = None, method: str = "pcg"):
         cfg = cfg or SolverConfig(mode="fast")
         if cfg.mode != "fast":
-            raise _lib.Error("PcgSolver runs the FAST device-resident iteration")
+            raise _lib.Error("DeviceSolver runs the FAST device-resident iteration")
         self.A, self.ctx, self.L = A, A.ctx, A.ctx.L
         self.cfg = cfg
         n = A.n_rows
@@ -551,9 +551,10 @@ class PcgSolver:
         self._x0 = x0 if isinstance(x0, DeviceArray) else A.ctx.to_device(np.zeros(n) if x0 is None else x0)
         h = C.c_void_p()
         cc = cfg.c()
-        check(self.L.krysp_gpu_solver_create(A.h, C.c_int32(METHODS["pcg"]), self._b.ptr, self._x0.ptr, C.byref(cc),
+        check(self.L.krysp_gpu_solver_create(A.h, C.c_int32(METHODS[method]), self._b.ptr, self._x0.ptr, C.byref(cc),
                                              C.byref(h)))
         self.h = h
+        self.method = method
 
     def iterate(self, n: int):
         check(self.L.krysp_gpu_solver_iterate(self.h, n))
@@ -597,6 +598,9 @@ class PcgSolver:
             self.close()
         except Exception:
             pass
+
+
+PcgSolver = DeviceSolver
 
 
 def solve_csr_host(ctx: Context, m: CsrMatrix, method: str, b, x0=None, cfg: Optional[SolverConfig] = None,

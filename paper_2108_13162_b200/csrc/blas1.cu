@@ -51,50 +51,7 @@ __global__ void mul_kernel(int64_t n, const double* __restrict__ a, const double
 // deterministic run to run and accurate as if summed in twice the working precision.  The
 // kernel is HBM-bound, so the extra FP64 work is free; it keeps order-sensitive recurrences
 // (BiCGStab under heavy cancellation) from seeing rounding-noise zeros.
-struct D2 {
-    double s, c;
-};
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-    s = __dadd_rn(a, b);
-    const double bb = __dsub_rn(s, a);
-    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
-}
-__device__ __forceinline__ void d2_add_prod(D2& acc, double a, double b) {
-    const double p = __dmul_rn(a, b);
-    const double ep = __fma_rn(a, b, -p);
-    double s, es;
-    two_sum(acc.s, p, s, es);
-    acc.s = s;
-    acc.c = __dadd_rn(acc.c, __dadd_rn(ep, es));
-}
-__device__ __forceinline__ D2 d2_merge(D2 a, D2 b) {
-    double s, e;
-    two_sum(a.s, b.s, s, e);
-    return {s, __dadd_rn(__dadd_rn(a.c, b.c), e)};
-}
-__device__ __forceinline__ D2 warp_d2(D2 v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        D2 w{__shfl_xor_sync(0xffffffffu, v.s, o), __shfl_xor_sync(0xffffffffu, v.c, o)};
-        v = d2_merge(v, w);
-    }
-    return v;
-}
-template <int NT>
-__device__ __forceinline__ D2 block_d2(D2 v, D2* sh) {
-    v = warp_d2(v);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) sh[w] = v;
-    __syncthreads();
-    D2 t = (threadIdx.x < NT / 32) ? sh[threadIdx.x] : D2{0.0, 0.0};
-    if (w == 0) t = warp_d2(t);
-    if (threadIdx.x == 0) sh[0] = t;
-    __syncthreads();
-    D2 r = sh[0];
-    __syncthreads();
-    return r;
-}
+// (D2 helpers live in internal.cuh.)
 
 template <int NT>
 __global__ void __launch_bounds__(NT) dot_fast_kernel(int64_t n, const double* __restrict__ x,

@@ -224,6 +224,65 @@ __device__ __forceinline__ double reduce_partials_dyn(const double* partials, in
     return block_sum_dyn(acc, sh);
 }
 
+// ---------------------------------------------------------------- compensated (Dot2) sums
+// Ogita-Rump-Oishi TwoSum / TwoProd accumulation: a (sum, compensation) pair per thread,
+// merged with TwoSum in a fixed tree — deterministic and as accurate as twice the precision.
+struct D2 {
+    double s, c;
+};
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+    s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+__device__ __forceinline__ void d2_add_prod(D2& acc, double a, double b) {
+    const double p = __dmul_rn(a, b);
+    const double ep = __fma_rn(a, b, -p);
+    double s, es;
+    two_sum(acc.s, p, s, es);
+    acc.s = s;
+    acc.c = __dadd_rn(acc.c, __dadd_rn(ep, es));
+}
+__device__ __forceinline__ D2 d2_merge(D2 a, D2 b) {
+    double s, e;
+    two_sum(a.s, b.s, s, e);
+    return {s, __dadd_rn(__dadd_rn(a.c, b.c), e)};
+}
+__device__ __forceinline__ D2 warp_d2(D2 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        D2 w{__shfl_xor_sync(0xffffffffu, v.s, o), __shfl_xor_sync(0xffffffffu, v.c, o)};
+        v = d2_merge(v, w);
+    }
+    return v;
+}
+// block reduction of D2 for a runtime block size (multiple of 32); valid in every thread
+__device__ __forceinline__ D2 block_d2_dyn(D2 v, D2* sh) {
+    v = warp_d2(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    D2 t = (threadIdx.x < nw) ? sh[threadIdx.x] : D2{0.0, 0.0};
+    if (w == 0) t = warp_d2(t);
+    if (threadIdx.x == 0) sh[0] = t;
+    __syncthreads();
+    D2 r = sh[0];
+    __syncthreads();
+    return r;
+}
+template <int NT>
+__device__ __forceinline__ D2 block_d2(D2 v, D2* sh) {
+    return block_d2_dyn(v, sh);
+}
+// merge `count` (s, c) partial pairs stored interleaved; one block; valid in every thread
+__device__ __forceinline__ D2 reduce_d2_partials(const double* partials, int count, D2* sh) {
+    D2 t{0.0, 0.0};
+    for (int i = threadIdx.x; i < count; i += blockDim.x)
+        t = d2_merge(t, D2{__ldcg(partials + 2 * i), __ldcg(partials + 2 * i + 1)});
+    return block_d2_dyn(t, sh);
+}
+
 // Deterministic reduction of `count` partials (fixed order) by one block.
 template <int NT>
 __device__ __forceinline__ double reduce_partials(const double* partials, int count, double* sh) {

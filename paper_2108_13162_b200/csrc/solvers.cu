@@ -842,6 +842,364 @@ struct PcgSession {
     }
 };
 
+// ------------------------------------------------------------------ device-resident BiCGStab
+// solve_bicgstab (solvers.cpp:344-438) as 5 kernels per iteration, scalars on device:
+//   K1  v = D^-1 A p            + <r^, v>   -> alpha = rho / <r^, v>
+//   K2  s = r - alpha v         + ||s||^2   -> half-step convergence test (counts an iteration)
+//   K3  t = D^-1 A s            + <t,t>, <t,s> -> omega
+//   K4  x += alpha p; x += omega s; r = s - omega t + ||r||^2, <r^, r> -> test, beta
+//   K5  p = r + beta (p - omega v)
+// Element-wise expressions keep the reference's roundings; the reductions are compensated
+// (Dot2) fixed trees.  Every breakdown / non-finite check of the reference is replayed on
+// device at the same point and reported with the same exception class and message.
+struct BiState {
+    double rho, alpha, omega, beta, norm_r0, tol;
+    long long iter, max_it;
+    int done, status, half;
+};
+enum : int {
+    kBsNonFiniteDenom = 1, kBsBreakdownDenom, kBsNonFiniteAlpha, kBsNonFiniteMeasure, kBsBreakdownTT,
+    kBsNonFiniteOmega, kBsBreakdownOmega, kBsBreakdownRho, kBsNonFiniteBeta
+};
+
+namespace {
+
+__device__ __forceinline__ bool dvanish(double v) { return fabs(v) < 1e-300; }
+__device__ __forceinline__ void bs_fail(BiState* st, int code) {
+    st->status = code;
+    st->done = 1;
+}
+
+struct FinAlpha {  // after K1
+    __device__ void operator()(BiState* st, double denom, double) const {
+        if (!isfinite(denom)) return bs_fail(st, kBsNonFiniteDenom);
+        if (dvanish(denom)) return bs_fail(st, kBsBreakdownDenom);
+        st->alpha = st->rho / denom;
+        if (!isfinite(st->alpha)) bs_fail(st, kBsNonFiniteAlpha);
+    }
+};
+struct FinOmega {  // after K3
+    __device__ void operator()(BiState* st, double tt, double ts) const {
+        if (dvanish(tt)) return bs_fail(st, kBsBreakdownTT);
+        st->omega = ts / tt;
+        if (!isfinite(st->omega)) return bs_fail(st, kBsNonFiniteOmega);
+        if (dvanish(st->omega)) bs_fail(st, kBsBreakdownOmega);
+    }
+};
+
+// SpMV epilogue: y = D^-1 (A x) (or A x), NACC compensated dot partials, grid finalize
+template <class Fin, int NACC>
+struct EpiBi {
+    double* __restrict__ y;
+    const double* __restrict__ dinv;
+    const double* __restrict__ w0;  // nullptr: <y, y>
+    const double* __restrict__ w1;
+    BiState* st;
+    double* partials;
+    unsigned* counter;
+    D2 a0, a1;
+    __device__ __forceinline__ bool active() const { return *(volatile int*)&st->done == 0; }
+    __device__ __forceinline__ void row(int64_t r, double v) {
+        if (dinv) v = __dmul_rn(v, dinv[r]);
+        y[r] = v;
+        d2_add_prod(a0, w0 ? w0[r] : v, v);
+        if (NACC == 2) d2_add_prod(a1, w1[r], v);
+    }
+    __device__ __forceinline__ void finish() {
+        __shared__ D2 sh[32];
+        const D2 b0 = block_d2_dyn(a0, sh);
+        const D2 b1 = NACC == 2 ? block_d2_dyn(a1, sh) : D2{0.0, 0.0};
+        if (threadIdx.x == 0) {
+            double* q = partials + 4 * blockIdx.x;
+            q[0] = b0.s;
+            q[1] = b0.c;
+            q[2] = b1.s;
+            q[3] = b1.c;
+        }
+        if (last_block(counter)) {
+            D2 t0{0.0, 0.0}, t1{0.0, 0.0};
+            for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+                const double* q = partials + 4 * i;
+                t0 = d2_merge(t0, D2{__ldcg(q), __ldcg(q + 1)});
+                t1 = d2_merge(t1, D2{__ldcg(q + 2), __ldcg(q + 3)});
+            }
+            t0 = block_d2_dyn(t0, sh);
+            t1 = block_d2_dyn(t1, sh);
+            if (threadIdx.x == 0) {
+                *counter = 0;
+                Fin()(st, __dadd_rn(t0.s, t0.c), __dadd_rn(t1.s, t1.c));
+            }
+        }
+    }
+};
+
+constexpr int kBiNT = 256;
+
+// K2: s = r - alpha v (copy_vec + daxpy, solvers.cpp:387-388), ||s||^2, half-step test
+__global__ void __launch_bounds__(kBiNT) bi_s_kernel(int64_t n, double* __restrict__ s, const double* __restrict__ r,
+                                                      const double* __restrict__ v, BiState* st, double* partials,
+                                                      unsigned* counter, double* history) {
+    if (*(volatile int*)&st->done) return;
+    __shared__ D2 sh[32];
+    const double ma = -st->alpha;
+    D2 acc{0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBiNT) {
+        const double si = __dadd_rn(__dmul_rn(ma, v[i]), r[i]);
+        s[i] = si;
+        d2_add_prod(acc, si, si);
+    }
+    const D2 b = block_d2_dyn(acc, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = b.s;
+        partials[2 * blockIdx.x + 1] = b.c;
+    }
+    if (last_block(counter)) {
+        const D2 t = reduce_d2_partials(partials, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            *counter = 0;
+            const double measure = sqrt(__dadd_rn(t.s, t.c)) / st->norm_r0;
+            if (!isfinite(measure)) return bs_fail(st, kBsNonFiniteMeasure);
+            if (measure <= st->tol) {  // solvers.cpp:391-397: x += alpha p pending, counts an iteration
+                history[st->iter] = measure;
+                st->iter += 1;
+                st->half = 1;
+                st->done = 1;
+            }
+        }
+    }
+}
+
+// K4: x += alpha p; x += omega s; r = s - omega t; ||r||^2, <r^, r>; test; beta (:410-432)
+__global__ void __launch_bounds__(kBiNT) bi_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                           const double* __restrict__ p, const double* __restrict__ s,
+                                                           const double* __restrict__ t, const double* __restrict__ rh,
+                                                           BiState* st, double* partials, unsigned* counter,
+                                                           double* history) {
+    const int done = *(volatile int*)&st->done, half = *(volatile int*)&st->half;
+    if (done && !half) return;
+    const double alpha = st->alpha;
+    if (half) {  // converged at the half step: only x += alpha p (solvers.cpp:392)
+        for (int64_t i = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBiNT)
+            x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        __syncthreads();
+        if (last_block(counter) && threadIdx.x == 0) {
+            *counter = 0;
+            st->half = 0;
+        }
+        return;
+    }
+    __shared__ D2 sh[32];
+    const double om = st->omega, mom = -om;
+    D2 a0{0.0, 0.0}, a1{0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBiNT) {
+        const double si = s[i];
+        x[i] = __dadd_rn(__dmul_rn(om, si), __dadd_rn(__dmul_rn(alpha, p[i]), x[i]));
+        const double ri = __dadd_rn(__dmul_rn(mom, t[i]), si);
+        r[i] = ri;
+        d2_add_prod(a0, ri, ri);
+        d2_add_prod(a1, rh[i], ri);
+    }
+    const D2 b0 = block_d2_dyn(a0, sh);
+    const D2 b1 = block_d2_dyn(a1, sh);
+    if (threadIdx.x == 0) {
+        double* q = partials + 4 * blockIdx.x;
+        q[0] = b0.s;
+        q[1] = b0.c;
+        q[2] = b1.s;
+        q[3] = b1.c;
+    }
+    if (last_block(counter)) {
+        D2 t0{0.0, 0.0}, t1{0.0, 0.0};
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+            const double* q = partials + 4 * i;
+            t0 = d2_merge(t0, D2{__ldcg(q), __ldcg(q + 1)});
+            t1 = d2_merge(t1, D2{__ldcg(q + 2), __ldcg(q + 3)});
+        }
+        t0 = block_d2_dyn(t0, sh);
+        t1 = block_d2_dyn(t1, sh);
+        if (threadIdx.x == 0) {
+            *counter = 0;
+            const double measure = sqrt(__dadd_rn(t0.s, t0.c)) / st->norm_r0;
+            if (!isfinite(measure)) return bs_fail(st, kBsNonFiniteMeasure);
+            const long long it = st->iter;
+            history[it] = measure;
+            st->iter = it + 1;
+            if (measure <= st->tol) {
+                st->done = 1;
+                return;
+            }
+            const double rho_new = __dadd_rn(t1.s, t1.c);
+            if (dvanish(rho_new)) return bs_fail(st, kBsBreakdownRho);
+            const double beta = (rho_new / st->rho) * (alpha / om);
+            if (!isfinite(beta)) return bs_fail(st, kBsNonFiniteBeta);
+            st->beta = beta;
+            st->rho = rho_new;
+            if (it + 1 >= st->max_it) st->done = 1;
+        }
+    }
+}
+
+// K5: p = p - omega v; p = r + beta p (daxpy + axpby, solvers.cpp:430-431)
+__global__ void __launch_bounds__(kBiNT) bi_p_kernel(int64_t n, double* __restrict__ p, const double* __restrict__ r,
+                                                      const double* __restrict__ v, const BiState* st) {
+    if (*(volatile const int*)&st->done) return;
+    const double mom = -st->omega, beta = st->beta;
+    for (int64_t i = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBiNT) {
+        const double pi = __dadd_rn(__dmul_rn(mom, v[i]), p[i]);
+        p[i] = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(beta, pi));
+    }
+}
+
+}  // namespace
+
+struct BicgstabSession {
+    static constexpr int kChunk = 8;
+    Engine e;
+    krysp_solver_cfg cfg;
+    int64_t n;
+    DVec x, r, rh, p, v, s, t;
+    BiState* st = nullptr;
+    double* hist = nullptr;
+    bool done_at_setup = false;
+    cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr;
+    int kernels_per_iteration = 0;
+
+    BicgstabSession(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg_, const double* b, const double* x0)
+        : e(A, cfg_), cfg(cfg_), n(A->n_rows), x(n, A->ctx->stream), r(n, A->ctx->stream), rh(n, A->ctx->stream),
+          p(n, A->ctx->stream), v(n, A->ctx->stream), s(n, A->ctx->stream), t(n, A->ctx->stream) {
+        krysp_gpu_ctx* c = e.c;
+        try {
+            if (n) KG_CUDA(cudaMemcpyAsync(x, x0, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+            // setup, solvers.cpp:357-374
+            e.residual(b, x, v);
+            e.precond(v, r);
+            const double norm_r0 = e.norm2(r);
+            BiState h{};
+            h.norm_r0 = norm_r0;
+            h.tol = cfg.tolerance;
+            h.max_it = cfg.max_iterations;
+            if (norm_r0 == 0.0) {
+                done_at_setup = true;
+                h.done = 1;
+            } else {
+                e.copy(r, rh);
+                e.copy(r, p);
+                h.rho = e.dot(rh, r);
+            }
+            st = dev_alloc<BiState>(1, false);
+            hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
+            KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+            KG_CUDA(cudaStreamSynchronize(c->stream));
+            exec_chunk = capture(kChunk);
+            exec_one = capture(1);
+        } catch (...) {
+            release();
+            throw;
+        }
+    }
+    ~BicgstabSession() { release(); }
+    void release() {
+        if (exec_chunk) cudaGraphExecDestroy(exec_chunk);
+        if (exec_one) cudaGraphExecDestroy(exec_one);
+        exec_chunk = exec_one = nullptr;
+        dev_free(st);
+        dev_free(hist);
+        st = nullptr;
+        hist = nullptr;
+    }
+
+    void iteration() {
+        krysp_gpu_ctx* c = e.c;
+        double* pa = c->d_partials + 2 * kPartialCap;
+        double* pb = c->d_partials + 3 * kPartialCap;
+        unsigned* ca = c->d_counters + 2;
+        unsigned* cb = c->d_counters + 3;
+        const double* dinv = e.jacobi ? (const double*)e.inv : nullptr;
+        const unsigned g = grid_for(n, kBiNT, (int64_t)c->sm_count * 8);
+        const int64_t before = c->launches;
+        spmv_fused(e, p, v, EpiBi<FinAlpha, 1>{v, dinv, rh, nullptr, st, pa, ca, {0, 0}, {0, 0}});
+        bi_s_kernel<<<g, kBiNT, 0, c->stream>>>(n, s, r, v, st, pb, cb, hist);
+        KG_LAUNCH(c);
+        spmv_fused(e, s, t, EpiBi<FinOmega, 2>{t, dinv, nullptr, s, st, pa, ca, {0, 0}, {0, 0}});
+        bi_update_kernel<<<g, kBiNT, 0, c->stream>>>(n, x, r, p, s, t, rh, st, pb, cb, hist);
+        KG_LAUNCH(c);
+        bi_p_kernel<<<g, kBiNT, 0, c->stream>>>(n, p, r, v, st);
+        KG_LAUNCH(c);
+        kernels_per_iteration = (int)(c->launches - before);
+    }
+
+    cudaGraphExec_t capture(int iters) {
+        krysp_gpu_ctx* c = e.c;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        KG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            for (int i = 0; i < iters; ++i) iteration();
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        KG_CUDA(cudaStreamEndCapture(c->stream, &graph));
+        KG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        return exec;
+    }
+
+    void enqueue(int64_t iters) {
+        for (int64_t i = 0; i + kChunk <= iters; i += kChunk) KG_CUDA(cudaGraphLaunch(exec_chunk, e.c->stream));
+        for (int64_t i = 0; i < iters % kChunk; ++i) KG_CUDA(cudaGraphLaunch(exec_one, e.c->stream));
+    }
+
+    bool finished() {
+        int* h_done = reinterpret_cast<int*>(e.c->h_pinned + 8);
+        KG_CUDA(cudaMemcpyAsync(h_done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, e.c->stream));
+        KG_CUDA(cudaStreamSynchronize(e.c->stream));
+        return *h_done != 0;
+    }
+
+    double run_to_convergence() {
+        cudaEvent_t a, b;
+        KG_CUDA(cudaEventCreate(&a));
+        KG_CUDA(cudaEventCreate(&b));
+        KG_CUDA(cudaEventRecord(a, e.c->stream));
+        // one extra graph after `done` lets a pending half-step x update (K4) run
+        while (!finished()) enqueue(kChunk);
+        enqueue(1);
+        KG_CUDA(cudaEventRecord(b, e.c->stream));
+        KG_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        KG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        return ms * 1e-3;
+    }
+
+    void finish(Report& rep) {
+        BiState h{};
+        KG_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, e.c->stream));
+        KG_CUDA(cudaStreamSynchronize(e.c->stream));
+        rep.history.resize((size_t)h.iter);
+        if (h.iter) KG_CUDA(cudaMemcpy(rep.history.data(), hist, 8 * (size_t)h.iter, cudaMemcpyDeviceToHost));
+        rep.iterations = h.iter;
+        rep.final_measure = h.iter ? rep.history.back() : 1.0;
+        rep.converged = done_at_setup || (h.iter && rep.final_measure <= cfg.tolerance);
+        if (done_at_setup) rep.final_measure = 0.0;
+        switch (h.status) {
+            case kBsNonFiniteDenom: fail(KRYSP_NON_FINITE, "<r_hat, v> became non-finite");
+            case kBsBreakdownDenom: fail(KRYSP_BREAKDOWN, "bicgstab: <r_hat, v> vanished");
+            case kBsNonFiniteAlpha: fail(KRYSP_NON_FINITE, "alpha became non-finite");
+            case kBsNonFiniteMeasure: fail(KRYSP_NON_FINITE, "residual measure became non-finite");
+            case kBsBreakdownTT: fail(KRYSP_BREAKDOWN, "bicgstab: <t, t> vanished");
+            case kBsNonFiniteOmega: fail(KRYSP_NON_FINITE, "omega became non-finite");
+            case kBsBreakdownOmega: fail(KRYSP_BREAKDOWN, "bicgstab: omega vanished");
+            case kBsBreakdownRho: fail(KRYSP_BREAKDOWN, "bicgstab: <r_hat, r> vanished");
+            case kBsNonFiniteBeta: fail(KRYSP_NON_FINITE, "beta became non-finite");
+            default: break;
+        }
+    }
+};
+
 namespace {
 
 void pcg_fused(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep,
@@ -850,6 +1208,14 @@ void pcg_fused(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg, const double
     if (!s.done_at_setup) *device_seconds = s.run_to_convergence();
     if (A->n_rows) KG_CUDA(cudaMemcpyAsync(x, s.x, 8 * A->n_rows, cudaMemcpyDeviceToDevice, A->ctx->stream));
     s.finish(rep, trace);
+}
+
+void bicgstab_fused(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep,
+                    double* device_seconds) {
+    BicgstabSession s(A, cfg, b, x);
+    if (!s.done_at_setup) *device_seconds = s.run_to_convergence();
+    if (A->n_rows) KG_CUDA(cudaMemcpyAsync(x, s.x, 8 * A->n_rows, cudaMemcpyDeviceToDevice, A->ctx->stream));
+    s.finish(rep);
 }
 
 }  // namespace
@@ -874,7 +1240,7 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
         }
     });
     cudaStream_t stream = A->ctx->stream;
-    const bool fused = method == KRYSP_PCG && cfg.mode == KRYSP_MODE_FAST;
+    const bool fused = (method == KRYSP_PCG || method == KRYSP_BICGSTAB) && cfg.mode == KRYSP_MODE_FAST;
     Report rep;
     double dev_s = 0.0;
     std::exception_ptr err;
@@ -884,7 +1250,8 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
     KG_CUDA(cudaEventRecord(ev0, stream));
     try {
         if (fused) {
-            pcg_fused(A, cfg, b, x, rep, h_trace != nullptr, &dev_s);
+            if (method == KRYSP_PCG) pcg_fused(A, cfg, b, x, rep, h_trace != nullptr, &dev_s);
+            else bicgstab_fused(A, cfg, b, x, rep, &dev_s);
         } else {
             Engine e(A, cfg);
             switch (method) {
@@ -925,7 +1292,15 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
 
 // ------------------------------------------------------------------ stepwise solver C-ABI
 struct krysp_gpu_solver {
-    kg::PcgSession* s = nullptr;
+    kg::PcgSession* pcg = nullptr;
+    kg::BicgstabSession* bicg = nullptr;
+    template <typename F>
+    void visit(F&& f) {
+        if (pcg) f(*pcg);
+        else if (bicg) f(*bicg);
+        else kg::fail(KRYSP_ERROR, "empty solver");
+    }
+    kg::Engine& engine() { return pcg ? pcg->e : bicg->e; }
 };
 
 using kg::guard;
@@ -936,15 +1311,16 @@ krysp_status krysp_gpu_solver_create(const krysp_gpu_mat* m, int32_t method, con
                                      const krysp_solver_cfg* cfg, krysp_gpu_solver** out) {
     return guard([&] {
         if (!m || !cfg || !out || !b || !x0) kg::fail(KRYSP_ERROR, "solver_create: NULL argument");
-        if (method != KRYSP_PCG || cfg->mode != KRYSP_MODE_FAST)
-            kg::fail(KRYSP_ERROR, "stepwise solver supports method KRYSP_PCG in KRYSP_MODE_FAST");
+        if ((method != KRYSP_PCG && method != KRYSP_BICGSTAB) || cfg->mode != KRYSP_MODE_FAST)
+            kg::fail(KRYSP_ERROR, "stepwise solver supports KRYSP_PCG / KRYSP_BICGSTAB in KRYSP_MODE_FAST");
         if (m->n_rows != m->n_cols) kg::fail(KRYSP_DIMENSION_MISMATCH, "solver expects a square matrix");
         if (!(cfg->tolerance > 0.0) || cfg->max_iterations < 1)
             kg::fail(KRYSP_ERROR, "solver config requires tolerance > 0, max_iterations >= 1");
         KG_CUDA(cudaSetDevice(m->ctx->device));
         auto* h = new krysp_gpu_solver;
         try {
-            h->s = new kg::PcgSession(m, *cfg, b, x0, false);
+            if (method == KRYSP_PCG) h->pcg = new kg::PcgSession(m, *cfg, b, x0, false);
+            else h->bicg = new kg::BicgstabSession(m, *cfg, b, x0);
         } catch (...) {
             delete h;
             throw;
@@ -956,19 +1332,19 @@ krysp_status krysp_gpu_solver_create(const krysp_gpu_mat* m, int32_t method, con
 krysp_status krysp_gpu_solver_iterate(krysp_gpu_solver* h, int64_t n) {
     return guard([&] {
         if (!h) kg::fail(KRYSP_ERROR, "NULL solver");
-        h->s->enqueue(n);
+        h->visit([&](auto& s) { s.enqueue(n); });
     });
 }
 
 krysp_status krysp_gpu_solver_time(krysp_gpu_solver* h, int64_t n, double* seconds) {
     return guard([&] {
         if (!h || !seconds) kg::fail(KRYSP_ERROR, "NULL argument");
-        cudaStream_t st = h->s->e.c->stream;
+        cudaStream_t st = h->engine().c->stream;
         cudaEvent_t a, b;
         KG_CUDA(cudaEventCreate(&a));
         KG_CUDA(cudaEventCreate(&b));
         KG_CUDA(cudaEventRecord(a, st));
-        h->s->enqueue(n);
+        h->visit([&](auto& s) { s.enqueue(n); });
         KG_CUDA(cudaEventRecord(b, st));
         KG_CUDA(cudaEventSynchronize(b));
         float ms = 0.f;
@@ -982,14 +1358,16 @@ krysp_status krysp_gpu_solver_time(krysp_gpu_solver* h, int64_t n, double* secon
 krysp_status krysp_gpu_solver_profile(krysp_gpu_solver* h, int64_t n, double seconds[3]) {
     return guard([&] {
         if (!h || !seconds) kg::fail(KRYSP_ERROR, "NULL argument");
-        h->s->profile(n, seconds);
+        if (!h->pcg) kg::fail(KRYSP_ERROR, "per-kernel profile is available for the P-CG solver");
+        h->pcg->profile(n, seconds);
     });
 }
 
 krysp_status krysp_gpu_solver_run(krysp_gpu_solver* h, double* seconds) {
     return guard([&] {
         if (!h) kg::fail(KRYSP_ERROR, "NULL solver");
-        double t = h->s->run_to_convergence();
+        double t = 0.0;
+        h->visit([&](auto& s) { t = s.run_to_convergence(); });
         if (seconds) *seconds = t;
     });
 }
@@ -1001,7 +1379,8 @@ krysp_status krysp_gpu_solver_report(krysp_gpu_solver* h, krysp_report* rep, dou
         kg::Report r;
         std::exception_ptr err;
         try {
-            h->s->finish(r, false);
+            if (h->pcg) h->pcg->finish(r, false);
+            else h->bicg->finish(r);
         } catch (...) {
             err = std::current_exception();
         }
@@ -1016,21 +1395,24 @@ krysp_status krysp_gpu_solver_report(krysp_gpu_solver* h, krysp_report* rep, dou
 krysp_status krysp_gpu_solver_solution(krysp_gpu_solver* h, double* x) {
     return guard([&] {
         if (!h || !x) kg::fail(KRYSP_ERROR, "NULL argument");
-        auto* s = h->s;
-        if (s->n) KG_CUDA(cudaMemcpyAsync(x, s->x, 8 * s->n, cudaMemcpyDeviceToDevice, s->e.c->stream));
-        KG_CUDA(cudaStreamSynchronize(s->e.c->stream));
+        h->visit([&](auto& s) {
+            if (s.n) KG_CUDA(cudaMemcpyAsync(x, s.x, 8 * s.n, cudaMemcpyDeviceToDevice, s.e.c->stream));
+            KG_CUDA(cudaStreamSynchronize(s.e.c->stream));
+        });
     });
 }
 
 int32_t krysp_gpu_solver_kernels_per_iteration(const krysp_gpu_solver* h) {
-    return h && h->s ? h->s->kernels_per_iteration : 0;
+    if (!h) return 0;
+    return h->pcg ? h->pcg->kernels_per_iteration : h->bicg ? h->bicg->kernels_per_iteration : 0;
 }
 
 krysp_status krysp_gpu_solver_destroy(krysp_gpu_solver* h) {
     return guard([&] {
         if (!h) return;
-        if (h->s) cudaStreamSynchronize(h->s->e.c->stream);
-        delete h->s;
+        if (h->pcg || h->bicg) cudaStreamSynchronize(h->engine().c->stream);
+        delete h->pcg;
+        delete h->bicg;
         delete h;
     });
 }
