@@ -1,0 +1,152 @@
+"""SURVEY §8(d) configs other than the headline C3 (which is bench.py): throughput, roofline
+and parity against the reference on the B200.  One JSON object per line.
+
+  C1  P-CG + Jacobi, poisson2d(1000), CSR: full solve FAST + EXACT (1422 it golden)
+  C2  BiCGStab, convdiff2d(4000) (16M rows), CSR and ELL: FAST it/s + roofline; EXACT first
+      50 iterations bit-identical to the reference library at <256,8>
+  C4  GCR(50) / BiCGStab(4) / tfQMR / BiCGStab on the 27-point stencil 320^3, HYB (auto width and
+      w = 26): FAST it/s; parity at 80^3 vs the survey goldens
+  C5  SpMV on power-law rows (1M-10M rows), CSR/HYB/COO + tune_spmv
+Usage: python scripts/bench_configs.py [C1 C2 C4 C5]
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import paper_2108_13162_b200 as kg  # noqa: E402
+from oracle.oracle import REF_SO, Port, Ref  # noqa: E402  (checker only)
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def spmv_bytes(info):
+    return 12 * info["nnz"] + 4 * (info["n_rows"] + 1) + 8 * info["n_cols"] + 8 * info["n_rows"]
+
+
+def rate(A, method, its, stab_l=1, restart=50):
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=its, tolerance=1e-30,
+                          stab_l=stab_l, restart=restart)
+    o = kg.solve(A, method, np.ones(A.n_rows), cfg=cfg)
+    return o.iterations / o.device_time, o.iterations
+
+
+def c1(ctx, R):
+    A = ctx.generate("poisson2d", 1000)
+    b = np.ones(A.n_rows)
+    t0 = time.perf_counter()
+    f = kg.solve_pcg(A, b, cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0)))
+    wall = time.perf_counter() - t0
+    e = kg.solve_pcg(A, b, cfg=kg.SolverConfig(mode="exact"))
+    out = {"config": "C1", "workload": "P-CG + Jacobi poisson2d(1000), 1M rows, CSR", "fast_iterations": f.iterations,
+           "fast_final": f.final_residual_measure, "fast_it_per_s": f.iterations / f.device_time,
+           "fast_wall_s": wall, "exact_iterations": e.iterations, "exact_final": e.final_residual_measure,
+           "exact_it_per_s": e.iterations / e.device_time, "golden_iterations": 1422}
+    if R:
+        rm = R.from_csr(Port().generate("poisson2d", 1000))
+        o = R.solve(rm, "pcg", b, bs=256, tw=8)
+        out.update(ref_iterations=o["iterations"], ref_final=o["final_residual_measure"], ref_seconds=o["wall_time"],
+                   exact_bitwise_history=bool(np.array_equal(o["residual_history"], e.residual_history)),
+                   exact_bitwise_solution=bool(np.array_equal(o["solution"], e.solution)),
+                   fast_measure_abs_diff=abs(f.final_residual_measure - o["final_residual_measure"]))
+    emit(out)
+
+
+def c2(ctx, R):
+    n = 4000
+    A = ctx.generate("convdiff2d", n, 0.5)
+    info = A.info
+    B = 2 * spmv_bytes(info) + 136 * info["n_rows"]
+    for fmt in ["csr", "ell"]:
+        M = A if fmt == "csr" else A.convert("ell", slot_cap=1 << 40)
+        r, its = rate(M, "bicgstab", 60)
+        emit({"config": "C2", "format": fmt, "workload": "BiCGStab convdiff2d(4000) 16M rows", "it_per_s": r,
+              "iterations": its, "bytes_per_iteration": B, "roofline_frac": B * r / 1e9 / PEAK})
+    # EXACT mode parity: first 50 iterations against the reference at <256,8>
+    b = np.ones(info["n_rows"])
+    e = kg.solve_bicgstab(A, b, cfg=kg.SolverConfig(mode="exact", max_iterations=50))
+    out = {"config": "C2", "check": "EXACT first 50 iterations vs reference <256,8>",
+           "exact_it_per_s": e.iterations / e.device_time}
+    if R:
+        rm = R.from_csr(Port().generate("convdiff2d", n, pe=0.5))
+        o = R.solve(rm, "bicgstab", b, max_it=50, bs=256, tw=8)
+        out.update(ref_seconds=o["wall_time"], bitwise_history=bool(np.array_equal(o["residual_history"],
+                                                                                   e.residual_history)),
+                   bitwise_solution=bool(np.array_equal(o["solution"], e.solution)))
+    emit(out)
+
+
+def c4(ctx, R):
+    n = 320
+    A = ctx.generate("fem27", n, 0.5)
+    info = A.info
+    Bs = spmv_bytes(info)
+    N = info["n_rows"]
+    for w in [-1, 26]:
+        H = A.convert("hyb", hyb_width=w)
+        hi = H.info
+        for method, its, k, V, sl in [("bicgstab", 20, 2, 17, 1), ("tfqmr", 10, 3, 30, 1),
+                                      ("bicgstab_l", 4, 8, 60, 4), ("gcr", 20, 1, 12, 1)]:
+            r, got = rate(H, method, its, stab_l=sl)
+            B = k * Bs + 8 * N * V
+            emit({"config": "C4", "format": f"hyb(w={hi['width']}, coo={hi['coo_nnz']})", "method": method,
+                  "workload": "27-point fem27 320^3 (32.8M rows, 879M nnz)", "it_per_s": r, "iterations": got,
+                  "bytes_per_iteration_est": B, "roofline_frac_est": B * r / 1e9 / PEAK})
+        del H
+    # parity at 80^3 vs the survey goldens (GCR 245, BiCGStab(4) 25, tfQMR 123, BiCGStab 93)
+    A80 = ctx.generate("fem27", 80, 0.5).convert("hyb")
+    gold = {"gcr": 245, "bicgstab_l": 25, "tfqmr": 123, "bicgstab": 93}
+    for method, g in gold.items():
+        cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), stab_l=4 if method == "bicgstab_l" else 1)
+        o = kg.solve(A80, method, np.ones(A80.n_rows), cfg=cfg)
+        ex = kg.solve(A80, method, np.ones(A80.n_rows),
+                      cfg=kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(1024, 1),
+                                          stab_l=4 if method == "bicgstab_l" else 1))
+        emit({"config": "C4", "check": f"{method} 80^3", "golden": g, "fast_iterations": o.iterations,
+              "exact_iterations": ex.iterations, "fast_final": o.final_residual_measure,
+              "exact_final": ex.final_residual_measure})
+
+
+def c5(ctx, R):
+    for n, alpha in [(1_000_000, 2.0), (1_000_000, 1.5), (10_000_000, 2.0), (10_000_000, 1.5)]:
+        t0 = time.perf_counter()
+        m = kg.generate_csr("powerlaw", n, alpha=alpha, seed=2108)
+        gen = time.perf_counter() - t0
+        A = ctx.upload(m)
+        info = A.info
+        B = spmv_bytes(info)
+        row = {"config": "C5", "n": n, "alpha": alpha, "nnz": info["nnz"], "host_gen_s": gen}
+        proto = kg.TimingProtocol(min_repetitions=10)
+        for fmt, pol, mode in [("csr", kg.ExecPolicy(0, 0), "fast"), ("csr", kg.ExecPolicy(256, 8), "exact"),
+                               ("hyb", kg.ExecPolicy(256, 1), "exact"), ("coo", kg.ExecPolicy(256, 1), "exact")]:
+            M = A if fmt == "csr" else A.convert(fmt)
+            r = kg.time_spmv(M, pol, mode, proto)
+            key = f"{fmt}_{'auto' if pol.block_size == 0 else str(pol.block_size) + '_' + str(pol.workers_per_row)}"
+            row[key] = {"ms": r.mean_time * 1e3, "gflops": 2 * info["nnz"] / r.mean_time / 1e9,
+                        "gbs": B / r.mean_time / 1e9, "variant": r.kernel_variant}
+        if n == 1_000_000:
+            tr = kg.tune_spmv(A, protocol=kg.TimingProtocol(min_repetitions=5))
+            row["tune"] = {"best": [tr.best_policy.block_size, tr.best_policy.workers_per_row,
+                                    tr.best_policy.grid_strategy], "speedup_vs_default": tr.speedup_vs_default}
+        emit(row)
+
+
+def main():
+    which = sys.argv[1:] or ["C1", "C2", "C4", "C5"]
+    ctx = kg.Context(0)
+    R = Ref() if os.path.exists(REF_SO) else None
+    for w in which:
+        {"C1": c1, "C2": c2, "C4": c4, "C5": c5}[w](ctx, R)
+
+
+if __name__ == "__main__":
+    main()
