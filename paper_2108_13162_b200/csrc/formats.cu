@@ -32,8 +32,11 @@ void mat_free_arrays(krysp_gpu_mat* m) {
     dev_free(m->co_r);
     dev_free(m->co_c);
     dev_free(m->co_v);
-    m->rp = m->ci = m->jcoef = m->co_r = m->co_c = nullptr;
+    dev_free(m->coo_rp);
+    m->rp = m->ci = m->jcoef = m->co_r = m->co_c = m->coo_rp = nullptr;
     m->cv = m->coef = m->co_v = nullptr;
+    adaptive_free(m->ad_csr);
+    adaptive_free(m->ad_coo);
 }
 
 krysp_gpu_mat* mat_new(krysp_gpu_ctx* ctx, int32_t fmt, int64_t n_rows, int64_t n_cols) {

@@ -93,8 +93,26 @@ struct CooView {
 
 }  // namespace kg
 
+// Load-balanced row blocking of a CSR structure for the FAST irregular-row SpMV
+// (adaptive.cu): row blocks of <= 256 rows and <= kAdTile nnz, single-row blocks for long
+// rows, and rows longer than kAdSplit split into kAdChunk-nnz chunks (partials + fixup).
+namespace kg {
+struct AdaptivePlan {
+    int32_t* blk = nullptr;    // nblk + 1 row boundaries
+    int64_t nblk = 0;
+    int32_t* chunk = nullptr;  // (row, k0, k1) per chunk of a giant row
+    int64_t nchunk = 0;
+    int32_t* giant = nullptr;  // (row, c0, c1) per giant row
+    int64_t ngiant = 0;
+    double* partials = nullptr;
+    bool built = false;
+};
+}  // namespace kg
+
 struct krysp_gpu_mat {
     krysp_gpu_ctx* ctx = nullptr;
+    kg::AdaptivePlan ad_csr, ad_coo;  // FAST irregular-row plans (CSR rows / COO overflow rows)
+    int32_t* coo_rp = nullptr;        // row pointer over the COO entries (FAST COO / HYB)
     int32_t format = KRYSP_FMT_CSR;
     int64_t n_rows = 0, n_cols = 0, nnz = 0;
     // CSR
@@ -321,6 +339,13 @@ krysp_gpu_mat* mat_new(krysp_gpu_ctx* ctx, int32_t fmt, int64_t n_rows, int64_t 
 void mat_row_stats(krysp_gpu_mat* m);  // fills max_row / max_tile_nnz for CSR
 krysp_gpu_mat* convert_to_csr(const krysp_gpu_mat* m);
 
+// adaptive.cu
+void adaptive_free(AdaptivePlan& p);
+bool csr_is_irregular(const krysp_gpu_mat* m);
+// y (=|+=) A x over the CSR arrays (or the COO part via coo_rp) with the load-balanced plan
+void launch_adaptive(const krysp_gpu_mat* m, bool coo_part, const double* x, double* y, bool accumulate,
+                     cudaStream_t s);
+
 // spmv.cu
 enum SpmvVariant : int32_t {
     kVarCsrVector = 0,  // paper's CSR-vector kernel, tw lanes per row, exact policy order
@@ -328,6 +353,9 @@ enum SpmvVariant : int32_t {
     kVarEll = 2,
     kVarHyb = 3,
     kVarCoo = 4,
+    kVarCsrAdaptive = 5,  // FAST: load-balanced row blocks (irregular rows)
+    kVarHybAdaptive = 6,  // FAST: ELL + load-balanced COO overflow
+    kVarCooAdaptive = 7,  // FAST: load-balanced COO
 };
 int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const krysp_policy& pol,
                     int32_t mode, cudaStream_t s);

@@ -47,6 +47,7 @@ struct Engine {
         if (pol.block_size == 0) {
             if (mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "auto policy (block_size 0) requires FAST mode");
             krysp_gpu_autotune_policy(A, &pol);
+            auto_pol = true;
         }
         check_policy(pol);
         if (cfg.preconditioner) make_jacobi();
@@ -70,7 +71,9 @@ struct Engine {
         if (hz != INT32_MAX) fail(KRYSP_BREAKDOWN, "zero diagonal entry at row %d; Jacobi preconditioner undefined", hz);
     }
 
-    void spmv(const krysp_gpu_mat* M, const double* x, double* y) { spmv_launch(M, x, y, pol, mode, c->stream); }
+    bool auto_pol = false;  // FAST + library's kernel choice (load-balanced kernels for irregular rows)
+    krysp_policy launch_pol() const { return auto_pol ? krysp_policy{0, 0, 0, 0} : pol; }
+    void spmv(const krysp_gpu_mat* M, const double* x, double* y) { spmv_launch(M, x, y, launch_pol(), mode, c->stream); }
     void spmv(const double* x, double* y) { spmv(A, x, y); }
     // apply_precond solvers.cpp:46-52: z = copy(r), then z *= inv
     void precond(const double* r, double* z) {
@@ -639,13 +642,15 @@ template <class Epi>
 void spmv_fused(Engine& e, const double* x, double* y, Epi epi) {
     const krysp_gpu_mat* m = e.A;
     cudaStream_t s = e.c->stream;
-    if (m->format == KRYSP_FMT_CSR) {
+    const bool irregular = e.auto_pol && ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) ||
+                                          m->format == KRYSP_FMT_COO || (m->format == KRYSP_FMT_HYB && m->coo_nnz));
+    if (!irregular && m->format == KRYSP_FMT_CSR) {
         if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, x, epi, s);
         else launch_csr_vector(m, x, epi, e.pol.block_size, e.pol.workers_per_row, s);
-    } else if (m->format == KRYSP_FMT_ELL || (m->format == KRYSP_FMT_HYB && m->coo_nnz == 0)) {
+    } else if (!irregular && (m->format == KRYSP_FMT_ELL || (m->format == KRYSP_FMT_HYB && m->coo_nnz == 0))) {
         launch_ell(m, x, epi, e.pol.block_size, s);
     } else {
-        spmv_launch(m, x, y, e.pol, e.mode, s);
+        spmv_launch(m, x, y, e.launch_pol(), e.mode, s);
         vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y, epi);
         KG_LAUNCH(e.c);
     }

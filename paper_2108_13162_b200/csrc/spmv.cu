@@ -46,12 +46,28 @@ bool csr_use_tile(const krysp_gpu_mat* m, int64_t tw) {
 int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const krysp_policy& pol0,
                     int32_t mode, cudaStream_t s) {
     krysp_policy pol = pol0;
-    if (pol.block_size == 0) {
+    const bool auto_pol = pol.block_size == 0;
+    if (auto_pol) {
         if (mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "auto policy (block_size 0) requires FAST mode");
         krysp_gpu_autotune_policy(m, &pol);
     }
     check_policy(pol);
     EpiStore epi{y};
+    if (auto_pol) {  // FAST, library's choice: load-balanced kernels for irregular rows
+        if (m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) {
+            launch_adaptive(m, false, x, y, false, s);
+            return kVarCsrAdaptive;
+        }
+        if (m->format == KRYSP_FMT_HYB && m->coo_nnz) {
+            launch_ell(m, x, epi, pol.block_size, s);
+            launch_adaptive(m, true, x, y, true, s);
+            return kVarHybAdaptive;
+        }
+        if (m->format == KRYSP_FMT_COO) {
+            launch_adaptive(m, true, x, y, false, s);
+            return kVarCooAdaptive;
+        }
+    }
     switch (m->format) {
         case KRYSP_FMT_CSR:
             if (csr_use_tile(m, pol.workers_per_row)) {

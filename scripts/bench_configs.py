@@ -126,11 +126,14 @@ def c5(ctx, R):
         B = spmv_bytes(info)
         row = {"config": "C5", "n": n, "alpha": alpha, "nnz": info["nnz"], "host_gen_s": gen}
         proto = kg.TimingProtocol(min_repetitions=10)
+        conv = {"csr": A, "hyb": A.convert("hyb"), "coo": A.convert("coo")}
         for fmt, pol, mode in [("csr", kg.ExecPolicy(0, 0), "fast"), ("csr", kg.ExecPolicy(256, 8), "exact"),
-                               ("hyb", kg.ExecPolicy(256, 1), "exact"), ("coo", kg.ExecPolicy(256, 1), "exact")]:
-            M = A if fmt == "csr" else A.convert(fmt)
+                               ("csr", kg.ExecPolicy(256, 1), "exact"), ("hyb", kg.ExecPolicy(0, 0), "fast"),
+                               ("hyb", kg.ExecPolicy(256, 1), "exact"), ("coo", kg.ExecPolicy(0, 0), "fast"),
+                               ("coo", kg.ExecPolicy(256, 1), "exact")]:
+            M = conv[fmt]
             r = kg.time_spmv(M, pol, mode, proto)
-            key = f"{fmt}_{'auto' if pol.block_size == 0 else str(pol.block_size) + '_' + str(pol.workers_per_row)}"
+            key = f"{fmt}_{mode}_{'auto' if pol.block_size == 0 else str(pol.block_size) + '_' + str(pol.workers_per_row)}"
             row[key] = {"ms": r.mean_time * 1e3, "gflops": 2 * info["nnz"] / r.mean_time / 1e9,
                         "gbs": B / r.mean_time / 1e9, "variant": r.kernel_variant}
         if n == 1_000_000:

@@ -167,6 +167,24 @@ def test_spmv_powerlaw_bitexact(ctx, spmv_fixtures):
             np.testing.assert_array_equal(kg.spmv(M, x, kg.ExecPolicy(bs, tw)), f[f"pl_y_{fmt}_{bs}_{tw}"])
 
 
+@pytest.mark.parametrize("n,alpha", [(1_000_000, 1.5), (300_000, 2.0)])
+def test_spmv_fast_adaptive_powerlaw(ctx, port, n, alpha):
+    # FAST auto policy on irregular rows: load-balanced blocks, long rows per CTA, giant rows
+    # split in chunks (+ ordered fixup); HYB overflow / COO via the same plan.  <= 1e-13.
+    m = kg.generate_csr("powerlaw", n, alpha=alpha, seed=5)
+    x = np.random.default_rng(1).uniform(-1, 1, n)
+    want = port.spmv(port.generate("powerlaw", n, alpha=alpha, seed=5), x, "csr", 256, 1)
+    A = ctx.upload(m)
+    for fmt in ["csr", "hyb", "coo"]:
+        M = A if fmt == "csr" else A.convert(fmt)
+        y1 = kg.spmv(M, x, kg.ExecPolicy(0, 0), mode="fast")
+        y2 = kg.spmv(M, x, kg.ExecPolicy(0, 0), mode="fast")
+        assert rel_err(y1, want) <= 1e-13, fmt
+        np.testing.assert_array_equal(y1, y2)  # deterministic
+        r = kg.time_spmv(M, kg.ExecPolicy(0, 0), "fast", kg.TimingProtocol(min_repetitions=3))
+        assert r.kernel_variant.endswith("adaptive") or r.kernel_variant in ("csr_tile",), r.kernel_variant
+
+
 def test_spmv_device_arrays_and_repeat_determinism(ctx, port):
     m = port.generate("lap3d7", 24)
     A = ctx.upload(csr_of(m))
