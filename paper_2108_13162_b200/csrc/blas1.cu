@@ -248,7 +248,7 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
 double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode) {
     k_dot(c, n, x, y, bs, mode, c->d_scalars);
     KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    KG_CUDA(cudaStreamSynchronize(c->stream));
+    stream_wait(c);
     return c->h_pinned[0];
 }
 

@@ -74,6 +74,7 @@ krysp_status krysp_gpu_ctx_create(int device, krysp_gpu_ctx** out) {
         c->d_counters = dev_alloc<unsigned>(kSlots * 4, true, c->stream);
         c->d_scalars = dev_alloc<double>(kScalarCap, true, c->stream);
         KG_CUDA(cudaMallocHost(&c->h_pinned, sizeof(double) * kScalarCap));
+        KG_CUDA(cudaEventCreateWithFlags(&c->sync_ev, cudaEventDisableTiming));
         KG_CUDA(cudaStreamSynchronize(c->stream));
         *out = c;
     });
@@ -88,6 +89,7 @@ krysp_status krysp_gpu_ctx_destroy(krysp_gpu_ctx* c) {
         dev_free(c->d_counters);
         dev_free(c->d_scalars);
         if (c->h_pinned) cudaFreeHost(c->h_pinned);
+        if (c->sync_ev) cudaEventDestroy(c->sync_ev);
         if (c->own_stream) cudaStreamDestroy(c->own_stream);
         delete c;
     });

@@ -57,6 +57,7 @@ struct krysp_gpu_ctx {
     unsigned* d_counters = nullptr;
     double* d_scalars = nullptr;
     double* h_pinned = nullptr;
+    cudaEvent_t sync_ev = nullptr;  // host waits on solver scalars (spin, see stream_wait)
 };
 
 namespace kg {
@@ -327,6 +328,17 @@ krysp_status guard(F&& f) {
         g_last_error = e.what();
         return KRYSP_ERROR;
     }
+}
+
+// Wait for the context stream by spinning on an event: host-driven solvers round-trip a
+// scalar every few hundred microseconds, and a sleeping cudaStreamSynchronize can wake up
+// milliseconds late (measured: 4-11 ms of idle GPU per tfQMR iteration).
+inline void stream_wait(krysp_gpu_ctx* c) {
+    KG_CUDA(cudaEventRecord(c->sync_ev, c->stream));
+    cudaError_t e;
+    while ((e = cudaEventQuery(c->sync_ev)) == cudaErrorNotReady) {
+    }
+    if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "stream wait: %s", cudaGetErrorString(e));
 }
 
 // ---------------------------------------------------------------- host-side internals

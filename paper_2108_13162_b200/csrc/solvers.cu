@@ -66,7 +66,7 @@ struct Engine {
         k_invert_diag(c, n, inv, zr);
         int hz;
         KG_CUDA(cudaMemcpyAsync(&hz, zr, sizeof hz, cudaMemcpyDeviceToHost, c->stream));
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        stream_wait(c);
         dev_free(zr);
         if (hz != INT32_MAX) fail(KRYSP_BREAKDOWN, "zero diagonal entry at row %d; Jacobi preconditioner undefined", hz);
     }
@@ -94,7 +94,15 @@ struct Engine {
         k_scale(c, n, -1.0, r);
         k_daxpy(c, n, 1.0, b, r);
     }
-    double dot(const double* x, const double* y) { return host_dot(c, n, x, y, pol.block_size, mode); }
+    double dot(const double* x, const double* y) {
+        static const bool trace = std::getenv("KRYSP_TRACE") != nullptr;
+        if (!trace) return host_dot(c, n, x, y, pol.block_size, mode);
+        auto t0 = std::chrono::steady_clock::now();
+        const double v = host_dot(c, n, x, y, pol.block_size, mode);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 5.0) fprintf(stderr, "[krysp trace] dot wait %.2f ms (n=%lld)\n", ms, (long long)n);
+        return v;
+    }
     double norm2(const double* x) { return std::sqrt(dot(x, x)); }
     void daxpy(double a, const double* x, double* y) { k_daxpy(c, n, a, x, y); }
     void axpby(double a, const double* x, double b, double* y) { k_axpby(c, n, a, x, b, y); }
@@ -107,9 +115,24 @@ struct Report {
     double final_measure = 0.0;
     std::vector<double> history;
     std::vector<double> trace;  // 4 per iteration (pcg)
+    // recorded after setup / right after the iteration loop (before the work vectors are
+    // freed — cudaFree of GB-sized buffers takes milliseconds): device_time covers iterations
+    cudaEvent_t loop_start = nullptr, loop_end = nullptr;
     void push(double m) {
         history.push_back(m);
         ++iterations;
+    }
+    void mark(cudaStream_t s) {
+        if (!loop_start) KG_CUDA(cudaEventCreate(&loop_start));
+        KG_CUDA(cudaEventRecord(loop_start, s));
+    }
+    void end(cudaStream_t s) {
+        if (!loop_end) KG_CUDA(cudaEventCreate(&loop_end));
+        KG_CUDA(cudaEventRecord(loop_end, s));
+    }
+    ~Report() {
+        if (loop_start) cudaEventDestroy(loop_start);
+        if (loop_end) cudaEventDestroy(loop_end);
     }
 };
 
@@ -129,7 +152,7 @@ void pcg(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
         return;
     }
     bool first = true;
-    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+    for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         double beta = 0.0;
         if (first) first = false;
         else {
@@ -155,6 +178,7 @@ void pcg(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
         if (norm_r <= cfg.tolerance) rep.converged = true;
     }
     rep.final_measure = norm_r;
+    rep.end(e.c->stream);
 }
 
 // solve_cg_classic solvers.cpp:193-250
@@ -170,7 +194,7 @@ void cg_classic(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
     e.precond(g, z);
     e.copy(z, w);
     double measure = 1.0;
-    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+    for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         e.spmv(w, kw);
         double denom = e.dot(kw, w);
         check_finite(denom, "descent denominator");
@@ -189,6 +213,7 @@ void cg_classic(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
         if (measure <= cfg.tolerance) rep.converged = true;
     }
     rep.final_measure = measure;
+    rep.end(e.c->stream);
 }
 
 // solve_gcr solvers.cpp:256-338
@@ -204,7 +229,7 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
     }
     std::vector<DVec> dirs, op_dirs;
     double measure = 1.0;
-    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+    for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         // the basis storage is reused across restarts (dirs.clear() in the reference)
         auto slot = [&](std::vector<DVec>& v, int64_t j) -> DVec& {
             while ((int64_t)v.size() <= j) v.emplace_back(e.vec());
@@ -244,6 +269,7 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
         }
     }
     rep.final_measure = measure;
+    rep.end(e.c->stream);
 }
 
 // solve_bicgstab solvers.cpp:344-438
@@ -260,7 +286,7 @@ void bicgstab(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
     e.copy(r, p);
     double rho = e.dot(rh, r);
     double measure = 1.0;
-    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+    for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         e.op(p, v);
         double denom = e.dot(rh, v);
         check_finite(denom, "<r_hat, v>");
@@ -303,6 +329,7 @@ void bicgstab(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
         rho = rho_new;
     }
     rep.final_measure = measure;
+    rep.end(e.c->stream);
 }
 
 // solve_bicgstab_l solvers.cpp:444-572
@@ -326,7 +353,7 @@ void bicgstab_l(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
     std::vector<double> sigma(L + 1), gp(L + 1), g(L + 1), gpp(L + 1);
     std::vector<double> tau((size_t)((L + 1) * (L + 1)), 0.0);
     auto TAU = [&](int64_t i, int64_t j) -> double& { return tau[(size_t)(i * (L + 1) + j)]; };
-    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+    for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         rho0 = -omega * rho0;
         for (int64_t j = 0; j < L && !rep.converged; ++j) {
             double rho1 = e.dot(rr[j], rs);
@@ -387,6 +414,7 @@ void bicgstab_l(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
         if (measure <= cfg.tolerance) rep.converged = true;
     }
     rep.final_measure = measure;
+    rep.end(e.c->stream);
 }
 
 // solve_tfqmr solvers.cpp:578-696
@@ -414,7 +442,7 @@ void tfqmr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, R
     e.copy(v, bu);
     double tau = norm_r0, theta = 0.0, eta = 0.0;
     double rho = e.dot(r0, r0), alpha = 0.0, measure = 1.0;
-    for (int64_t m = 0; rep.iterations < cfg.max_iterations && !rep.converged; ++m) {
+    for (int64_t m = (rep.mark(e.c->stream), 0); rep.iterations < cfg.max_iterations && !rep.converged; ++m) {
         const bool even = (m % 2 == 0);
         if (even) {
             double denom = e.dot(v, r0);
@@ -465,6 +493,7 @@ void tfqmr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, R
         std::swap(u, un);
     }
     rep.final_measure = measure;
+    rep.end(e.c->stream);
 }
 
 // solve_bicgcr solvers.cpp:702-787 (transpose built on device, formats.cpp:312-334)
@@ -484,7 +513,7 @@ void bicgcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, 
     e.op(z, bz);
     e.copy(bz, bp);
     double num = e.dot(zt, bz), measure = 1.0;
-    while (rep.iterations < cfg.max_iterations && !rep.converged) {
+    for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         e.op_t(pt, btpt);
         double denom = e.dot(btpt, bp);
         check_finite(denom, "<B'p', Bp>");
@@ -513,6 +542,7 @@ void bicgcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, 
         num = num_new;
     }
     rep.final_measure = measure;
+    rep.end(e.c->stream);
 }
 
 // ------------------------------------------------------------------ device-resident P-CG
@@ -639,8 +669,7 @@ __global__ void __launch_bounds__(1024) vec_epi_kernel(int64_t n, const double* 
 }
 
 template <class Epi>
-void spmv_fused(Engine& e, const double* x, double* y, Epi epi) {
-    const krysp_gpu_mat* m = e.A;
+void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y, Epi epi) {
     cudaStream_t s = e.c->stream;
     const bool irregular = e.auto_pol && ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) ||
                                           m->format == KRYSP_FMT_COO || (m->format == KRYSP_FMT_HYB && m->coo_nnz));
@@ -654,6 +683,724 @@ void spmv_fused(Engine& e, const double* x, double* y, Epi epi) {
         vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y, epi);
         KG_LAUNCH(e.c);
     }
+}
+
+template <class Epi>
+void spmv_fused(Engine& e, const double* x, double* y, Epi epi) {
+    spmv_fused_m(e, e.A, x, y, epi);
+}
+
+// y = D^-1 (A x): the left-Jacobi operator in one pass (spmv_into + copy + scal_elementwise,
+// solvers.cpp:367-370 — the same single rounding fl(sum * inv))
+struct EpiScale {
+    double* __restrict__ y;
+    const double* __restrict__ dinv;
+    __device__ __forceinline__ bool active() const { return true; }
+    __device__ __forceinline__ void row(int64_t r, double v) { y[r] = dinv ? __dmul_rn(v, dinv[r]) : v; }
+    __device__ __forceinline__ void finish() {}
+};
+
+// CTAs per SM of the fused multi-vector kernels (KRYSP_FUSED_GRID overrides, for tuning)
+int fused_grid_mult() {
+    static int v = [] {
+        const char* s = std::getenv("KRYSP_FUSED_GRID");
+        int k = s ? std::atoi(s) : 4;
+        return k >= 1 && k <= 64 ? k : 4;
+    }();
+    return v;
+}
+
+// ------------------------------------------------------------------ fused GCR(m) kernels
+// Multi-dot: out[q] = <w, V_q> for q < k (k <= 8) in one pass over w (Dot2 compensated).
+constexpr int kMdNT = 256;
+constexpr int kMdG = 8;
+
+__global__ void __launch_bounds__(kMdNT) multidot_kernel(int64_t n, const double* __restrict__ w,
+                                                          const double* const* __restrict__ vs, int k,
+                                                          double* partials, unsigned* counter, double* out) {
+    __shared__ D2 sh[32];
+    D2 acc[kMdG];
+#pragma unroll
+    for (int q = 0; q < kMdG; ++q) acc[q] = D2{0.0, 0.0};
+    const double* v[kMdG];
+#pragma unroll
+    for (int q = 0; q < kMdG; ++q) v[q] = q < k ? vs[q] : nullptr;
+    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
+        const double wi = w[i];
+#pragma unroll
+        for (int q = 0; q < kMdG; ++q)
+            if (q < k) d2_add_prod(acc[q], wi, v[q][i]);
+    }
+    for (int q = 0; q < k; ++q) {
+        const D2 b = block_d2_dyn(acc[q], sh);
+        if (threadIdx.x == 0) {
+            partials[2 * (blockIdx.x * kMdG + q)] = b.s;
+            partials[2 * (blockIdx.x * kMdG + q) + 1] = b.c;
+        }
+    }
+    if (last_block(counter)) {
+        for (int q = 0; q < k; ++q) {
+            D2 t{0.0, 0.0};
+            for (int i = threadIdx.x; i < (int)gridDim.x; i += kMdNT)
+                t = d2_merge(t, D2{__ldcg(partials + 2 * (i * kMdG + q)), __ldcg(partials + 2 * (i * kMdG + q) + 1)});
+            t = block_d2_dyn(t, sh);
+            if (threadIdx.x == 0) out[q] = __dadd_rn(t.s, t.c);
+        }
+        if (threadIdx.x == 0) *counter = 0;
+    }
+}
+
+// x += alpha p_j; r -= alpha ap_j (two daxpy, solvers.cpp:306-307) and ||r||^2
+__global__ void __launch_bounds__(kMdNT) gcr_xr_kernel(int64_t n, double alpha, const double* __restrict__ p,
+                                                        const double* __restrict__ ap, double* __restrict__ x,
+                                                        double* __restrict__ r, double* partials, unsigned* counter,
+                                                        double* out) {
+    __shared__ D2 sh[32];
+    D2 acc{0.0, 0.0};
+    const double ma = -alpha;
+    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
+        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        const double ri = __dadd_rn(__dmul_rn(ma, ap[i]), r[i]);
+        r[i] = ri;
+        d2_add_prod(acc, ri, ri);
+    }
+    const D2 b = block_d2_dyn(acc, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = b.s;
+        partials[2 * blockIdx.x + 1] = b.c;
+    }
+    if (last_block(counter)) {
+        const D2 t = reduce_d2_partials(partials, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            *out = __dadd_rn(t.s, t.c);
+            *counter = 0;
+        }
+    }
+}
+
+// p_next = r - sum_i beta_i p_i, ap_next = w - sum_i beta_i ap_i, in the reference's daxpy
+// order (solvers.cpp:323-329: one rounding per term, i ascending), and ||ap_next||^2
+__global__ void __launch_bounds__(kMdNT) gcr_next_kernel(int64_t n, const double* __restrict__ r,
+                                                          const double* __restrict__ w,
+                                                          const double* const* __restrict__ P,
+                                                          const double* const* __restrict__ AP,
+                                                          const double* __restrict__ betas, int k,
+                                                          double* __restrict__ p_next, double* __restrict__ ap_next,
+                                                          double* partials, unsigned* counter, double* out) {
+    __shared__ D2 sh[32];
+    __shared__ double s_mb[128];
+    __shared__ const double* s_p[128];
+    __shared__ const double* s_ap[128];
+    for (int i = threadIdx.x; i < k; i += kMdNT) {
+        s_mb[i] = -betas[i];
+        s_p[i] = P[i];
+        s_ap[i] = AP[i];
+    }
+    __syncthreads();
+    D2 acc{0.0, 0.0};
+    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
+        double pn = r[e], an = w[e];
+        for (int i = 0; i < k; ++i) {
+            pn = __dadd_rn(__dmul_rn(s_mb[i], s_p[i][e]), pn);
+            an = __dadd_rn(__dmul_rn(s_mb[i], s_ap[i][e]), an);
+        }
+        p_next[e] = pn;
+        ap_next[e] = an;
+        d2_add_prod(acc, an, an);
+    }
+    const D2 b = block_d2_dyn(acc, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = b.s;
+        partials[2 * blockIdx.x + 1] = b.c;
+    }
+    if (last_block(counter)) {
+        const D2 t = reduce_d2_partials(partials, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            *out = __dadd_rn(t.s, t.c);
+            *counter = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ fused tfQMR kernels
+// Grid-wide D2 finalize of NACC accumulators into out[0..NACC) by the last block.
+template <int NACC>
+__device__ __forceinline__ void d2_grid_finish(const D2* acc, D2* sh, double* partials, unsigned* counter, double* out) {
+    D2 b[NACC];
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) b[q] = block_d2_dyn(acc[q], sh);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < NACC; ++q) {
+            partials[2 * (blockIdx.x * NACC + q)] = b[q].s;
+            partials[2 * (blockIdx.x * NACC + q) + 1] = b[q].c;
+        }
+    if (last_block(counter)) {
+#pragma unroll
+        for (int q = 0; q < NACC; ++q) {
+            D2 t{0.0, 0.0};
+            for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+                t = d2_merge(t, D2{__ldcg(partials + 2 * (i * NACC + q)), __ldcg(partials + 2 * (i * NACC + q) + 1)});
+            t = block_d2_dyn(t, sh);
+            if (threadIdx.x == 0) out[q] = __dadd_rn(t.s, t.c);
+        }
+        if (threadIdx.x == 0) *counter = 0;
+    }
+}
+
+// SpMV epilogue of true_measure (solvers.cpp:607-613): res = D^-1 (b - A x), ||res||^2
+struct EpiTrueRes {
+    const double* __restrict__ b;
+    const double* __restrict__ dinv;
+    double* partials;
+    unsigned* counter;
+    double* out;
+    D2 acc;
+    __device__ __forceinline__ bool active() const { return true; }
+    __device__ __forceinline__ void row(int64_t r, double v) {
+        const double t = __dadd_rn(b[r], -v);  // scale_vec(-1) then daxpy(1, b): fl(b + (-Ax))
+        const double res = dinv ? __dmul_rn(t, dinv[r]) : t;
+        d2_add_prod(acc, res, res);
+    }
+    __device__ __forceinline__ void finish() {
+        __shared__ D2 sh[32];
+        d2_grid_finish<1>(&acc, sh, partials, counter, out);
+    }
+};
+
+// SpMV epilogue of the odd half-step (solvers.cpp:676-679): bu_next = op(u_next);
+// v = beta*bu + (beta*beta)*v; v = bu_next + v
+// Also accumulates <v_new, r0>, the next even half-step's denominator (:628).
+struct EpiTfqmrV {
+    double* __restrict__ bu_next;
+    const double* __restrict__ dinv;
+    const double* __restrict__ bu;
+    double* __restrict__ v;
+    const double* __restrict__ r0;
+    double beta, beta2;
+    double* partials;
+    unsigned* counter;
+    double* out;
+    D2 acc;
+    __device__ __forceinline__ bool active() const { return true; }
+    __device__ __forceinline__ void row(int64_t r, double val) {
+        const double bn = dinv ? __dmul_rn(val, dinv[r]) : val;
+        bu_next[r] = bn;
+        const double vv = __dadd_rn(__dmul_rn(beta, bu[r]), __dmul_rn(beta2, v[r]));
+        const double vn = __dadd_rn(__dmul_rn(1.0, bn), vv);
+        v[r] = vn;
+        d2_add_prod(acc, vn, r0[r]);
+    }
+    __device__ __forceinline__ void finish() {
+        __shared__ D2 sh[32];
+        d2_grid_finish<1>(&acc, sh, partials, counter, out);
+    }
+};
+
+// even: u_next = u - alpha v (copy + daxpy); both: w -= alpha bu; d = u + scale d;
+// ||w||^2 and (odd) <w, r0>
+__global__ void __launch_bounds__(kMdNT) tfqmr_wd_kernel(int64_t n, int even, double alpha, double scale,
+                                                          const double* __restrict__ u, const double* __restrict__ v,
+                                                          double* __restrict__ u_next, const double* __restrict__ bu,
+                                                          double* __restrict__ w, double* __restrict__ d,
+                                                          const double* __restrict__ r0, double* partials,
+                                                          unsigned* counter, double* out) {
+    __shared__ D2 sh[32];
+    D2 acc[2] = {D2{0.0, 0.0}, D2{0.0, 0.0}};
+    const double ma = -alpha;
+    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
+        const double ui = u[i];
+        if (even) u_next[i] = __dadd_rn(__dmul_rn(ma, v[i]), ui);
+        const double wi = __dadd_rn(__dmul_rn(ma, bu[i]), w[i]);
+        w[i] = wi;
+        d[i] = __dadd_rn(__dmul_rn(1.0, ui), __dmul_rn(scale, d[i]));
+        d2_add_prod(acc[0], wi, wi);
+        if (!even) d2_add_prod(acc[1], wi, r0[i]);
+    }
+    d2_grid_finish<2>(acc, sh, partials, counter, out);
+}
+
+// x += eta d; (odd, after rho) u_next = w + beta u (copy(w) + daxpy(beta, u))
+__global__ void __launch_bounds__(kMdNT) tfqmr_xu_kernel(int64_t n, double eta, const double* __restrict__ d,
+                                                          double* __restrict__ x, int odd, double beta,
+                                                          const double* __restrict__ w, const double* __restrict__ u,
+                                                          double* __restrict__ u_next) {
+    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
+        x[i] = __dadd_rn(__dmul_rn(eta, d[i]), x[i]);
+        if (odd) u_next[i] = __dadd_rn(__dmul_rn(beta, u[i]), w[i]);
+    }
+}
+
+// FAST tfQMR (solvers.cpp:578-696): same recurrence and scalar expressions on the host, the
+// vector work fused into 2-3 kernels per half-step (+ the reference's SpMVs, two of them with
+// fused epilogues: the true residual and the v update).
+void tfqmr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    krysp_gpu_ctx* c = e.c;
+    const int64_t n = e.n;
+    DVec raw = e.vec(), r0 = e.vec(), w = e.vec(), u = e.vec(), un = e.vec(), v = e.vec(), d = e.vec();
+    DVec bu = e.vec(), bun = e.vec();
+    e.residual(b, x, raw);
+    e.precond(raw, r0);
+    const double norm_r0 = e.norm2(r0);
+    if (norm_r0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    const double* dinv = e.jacobi ? (const double*)e.inv : nullptr;
+    double* part = c->d_partials + 4 * kPartialCap;
+    unsigned* cnt = c->d_counters + 4;
+    double* d_scal = dev_alloc<double>(8, true, c->stream);
+    const unsigned g = grid_for(n, kMdNT, (int64_t)c->sm_count * fused_grid_mult());
+    auto d2h = [&](double* dst, size_t k) {
+        KG_CUDA(cudaMemcpyAsync(dst, d_scal, 8 * k, cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+    };
+    auto true_measure = [&]() {
+        spmv_fused(e, x, raw, EpiTrueRes{b, dinv, part, cnt, d_scal, D2{0.0, 0.0}});
+        double rr;
+        d2h(&rr, 1);
+        return std::sqrt(rr) / norm_r0;
+    };
+    std::exception_ptr err;
+    double measure = 1.0;
+    try {
+        e.copy(r0, w);
+        e.copy(r0, u);
+        spmv_fused(e, u, v, EpiScale{v, dinv});
+        e.copy(v, bu);
+        double tau = norm_r0, theta = 0.0, eta = 0.0;
+        double rho = e.dot(r0, r0), alpha = 0.0;
+        double next_denom = e.dot(v, r0);  // later fused into the v-update SpMV epilogue
+        for (int64_t m = (rep.mark(e.c->stream), 0); rep.iterations < cfg.max_iterations && !rep.converged; ++m) {
+            const bool even = (m % 2 == 0);
+            if (even) {
+                const double denom = next_denom;
+                if (vanishes(denom)) fail(KRYSP_BREAKDOWN, "tfqmr: <v, r_shadow> vanished");
+                alpha = rho / denom;
+                check_finite(alpha, "alpha");
+            } else {
+                spmv_fused(e, u, bu, EpiScale{bu, dinv});  // bu = op(u)
+            }
+            const double scale = (theta * theta * eta) / alpha;
+            check_finite(scale, "direction scale");
+            tfqmr_wd_kernel<<<g, kMdNT, 0, c->stream>>>(n, even ? 1 : 0, alpha, scale, u, v, un, bu, w, d, r0, part, cnt,
+                                                         d_scal);
+            KG_LAUNCH(c);
+            double red[2];
+            d2h(red, 2);
+            theta = std::sqrt(red[0]) / tau;
+            const double cc = 1.0 / std::sqrt(1.0 + theta * theta);
+            tau = tau * theta * cc;
+            eta = cc * cc * alpha;
+            check_finite(tau, "tau");
+            const double bound = tau * std::sqrt((double)(m + 2)) / norm_r0;
+            double beta = 0.0;
+            if (!even) {
+                const double rho_new = red[1];
+                if (vanishes(rho_new)) {  // after x += eta d, as the reference (x is updated first)
+                    tfqmr_xu_kernel<<<g, kMdNT, 0, c->stream>>>(n, eta, d, x, 0, 0.0, w, u, un);
+                    KG_LAUNCH(c);
+                    if (bound <= cfg.tolerance) {
+                        measure = true_measure();
+                        if (measure <= cfg.tolerance) {
+                            rep.push(measure);
+                            rep.converged = true;
+                            break;
+                        }
+                    }
+                    fail(KRYSP_BREAKDOWN, "tfqmr: rho vanished");
+                }
+                beta = rho_new / rho;
+            }
+            // x += eta d (+ odd: u_next = w + beta u, which needs beta: checked below as the
+            // reference does, after the true-residual test)
+            tfqmr_xu_kernel<<<g, kMdNT, 0, c->stream>>>(n, eta, d, x, even ? 0 : 1, beta, w, u, un);
+            KG_LAUNCH(c);
+            if (bound <= cfg.tolerance) {
+                measure = true_measure();
+                if (measure <= cfg.tolerance) {
+                    rep.push(measure);
+                    rep.converged = true;
+                    break;
+                }
+            }
+            if (!even) {
+                check_finite(beta, "beta");
+                rho = red[1];
+                spmv_fused(e, un, bun,
+                           EpiTfqmrV{bun, dinv, bu, v, r0, beta, beta * beta, part, cnt, d_scal + 4, D2{0.0, 0.0}});
+                std::swap(bu, bun);
+                double dn;
+                KG_CUDA(cudaMemcpyAsync(&dn, d_scal + 4, 8, cudaMemcpyDeviceToHost, c->stream));
+                stream_wait(c);
+                next_denom = dn;
+                measure = true_measure();
+                check_finite(measure, "residual measure");
+                rep.push(measure);
+                if (measure <= cfg.tolerance) rep.converged = true;
+            }
+            std::swap(u, un);
+        }
+    } catch (...) {
+        err = std::current_exception();
+    }
+    rep.end(c->stream);
+    stream_wait(c);
+    dev_free(d_scal);
+    rep.final_measure = measure;
+    if (err) std::rethrow_exception(err);
+}
+
+// ------------------------------------------------------------------ fused BiCGStab(l) kernels
+// y = D^-1 A x and <w, y> in one pass
+struct EpiScaleDot {
+    double* __restrict__ y;
+    const double* __restrict__ dinv;
+    const double* __restrict__ w;
+    double* partials;
+    unsigned* counter;
+    double* out;
+    D2 acc;
+    __device__ __forceinline__ bool active() const { return true; }
+    __device__ __forceinline__ void row(int64_t r, double v) {
+        if (dinv) v = __dmul_rn(v, dinv[r]);
+        y[r] = v;
+        d2_add_prod(acc, w[r], v);
+    }
+    __device__ __forceinline__ void finish() {
+        __shared__ D2 sh[32];
+        d2_grid_finish<1>(&acc, sh, partials, counter, out);
+    }
+};
+
+// u_i = r_i - beta u_i for i < k (axpby(1, rr[i], -beta, uu[i]), solvers.cpp:497-499)
+__global__ void __launch_bounds__(kMdNT) bl_beta_kernel(int64_t n, int k, double beta, double* const* __restrict__ rr,
+                                                         double* const* __restrict__ uu) {
+    const double mb = -beta;
+    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT)
+        for (int i = 0; i < k; ++i) uu[i][e] = __dadd_rn(__dmul_rn(1.0, rr[i][e]), __dmul_rn(mb, uu[i][e]));
+}
+
+// r_i -= alpha u_{i+1} (i < k), x += alpha u_0, ||r_0||^2 (solvers.cpp:507-513)
+__global__ void __launch_bounds__(kMdNT) bl_alpha_kernel(int64_t n, int k, double alpha, double* const* __restrict__ rr,
+                                                          double* const* __restrict__ uu, double* __restrict__ x,
+                                                          double* partials, unsigned* counter, double* out) {
+    __shared__ D2 sh[32];
+    D2 acc{0.0, 0.0};
+    const double ma = -alpha;
+    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
+        for (int i = 0; i < k; ++i) rr[i][e] = __dadd_rn(__dmul_rn(ma, uu[i + 1][e]), rr[i][e]);
+        x[e] = __dadd_rn(__dmul_rn(alpha, uu[0][e]), x[e]);
+        const double r0 = rr[0][e];
+        d2_add_prod(acc, r0, r0);
+    }
+    d2_grid_finish<1>(&acc, sh, partials, counter, out);
+}
+
+// one modified Gram-Schmidt step (solvers.cpp:528-537): r_j -= tau r_i (when r_i), then either
+// <r_j, r_next> (the next tau numerator) or sigma_j = <r_j, r_j> and <r_0, r_j>
+__global__ void __launch_bounds__(kMdNT) bl_mgs_kernel(int64_t n, double* __restrict__ rj, const double* __restrict__ ri,
+                                                        double tau, const double* __restrict__ rnext,
+                                                        const double* __restrict__ r0, double* partials,
+                                                        unsigned* counter, double* out) {
+    __shared__ D2 sh[32];
+    D2 acc[2] = {D2{0.0, 0.0}, D2{0.0, 0.0}};
+    const double mt = -tau;
+    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
+        double v = rj[e];
+        if (ri) {
+            v = __dadd_rn(__dmul_rn(mt, ri[e]), v);
+            rj[e] = v;
+        }
+        if (rnext) {
+            d2_add_prod(acc[0], v, rnext[e]);
+        } else {
+            d2_add_prod(acc[0], v, v);
+            d2_add_prod(acc[1], r0[e], v);
+        }
+    }
+    d2_grid_finish<2>(acc, sh, partials, counter, out);
+}
+
+// polynomial update (solvers.cpp:551-558) in the reference's daxpy order per element:
+//   x += g[1] r_0 (old r_0); r_0 -= gp[L] r_L; u_0 -= g[L] u_L;
+//   for j in 1..L-1: u_0 -= g[j] u_j; x += gpp[j] r_j; r_0 -= gp[j] r_j
+// then ||r_0||^2 and <r_0, r_shadow>
+__global__ void __launch_bounds__(kMdNT) bl_final_kernel(int64_t n, int L, const double* __restrict__ coef,
+                                                          double* const* __restrict__ rr, double* const* __restrict__ uu,
+                                                          double* __restrict__ x, const double* __restrict__ rs,
+                                                          double* partials, unsigned* counter, double* out) {
+    // coef: g[0..L], gp[0..L], gpp[0..L] (3 (L+1) doubles)
+    __shared__ double s_c[3 * 10];
+    __shared__ D2 sh[32];
+    for (int i = threadIdx.x; i < 3 * (L + 1); i += kMdNT) s_c[i] = coef[i];
+    __syncthreads();
+    const double* g = s_c;
+    const double* gp = s_c + (L + 1);
+    const double* gpp = s_c + 2 * (L + 1);
+    D2 acc[2] = {D2{0.0, 0.0}, D2{0.0, 0.0}};
+    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
+        const double r0o = rr[0][e];
+        double xe = __dadd_rn(__dmul_rn(g[1], r0o), x[e]);
+        double r0 = __dadd_rn(__dmul_rn(-gp[L], rr[L][e]), r0o);
+        double u0 = __dadd_rn(__dmul_rn(-g[L], uu[L][e]), uu[0][e]);
+        for (int j = 1; j < L; ++j) {
+            const double rj = rr[j][e];
+            u0 = __dadd_rn(__dmul_rn(-g[j], uu[j][e]), u0);
+            xe = __dadd_rn(__dmul_rn(gpp[j], rj), xe);
+            r0 = __dadd_rn(__dmul_rn(-gp[j], rj), r0);
+        }
+        x[e] = xe;
+        rr[0][e] = r0;
+        uu[0][e] = u0;
+        d2_add_prod(acc[0], r0, r0);
+        d2_add_prod(acc[1], r0, rs[e]);
+    }
+    d2_grid_finish<2>(acc, sh, partials, counter, out);
+}
+
+// FAST BiCGStab(l) (solvers.cpp:444-572): the reference's recurrences and host scalar
+// algebra, vector work fused (the i-loops of the BiCG part in one pass each, MGS steps with
+// their next dot, the polynomial update in one pass) and dots fused into the op() epilogues.
+void bicgstab_l_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    krysp_gpu_ctx* c = e.c;
+    const int64_t n = e.n, L = cfg.stab_l;
+    if (L > 9) fail(KRYSP_ERROR, "FAST BiCGStab(l) supports l <= 9 (use EXACT mode)");
+    DVec raw = e.vec(), rs = e.vec();
+    std::vector<DVec> rr, uu;
+    for (int64_t j = 0; j <= L; ++j) {
+        rr.emplace_back(e.vec());
+        uu.emplace_back(e.vec());
+    }
+    e.residual(b, x, raw);
+    e.precond(raw, rr[0]);
+    const double norm_r0 = e.norm2(rr[0]);
+    if (norm_r0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    e.copy(rr[0], rs);
+    const double* dinv = e.jacobi ? (const double*)e.inv : nullptr;
+    double* part = c->d_partials + 4 * kPartialCap;
+    unsigned* cnt = c->d_counters + 4;
+    double* d_scal = dev_alloc<double>(64, true, c->stream);
+    double** d_rr = reinterpret_cast<double**>(dev_alloc<char>(8 * 2 * (L + 1), false));
+    double** d_uu = d_rr + (L + 1);
+    {
+        std::vector<double*> hp;
+        for (auto& v : rr) hp.push_back(v);
+        for (auto& v : uu) hp.push_back(v);
+        KG_CUDA(cudaMemcpyAsync(d_rr, hp.data(), 8 * hp.size(), cudaMemcpyHostToDevice, c->stream));
+    }
+    const unsigned g = grid_for(n, kMdNT, (int64_t)c->sm_count * fused_grid_mult());
+    auto d2h = [&](double* dst, size_t k) {
+        KG_CUDA(cudaMemcpyAsync(dst, d_scal, 8 * k, cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+    };
+    std::exception_ptr err;
+    double measure = 1.0;
+    try {
+        double rho0 = 1.0, alpha = 0.0, omega = 1.0;
+        double next_rho1 = e.dot(rr[0], rs);
+        std::vector<double> sigma(L + 1), gp(L + 1), gg(L + 1), gpp(L + 1);
+        std::vector<double> tau((size_t)((L + 1) * (L + 1)), 0.0);
+        auto TAU = [&](int64_t i, int64_t j) -> double& { return tau[(size_t)(i * (L + 1) + j)]; };
+        for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
+            rho0 = -omega * rho0;
+            for (int64_t j = 0; j < L && !rep.converged; ++j) {
+                const double rho1 = next_rho1;
+                check_finite(rho1, "rho");
+                if (vanishes(rho0)) fail(KRYSP_BREAKDOWN, "bicgstab(l): rho vanished");
+                const double beta = alpha * rho1 / rho0;
+                check_finite(beta, "beta");
+                rho0 = rho1;
+                bl_beta_kernel<<<g, kMdNT, 0, c->stream>>>(n, (int)(j + 1), beta, d_rr, d_uu);
+                KG_LAUNCH(c);
+                spmv_fused(e, uu[j], uu[j + 1], EpiScaleDot{uu[j + 1], dinv, rs, part, cnt, d_scal, D2{0.0, 0.0}});
+                double gd;
+                d2h(&gd, 1);
+                if (vanishes(gd)) fail(KRYSP_BREAKDOWN, "bicgstab(l): <u, r_shadow> vanished");
+                alpha = rho0 / gd;
+                check_finite(alpha, "alpha");
+                bl_alpha_kernel<<<g, kMdNT, 0, c->stream>>>(n, (int)(j + 1), alpha, d_rr, d_uu, x, part, cnt, d_scal);
+                KG_LAUNCH(c);
+                spmv_fused(e, rr[j], rr[j + 1],
+                           EpiScaleDot{rr[j + 1], dinv, rs, part, cnt, d_scal + 1, D2{0.0, 0.0}});
+                double two[2];
+                d2h(two, 2);
+                next_rho1 = two[1];  // <rr[j+1], rs>: the next step's rho1
+                measure = std::sqrt(two[0]) / norm_r0;
+                check_finite(measure, "residual measure");
+                if (measure <= cfg.tolerance) rep.converged = true;
+            }
+            if (rep.converged) {
+                rep.push(measure);
+                break;
+            }
+            // modified Gram-Schmidt + back substitution (solvers.cpp:527-549)
+            for (int64_t j = 1; j <= L; ++j) {
+                double num = 0.0;
+                if (j > 1) num = e.dot(rr[j], rr[1]);
+                for (int64_t i = 1; i < j; ++i) {
+                    TAU(i, j) = num / sigma[i];
+                    const bool last = (i + 1 == j);
+                    bl_mgs_kernel<<<g, kMdNT, 0, c->stream>>>(n, rr[j], rr[i], TAU(i, j), last ? nullptr : (const double*)rr[i + 1],
+                                                              rr[0], part, cnt, d_scal);
+                    KG_LAUNCH(c);
+                    double two[2];
+                    d2h(two, last ? 2 : 1);
+                    if (!last) num = two[0];
+                    else {
+                        sigma[j] = two[0];
+                        gp[j] = two[1];
+                    }
+                }
+                if (j == 1) {
+                    bl_mgs_kernel<<<g, kMdNT, 0, c->stream>>>(n, rr[1], nullptr, 0.0, nullptr, rr[0], part, cnt, d_scal);
+                    KG_LAUNCH(c);
+                    double two[2];
+                    d2h(two, 2);
+                    sigma[1] = two[0];
+                    gp[1] = two[1];
+                }
+                if (vanishes(sigma[j])) fail(KRYSP_BREAKDOWN, "bicgstab(l): minimal-residual system singular");
+                gp[j] = gp[j] / sigma[j];
+            }
+            gg[L] = gp[L];
+            omega = gg[L];
+            for (int64_t j = L - 1; j >= 1; --j) {
+                double s = 0.0;
+                for (int64_t i = j + 1; i <= L; ++i) s += TAU(j, i) * gg[i];
+                gg[j] = gp[j] - s;
+            }
+            for (int64_t j = 1; j < L; ++j) {
+                double s = 0.0;
+                for (int64_t i = j + 1; i < L; ++i) s += TAU(j, i) * gg[i + 1];
+                gpp[j] = gg[j + 1] + s;
+            }
+            std::vector<double> coef;
+            coef.insert(coef.end(), gg.begin(), gg.end());
+            coef.insert(coef.end(), gp.begin(), gp.end());
+            coef.insert(coef.end(), gpp.begin(), gpp.end());
+            KG_CUDA(cudaMemcpyAsync(d_scal + 16, coef.data(), 8 * coef.size(), cudaMemcpyHostToDevice, c->stream));
+            bl_final_kernel<<<g, kMdNT, 0, c->stream>>>(n, (int)L, d_scal + 16, d_rr, d_uu, x, rs, part, cnt, d_scal);
+            KG_LAUNCH(c);
+            double two[2];
+            d2h(two, 2);
+            next_rho1 = two[1];
+            measure = std::sqrt(two[0]) / norm_r0;
+            check_finite(measure, "residual measure");
+            rep.push(measure);
+            if (measure <= cfg.tolerance) rep.converged = true;
+        }
+    } catch (...) {
+        err = std::current_exception();
+    }
+    rep.end(c->stream);
+    stream_wait(c);
+    dev_free(d_scal);
+    dev_free(d_rr);
+    rep.final_measure = measure;
+    if (err) std::rethrow_exception(err);
+}
+
+// FAST GCR(m): the reference recurrence (solvers.cpp:256-338) with the classical
+// Gram-Schmidt of the next direction done as one multi-dot pass + one multi-axpy pass, and
+// the (unchanging) <Ap_i, Ap_i> of the kept basis cached instead of recomputed.
+void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    krysp_gpu_ctx* c = e.c;
+    const int64_t n = e.n, m = cfg.restart;
+    if (m > 128) fail(KRYSP_ERROR, "FAST GCR supports restart <= 128 (use EXACT mode)");
+    DVec raw = e.vec(), r = e.vec(), w = e.vec();
+    e.residual(b, x, raw);
+    e.precond(raw, r);
+    const double norm_r0 = e.norm2(r);
+    if (norm_r0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    std::vector<DVec> P, AP;
+    std::vector<double> dd((size_t)m + 1);
+    const double** d_ptrs = reinterpret_cast<const double**>(dev_alloc<char>(8 * 2 * (m + 1), false));
+    double* d_scal = dev_alloc<double>(2 * (m + 2), true, c->stream);  // [0]: scalar out, [8..]: betas / nums
+    std::vector<const double*> hp((size_t)(2 * (m + 1)), nullptr);
+    auto slot = [&](std::vector<DVec>& v, int64_t j) -> DVec& {
+        while ((int64_t)v.size() <= j) v.emplace_back(e.vec());
+        return v[(size_t)j];
+    };
+    auto sync_ptrs = [&]() {
+        for (size_t i = 0; i < P.size(); ++i) hp[i] = P[i];
+        for (size_t i = 0; i < AP.size(); ++i) hp[(size_t)(m + 1) + i] = AP[i];
+        KG_CUDA(cudaMemcpyAsync(d_ptrs, hp.data(), 8 * hp.size(), cudaMemcpyHostToDevice, c->stream));
+    };
+    double* part = c->d_partials + 4 * kPartialCap;
+    unsigned* cnt = c->d_counters + 4;
+    const unsigned g = grid_for(n, kMdNT, (int64_t)c->sm_count * fused_grid_mult());
+    auto d2h = [&](double* dst, const double* src, size_t k) {
+        KG_CUDA(cudaMemcpyAsync(dst, src, 8 * k, cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+    };
+    const double* dinv = e.jacobi ? (const double*)e.inv : nullptr;
+    double measure = 1.0;
+    std::exception_ptr err;
+    for (int64_t j = 0; j <= std::min<int64_t>(m, cfg.max_iterations); ++j) {  // the basis, allocated once
+        slot(P, j);
+        slot(AP, j);
+    }
+    try {
+        for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
+            e.copy(r, slot(P, 0));
+            spmv_fused(e, slot(P, 0), slot(AP, 0), EpiScale{slot(AP, 0), dinv});  // op(p_0)
+            sync_ptrs();
+            dd[0] = e.dot(AP[0], AP[0]);
+            for (int64_t j = 0; j < m; ++j) {
+                const double d = dd[(size_t)j];
+                check_finite(d, "direction norm");
+                if (vanishes(d)) fail(KRYSP_BREAKDOWN, "gcr: direction norm vanished");
+                const double alpha = e.dot(r, AP[(size_t)j]) / d;
+                check_finite(alpha, "alpha");
+                gcr_xr_kernel<<<g, kMdNT, 0, c->stream>>>(n, alpha, P[(size_t)j], AP[(size_t)j], x, r, part, cnt, d_scal);
+                KG_LAUNCH(c);
+                double rr;
+                d2h(&rr, d_scal, 1);
+                measure = std::sqrt(rr) / norm_r0;
+                check_finite(measure, "residual measure");
+                rep.push(measure);
+                if (measure <= cfg.tolerance) {
+                    rep.converged = true;
+                    break;
+                }
+                if (rep.iterations >= cfg.max_iterations) break;
+                if (j + 1 == m) break;
+                spmv_fused(e, r, w, EpiScale{w, dinv});  // w = op(r)
+                const int k = (int)(j + 1);
+                std::vector<double> nums((size_t)k), betas((size_t)k);
+                for (int q0 = 0; q0 < k; q0 += kMdG) {
+                    multidot_kernel<<<g, kMdNT, 0, c->stream>>>(n, w, d_ptrs + (m + 1) + q0, std::min(kMdG, k - q0),
+                                                                part, cnt, d_scal + 8 + q0);
+                    KG_LAUNCH(c);
+                }
+                d2h(nums.data(), d_scal + 8, (size_t)k);
+                for (int i = 0; i < k; ++i) betas[(size_t)i] = nums[(size_t)i] / dd[(size_t)i];
+                KG_CUDA(cudaMemcpyAsync(d_scal + 8, betas.data(), 8 * (size_t)k, cudaMemcpyHostToDevice, c->stream));
+                DVec& pn = slot(P, j + 1);
+                DVec& apn = slot(AP, j + 1);
+                sync_ptrs();
+                gcr_next_kernel<<<g, kMdNT, 0, c->stream>>>(n, r, w, d_ptrs, d_ptrs + (m + 1), d_scal + 8, k, pn, apn,
+                                                            part, cnt, d_scal);
+                KG_LAUNCH(c);
+                d2h(&dd[(size_t)j + 1], d_scal, 1);
+            }
+        }
+    } catch (...) {
+        err = std::current_exception();
+    }
+    rep.end(c->stream);
+    stream_wait(c);
+    dev_free(d_ptrs);
+    dev_free(d_scal);
+    rep.final_measure = measure;
+    if (err) std::rethrow_exception(err);
 }
 
 }  // namespace
@@ -702,7 +1449,7 @@ struct PcgSession {
             hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
             if (trace) d_trace = dev_alloc<double>(4 * cfg.max_iterations, true, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
-            KG_CUDA(cudaStreamSynchronize(c->stream));
+            stream_wait(c);
             for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
             exec_chunk = capture(kChunk, false);
             exec_one = capture(1, false);
@@ -782,7 +1529,7 @@ struct PcgSession {
         krysp_gpu_ctx* c = e.c;
         int* h_done = reinterpret_cast<int*>(c->h_pinned + 8);
         KG_CUDA(cudaMemcpyAsync(h_done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        stream_wait(c);
         return *h_done != 0;
     }
 
@@ -821,7 +1568,7 @@ struct PcgSession {
     CgState state() {
         CgState h{};
         KG_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, e.c->stream));
-        KG_CUDA(cudaStreamSynchronize(e.c->stream));
+        stream_wait(e.c);
         return h;
     }
 
@@ -1094,7 +1841,7 @@ struct BicgstabSession {
             st = dev_alloc<BiState>(1, false);
             hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
-            KG_CUDA(cudaStreamSynchronize(c->stream));
+            stream_wait(c);
             exec_chunk = capture(kChunk);
             exec_one = capture(1);
         } catch (...) {
@@ -1159,7 +1906,7 @@ struct BicgstabSession {
     bool finished() {
         int* h_done = reinterpret_cast<int*>(e.c->h_pinned + 8);
         KG_CUDA(cudaMemcpyAsync(h_done, &st->done, sizeof(int), cudaMemcpyDeviceToHost, e.c->stream));
-        KG_CUDA(cudaStreamSynchronize(e.c->stream));
+        stream_wait(e.c);
         return *h_done != 0;
     }
 
@@ -1183,7 +1930,7 @@ struct BicgstabSession {
     void finish(Report& rep) {
         BiState h{};
         KG_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, e.c->stream));
-        KG_CUDA(cudaStreamSynchronize(e.c->stream));
+        stream_wait(e.c);
         rep.history.resize((size_t)h.iter);
         if (h.iter) KG_CUDA(cudaMemcpy(rep.history.data(), hist, 8 * (size_t)h.iter, cudaMemcpyDeviceToHost));
         rep.iterations = h.iter;
@@ -1262,10 +2009,19 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
             switch (method) {
                 case KRYSP_PCG: pcg(e, cfg, b, x, rep, h_trace != nullptr); break;
                 case KRYSP_CG_CLASSIC: cg_classic(e, cfg, b, x, rep); break;
-                case KRYSP_GCR: gcr(e, cfg, b, x, rep); break;
+                case KRYSP_GCR:
+                    if (cfg.mode == KRYSP_MODE_FAST) gcr_fast(e, cfg, b, x, rep);
+                    else gcr(e, cfg, b, x, rep);
+                    break;
                 case KRYSP_BICGSTAB: bicgstab(e, cfg, b, x, rep); break;
-                case KRYSP_BICGSTAB_L: bicgstab_l(e, cfg, b, x, rep); break;
-                case KRYSP_TFQMR: tfqmr(e, cfg, b, x, rep); break;
+                case KRYSP_BICGSTAB_L:
+                    if (cfg.mode == KRYSP_MODE_FAST) bicgstab_l_fast(e, cfg, b, x, rep);
+                    else bicgstab_l(e, cfg, b, x, rep);
+                    break;
+                case KRYSP_TFQMR:
+                    if (cfg.mode == KRYSP_MODE_FAST) tfqmr_fast(e, cfg, b, x, rep);
+                    else tfqmr(e, cfg, b, x, rep);
+                    break;
                 case KRYSP_BICGCR:
                     at.reset(transpose(A));
                     e.At = at.get();
@@ -1279,7 +2035,7 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
     KG_CUDA(cudaEventRecord(ev1, stream));
     KG_CUDA(cudaEventSynchronize(ev1));
     float ms = 0.f;
-    KG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    KG_CUDA(cudaEventElapsedTime(&ms, rep.loop_start ? rep.loop_start : ev0, rep.loop_end ? rep.loop_end : ev1));
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     out->converged = rep.converged ? 1 : 0;
