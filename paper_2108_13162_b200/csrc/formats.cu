@@ -196,10 +196,22 @@ __global__ void overflow_count(const int32_t* __restrict__ rp, int32_t n_rows, i
     }
 }
 
+// Row-length histogram: short lengths counted in a per-block shared histogram first (a
+// stencil puts every row in one bin — same-address global atomics would serialise in L2).
+constexpr int kHistSmem = 2048;
 __global__ void row_len_hist(const int32_t* __restrict__ rp, int32_t n_rows, int* hist) {
+    __shared__ int sh[kHistSmem];
+    for (int i = threadIdx.x; i < kHistSmem; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows;
-         r += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(hist + (rp[r + 1] - rp[r]), 1);
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int len = rp[r + 1] - rp[r];
+        if (len < kHistSmem) atomicAdd(sh + len, 1);
+        else atomicAdd(hist + len, 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHistSmem; i += blockDim.x)
+        if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
 // ell_to_csr (formats.cpp:155-182) / the ELL half of hyb_to_csr: per-row count of
