@@ -304,12 +304,13 @@ def run_ours(args, dist):
         import torch
         hb = torch.ones(n, dtype=torch.float64, pin_memory=True).numpy()
         hx0 = torch.zeros(n, dtype=torch.float64, pin_memory=True).numpy()
+        hsol = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
         e2e_cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0))
         its, secs, rep2 = 0, 0.0, None
         dist.barrier()
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()
-            rep2 = kg.solve_csr_host(ctx, hm, "pcg", hb, hx0, e2e_cfg, fmt=args.format)
+            rep2 = kg.solve_csr_host(ctx, hm, "pcg", hb, hx0, e2e_cfg, fmt=args.format, out=hsol)
             secs += time.perf_counter() - t0
             its += rep2.iterations
         secs = dist.max(secs)

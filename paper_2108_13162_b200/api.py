@@ -605,9 +605,10 @@ PcgSolver = DeviceSolver
 
 
 def solve_csr_host(ctx: Context, m: CsrMatrix, method: str, b, x0=None, cfg: Optional[SolverConfig] = None,
-                   fmt: str = "csr") -> SolveReport:
+                   fmt: str = "csr", out: Optional[np.ndarray] = None) -> SolveReport:
     """The whole reference call shape with a HOST CSR (krysp_gpu_solve_csr_host): upload,
-    convert, solve, download inside one C-ABI call."""
+    convert, solve, download inside one C-ABI call.  `out` (optional, e.g. pinned) receives
+    the solution."""
     cfg = cfg or SolverConfig()
     n = m.n_rows
     b = _f64(b)
@@ -615,7 +616,9 @@ def solve_csr_host(ctx: Context, m: CsrMatrix, method: str, b, x0=None, cfg: Opt
     cc = cfg.c()
     rep = _lib.Report()
     hist = np.zeros(max(cfg.max_iterations, 1))
-    sol = np.zeros(n)
+    sol = out if out is not None else np.zeros(n)
+    if sol.dtype != np.float64 or len(sol) != n or not sol.flags.c_contiguous:
+        raise _lib.DimensionMismatch("out must be a contiguous float64 array of n_rows")
     rp, ci, va = _i64(m.row_ptr), _i64(m.col_idx), _f64(m.values)  # keep alive across the call
     check(ctx.L.krysp_gpu_solve_csr_host(ctx.h, n, _p(rp), _p(ci), _p(va),
                                          FORMATS[fmt], METHODS[method], _p(b), _p(x0), C.byref(cc), C.byref(rep),

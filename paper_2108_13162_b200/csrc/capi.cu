@@ -15,6 +15,21 @@ namespace kg {
 
 thread_local std::string g_last_error;
 
+bool trace_enabled() {
+    static const bool on = std::getenv("KRYSP_TRACE") != nullptr;
+    return on;
+}
+
+void trace_lap(krysp_gpu_ctx* c, const char* where, const char* what) {
+    if (!trace_enabled()) return;
+    static thread_local auto t_prev = std::chrono::steady_clock::now();
+    if (c) cudaStreamSynchronize(c->stream);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[krysp trace] %-16s %-18s +%.4f s\n", where, what,
+            std::chrono::duration<double>(now - t_prev).count());
+    t_prev = now;
+}
+
 void fail(krysp_status code, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
@@ -409,21 +424,25 @@ krysp_status krysp_gpu_solve_host(const krysp_gpu_mat* m, int32_t method, const 
         set_dev(c);
         auto t0 = std::chrono::steady_clock::now();
         const int64_t n = m->n_rows;
+        trace_lap(c, "solve_host", "start");
         DVec b(n, c->stream), x(n, c->stream);
         if (n) {
             KG_CUDA(cudaMemcpyAsync(b, hb, 8 * n, cudaMemcpyHostToDevice, c->stream));
             KG_CUDA(cudaMemcpyAsync(x, hx0, 8 * n, cudaMemcpyHostToDevice, c->stream));
         }
+        trace_lap(c, "solve_host", "h2d b, x0");
         std::exception_ptr err;
         try {
             solve(m, method, b, x, *cfg, rep, h_hist, h_trace);
         } catch (...) {
             err = std::current_exception();
         }
+        trace_lap(c, "solve_host", "solve");
         if (!err && hx && n) {
             KG_CUDA(cudaMemcpyAsync(hx, x, 8 * n, cudaMemcpyDeviceToHost, c->stream));
             KG_CUDA(cudaStreamSynchronize(c->stream));
         }
+        trace_lap(c, "solve_host", "d2h x");
         rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (err) std::rethrow_exception(err);
     });
@@ -439,13 +458,23 @@ krysp_status krysp_gpu_solve_csr_host(krysp_gpu_ctx* c, int64_t n_rows, const in
         need(rep, "report");
         set_dev(c);
         auto t0 = std::chrono::steady_clock::now();
+        static const bool trace = std::getenv("KRYSP_TRACE") != nullptr;
+        auto lap = [&](const char* what) {
+            if (!trace) return;
+            KG_CUDA(cudaStreamSynchronize(c->stream));
+            fprintf(stderr, "[krysp trace] solve_csr_host %-10s %.3f s\n", what,
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        };
         krysp_gpu_mat* a = upload_csr(c, n_rows, n_rows, rp, ci, cv);
+        lap("upload");
         krysp_gpu_mat* m = a;
         std::exception_ptr err;
         try {
             if (format != KRYSP_FMT_CSR) m = convert(a, format, -1, INT64_MAX);
+            lap("convert");
             krysp_status st = krysp_gpu_solve_host(m, method, hb, hx0, cfg, rep, h_hist, hx, nullptr);
             if (st != KRYSP_OK) fail(st, "%s", g_last_error.c_str());
+            lap("solve");
         } catch (...) {
             err = std::current_exception();
         }
@@ -455,6 +484,7 @@ krysp_status krysp_gpu_solve_csr_host(krysp_gpu_ctx* c, int64_t n_rows, const in
         }
         mat_free_arrays(a);
         delete a;
+        lap("free");
         rep->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (err) std::rethrow_exception(err);
     });

@@ -341,6 +341,10 @@ inline void stream_wait(krysp_gpu_ctx* c) {
     if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "stream wait: %s", cudaGetErrorString(e));
 }
 
+// KRYSP_TRACE=1: host wall-clock laps of the big C-ABI calls (stderr)
+bool trace_enabled();
+void trace_lap(krysp_gpu_ctx* c, const char* where, const char* what);
+
 // ---------------------------------------------------------------- host-side internals
 void ctx_check_device(krysp_gpu_ctx* ctx);
 int64_t kernel_launches(krysp_gpu_ctx* ctx);

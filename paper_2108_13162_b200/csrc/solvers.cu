@@ -1427,6 +1427,7 @@ struct PcgSession {
         : e(A, cfg_), cfg(cfg_), n(A->n_rows), x(A->n_rows, A->ctx->stream), r(A->n_rows, A->ctx->stream),
           p(A->n_rows, A->ctx->stream), ap(A->n_rows, A->ctx->stream) {
         krysp_gpu_ctx* c = e.c;
+        trace_lap(c, "pcg_session", "engine+alloc");
         try {
             if (n) KG_CUDA(cudaMemcpyAsync(x, x0, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
             // solve_pcg setup, solvers.cpp:131-146
@@ -1450,10 +1451,11 @@ struct PcgSession {
             if (trace) d_trace = dev_alloc<double>(4 * cfg.max_iterations, true, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
             stream_wait(c);
+            trace_lap(c, "pcg_session", "setup kernels");
             for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
             exec_chunk = capture(kChunk, false);
             exec_one = capture(1, false);
-            exec_prof = capture(1, true);
+            trace_lap(c, "pcg_session", "graph capture");
         } catch (...) {
             release();
             throw;
@@ -1552,6 +1554,7 @@ struct PcgSession {
     // n single-iteration graphs with event nodes: mean seconds of [spmv, update, direction]
     void profile(int64_t iters, double out[3]) {
         krysp_gpu_ctx* c = e.c;
+        if (!exec_prof) exec_prof = capture(1, true);  // event-node graph, built on first use
         out[0] = out[1] = out[2] = 0.0;
         for (int64_t i = 0; i < iters; ++i) {
             KG_CUDA(cudaGraphLaunch(exec_prof, c->stream));
