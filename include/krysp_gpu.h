@@ -293,6 +293,10 @@ krysp_status krysp_gpu_dist_part_info(krysp_gpu_dist* d, int32_t part, int64_t i
 krysp_status krysp_gpu_dist_spmv(krysp_gpu_dist* d, const double* const* d_x, double* const* d_y);
 krysp_status krysp_gpu_dist_pcg_create(krysp_gpu_dist* d, const double* const* d_b, const double* const* d_x0,
                                        const krysp_solver_cfg* cfg);
+/* method KRYSP_PCG (= dist_pcg_create) or KRYSP_BICGSTAB (FAST arithmetic, solvers.cpp:357-438
+ * over the partitioned operator); the pcg_iterate/time/run/report/solution calls drive either */
+krysp_status krysp_gpu_dist_krylov_create(krysp_gpu_dist* d, int32_t method, const double* const* d_b,
+                                          const double* const* d_x0, const krysp_solver_cfg* cfg);
 krysp_status krysp_gpu_dist_pcg_iterate(krysp_gpu_dist* d, int64_t n_iterations);
 krysp_status krysp_gpu_dist_pcg_time(krysp_gpu_dist* d, int64_t n_iterations, double* seconds);
 krysp_status krysp_gpu_dist_pcg_run(krysp_gpu_dist* d, double* seconds);

@@ -110,12 +110,22 @@ int64_t band_owner(int64_t n, int64_t parts, int64_t c) {
     return s < parts - 1 ? s : parts - 1;
 }
 
+// Device state of a partitioned solve (P-CG fields, then the BiCGStab ones).  The *_loc /
+// red_loc fields are this part's partial reductions, allreduced into sigma / rho_new / red.
 struct DistCgState {
     double rho, rho_1, sigma_loc, sigma, alpha, beta, norm_r0, tol, rho_loc, rho_new;
     long long iter, max_it;
     int done, status;
+    double omega;
+    double red_loc[4], red[4];  // (sum, compensation) pairs
+    int half;
 };
-enum : int { kDsBreakdownSigma = 1, kDsNonFiniteSigma = 2, kDsNonFiniteAlpha = 3, kDsNonFiniteRho = 4 };
+enum : int {
+    kDsBreakdownSigma = 1, kDsNonFiniteSigma = 2, kDsNonFiniteAlpha = 3, kDsNonFiniteRho = 4,
+    // BiCGStab (solvers.cpp:379-428)
+    kDbNonFiniteDenom = 11, kDbBreakdownDenom, kDbNonFiniteMeasure, kDbBreakdownTT, kDbNonFiniteOmega,
+    kDbBreakdownOmega, kDbBreakdownRho, kDbNonFiniteBeta
+};
 
 struct DistPart {
     int id = 0;
@@ -130,8 +140,9 @@ struct DistPart {
     double* sendbuf = nullptr;
     int64_t n_send = 0;
     int64_t clean_a = 0, clean_b = 0;
-    // P-CG state
+    // solver state (P-CG: x r p ap inv; BiCGStab adds rh, sx (s, with ghost tail), t; v = ap)
     DVec x, r, p, ap, inv;  // p has n_local + n_ghost entries
+    DVec rh, sx, t;
     DistCgState* st = nullptr;
     double* hist = nullptr;
     double* part_slot = nullptr;  // 3 x kPartialCap partials (interior, lower, upper boundary)
@@ -317,12 +328,222 @@ __global__ void __launch_bounds__(kNT) dist_direction_kernel(int64_t n, double* 
     }
 }
 
-// in-process "allreduce": ordered sum over parts of the field at byte offset `src`
-__global__ void emu_allreduce(DistCgState** sts, int nparts, int src, int dst) {
-    if (threadIdx.x != 0) return;
+// in-process "allreduce": ordered sum over parts of `count` doubles at byte offset `src`
+__global__ void emu_allreduce(DistCgState** sts, int nparts, int src, int dst, int count) {
+    if (threadIdx.x >= count) return;
+    const int q = threadIdx.x;
     double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += *reinterpret_cast<const double*>(reinterpret_cast<const char*>(sts[p]) + src);
-    for (int p = 0; p < nparts; ++p) *reinterpret_cast<double*>(reinterpret_cast<char*>(sts[p]) + dst) = s;
+    for (int p = 0; p < nparts; ++p)
+        s += reinterpret_cast<const double*>(reinterpret_cast<const char*>(sts[p]) + src)[q];
+    for (int p = 0; p < nparts; ++p) reinterpret_cast<double*>(reinterpret_cast<char*>(sts[p]) + dst)[q] = s;
+}
+
+// ------------------------------------------------------------------ partitioned BiCGStab
+__device__ __forceinline__ void db_fail(DistCgState* st, int code) {
+    st->status = code;
+    st->done = 1;
+}
+__device__ __forceinline__ double red_val(const DistCgState* st, int q) { return st->red[2 * q] + st->red[2 * q + 1]; }
+
+// SpMV epilogue: y = D^-1 (A x); compensated partials of <w0, y> (w0 null: <y, y>) and <w1, y>
+template <int NACC>
+struct EpiBiPart {
+    double* __restrict__ y;
+    const double* __restrict__ dinv;
+    const double* __restrict__ w0;
+    const double* __restrict__ w1;
+    double* partials;
+    const DistCgState* st;
+    D2 a0, a1;
+    __device__ __forceinline__ bool active() const { return *(volatile const int*)&st->done == 0; }
+    __device__ __forceinline__ void row(int64_t r, double v) {
+        if (dinv) v = __dmul_rn(v, dinv[r]);
+        y[r] = v;
+        d2_add_prod(a0, w0 ? w0[r] : v, v);
+        if (NACC == 2) d2_add_prod(a1, w1[r], v);
+    }
+    __device__ __forceinline__ void finish() {
+        __shared__ D2 sh[32];
+        const D2 b0 = block_d2_dyn(a0, sh);
+        const D2 b1 = NACC == 2 ? block_d2_dyn(a1, sh) : D2{0.0, 0.0};
+        if (threadIdx.x == 0) {
+            double* q = partials + 4 * blockIdx.x;
+            q[0] = b0.s;
+            q[1] = b0.c;
+            q[2] = b1.s;
+            q[3] = b1.c;
+        }
+    }
+};
+
+// merge the 4-double partial records of up to three launches into red_loc (one block)
+__global__ void sum_d2_partials(DistCgState* st, const double* a, int na, const double* b, int nb, const double* c,
+                                int nc) {
+    if (*(volatile int*)&st->done) return;
+    __shared__ D2 sh[32];
+    D2 t0{0.0, 0.0}, t1{0.0, 0.0};
+    auto take = [&](const double* p, int n) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            t0 = d2_merge(t0, D2{p[4 * i], p[4 * i + 1]});
+            t1 = d2_merge(t1, D2{p[4 * i + 2], p[4 * i + 3]});
+        }
+    };
+    take(a, na);
+    take(b, nb);
+    take(c, nc);
+    t0 = block_d2_dyn(t0, sh);
+    t1 = block_d2_dyn(t1, sh);
+    if (threadIdx.x == 0) {
+        st->red_loc[0] = t0.s;
+        st->red_loc[1] = t0.c;
+        st->red_loc[2] = t1.s;
+        st->red_loc[3] = t1.c;
+    }
+}
+
+__global__ void db_alpha_kernel(DistCgState* st) {  // solvers.cpp:379-385
+    if (st->done) return;
+    const double denom = red_val(st, 0);
+    if (!isfinite(denom)) return db_fail(st, kDbNonFiniteDenom);
+    if (fabs(denom) < 1e-300) return db_fail(st, kDbBreakdownDenom);
+    st->alpha = st->rho / denom;
+    if (!isfinite(st->alpha)) db_fail(st, kDsNonFiniteAlpha);
+}
+
+// s = r - alpha v and ||s||^2 (solvers.cpp:387-389)
+__global__ void __launch_bounds__(kNT) db_s_kernel(int64_t n, double* __restrict__ s, const double* __restrict__ r,
+                                                    const double* __restrict__ v, DistCgState* st, double* partials,
+                                                    unsigned* counter) {
+    if (*(volatile int*)&st->done) return;
+    __shared__ D2 sh[32];
+    const double ma = -st->alpha;
+    D2 acc{0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+        const double si = __dadd_rn(__dmul_rn(ma, v[i]), r[i]);
+        s[i] = si;
+        d2_add_prod(acc, si, si);
+    }
+    const D2 b = block_d2_dyn(acc, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = b.s;
+        partials[2 * blockIdx.x + 1] = b.c;
+    }
+    if (last_block(counter)) {
+        const D2 t = reduce_d2_partials(partials, gridDim.x, sh);
+        if (threadIdx.x == 0) {
+            st->red_loc[0] = t.s;
+            st->red_loc[1] = t.c;
+            *counter = 0;
+        }
+    }
+}
+
+__global__ void db_half_kernel(DistCgState* st, double* history) {  // solvers.cpp:389-397
+    if (st->done) return;
+    const double measure = sqrt(red_val(st, 0)) / st->norm_r0;
+    if (!isfinite(measure)) return db_fail(st, kDbNonFiniteMeasure);
+    if (measure <= st->tol) {
+        history[st->iter] = measure;
+        st->iter += 1;
+        st->half = 1;
+        st->done = 1;
+    }
+}
+
+__global__ void db_omega_kernel(DistCgState* st) {  // solvers.cpp:400-408
+    if (st->done) return;
+    const double tt = red_val(st, 0), ts = red_val(st, 1);
+    if (fabs(tt) < 1e-300) return db_fail(st, kDbBreakdownTT);
+    st->omega = ts / tt;
+    if (!isfinite(st->omega)) return db_fail(st, kDbNonFiniteOmega);
+    if (fabs(st->omega) < 1e-300) db_fail(st, kDbBreakdownOmega);
+}
+
+// x += alpha p; x += omega s; r = s - omega t; ||r||^2, <r^, r> (solvers.cpp:410-415)
+__global__ void __launch_bounds__(kNT) db_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                         const double* __restrict__ p, const double* __restrict__ s,
+                                                         const double* __restrict__ t, const double* __restrict__ rh,
+                                                         DistCgState* st, double* partials, unsigned* counter) {
+    const int done = *(volatile int*)&st->done, half = *(volatile int*)&st->half;
+    if (done && !half) return;
+    const double alpha = st->alpha;
+    if (half) {  // converged at the half step: x += alpha p only
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT)
+            x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        if (last_block(counter) && threadIdx.x == 0) {
+            *counter = 0;
+            st->half = 0;
+        }
+        return;
+    }
+    __shared__ D2 sh[32];
+    const double om = st->omega, mom = -om;
+    D2 a0{0.0, 0.0}, a1{0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+        const double si = s[i];
+        x[i] = __dadd_rn(__dmul_rn(om, si), __dadd_rn(__dmul_rn(alpha, p[i]), x[i]));
+        const double ri = __dadd_rn(__dmul_rn(mom, t[i]), si);
+        r[i] = ri;
+        d2_add_prod(a0, ri, ri);
+        d2_add_prod(a1, rh[i], ri);
+    }
+    const D2 b0 = block_d2_dyn(a0, sh);
+    const D2 b1 = block_d2_dyn(a1, sh);
+    if (threadIdx.x == 0) {
+        double* q = partials + 4 * blockIdx.x;
+        q[0] = b0.s;
+        q[1] = b0.c;
+        q[2] = b1.s;
+        q[3] = b1.c;
+    }
+    if (last_block(counter)) {
+        D2 t0{0.0, 0.0}, t1{0.0, 0.0};
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+            const double* q = partials + 4 * i;
+            t0 = d2_merge(t0, D2{__ldcg(q), __ldcg(q + 1)});
+            t1 = d2_merge(t1, D2{__ldcg(q + 2), __ldcg(q + 3)});
+        }
+        t0 = block_d2_dyn(t0, sh);
+        t1 = block_d2_dyn(t1, sh);
+        if (threadIdx.x == 0) {
+            st->red_loc[0] = t0.s;
+            st->red_loc[1] = t0.c;
+            st->red_loc[2] = t1.s;
+            st->red_loc[3] = t1.c;
+            *counter = 0;
+        }
+    }
+}
+
+__global__ void db_converge_kernel(DistCgState* st, double* history) {  // solvers.cpp:415-432
+    if (st->done) return;
+    const double measure = sqrt(red_val(st, 0)) / st->norm_r0;
+    if (!isfinite(measure)) return db_fail(st, kDbNonFiniteMeasure);
+    const long long it = st->iter;
+    history[it] = measure;
+    st->iter = it + 1;
+    if (measure <= st->tol) {
+        st->done = 1;
+        return;
+    }
+    const double rho_new = red_val(st, 1);
+    if (fabs(rho_new) < 1e-300) return db_fail(st, kDbBreakdownRho);
+    const double beta = (rho_new / st->rho) * (st->alpha / st->omega);
+    if (!isfinite(beta)) return db_fail(st, kDbNonFiniteBeta);
+    st->beta = beta;
+    st->rho = rho_new;
+    if (it + 1 >= st->max_it) st->done = 1;
+}
+
+// p = r + beta (p - omega v) (solvers.cpp:430-431)
+__global__ void __launch_bounds__(kNT) db_p_kernel(int64_t n, double* __restrict__ p, const double* __restrict__ r,
+                                                    const double* __restrict__ v, const DistCgState* st) {
+    if (*(volatile const int*)&st->done) return;
+    const double mom = -st->omega, beta = st->beta;
+    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+        const double pi = __dadd_rn(__dmul_rn(mom, v[i]), p[i]);
+        p[i] = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(beta, pi));
+    }
 }
 
 }  // namespace
@@ -338,8 +559,9 @@ struct krysp_gpu_dist {
     cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
     std::vector<kg::DistPart> parts;
     bool ready = false;
-    // P-CG
+    // Krylov solver (P-CG or BiCGStab)
     bool pcg = false;
+    int method = KRYSP_PCG;
     krysp_solver_cfg cfg{};
     kg::DistCgState** d_sts = nullptr;
     cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr;
@@ -609,15 +831,106 @@ double allreduce_host(krysp_gpu_dist* d, const std::vector<double*>& d_vals) {
     return v;
 }
 
-void device_allreduce(krysp_gpu_dist* d, size_t src, size_t dst, cudaStream_t s) {
+void device_allreduce(krysp_gpu_dist* d, size_t src, size_t dst, cudaStream_t s, int count = 1) {
     if (d->emulated()) {
-        emu_allreduce<<<1, 32, 0, s>>>(d->d_sts, d->nparts, (int)src, (int)dst);
+        emu_allreduce<<<1, 32, 0, s>>>(d->d_sts, d->nparts, (int)src, (int)dst, count);
         KG_LAUNCH(d->ctx);
         return;
     }
     DistCgState* st = d->parts[0].st;
-    KG_NCCL(NcclApi::get().AllReduce(reinterpret_cast<char*>(st) + src, reinterpret_cast<char*>(st) + dst, 1,
-                                     ncclDouble, ncclSum, d->comm, s));
+    KG_NCCL(NcclApi::get().AllReduce(reinterpret_cast<char*>(st) + src, reinterpret_cast<char*>(st) + dst,
+                                     (size_t)count, ncclDouble, ncclSum, d->comm, s));
+}
+
+// y = D^-1 A xe for every held part with the halo of xe overlapped with the interior rows;
+// EpiBiPart partials into the part's three slots, merged into red_loc, allreduced into red
+template <int NACC>
+void bi_spmv(krysp_gpu_dist* d, const std::vector<double*>& xe, const std::vector<double*>& ys,
+             const std::vector<const double*>& w0, const std::vector<const double*>& w1) {
+    krysp_gpu_ctx* c = d->ctx;
+    cudaStream_t s = c->stream;
+    const bool overlap = !d->emulated();
+    if (overlap) {
+        KG_CUDA(cudaEventRecord(d->ev_fork, s));
+        KG_CUDA(cudaStreamWaitEvent(d->cstream, d->ev_fork, 0));
+        halo(d, xe, d->cstream);
+        KG_CUDA(cudaEventRecord(d->ev_halo, d->cstream));
+    } else {
+        halo(d, xe, s);
+    }
+    const size_t np = d->parts.size();
+    std::vector<int64_t> ga(np), gb(np), gc(np);
+    auto epi = [&](size_t i, int64_t off, int slot) {
+        DistPart& P = d->parts[i];
+        return EpiBiPart<NACC>{ys[i] + off, d->cfg.preconditioner ? (const double*)P.inv + off : nullptr,
+                               w0[i] ? w0[i] + off : nullptr, w1[i] ? w1[i] + off : nullptr,
+                               P.part_slot + slot * kPartialCap, P.st, D2{0.0, 0.0}, D2{0.0, 0.0}};
+    };
+    for (size_t i = 0; i < np; ++i) {
+        DistPart& P = d->parts[i];
+        ga[i] = launch_rows(row_view(P.A, P.clean_a, P.clean_b), xe[i], epi(i, P.clean_a, 0), s);
+    }
+    if (overlap) KG_CUDA(cudaStreamWaitEvent(s, d->ev_halo, 0));
+    for (size_t i = 0; i < np; ++i) {
+        DistPart& P = d->parts[i];
+        gb[i] = launch_rows(row_view(P.A, 0, P.clean_a), xe[i], epi(i, 0, 1), s);
+        gc[i] = launch_rows(row_view(P.A, P.clean_b, P.n_local), xe[i], epi(i, P.clean_b, 2), s);
+        sum_d2_partials<<<1, kNT, 0, s>>>(P.st, P.part_slot, (int)ga[i], P.part_slot + kPartialCap, (int)gb[i],
+                                          P.part_slot + 2 * kPartialCap, (int)gc[i]);
+        KG_LAUNCH(c);
+    }
+    device_allreduce(d, offsetof(DistCgState, red_loc), offsetof(DistCgState, red), s, 2 * NACC);
+}
+
+// one distributed BiCGStab iteration (all held parts), enqueued on ctx->stream
+void dist_iteration_bicg(krysp_gpu_dist* d) {
+    krysp_gpu_ctx* c = d->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t before = c->launches;
+    const size_t np = d->parts.size();
+    std::vector<double*> ps, vs, ss, ts;
+    std::vector<const double*> rhs, sws, nul(np, nullptr);
+    for (auto& P : d->parts) {
+        ps.push_back(P.p);
+        vs.push_back(P.ap);
+        ss.push_back(P.sx);
+        ts.push_back(P.t);
+        rhs.push_back(P.rh);
+        sws.push_back(P.sx);
+    }
+    auto g_of = [&](const DistPart& P) { return grid_for(P.n_local, kNT, (int64_t)c->sm_count * 8); };
+    bi_spmv<1>(d, ps, vs, rhs, nul);  // v = op(p), <r^, v>
+    for (size_t i = 0; i < np; ++i) {
+        DistPart& P = d->parts[i];
+        db_alpha_kernel<<<1, 1, 0, s>>>(P.st);
+        KG_LAUNCH(c);
+        db_s_kernel<<<g_of(P), kNT, 0, s>>>(P.n_local, P.sx, P.r, P.ap, P.st, c->d_partials + (4 + (i % 4)) * kPartialCap,
+                                             c->d_counters + 4 + (i % 4));
+        KG_LAUNCH(c);
+    }
+    device_allreduce(d, offsetof(DistCgState, red_loc), offsetof(DistCgState, red), s, 2);
+    for (size_t i = 0; i < np; ++i) {
+        db_half_kernel<<<1, 1, 0, s>>>(d->parts[i].st, d->parts[i].hist);
+        KG_LAUNCH(c);
+    }
+    bi_spmv<2>(d, ss, ts, nul, sws);  // t = op(s), <t, t>, <t, s>
+    for (size_t i = 0; i < np; ++i) {
+        DistPart& P = d->parts[i];
+        db_omega_kernel<<<1, 1, 0, s>>>(P.st);
+        KG_LAUNCH(c);
+        db_update_kernel<<<g_of(P), kNT, 0, s>>>(P.n_local, P.x, P.r, P.p, P.sx, P.t, P.rh, P.st,
+                                                  c->d_partials + (4 + (i % 4)) * kPartialCap, c->d_counters + 4 + (i % 4));
+        KG_LAUNCH(c);
+    }
+    device_allreduce(d, offsetof(DistCgState, red_loc), offsetof(DistCgState, red), s, 4);
+    for (size_t i = 0; i < np; ++i) {
+        DistPart& P = d->parts[i];
+        db_converge_kernel<<<1, 1, 0, s>>>(P.st, P.hist);
+        KG_LAUNCH(c);
+        db_p_kernel<<<g_of(P), kNT, 0, s>>>(P.n_local, P.p, P.r, P.ap, P.st);
+        KG_LAUNCH(c);
+    }
+    d->kernels_per_iteration = (int)(c->launches - before);
 }
 
 // one distributed P-CG iteration (all held parts), enqueued on ctx->stream
@@ -684,7 +997,10 @@ cudaGraphExec_t capture(krysp_gpu_dist* d, int iters) {
     cudaGraphExec_t exec = nullptr;
     KG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     try {
-        for (int i = 0; i < iters; ++i) dist_iteration(d);
+        for (int i = 0; i < iters; ++i) {
+            if (d->method == KRYSP_BICGSTAB) dist_iteration_bicg(d);
+            else dist_iteration(d);
+        }
     } catch (...) {
         cudaStreamEndCapture(c->stream, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -713,20 +1029,29 @@ void pcg_release(krysp_gpu_dist* d) {
         P.p = DVec();
         P.ap = DVec();
         P.inv = DVec();
+        P.rh = DVec();
+        P.sx = DVec();
+        P.t = DVec();
     }
     d->pcg = false;
 }
 
-// setup of solve_pcg (solvers.cpp:131-146) on the partitioned system
-void pcg_create(krysp_gpu_dist* d, const double* const* bs, const double* const* x0s, const krysp_solver_cfg& cfg) {
+// Setup of solve_pcg (solvers.cpp:131-146) or solve_bicgstab (:357-374) on the partitioned
+// system: halo of x0, r = b - A x0 (BiCGStab: then r = D^-1 r), allreduced norms / rho.
+void krylov_create(krysp_gpu_dist* d, int method, const double* const* bs, const double* const* x0s,
+                   const krysp_solver_cfg& cfg) {
     if (!d->ready) fail(KRYSP_ERROR, "krysp_gpu_dist_setup must run before the solver");
-    if (cfg.mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "the partitioned P-CG runs in KRYSP_MODE_FAST");
+    if (method != KRYSP_PCG && method != KRYSP_BICGSTAB)
+        fail(KRYSP_ERROR, "the partitioned solver runs KRYSP_PCG or KRYSP_BICGSTAB");
+    if (cfg.mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "the partitioned solvers run in KRYSP_MODE_FAST");
     if (!(cfg.tolerance > 0.0) || cfg.max_iterations < 1) fail(KRYSP_ERROR, "solver config requires tolerance > 0, max_iterations >= 1");
     pcg_release(d);
+    d->method = method;
+    const bool bicg = method == KRYSP_BICGSTAB;
     krysp_gpu_ctx* c = d->ctx;
     cudaStream_t s = c->stream;
     d->cfg = cfg;
-    std::vector<double*> xs, rs, dots;
+    std::vector<double*> xs, dots;
     double* d_dot = dev_alloc<double>((int64_t)d->parts.size() * 2, true, s);
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
@@ -734,29 +1059,20 @@ void pcg_create(krysp_gpu_dist* d, const double* const* bs, const double* const*
         P.r = DVec(P.n_local, s);
         P.p = DVec(P.n_local + P.n_ghost, s);
         P.ap = DVec(P.n_local, s);
+        if (bicg) {
+            P.rh = DVec(P.n_local, s);
+            P.sx = DVec(P.n_local + P.n_ghost, s);
+            P.t = DVec(P.n_local, s);
+        }
         P.part_slot = dev_alloc<double>(3 * (int64_t)kPartialCap, true, s);
         P.hist = dev_alloc<double>(cfg.max_iterations, true, s);
         P.st = dev_alloc<DistCgState>(1, true, s);
         if (P.n_local) KG_CUDA(cudaMemcpyAsync(P.p, x0s[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, s));
         if (P.n_local) KG_CUDA(cudaMemcpyAsync(P.x, x0s[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, s));
         xs.push_back(P.p);
+        dots.push_back(d_dot + 2 * i);
     }
-    // r = b - A x0 (spmv, scale(-1), daxpy(1, b)) with a halo of x0
-    halo(d, xs, s);
-    for (size_t i = 0; i < d->parts.size(); ++i) {
-        DistPart& P = d->parts[i];
-        krysp_policy pol{256, 1, 0, 0};
-        spmv_launch(P.A, P.p, P.r, pol, KRYSP_MODE_FAST, s);
-        k_scale(c, P.n_local, -1.0, P.r);
-        k_daxpy(c, P.n_local, 1.0, bs[i], P.r);
-        k_dot(c, P.n_local, P.r, P.r, 256, KRYSP_MODE_FAST, d_dot + 2 * i);
-    }
-    dots.clear();
-    for (size_t i = 0; i < d->parts.size(); ++i) dots.push_back(d_dot + 2 * i);
-    double norm_r0 = std::sqrt(allreduce_host(d, dots));
-    if (norm_r0 == 0.0) norm_r0 = 1.0;
-    // Jacobi (zero diagonal anywhere -> Breakdown on every rank)
-    std::vector<double*> zeros;
+    // Jacobi first (zero diagonal anywhere -> Breakdown on every rank)
     int* zr = dev_alloc<int>((int64_t)d->parts.size(), false);
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
@@ -785,22 +1101,50 @@ void pcg_create(krysp_gpu_dist* d, const double* const* bs, const double* const*
         dev_free(d_dot);
         fail(KRYSP_BREAKDOWN, "zero diagonal entry; Jacobi preconditioner undefined");
     }
-    // z = D^-1 r -> p, rho = <r, z>
+    // r = b - A x0 (spmv, scale(-1), daxpy(1, b)) with a halo of x0
+    halo(d, xs, s);
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
-        if (cfg.preconditioner) k_mul(c, P.n_local, P.r, P.inv, P.p);
-        else k_copy(c, P.n_local, P.r, P.p);
-        k_dot(c, P.n_local, P.r, P.p, 256, KRYSP_MODE_FAST, d_dot + 2 * i);
+        krysp_policy pol{256, 1, 0, 0};
+        spmv_launch(P.A, P.p, P.r, pol, KRYSP_MODE_FAST, s);
+        k_scale(c, P.n_local, -1.0, P.r);
+        k_daxpy(c, P.n_local, 1.0, bs[i], P.r);
+        if (bicg && cfg.preconditioner) k_scal_elementwise(c, P.n_local, P.r, P.inv);  // r = D^-1 raw
+        k_dot(c, P.n_local, P.r, P.r, 256, KRYSP_MODE_FAST, d_dot + 2 * i);
     }
-    const double rho = allreduce_host(d, dots);
-    dev_free(d_dot);
-    d->measure0 = rho / norm_r0;
+    double norm_r0 = std::sqrt(allreduce_host(d, dots));
     DistCgState h{};
+    double rho = 0.0;
+    if (!bicg) {
+        if (norm_r0 == 0.0) norm_r0 = 1.0;
+        // z = D^-1 r -> p, rho = <r, z>
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            DistPart& P = d->parts[i];
+            if (cfg.preconditioner) k_mul(c, P.n_local, P.r, P.inv, P.p);
+            else k_copy(c, P.n_local, P.r, P.p);
+            k_dot(c, P.n_local, P.r, P.p, 256, KRYSP_MODE_FAST, d_dot + 2 * i);
+        }
+        rho = allreduce_host(d, dots);
+        d->measure0 = rho / norm_r0;
+        d->done_at_setup = d->measure0 <= cfg.tolerance;
+    } else {
+        d->done_at_setup = norm_r0 == 0.0;
+        d->measure0 = 0.0;
+        if (!d->done_at_setup) {
+            for (size_t i = 0; i < d->parts.size(); ++i) {  // r^ = r, p = r, rho = <r^, r>
+                DistPart& P = d->parts[i];
+                k_copy(c, P.n_local, P.r, P.rh);
+                k_copy(c, P.n_local, P.r, P.p);
+                k_dot(c, P.n_local, P.rh, P.r, 256, KRYSP_MODE_FAST, d_dot + 2 * i);
+            }
+            rho = allreduce_host(d, dots);
+        }
+    }
+    dev_free(d_dot);
     h.rho = rho;
     h.norm_r0 = norm_r0;
     h.tol = cfg.tolerance;
     h.max_it = cfg.max_iterations;
-    d->done_at_setup = d->measure0 <= cfg.tolerance;
     h.done = d->done_at_setup ? 1 : 0;
     std::vector<DistCgState*> sts;
     for (auto& P : d->parts) {
@@ -992,7 +1336,15 @@ krysp_status krysp_gpu_dist_pcg_create(krysp_gpu_dist* d, const double* const* d
                                        const krysp_solver_cfg* cfg) {
     return guard([&] {
         if (!d || !d_b || !d_x0 || !cfg) kg::fail(KRYSP_ERROR, "NULL argument");
-        kg::pcg_create(d, d_b, d_x0, *cfg);
+        kg::krylov_create(d, KRYSP_PCG, d_b, d_x0, *cfg);
+    });
+}
+
+krysp_status krysp_gpu_dist_krylov_create(krysp_gpu_dist* d, int32_t method, const double* const* d_b,
+                                          const double* const* d_x0, const krysp_solver_cfg* cfg) {
+    return guard([&] {
+        if (!d || !d_b || !d_x0 || !cfg) kg::fail(KRYSP_ERROR, "NULL argument");
+        kg::krylov_create(d, method, d_b, d_x0, *cfg);
     });
 }
 
@@ -1037,13 +1389,22 @@ krysp_status krysp_gpu_dist_pcg_report(krysp_gpu_dist* d, krysp_report* rep, dou
         if (h.iter) KG_CUDA(cudaMemcpy(hist.data(), d->parts[0].hist, 8 * (size_t)h.iter, cudaMemcpyDeviceToHost));
         rep->iterations = h.iter;
         rep->final_residual_measure = h.iter ? hist.back() : d->measure0;
-        rep->converged = rep->final_residual_measure <= d->cfg.tolerance;
+        rep->converged = rep->final_residual_measure <= d->cfg.tolerance ||
+                         (d->method == KRYSP_BICGSTAB && d->done_at_setup);
         if (h_hist && h.iter) std::memcpy(h_hist, hist.data(), 8 * (size_t)h.iter);
         switch (h.status) {
             case kg::kDsBreakdownSigma: kg::fail(KRYSP_BREAKDOWN, "pcg: <p, Ap> vanished before convergence");
             case kg::kDsNonFiniteSigma: kg::fail(KRYSP_NON_FINITE, "sigma became non-finite");
             case kg::kDsNonFiniteAlpha: kg::fail(KRYSP_NON_FINITE, "alpha became non-finite");
             case kg::kDsNonFiniteRho: kg::fail(KRYSP_NON_FINITE, "rho became non-finite");
+            case kg::kDbNonFiniteDenom: kg::fail(KRYSP_NON_FINITE, "<r_hat, v> became non-finite");
+            case kg::kDbBreakdownDenom: kg::fail(KRYSP_BREAKDOWN, "bicgstab: <r_hat, v> vanished");
+            case kg::kDbNonFiniteMeasure: kg::fail(KRYSP_NON_FINITE, "residual measure became non-finite");
+            case kg::kDbBreakdownTT: kg::fail(KRYSP_BREAKDOWN, "bicgstab: <t, t> vanished");
+            case kg::kDbNonFiniteOmega: kg::fail(KRYSP_NON_FINITE, "omega became non-finite");
+            case kg::kDbBreakdownOmega: kg::fail(KRYSP_BREAKDOWN, "bicgstab: omega vanished");
+            case kg::kDbBreakdownRho: kg::fail(KRYSP_BREAKDOWN, "bicgstab: <r_hat, r> vanished");
+            case kg::kDbNonFiniteBeta: kg::fail(KRYSP_NON_FINITE, "beta became non-finite");
             default: break;
         }
     });

@@ -103,13 +103,24 @@ class DistSystem:
         check(self.L.krysp_gpu_dist_spmv(self.h, self._ptrs(xs), self._ptrs(ys)))
         return ys
 
-    # --- P-CG -------------------------------------------------------------------
+    # --- P-CG / BiCGStab --------------------------------------------------------
     def pcg_create(self, bs: Sequence[DeviceArray], x0s: Sequence[DeviceArray], cfg: Optional[SolverConfig] = None):
         cfg = cfg or SolverConfig(mode="fast")
         self.cfg = cfg
         cc = cfg.c()
         self._keep = (bs, x0s)
         check(self.L.krysp_gpu_dist_pcg_create(self.h, self._ptrs(bs), self._ptrs(x0s), C.byref(cc)))
+
+    def krylov_create(self, method: str, bs: Sequence[DeviceArray], x0s: Sequence[DeviceArray],
+                      cfg: Optional[SolverConfig] = None):
+        """method "pcg" or "bicgstab"; then drive with pcg_iterate/time/run/report/solution."""
+        from .api import METHODS
+        cfg = cfg or SolverConfig(mode="fast")
+        self.cfg = cfg
+        cc = cfg.c()
+        self._keep = (bs, x0s)
+        check(self.L.krysp_gpu_dist_krylov_create(self.h, C.c_int32(METHODS[method]), self._ptrs(bs),
+                                                  self._ptrs(x0s), C.byref(cc)))
 
     def pcg_iterate(self, n: int):
         check(self.L.krysp_gpu_dist_pcg_iterate(self.h, I64(n)))

@@ -98,3 +98,58 @@ def test_nccl_single_rank(ctx, golden):
     assert abs(rep.iterations - c["iterations"]) <= 1
     assert abs(rep.final_residual_measure - c["final_residual_measure"]) <= 1e-10
     D.close()
+
+
+def _true_measure(m, x):
+    import scipy.sparse as sp
+    S = sp.csr_matrix((m.values, m.col_idx, m.row_ptr), shape=(m.n_rows, m.n_cols))
+    dinv = 1.0 / S.diagonal()
+    b = np.ones(m.n_rows)
+    return np.linalg.norm(dinv * (b - S @ x)) / np.linalg.norm(dinv * b)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("key", ["convdiff2d_100_bicgstab", "fem27_20_bicgstab", "fem27_40_bicgstab"])
+def test_dist_bicgstab_parity(ctx, port, golden, P, key):
+    c = golden["configs"][key]
+    D = DistSystem.emulated(ctx, P)
+    D.generate(c["kind"], c["n"], 0.5)
+    D.setup()
+    N = D.part_info(P - 1)["hi"]
+    bs = [ctx.to_device(np.ones(len(v))) for v in split(np.ones(N), N, P)]
+    x0 = [ctx.to_device(np.zeros(len(v))) for v in split(np.ones(N), N, P)]
+    D.krylov_create("bicgstab", bs, x0, kg.SolverConfig(mode="fast"))
+    D.pcg_run()
+    rep = D.pcg_report()
+    assert rep.converged and rep.final_residual_measure <= 1e-6
+    # order-sensitive: inside the oracle's own cross-policy spread
+    assert abs(rep.iterations - c["iterations"]) <= max(2, 0.2 * c["iterations"])
+    x = np.concatenate([D.pcg_solution(p) for p in range(P)])
+    assert _true_measure(port.generate(c["kind"], c["n"], pe=0.5), x) <= 1e-5
+
+
+def test_dist_bicgstab_trivial_rhs(ctx):
+    D = DistSystem.emulated(ctx, 2)
+    D.generate("convdiff2d", 20, 0.5)
+    D.setup()
+    N = 400
+    zs = [ctx.to_device(np.zeros(len(v))) for v in split(np.ones(N), N, 2)]
+    D.krylov_create("bicgstab", zs, zs, kg.SolverConfig(mode="fast"))
+    D.pcg_run()
+    rep = D.pcg_report()
+    assert rep.converged and rep.iterations == 0
+
+
+def test_nccl_single_rank_bicgstab(ctx, golden):
+    c = golden["configs"]["convdiff2d_100_bicgstab"]
+    D = DistSystem(ctx, 1, 0, nccl_unique_id())
+    D.generate("convdiff2d", 100, 0.5)
+    D.setup()
+    N = 100 ** 2
+    D.krylov_create("bicgstab", [ctx.to_device(np.ones(N))], [ctx.to_device(np.zeros(N))],
+                    kg.SolverConfig(mode="fast"))
+    D.pcg_run()
+    rep = D.pcg_report()
+    assert rep.converged
+    assert abs(rep.iterations - c["iterations"]) <= max(2, 0.2 * c["iterations"])
+    D.close()
