@@ -369,6 +369,14 @@ def run_ours_dist(args, dist):
     # finish the solve for the parity check (same problem as the single-GPU golden)
     D.pcg_run()
     fin = D.pcg_report()
+    # partitioned BiCGStab on the same bands (bounded: it converges in ~700 iterations)
+    bi_steps = min(args.steps, 100)
+    D.krylov_create("bicgstab", [b], [x0], kg.SolverConfig(mode="fast", tolerance=1e-6, max_iterations=30000))
+    D.pcg_time(args.warmup)
+    dist.barrier()
+    t_bi = dist.max(D.pcg_time(bi_steps))
+    bi_ran = D.pcg_report().iterations
+    bi_kpi = D.kernels_per_iteration
     # e2e: a whole partitioned solve from pinned host b / x0 to the host solution
     import torch
     hb = torch.ones(n_loc, dtype=torch.float64, pin_memory=True).numpy()
@@ -400,6 +408,12 @@ def run_ours_dist(args, dist):
                          "achieved": B_iter_gpu / t_it / 1e9, "peak": bw_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": B_iter_gpu / t_it / 1e9 / bw_peak, "traffic": None},
             "gpu_launches": kpi * args.steps, "clocks": ck,
+            "bicgstab": {"value": bi_steps / t_bi, "unit": "iterations/s", "iterations_timed": bi_steps,
+                         "converged_early": bi_ran < args.warmup + bi_steps, "kernels_per_iteration": bi_kpi,
+                         "frac": (2 * spmv_bytes(N, N, nnz_total) + 136 * N) / dist.world / (t_bi / bi_steps) / 1e9
+                                 / bw_peak,
+                         "what": "row-partitioned FAST BiCGStab (2 halo-overlapped SpMVs, 3 NCCL allreduces "
+                                 "/ iteration, CUDA graphs), CUDA events, max over ranks"},
             "e2e": {"value": e2e_rep.iterations / e2e_s, "unit": "iterations/s",
                     "h2d_bytes_per_step": int(hb.nbytes + hx0.nbytes), "d2h_bytes_per_step": int(sol.nbytes),
                     "what": "krysp_gpu_dist_pcg_create/run/solution from pinned host b, x0 to the host solution "

@@ -303,6 +303,15 @@ krysp_status krysp_gpu_dist_pcg_run(krysp_gpu_dist* d, double* seconds);
 krysp_status krysp_gpu_dist_pcg_report(krysp_gpu_dist* d, krysp_report* report, double* h_history);
 krysp_status krysp_gpu_dist_pcg_solution(krysp_gpu_dist* d, int32_t part, double* d_x);
 int32_t krysp_gpu_dist_kernels_per_iteration(const krysp_gpu_dist* d);
+/* Any host-driven recurrence (PCG, CG_CLASSIC, GCR, BICGSTAB, BICGSTAB_L, TFQMR; not BICGCR)
+ * over the partition, solve_* semantics (solvers.hpp:54-87) per held band: d_x holds x0 on
+ * entry and the band of the solution on return.  KRYSP_MODE_EXACT replays the reference's
+ * floating-point sequence for cfg->policy over the GLOBAL row order (dot chunks straddling
+ * bands are folded from the gathered products), so history and solution are bit-identical
+ * to the single-domain reference solve for every part count; FAST uses compensated dots. */
+krysp_status krysp_gpu_dist_solve(krysp_gpu_dist* d, int32_t method, const double* const* d_b,
+                                  double* const* d_x, const krysp_solver_cfg* cfg, krysp_report* report,
+                                  double* h_history);
 krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d);
 
 /* ------------------------------------------------------------------ autotune.hpp:40-64 */

@@ -138,7 +138,7 @@ EXPORTS = [
     "krysp_gpu_dist_generate", "krysp_gpu_dist_set_csr", "krysp_gpu_dist_setup", "krysp_gpu_dist_part_info",
     "krysp_gpu_dist_spmv", "krysp_gpu_dist_pcg_create", "krysp_gpu_dist_krylov_create", "krysp_gpu_dist_pcg_iterate", "krysp_gpu_dist_pcg_time",
     "krysp_gpu_dist_pcg_run", "krysp_gpu_dist_pcg_report", "krysp_gpu_dist_pcg_solution",
-    "krysp_gpu_dist_kernels_per_iteration", "krysp_gpu_dist_destroy",
+    "krysp_gpu_dist_kernels_per_iteration", "krysp_gpu_dist_solve", "krysp_gpu_dist_destroy",
 ]
 
 _lib = None

@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(32 * kExactWarps)
         __syncwarp();
     }
     if (c0 + lane < n_chunks) partials[c0 + lane] = acc;
+    if (!out) return;  // partials only (k_chunk_partials)
     __threadfence();  // every lane wrote a partial (last_block fences thread 0 only)
     if (last_block(counter)) {
         if (w == 0) {
@@ -243,6 +244,17 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
         dot_fast_kernel<kNT><<<g, kNT, 0, c->stream>>>(n, x, y, c->d_partials, c->d_counters, d_out);
         KG_LAUNCH(c);
     }
+}
+
+// the reference's per-chunk partial sums (kernels.cpp:74-78) of n elements, without the fold
+void k_chunk_partials(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, double* partials) {
+    if (n <= 0) return;
+    if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
+    const int64_t n_chunks = (n + bs - 1) / bs;
+    const int64_t per_block = 32 * kExactWarps;
+    dot_exact_kernel<<<(unsigned)((n_chunks + per_block - 1) / per_block), 32 * kExactWarps, 0, c->stream>>>(
+        n, x, y, (int)bs, n_chunks, partials, nullptr, nullptr);
+    KG_LAUNCH(c);
 }
 
 double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode) {

@@ -26,6 +26,7 @@
 #include <cub/cub.cuh>
 #include <numeric>
 
+#include "engine.cuh"
 #include "spmv_kernels.cuh"
 
 namespace kg {
@@ -1173,6 +1174,222 @@ bool pcg_done(krysp_gpu_dist* d) {
     return v != 0;
 }
 
+// ------------------------------------------------------------------ partitioned engine
+// Every host-driven recurrence of solvers.cu (P-CG, CG-classic, GCR, BiCGStab, BiCGStab(l),
+// tfQMR) over the band partition.  The engine's vectors are the held bands concatenated in
+// part order (one band per rank under NCCL; all bands, i.e. the global vector, in emulation),
+// so every elementwise kernel is row-local and bit-identical to the single-domain one.  The
+// operator adds the halo; the dots are where the partition shows:
+//  * EXACT: the reference's chunk sums and left-to-right fold (kernels.cpp:66-84) over the
+//    GLOBAL row order.  Chunks of block_size rows straddle band boundaries, so every rank
+//    ships the products of its partial head/tail chunks and the sums of its whole chunks
+//    (one allgather); every rank then folds the same sequence — bit-identical to the
+//    single-domain EXACT dot, hence to the reference, for any P.
+//  * FAST: the compensated local dot, then an NCCL sum.
+
+// gathered dot record of one band: [head products | whole-chunk sums | tail products]
+struct DotLayout {
+    int64_t lo, hi, first, last;  // first / last: the band's whole-chunk range [first, last)
+    int64_t head() const { return first - lo; }
+    int64_t whole() const { return (last - first); }
+    int64_t tail() const { return hi - last; }
+};
+
+DotLayout dot_layout(int64_t lo, int64_t hi, int64_t bs) {
+    DotLayout L{lo, hi, 0, 0};
+    L.first = std::min(hi, (lo + bs - 1) / bs * bs);
+    L.last = std::max(L.first, hi / bs * bs);
+    return L;
+}
+
+__global__ void dot_fragments_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t head,
+                                     int64_t tail_off, int64_t tail, double* __restrict__ rec_head,
+                                     double* __restrict__ rec_tail) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < head + tail; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < head) rec_head[i] = __dmul_rn(x[i], y[i]);
+        else rec_tail[i - head] = __dmul_rn(x[tail_off + i - head], y[tail_off + i - head]);
+    }
+}
+
+// one warp: the reference fold over all ranks' records in global row order.  bands: 2P
+// int64 (lo, hi); each record starts at rank * cap.
+__global__ void dot_fold_kernel(const double* __restrict__ G, int64_t cap, const int64_t* __restrict__ bands, int P,
+                                int64_t bs, int64_t N, double* out) {
+    const int lane = threadIdx.x;
+    double total = 0.0, chunk = 0.0;
+    for (int r = 0; r < P; ++r) {
+        const int64_t lo = bands[2 * r], hi = bands[2 * r + 1];
+        const int64_t first = min(hi, (lo + bs - 1) / bs * bs);
+        const int64_t last = max(first, hi / bs * bs);
+        const double* rec = G + (int64_t)r * cap;
+        const int64_t H = first - lo, F = (last - first) / bs, T = hi - last;
+        // head products: rows lo .. first-1 (continue the chunk opened by the previous band)
+        for (int64_t i = 0; i < H; ++i) {
+            chunk = __dadd_rn(chunk, __ldcg(rec + i));
+            const int64_t g = lo + i + 1;
+            if (g % bs == 0 || g == N) {
+                total = __dadd_rn(total, chunk);
+                chunk = 0.0;
+            }
+        }
+        // whole chunks, folded left to right (warp-prefetched)
+        for (int64_t b0 = 0; b0 < F; b0 += 32) {
+            const double v = (b0 + lane < F) ? __ldcg(rec + H + b0 + lane) : 0.0;
+            const int cnt = (int)(F - b0 < 32 ? F - b0 : 32);
+            for (int q = 0; q < cnt; ++q) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, q));
+        }
+        // tail products: rows last .. hi-1 (a chunk the next band may continue)
+        for (int64_t i = 0; i < T; ++i) {
+            chunk = __dadd_rn(chunk, __ldcg(rec + H + F + i));
+            const int64_t g = last + i + 1;
+            if (g % bs == 0 || g == N) {
+                total = __dadd_rn(total, chunk);
+                chunk = 0.0;
+            }
+        }
+    }
+    if (lane == 0) *out = total;
+}
+
+struct DistEngine : Engine {
+    krysp_gpu_dist* d;
+    std::vector<int64_t> off;  // offset of each held band in the engine vectors
+    std::vector<DVec> xe;      // per held band: n_local + n_ghost
+    // EXACT NCCL dots
+    int64_t cap = 0;
+    double* rec = nullptr;
+    double* gathered = nullptr;
+    int64_t* d_bands = nullptr;
+    double* part_dots = nullptr;  // FAST: one per held band
+    int64_t N = 0;
+
+    static int64_t held_rows(krysp_gpu_dist* d) {
+        int64_t s = 0;
+        for (auto& P : d->parts) s += P.n_local;
+        return s;
+    }
+
+    DistEngine(krysp_gpu_dist* d_, const krysp_solver_cfg& cfg) : Engine(d_->ctx, held_rows(d_), cfg), d(d_) {
+        int64_t o = 0;
+        for (auto& P : d->parts) {
+            off.push_back(o);
+            o += P.n_local;
+            xe.emplace_back(P.n_local + P.n_ghost, c->stream);
+        }
+        N = d->parts[0].n_global;
+        if ((int64_t)d->parts.size() > kScalarCap) fail(KRYSP_ERROR, "too many held bands");
+        part_dots = dev_alloc<double>(d->parts.size(), true, c->stream);
+        if (d->nparts > 1 && mode == KRYSP_MODE_EXACT) {
+            const int64_t bs = pol.block_size;
+            std::vector<int64_t> bands(2 * (size_t)d->nparts);
+            int64_t max_whole = 0;
+            for (int p = 0; p < d->nparts; ++p) {
+                band_rows(N, d->nparts, p, &bands[2 * p], &bands[2 * p + 1]);
+                max_whole = std::max(max_whole, dot_layout(bands[2 * p], bands[2 * p + 1], bs).whole() / bs);
+            }
+            cap = 2 * bs + max_whole;
+            rec = dev_alloc<double>(cap, true, c->stream);
+            gathered = dev_alloc<double>(cap * d->nparts, true, c->stream);
+            d_bands = dev_alloc<int64_t>(2 * d->nparts, false);
+            KG_CUDA(cudaMemcpyAsync(d_bands, bands.data(), 8 * bands.size(), cudaMemcpyHostToDevice, c->stream));
+        }
+        if (cfg.preconditioner) make_dist_jacobi();
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    ~DistEngine() override {
+        if (c && c->stream) cudaStreamSynchronize(c->stream);
+        dev_free(rec);
+        dev_free(gathered);
+        dev_free(d_bands);
+        dev_free(part_dots);
+    }
+
+    bool distributed() const { return !d->emulated() && d->nparts > 1; }
+
+    // a zero diagonal anywhere stops every rank with the same (global, smallest) row
+    void make_dist_jacobi() {
+        jacobi = true;
+        inv = DVec(n, c->stream);
+        int* zr = dev_alloc<int>(d->parts.size(), false);
+        std::vector<int> big(d->parts.size(), INT32_MAX), hz(d->parts.size());
+        KG_CUDA(cudaMemcpyAsync(zr, big.data(), 4 * big.size(), cudaMemcpyHostToDevice, c->stream));
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            DistPart& P = d->parts[i];
+            k_diagonal(P.A, inv + off[i]);
+            k_invert_diag(c, P.n_local, inv + off[i], zr + i);
+        }
+        KG_CUDA(cudaMemcpyAsync(hz.data(), zr, 4 * hz.size(), cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+        dev_free(zr);
+        double bad = (double)INT64_MAX;
+        for (size_t i = 0; i < d->parts.size(); ++i)
+            if (hz[i] != INT32_MAX) bad = std::min(bad, (double)(d->parts[i].lo + hz[i]));
+        if (distributed()) {
+            c->h_pinned[0] = bad;
+            KG_CUDA(cudaMemcpyAsync(c->d_scalars, c->h_pinned, 8, cudaMemcpyHostToDevice, c->stream));
+            KG_NCCL(NcclApi::get().AllReduce(c->d_scalars, c->d_scalars, 1, ncclDouble, ncclMin, d->comm, c->stream));
+            KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
+            stream_wait(c);
+            bad = c->h_pinned[0];
+        }
+        if (bad < (double)INT64_MAX)
+            fail(KRYSP_BREAKDOWN, "zero diagonal entry at row %lld; Jacobi preconditioner undefined", (long long)bad);
+    }
+
+    void spmv(const double* x, double* y) override {
+        std::vector<double*> xs;
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            DistPart& P = d->parts[i];
+            if (P.n_local)
+                KG_CUDA(cudaMemcpyAsync(xe[i], x + off[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, c->stream));
+            xs.push_back(xe[i]);
+        }
+        halo(d, xs, c->stream);
+        for (size_t i = 0; i < d->parts.size(); ++i)
+            spmv_launch(d->parts[i].A, xe[i], y + off[i], launch_pol(), mode, c->stream);
+    }
+
+    // bands in part order: every rank (or, emulated, every held band) contributes its record
+    double local_dot(const double* x, const double* y) override {
+        if (d->nparts == 1) return host_dot(c, n, x, y, pol.block_size, mode);
+        if (mode == KRYSP_MODE_EXACT) {
+            const int64_t bs = pol.block_size;
+            for (size_t i = 0; i < d->parts.size(); ++i) {
+                const DistPart& P = d->parts[i];
+                const DotLayout L = dot_layout(P.lo, P.hi, bs);
+                const int64_t H = L.head(), F = L.whole() / bs, T = L.tail();
+                double* r = d->emulated() ? gathered + (int64_t)P.id * cap : rec;
+                const double* xi = x + off[i];
+                const double* yi = y + off[i];
+                if (H + T) {
+                    dot_fragments_kernel<<<grid_for(H + T, kNT, 64), kNT, 0, c->stream>>>(xi, yi, H, L.last - P.lo, T,
+                                                                                      r, r + H + F);
+                    KG_LAUNCH(c);
+                }
+                k_chunk_partials(c, F * bs, xi + H, yi + H, bs, r + H);
+            }
+            if (!d->emulated())
+                KG_NCCL(NcclApi::get().AllGather(rec, gathered, (size_t)cap, ncclDouble, d->comm, c->stream));
+            dot_fold_kernel<<<1, 32, 0, c->stream>>>(gathered, cap, d_bands, d->nparts, bs, N, c->d_scalars);
+            KG_LAUNCH(c);
+            KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
+            stream_wait(c);
+            return c->h_pinned[0];
+        }
+        // FAST: per-band compensated dot, then the sum over bands (NCCL, or in part order)
+        for (size_t i = 0; i < d->parts.size(); ++i)
+            k_dot(c, d->parts[i].n_local, x + off[i], y + off[i], pol.block_size, mode, part_dots + i);
+        if (!d->emulated())
+            KG_NCCL(NcclApi::get().AllReduce(part_dots, part_dots, 1, ncclDouble, ncclSum, d->comm, c->stream));
+        const size_t k = d->emulated() ? d->parts.size() : 1;
+        KG_CUDA(cudaMemcpyAsync(c->h_pinned, part_dots, 8 * k, cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+        double s = 0.0;
+        for (size_t i = 0; i < k; ++i) s += c->h_pinned[i];
+        return s;
+    }
+};
+
 }  // namespace
 }  // namespace kg
 
@@ -1420,6 +1637,32 @@ krysp_status krysp_gpu_dist_pcg_solution(krysp_gpu_dist* d, int32_t part, double
 }
 
 int32_t krysp_gpu_dist_kernels_per_iteration(const krysp_gpu_dist* d) { return d ? d->kernels_per_iteration : 0; }
+
+krysp_status krysp_gpu_dist_solve(krysp_gpu_dist* d, int32_t method, const double* const* d_b, double* const* d_x,
+                                  const krysp_solver_cfg* cfg, krysp_report* report, double* h_history) {
+    return guard([&] {
+        if (!d || !d_b || !d_x || !cfg || !report) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (!d->ready) kg::fail(KRYSP_ERROR, "krysp_gpu_dist_setup must run first");
+        if (cfg->mode != KRYSP_MODE_EXACT && cfg->mode != KRYSP_MODE_FAST) kg::fail(KRYSP_ERROR, "unknown mode %d", cfg->mode);
+        if (method == KRYSP_BICGCR)
+            kg::fail(KRYSP_ERROR, "bicgcr needs the transposed operator (single-domain solve only)");
+        krysp_gpu_ctx* c = d->ctx;
+        kg::DistEngine e(d, *cfg);
+        kg::DVec b(e.n, c->stream), x(e.n, c->stream);
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            const int64_t nl = d->parts[i].n_local;
+            if (!nl) continue;
+            KG_CUDA(cudaMemcpyAsync(b + e.off[i], d_b[i], 8 * nl, cudaMemcpyDeviceToDevice, c->stream));
+            KG_CUDA(cudaMemcpyAsync(x + e.off[i], d_x[i], 8 * nl, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        kg::solve_on_engine(e, method, *cfg, b, x, report, h_history);
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            const int64_t nl = d->parts[i].n_local;
+            if (nl) KG_CUDA(cudaMemcpyAsync(d_x[i], x + e.off[i], 8 * nl, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
 
 krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d) {
     return guard([&] {

@@ -1,0 +1,121 @@
+// The operator/vector engine the host-driven Krylov recurrences run on (solvers.cu).
+//
+// One Engine = one linear system: the operator y = A x, the Jacobi inverse diagonal, the
+// reductions and the elementwise kernels, all stream-ordered on the context stream.  The
+// single-domain engine works on one device matrix; dist.cu derives a row-partitioned engine
+// (halo + per-band SpMV, distributed dots) so the same recurrences run unchanged over a
+// band-row partition.
+#pragma once
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "internal.cuh"
+
+namespace kg {
+
+struct Engine {
+    krysp_gpu_ctx* c;
+    const krysp_gpu_mat* A;
+    const krysp_gpu_mat* At = nullptr;  // bicgcr
+    krysp_policy pol;
+    int32_t mode;
+    int64_t n;
+    DVec inv;  // Jacobi inverse diagonal (empty when unpreconditioned)
+    bool jacobi = false;
+    DVec tmp;
+    bool auto_pol = false;  // FAST + library's kernel choice (load-balanced kernels for irregular rows)
+
+    Engine(const krysp_gpu_mat* A_, const krysp_solver_cfg& cfg)
+        : c(A_->ctx), A(A_), pol(cfg.policy), mode(cfg.mode), n(A_->n_rows), tmp(A_->n_rows, A_->ctx->stream) {
+        if (pol.block_size == 0) {
+            if (mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "auto policy (block_size 0) requires FAST mode");
+            krysp_gpu_autotune_policy(A, &pol);
+            auto_pol = true;
+        }
+        check_policy(pol);
+        if (cfg.preconditioner) make_jacobi();
+    }
+    virtual ~Engine() = default;
+
+    DVec vec() { return DVec(n, c->stream); }
+
+    // maybe_jacobi / make_jacobi, solvers.cpp:54-59, 102-113
+    void make_jacobi() {
+        jacobi = true;
+        inv = DVec(n, c->stream);
+        k_diagonal(A, inv);
+        int* zr = dev_alloc<int>(1, false);
+        int big = INT32_MAX;
+        KG_CUDA(cudaMemcpyAsync(zr, &big, sizeof big, cudaMemcpyHostToDevice, c->stream));
+        k_invert_diag(c, n, inv, zr);
+        int hz;
+        KG_CUDA(cudaMemcpyAsync(&hz, zr, sizeof hz, cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+        dev_free(zr);
+        if (hz != INT32_MAX) fail(KRYSP_BREAKDOWN, "zero diagonal entry at row %d; Jacobi preconditioner undefined", hz);
+    }
+
+    krysp_policy launch_pol() const { return auto_pol ? krysp_policy{0, 0, 0, 0} : pol; }
+    void spmv(const krysp_gpu_mat* M, const double* x, double* y) { spmv_launch(M, x, y, launch_pol(), mode, c->stream); }
+    // y = A x of the system (virtual: the partitioned engine adds the halo exchange)
+    virtual void spmv(const double* x, double* y) { spmv(A, x, y); }
+    // apply_precond solvers.cpp:46-52: z = copy(r), then z *= inv
+    void precond(const double* r, double* z) {
+        if (jacobi) k_mul(c, n, r, inv, z);  // fl(r*inv): the same single rounding as copy + scal
+        else k_copy(c, n, r, z);
+    }
+    void op(const double* in, double* out) {
+        spmv(in, tmp);
+        precond(tmp, out);
+    }
+    void op_t(const double* in, double* out) {
+        spmv(At, in, tmp);
+        precond(tmp, out);
+    }
+    // initial_residual solvers.cpp:62-68
+    void residual(const double* b, const double* x, double* r) {
+        spmv(x, r);
+        k_scale(c, n, -1.0, r);
+        k_daxpy(c, n, 1.0, b, r);
+    }
+    // <x, y> of the system's vectors, returned on the host (virtual: distributed dots)
+    virtual double local_dot(const double* x, const double* y) {
+        return host_dot(c, n, x, y, pol.block_size, mode);
+    }
+    double dot(const double* x, const double* y) {
+        static const bool trace = std::getenv("KRYSP_TRACE") != nullptr;
+        if (!trace) return local_dot(x, y);
+        auto t0 = std::chrono::steady_clock::now();
+        const double v = local_dot(x, y);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 5.0) fprintf(stderr, "[krysp trace] dot wait %.2f ms (n=%lld)\n", ms, (long long)n);
+        return v;
+    }
+    double norm2(const double* x) { return std::sqrt(dot(x, x)); }
+    void daxpy(double a, const double* x, double* y) { k_daxpy(c, n, a, x, y); }
+    void axpby(double a, const double* x, double b, double* y) { k_axpby(c, n, a, x, b, y); }
+    void copy(const double* s, double* d) { k_copy(c, n, s, d); }
+
+protected:
+    // engine over an operator supplied by a derived class (A stays NULL); the derived class
+    // fills inv / jacobi
+    Engine(krysp_gpu_ctx* ctx, int64_t n_, const krysp_solver_cfg& cfg)
+        : c(ctx), A(nullptr), pol(cfg.policy), mode(cfg.mode), n(n_), tmp(n_, ctx->stream) {
+        if (pol.block_size == 0) {
+            if (mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "auto policy (block_size 0) requires FAST mode");
+            auto_pol = true;
+        } else {
+            check_policy(pol);
+        }
+    }
+};
+
+// The host-driven recurrences (pcg, cg_classic, gcr, bicgstab, bicgstab_l, tfqmr; FAST mode
+// uses the fused GCR / BiCGStab(l) / tfQMR variants) on an engine; report as krysp_report.
+void solve_on_engine(Engine& e, int32_t method, const krysp_solver_cfg& cfg, const double* b, double* x,
+                     krysp_report* out, double* h_history);
+
+}  // namespace kg

@@ -388,6 +388,7 @@ void k_mul(krysp_gpu_ctx* c, int64_t n, const double* a, const double* b, double
 // Device-side dot into d_out (no sync).  EXACT: chunk + fold (policy.block_size).
 void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode,
            double* d_out);
+void k_chunk_partials(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, double* partials);
 double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs,
                 int32_t mode);
 void k_diagonal(const krysp_gpu_mat* m, double* d);

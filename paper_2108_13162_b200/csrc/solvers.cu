@@ -16,6 +16,7 @@
 #include <functional>
 #include <memory>
 
+#include "engine.cuh"
 #include "spmv_kernels.cuh"
 
 namespace kg {
@@ -29,85 +30,6 @@ bool vanishes(double v) { return std::fabs(v) < kBreakdownEps; }
 void check_finite(double v, const char* what) {
     if (!std::isfinite(v)) fail(KRYSP_NON_FINITE, "%s became non-finite", what);
 }
-
-// ------------------------------------------------------------------ engine
-struct Engine {
-    krysp_gpu_ctx* c;
-    const krysp_gpu_mat* A;
-    const krysp_gpu_mat* At = nullptr;  // bicgcr
-    krysp_policy pol;
-    int32_t mode;
-    int64_t n;
-    DVec inv;  // Jacobi inverse diagonal (empty when unpreconditioned)
-    bool jacobi = false;
-    DVec tmp;
-
-    Engine(const krysp_gpu_mat* A_, const krysp_solver_cfg& cfg)
-        : c(A_->ctx), A(A_), pol(cfg.policy), mode(cfg.mode), n(A_->n_rows), tmp(A_->n_rows, A_->ctx->stream) {
-        if (pol.block_size == 0) {
-            if (mode != KRYSP_MODE_FAST) fail(KRYSP_ERROR, "auto policy (block_size 0) requires FAST mode");
-            krysp_gpu_autotune_policy(A, &pol);
-            auto_pol = true;
-        }
-        check_policy(pol);
-        if (cfg.preconditioner) make_jacobi();
-    }
-
-    DVec vec() { return DVec(n, c->stream); }
-
-    // maybe_jacobi / make_jacobi, solvers.cpp:54-59, 102-113
-    void make_jacobi() {
-        jacobi = true;
-        inv = DVec(n, c->stream);
-        k_diagonal(A, inv);
-        int* zr = dev_alloc<int>(1, false);
-        int big = INT32_MAX;
-        KG_CUDA(cudaMemcpyAsync(zr, &big, sizeof big, cudaMemcpyHostToDevice, c->stream));
-        k_invert_diag(c, n, inv, zr);
-        int hz;
-        KG_CUDA(cudaMemcpyAsync(&hz, zr, sizeof hz, cudaMemcpyDeviceToHost, c->stream));
-        stream_wait(c);
-        dev_free(zr);
-        if (hz != INT32_MAX) fail(KRYSP_BREAKDOWN, "zero diagonal entry at row %d; Jacobi preconditioner undefined", hz);
-    }
-
-    bool auto_pol = false;  // FAST + library's kernel choice (load-balanced kernels for irregular rows)
-    krysp_policy launch_pol() const { return auto_pol ? krysp_policy{0, 0, 0, 0} : pol; }
-    void spmv(const krysp_gpu_mat* M, const double* x, double* y) { spmv_launch(M, x, y, launch_pol(), mode, c->stream); }
-    void spmv(const double* x, double* y) { spmv(A, x, y); }
-    // apply_precond solvers.cpp:46-52: z = copy(r), then z *= inv
-    void precond(const double* r, double* z) {
-        if (jacobi) k_mul(c, n, r, inv, z);  // fl(r*inv): the same single rounding as copy + scal
-        else k_copy(c, n, r, z);
-    }
-    void op(const double* in, double* out) {
-        spmv(in, tmp);
-        precond(tmp, out);
-    }
-    void op_t(const double* in, double* out) {
-        spmv(At, in, tmp);
-        precond(tmp, out);
-    }
-    // initial_residual solvers.cpp:62-68
-    void residual(const double* b, const double* x, double* r) {
-        spmv(x, r);
-        k_scale(c, n, -1.0, r);
-        k_daxpy(c, n, 1.0, b, r);
-    }
-    double dot(const double* x, const double* y) {
-        static const bool trace = std::getenv("KRYSP_TRACE") != nullptr;
-        if (!trace) return host_dot(c, n, x, y, pol.block_size, mode);
-        auto t0 = std::chrono::steady_clock::now();
-        const double v = host_dot(c, n, x, y, pol.block_size, mode);
-        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        if (ms > 5.0) fprintf(stderr, "[krysp trace] dot wait %.2f ms (n=%lld)\n", ms, (long long)n);
-        return v;
-    }
-    double norm2(const double* x) { return std::sqrt(dot(x, x)); }
-    void daxpy(double a, const double* x, double* y) { k_daxpy(c, n, a, x, y); }
-    void axpby(double a, const double* x, double b, double* y) { k_axpby(c, n, a, x, b, y); }
-    void copy(const double* s, double* d) { k_copy(c, n, s, d); }
-};
 
 struct Report {
     bool converged = false;
@@ -2048,6 +1970,62 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
     if (h_history && !rep.history.empty())
         std::memcpy(h_history, rep.history.data(), sizeof(double) * std::min<size_t>(rep.history.size(), (size_t)cfg.max_iterations));
     if (h_trace && !rep.trace.empty()) std::memcpy(h_trace, rep.trace.data(), sizeof(double) * rep.trace.size());
+    out->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (err) std::rethrow_exception(err);
+}
+
+void solve_on_engine(Engine& e, int32_t method, const krysp_solver_cfg& cfg, const double* b, double* x,
+                     krysp_report* out, double* h_history) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!(cfg.tolerance > 0.0) || cfg.max_iterations < 1 || cfg.restart < 1 || cfg.stab_l < 1)
+        fail(KRYSP_ERROR, "solver config requires tolerance > 0, max_iterations >= 1, restart >= 1, stab_l >= 1");
+    if (method < KRYSP_PCG || method > KRYSP_BICGCR) fail(KRYSP_ERROR, "unknown method %d", method);
+    const bool fused_ok = e.A != nullptr && cfg.mode == KRYSP_MODE_FAST;  // fused kernels need the one matrix
+    cudaStream_t stream = e.c->stream;
+    Report rep;
+    std::exception_ptr err;
+    cudaEvent_t ev0, ev1;
+    KG_CUDA(cudaEventCreate(&ev0));
+    KG_CUDA(cudaEventCreate(&ev1));
+    KG_CUDA(cudaEventRecord(ev0, stream));
+    try {
+        switch (method) {
+            case KRYSP_PCG: pcg(e, cfg, b, x, rep, false); break;
+            case KRYSP_CG_CLASSIC: cg_classic(e, cfg, b, x, rep); break;
+            case KRYSP_GCR:
+                if (fused_ok) gcr_fast(e, cfg, b, x, rep);
+                else gcr(e, cfg, b, x, rep);
+                break;
+            case KRYSP_BICGSTAB: bicgstab(e, cfg, b, x, rep); break;
+            case KRYSP_BICGSTAB_L:
+                if (fused_ok) bicgstab_l_fast(e, cfg, b, x, rep);
+                else bicgstab_l(e, cfg, b, x, rep);
+                break;
+            case KRYSP_TFQMR:
+                if (fused_ok) tfqmr_fast(e, cfg, b, x, rep);
+                else tfqmr(e, cfg, b, x, rep);
+                break;
+            case KRYSP_BICGCR:
+                if (!e.At) fail(KRYSP_ERROR, "bicgcr needs the transposed operator (single-domain solve only)");
+                bicgcr(e, cfg, b, x, rep);
+                break;
+        }
+    } catch (...) {
+        err = std::current_exception();
+    }
+    KG_CUDA(cudaEventRecord(ev1, stream));
+    KG_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    KG_CUDA(cudaEventElapsedTime(&ms, rep.loop_start ? rep.loop_start : ev0, rep.loop_end ? rep.loop_end : ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    out->converged = rep.converged ? 1 : 0;
+    out->iterations = rep.iterations;
+    out->final_residual_measure = rep.final_measure;
+    out->device_time = ms * 1e-3;
+    if (h_history && !rep.history.empty())
+        std::memcpy(h_history, rep.history.data(),
+                    sizeof(double) * std::min<size_t>(rep.history.size(), (size_t)cfg.max_iterations));
     out->wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (err) std::rethrow_exception(err);
 }

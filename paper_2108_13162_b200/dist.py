@@ -148,6 +148,30 @@ class DistSystem:
         check(self.L.krysp_gpu_dist_pcg_solution(self.h, C.c_int32(part), x.ptr))
         return x.to_host()
 
+    # --- any host-driven solver ----------------------------------------------------
+    def solve(self, method: str, bs: Sequence, x0s: Optional[Sequence] = None,
+              cfg: Optional[SolverConfig] = None):
+        """solve_<method> over the partition (krysp_gpu_dist_solve); bs / x0s: one host array
+        or DeviceArray per held part.  Returns (SolveReport, [solution band per held part])."""
+        from .api import METHODS
+        cfg = cfg or SolverConfig()
+        infos = [self.part_info(p) for p in self.parts]
+        dbs = [b if isinstance(b, DeviceArray) else self.ctx.to_device(np.asarray(b, np.float64)) for b in bs]
+        if x0s is None:
+            dxs = [self.ctx.to_device(np.zeros(i["n_local"])) for i in infos]
+        else:
+            dxs = [self.ctx.to_device(x.to_host() if isinstance(x, DeviceArray) else np.asarray(x, np.float64))
+                   for x in x0s]
+        rep = _lib.Report()
+        hist = np.zeros(max(cfg.max_iterations, 1))
+        cc = cfg.c()
+        check(self.L.krysp_gpu_dist_solve(self.h, C.c_int32(METHODS[method]), self._ptrs(dbs), self._ptrs(dxs),
+                                          C.byref(cc), C.byref(rep), _p(hist)))
+        it = int(rep.iterations)
+        sols = [x.to_host() for x in dxs]
+        return (SolveReport(bool(rep.converged), it, rep.final_residual_measure, hist[:it].copy(), rep.wall_time,
+                            np.concatenate(sols) if sols else np.empty(0), device_time=rep.device_time), sols)
+
     @property
     def kernels_per_iteration(self) -> int:
         self.L.krysp_gpu_dist_kernels_per_iteration.restype = C.c_int32

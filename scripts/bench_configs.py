@@ -40,6 +40,22 @@ def rate(A, method, its, stab_l=1, restart=50):
     return o.iterations / o.device_time, o.iterations
 
 
+def gcr_bytes(Bs, N, its, m=50):
+    """Average algorithmic bytes of one FAST GCR(m) iteration over `its` iterations
+    (solvers.cu gcr_fast): cycle start copy r->p0 + op(p0) + <Ap0,Ap0>; per direction j
+    (k = j+1 kept): <r,Ap_j>, x/r update, op(r), multi-dot over k Ap, next direction."""
+    tot = 0
+    for it in range(its):
+        j = it % m
+        if j == 0:
+            tot += 2 * 8 * N + Bs + 8 * N + 8 * N
+        k = j + 1
+        tot += 2 * 8 * N + 6 * 8 * N
+        if j + 1 < m:
+            tot += Bs + 8 * N + (k + 1) * 8 * N + (2 * k + 4) * 8 * N
+    return tot / max(its, 1)
+
+
 def c1(ctx, R):
     A = ctx.generate("poisson2d", 1000)
     b = np.ones(A.n_rows)
@@ -97,7 +113,7 @@ def c4(ctx, R):
         for method, its, k, V, sl in [("bicgstab", 20, 2, 17, 1), ("tfqmr", 10, 3, 30, 1),
                                       ("bicgstab_l", 4, 8, 60, 4), ("gcr", 20, 1, 12, 1)]:
             r, got = rate(H, method, its, stab_l=sl)
-            B = k * Bs + 8 * N * V
+            B = gcr_bytes(Bs, N, got) if method == "gcr" else k * Bs + 8 * N * V
             emit({"config": "C4", "format": f"hyb(w={hi['width']}, coo={hi['coo_nnz']})", "method": method,
                   "workload": "27-point fem27 320^3 (32.8M rows, 879M nnz)", "it_per_s": r, "iterations": got,
                   "bytes_per_iteration_est": B, "roofline_frac_est": B * r / 1e9 / PEAK})

@@ -153,3 +153,74 @@ def test_nccl_single_rank_bicgstab(ctx, golden):
     assert rep.converged
     assert abs(rep.iterations - c["iterations"]) <= max(2, 0.2 * c["iterations"])
     D.close()
+
+
+# ---------------------------------------------------------------- krysp_gpu_dist_solve
+EXACT_KEYS = ["lap3d7_30_pcg", "poisson2d_100_pcg", "convdiff2d_100_bicgstab", "fem27_20_gcr",
+              "fem27_20_bicgstab_l", "fem27_20_tfqmr", "fem27_20_bicgstab"]
+
+
+def _dist(ctx, P, kind, n, pe=0.5):
+    D = DistSystem.emulated(ctx, P)
+    D.generate(kind, n, pe)
+    D.setup()
+    N = D.part_info(P - 1)["hi"]
+    return D, N
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+@pytest.mark.parametrize("key", EXACT_KEYS)
+def test_dist_exact_bitwise(ctx, golden, P, key):
+    """EXACT over the partition == the reference bit for bit (golden iteration count and
+    final measure), history and solution identical to the single-domain EXACT solve."""
+    c = golden["configs"][key]
+    bs, tw = c["policy"]
+    cfg = kg.SolverConfig(policy=kg.ExecPolicy(bs, tw), stab_l=c["stab_l"], mode="exact")
+    D, N = _dist(ctx, P, c["kind"], c["n"])
+    rep, _ = D.solve(c["method"], split(np.ones(N), N, P), cfg=cfg)
+    assert rep.iterations == c["iterations"]
+    assert rep.final_residual_measure == c["final_residual_measure"]
+    single = kg.solve(ctx.generate(c["kind"], c["n"], pe=0.5), c["method"], np.ones(N), cfg=cfg)
+    np.testing.assert_array_equal(rep.residual_history, single.residual_history)
+    np.testing.assert_array_equal(rep.solution, single.solution)
+
+
+@pytest.mark.parametrize("bs", [32, 1024])
+@pytest.mark.parametrize("P", [5, 8])
+def test_dist_exact_chunks_straddle_many_bands(ctx, bs, P):
+    # 20x20 grid: bands of 50-80 rows, so one dot chunk spans several bands (bs = 1024) or a
+    # band holds head, whole chunks and tail (bs = 32)
+    cfg = kg.SolverConfig(policy=kg.ExecPolicy(bs, 4), mode="exact")
+    for method in ["pcg", "bicgstab", "cg_classic"]:
+        D, N = _dist(ctx, P, "convdiff2d" if method == "bicgstab" else "poisson2d", 20)
+        b = np.random.default_rng(7).uniform(0.5, 1.5, N)
+        x0 = np.random.default_rng(8).uniform(-0.1, 0.1, N)
+        rep, _ = D.solve(method, split(b, N, P), split(x0, N, P), cfg=cfg)
+        single = kg.solve(ctx.generate("convdiff2d" if method == "bicgstab" else "poisson2d", 20, pe=0.5),
+                          method, b, x0, cfg=cfg)
+        assert rep.iterations == single.iterations > 3
+        np.testing.assert_array_equal(rep.residual_history, single.residual_history)
+        np.testing.assert_array_equal(rep.solution, single.solution)
+
+
+@pytest.mark.parametrize("P", [1, 4])
+@pytest.mark.parametrize("method", ["pcg", "cg_classic", "gcr", "bicgstab", "bicgstab_l", "tfqmr"])
+def test_dist_fast_every_solver(ctx, port, golden, P, method):
+    key = {"pcg": "lap3d7_30_pcg", "cg_classic": "lap3d7_30_pcg", "gcr": "fem27_20_gcr",
+           "bicgstab": "fem27_20_bicgstab", "bicgstab_l": "fem27_20_bicgstab_l", "tfqmr": "fem27_20_tfqmr"}[method]
+    c = golden["configs"][key]
+    D, N = _dist(ctx, P, c["kind"], c["n"])
+    rep, _ = D.solve(method, split(np.ones(N), N, P), cfg=kg.SolverConfig(mode="fast", stab_l=c["stab_l"]))
+    assert rep.converged
+    if method in ("pcg", "gcr", "bicgstab_l", "tfqmr"):
+        assert abs(rep.iterations - c["iterations"]) <= 1
+    else:
+        assert rep.iterations <= 1.5 * c["iterations"] + 5
+
+
+def test_dist_solve_errors(ctx):
+    D, N = _dist(ctx, 2, "poisson2d", 10)
+    with pytest.raises(kg.Error):
+        D.solve("bicgcr", split(np.ones(N), N, 2))
+    with pytest.raises(kg.Error):
+        D.solve("pcg", split(np.ones(N), N, 2), cfg=kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(0, 0)))
