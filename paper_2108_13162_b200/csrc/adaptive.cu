@@ -1,16 +1,18 @@
 // FAST-mode SpMV for irregular row lengths (power-law rows; the COO
 // overflow of HYB).  CSR-Adaptive style load balancing, deterministic:
-//   * row blocks of <= 256 rows and <= kAdTile nonzeros: tpr = pow2(256 / rows) threads per
-//     row (<= 32) stride the row and fold with shuffles;
-//   * a row with more than kAdTile nonzeros is a block of its own: the whole CTA strides it
-//     and folds in shared memory;
+//   * stream blocks: consecutive rows of <= kAdShort nonzeros each, <= kAdRows rows and
+//     <= kAdTile nonzeros per block; products staged in shared memory, rows summed from it;
+//   * medium rows (kAdShort < len <= kAdMed): eight per CTA, one warp each;
+//   * long rows (<= kAdSplit): the whole CTA strides the row and folds in shared memory;
 //   * a row with more than kAdSplit nonzeros is cut into kAdChunk pieces processed by separate
 //     CTAs; an ordered fixup adds the piece sums.
 // The plan is built once per matrix (host scan of the row pointer) and cached.  Grids are
-// bounded (persistent CTAs loop over blocks).  Row sums use FMA in any order: FAST mode only
+// bounded (persistent CTAs loop over the work items: long rows, medium groups, stream
+// blocks).  Row sums use FMA in any order: FAST mode only
 // (EXACT mode keeps the policy-ordered kernels of spmv_kernels.cuh).
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <vector>
 
 #include "spmv_kernels.cuh"
@@ -19,12 +21,16 @@ namespace kg {
 
 constexpr int kAdNT = 256;
 constexpr int64_t kAdTile = 2048;
-constexpr int64_t kAdSplit = 16384;
-constexpr int64_t kAdChunk = 8192;
-constexpr int64_t kAdRows = 64;  // rows per block (>= 4 threads per row)
+constexpr int64_t kAdSplit = 4096;  // longer rows are cut into kAdChunk pieces
+constexpr int64_t kAdChunk = 2048;
+constexpr int64_t kAdMed = 512;     // medium rows (a warp each) up to this length
+constexpr int64_t kAdRows = 1024;  // rows per stream block (<= 4 per thread in the row phase)
+constexpr int64_t kAdShort = 64;   // longer rows get a CTA of their own
 
 void adaptive_free(AdaptivePlan& p) {
     dev_free(p.blk);
+    dev_free(p.med);
+    dev_free(p.lng);
     dev_free(p.chunk);
     dev_free(p.giant);
     dev_free(p.partials);
@@ -43,52 +49,124 @@ struct RowsView {
     const double* __restrict__ val;
 };
 
+// L2 residency split for random gathers (opt-in, KRYSP_GATHER_HINT=1): x (read ~nnz/n times,
+// in random order) is loaded with an evict_last policy, the once-read column/value streams
+// with evict_first.  Measured on C5 it does not pay: x misses are dominated by capacity.
+struct L2Hints {
+    uint64_t keep, stream;
+};
+__device__ __forceinline__ L2Hints l2_hints() {
+    L2Hints h;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(h.keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(h.stream));
+    return h;
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // a block's sum of one row strided by `nthreads` threads starting at `t`
+template <bool kHint>
 __device__ __forceinline__ double strided_row(RowsView A, const double* __restrict__ x, int64_t k0, int64_t k1,
-                                              int t, int nthreads) {
+                                              int t, int nthreads, L2Hints h) {
     double acc = 0.0;
-    for (int64_t k = k0 + t; k < k1; k += nthreads) acc = fma(__ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)), acc);
+#pragma unroll 4
+    for (int64_t k = k0 + t; k < k1; k += nthreads) {
+        if constexpr (kHint) acc = fma(ld_stream(A.val + k, h.stream), ld_hint(x + ld_stream(A.col + k, h.stream), h.keep), acc);
+        else acc = fma(__ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)), acc);
+    }
     return acc;
 }
 
-__global__ void __launch_bounds__(kAdNT) adaptive_kernel(RowsView A, const int32_t* __restrict__ blk, int64_t nblk,
+// Persistent over the plan's blocks.  A block of short rows (every row <= kAdShort) is
+// processed CSR-stream style: its <= kAdTile nonzeros are multiplied by all 256 threads with
+// kAdPer independent (col, val, x) loads each in flight — the random x gathers of power-law
+// rows are latency-bound, so memory-level parallelism is the lever — into shared memory,
+// then every thread sums whole rows from shared memory.  A long row (a block of its own) is
+// strided by the whole CTA.
+constexpr int kAdPer = kAdTile / kAdNT;
+
+template <bool kHint>
+__global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const int32_t* __restrict__ blk, int64_t nblk,
+                                                          const int32_t* __restrict__ med, int64_t nmed,
+                                                          const int32_t* __restrict__ lng, int64_t nlng,
+                                                          const int32_t* __restrict__ chunk, int64_t nchunk,
+                                                          double* __restrict__ partials,
                                                           const double* __restrict__ x, double* __restrict__ y,
                                                           int accumulate) {
     __shared__ double sh[32];
-    const int tid = threadIdx.x;
-    for (int64_t b = blockIdx.x; b < nblk; b += gridDim.x) {
-        const int32_t r0 = blk[b], r1 = blk[b + 1];
-        const int nrows = r1 - r0;
-        if (nrows == 1) {
-            const int64_t k0 = A.rp[r0], k1 = A.rp[r0 + 1];
-            if (k1 - k0 > kAdSplit) continue;  // giant row: chunk kernel + fixup
-            if (k1 - k0 > 32) {                // long row: whole CTA
-                const double s = block_sum_dyn(strided_row(A, x, k0, k1, tid, kAdNT), sh);
-                if (tid == 0) y[r0] = accumulate ? y[r0] + s : s;
-                continue;
+    __shared__ double prod[kAdTile];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const L2Hints h = kHint ? l2_hints() : L2Hints{0, 0};
+    const int64_t nmedg = (nmed + kAdNT / 32 - 1) / (kAdNT / 32);
+    const int64_t items = nchunk + nlng + nmedg + nblk;
+    for (int64_t bi = blockIdx.x; bi < items; bi += gridDim.x) {
+        if (bi < nchunk) {  // a piece of a giant row (fixup kernel adds the pieces in order)
+            const double s = block_sum_dyn(strided_row<kHint>(A, x, chunk[3 * bi + 1], chunk[3 * bi + 2], tid, kAdNT, h), sh);
+            if (tid == 0) partials[bi] = s;
+            continue;
+        }
+        const int64_t b = bi - nchunk;
+        if (b < nlng) {  // long row: the whole CTA
+            const int32_t r = lng[b];
+            const double s = block_sum_dyn(strided_row<kHint>(A, x, A.rp[r], A.rp[r + 1], tid, kAdNT, h), sh);
+            if (tid == 0) y[r] = accumulate ? y[r] + s : s;
+            continue;
+        }
+        if (b < nlng + nmedg) {  // medium rows: one warp each
+            const int64_t i = (b - nlng) * (kAdNT / 32) + warp;
+            if (i < nmed) {
+                const int32_t r = med[i];
+                double s = strided_row<kHint>(A, x, A.rp[r], A.rp[r + 1], lane, 32, h);
+                s = warp_sum(s);
+                if (lane == 0) y[r] = accumulate ? y[r] + s : s;
+            }
+            continue;
+        }
+        const int64_t q = b - nlng - nmedg;  // stream block of short rows
+        const int32_t r0 = blk[2 * q], r1 = blk[2 * q + 1];
+        const int64_t k0 = A.rp[r0];
+        const int nz = (int)(A.rp[r1] - k0);
+        int32_t cl[kAdPer];
+        double vl[kAdPer];
+#pragma unroll
+        for (int j = 0; j < kAdPer; ++j) {
+            const int k = tid + j * kAdNT;
+            if (k < nz) {
+                if constexpr (kHint) {
+                    cl[j] = ld_stream(A.col + k0 + k, h.stream);
+                    vl[j] = ld_stream(A.val + k0 + k, h.stream);
+                } else {
+                    cl[j] = __ldcs(A.col + k0 + k);
+                    vl[j] = __ldcs(A.val + k0 + k);
+                }
             }
         }
-        int tpr = 1;
-        while (tpr < 32 && tpr * 2 * nrows <= kAdNT) tpr *= 2;
-        const int g = tid / tpr, lane = tid & (tpr - 1), step = kAdNT / tpr;
-        for (int base = r0; base < r1; base += step) {  // uniform trip count per warp
-            const int row = base + g;
-            double s = 0.0;
-            if (row < r1) s = strided_row(A, x, A.rp[row], A.rp[row + 1], lane, tpr);
-            for (int o = tpr / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, tpr);
-            if (row < r1 && lane == 0) y[row] = accumulate ? y[row] + s : s;
+#pragma unroll
+        for (int j = 0; j < kAdPer; ++j) {
+            const int k = tid + j * kAdNT;
+            if (k < nz) prod[k] = vl[j] * (kHint ? ld_hint(x + cl[j], h.keep) : __ldg(x + cl[j]));
         }
-    }
-}
-
-__global__ void __launch_bounds__(kAdNT) giant_chunk_kernel(RowsView A, const int32_t* __restrict__ chunk,
-                                                             int64_t nchunk, const double* __restrict__ x,
-                                                             double* __restrict__ partials) {
-    __shared__ double sh[32];
-    for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x) {
-        const int64_t k0 = chunk[3 * c + 1], k1 = chunk[3 * c + 2];
-        const double s = block_sum_dyn(strided_row(A, x, k0, k1, threadIdx.x, kAdNT), sh);
-        if (threadIdx.x == 0) partials[c] = s;
+        __syncthreads();
+        for (int32_t row = r0 + tid; row < r1; row += kAdNT) {
+            const int e0 = (int)(A.rp[row] - k0), e1 = (int)(A.rp[row + 1] - k0);
+            double s = 0.0;
+            for (int k = e0; k < e1; ++k) s += prod[k];
+            y[row] = accumulate ? y[row] + s : s;
+        }
+        __syncthreads();
     }
 }
 
@@ -111,20 +189,24 @@ void build_plan(krysp_gpu_ctx* c, const int32_t* d_rp, int64_t n, AdaptivePlan& 
     std::vector<int32_t> rp((size_t)n + 1);
     KG_CUDA(cudaMemcpyAsync(rp.data(), d_rp, 4 * (n + 1), cudaMemcpyDeviceToHost, c->stream));
     KG_CUDA(cudaStreamSynchronize(c->stream));
-    std::vector<int32_t> blk{0}, chunk, giant;
-    int64_t cur_rows = 0, cur_nnz = 0, cur_max = 0;
-    // threads per row the kernel gives a block of `rows` rows
-    auto tpr_of = [](int64_t rows) {
-        int64_t t = 1;
-        while (t < 32 && t * 2 * rows <= kAdNT) t *= 2;
-        return t;
+    std::vector<int32_t> blk, med, lng, chunk, giant;
+    int64_t cur_r0 = -1, cur_rows = 0, cur_nnz = 0;
+    auto close = [&](int64_t r) {
+        if (cur_rows) {
+            blk.push_back((int32_t)cur_r0);
+            blk.push_back((int32_t)r);
+        }
+        cur_rows = cur_nnz = 0;
     };
     for (int64_t r = 0; r < n; ++r) {
         const int64_t len = rp[(size_t)r + 1] - rp[(size_t)r];
-        if (len > 4 * 32) {  // a CTA of its own (or chunks when giant)
-            if (cur_rows) blk.push_back((int32_t)r);
-            blk.push_back((int32_t)(r + 1));
-            if (len > kAdSplit) {
+        if (len > kAdShort) {
+            close(r);
+            if (len <= kAdMed) {
+                med.push_back((int32_t)r);
+            } else if (len <= kAdSplit) {
+                lng.push_back((int32_t)r);
+            } else {  // giant: chunks + ordered fixup
                 const int32_t c0 = (int32_t)(chunk.size() / 3);
                 for (int64_t k = rp[(size_t)r]; k < rp[(size_t)r + 1]; k += kAdChunk) {
                     chunk.push_back((int32_t)r);
@@ -135,34 +217,32 @@ void build_plan(krysp_gpu_ctx* c, const int32_t* d_rp, int64_t n, AdaptivePlan& 
                 giant.push_back(c0);
                 giant.push_back((int32_t)(chunk.size() / 3));
             }
-            cur_rows = cur_nnz = cur_max = 0;
             continue;
         }
-        // close the block when it would exceed kAdRows rows / kAdTile nnz, or when its longest
-        // row would need more than 4 strides of its threads-per-row
-        const int64_t mx = std::max(cur_max, len);
-        if (cur_rows && (cur_rows == kAdRows || cur_nnz + len > kAdTile || mx > 4 * tpr_of(cur_rows + 1))) {
-            blk.push_back((int32_t)r);
-            cur_rows = cur_nnz = cur_max = 0;
-        }
+        // a stream block holds <= kAdRows rows and <= kAdTile nonzeros
+        if (cur_rows && (cur_rows == kAdRows || cur_nnz + len > kAdTile)) close(r);
+        if (!cur_rows) cur_r0 = r;
         ++cur_rows;
         cur_nnz += len;
-        cur_max = std::max(cur_max, len);
     }
-    if (cur_rows || blk.size() == 1) blk.push_back((int32_t)n);
-    if (blk.back() != n) blk.push_back((int32_t)n);
-    P.nblk = (int64_t)blk.size() - 1;
+    close(n);
+    P.nblk = (int64_t)blk.size() / 2;
+    P.nmed = (int64_t)med.size();
+    P.nlng = (int64_t)lng.size();
     P.nchunk = (int64_t)chunk.size() / 3;
     P.ngiant = (int64_t)giant.size() / 3;
-    P.blk = dev_alloc<int32_t>((int64_t)blk.size(), false);
-    KG_CUDA(cudaMemcpy(P.blk, blk.data(), 4 * blk.size(), cudaMemcpyHostToDevice));
-    if (P.nchunk) {
-        P.chunk = dev_alloc<int32_t>((int64_t)chunk.size(), false);
-        P.giant = dev_alloc<int32_t>((int64_t)giant.size(), false);
-        P.partials = dev_alloc<double>(P.nchunk, false);
-        KG_CUDA(cudaMemcpy(P.chunk, chunk.data(), 4 * chunk.size(), cudaMemcpyHostToDevice));
-        KG_CUDA(cudaMemcpy(P.giant, giant.data(), 4 * giant.size(), cudaMemcpyHostToDevice));
-    }
+    auto up = [&](const std::vector<int32_t>& v) -> int32_t* {
+        if (v.empty()) return nullptr;
+        int32_t* d = dev_alloc<int32_t>((int64_t)v.size(), false);
+        KG_CUDA(cudaMemcpy(d, v.data(), 4 * v.size(), cudaMemcpyHostToDevice));
+        return d;
+    };
+    P.blk = up(blk);
+    P.med = up(med);
+    P.lng = up(lng);
+    P.chunk = up(chunk);
+    P.giant = up(giant);
+    if (P.nchunk) P.partials = dev_alloc<double>(P.nchunk, false);
     P.built = true;
 }
 
@@ -207,13 +287,22 @@ void launch_adaptive(const krysp_gpu_mat* cm, bool coo_part, const double* x, do
         P = &m->ad_csr;
     }
     if (!P->built) build_plan(c, A.rp, m->n_rows, *P);
-    if (P->nchunk) {
-        giant_chunk_kernel<<<(unsigned)std::min<int64_t>(P->nchunk, (int64_t)c->sm_count * 8), kAdNT, 0, s>>>(
-            A, P->chunk, P->nchunk, x, P->partials);
-        KG_LAUNCH(c);
+    static const bool hint = [] {
+        // opt-in: measured slower (the policy registers spill under the 5-CTA register cap)
+        const char* e = std::getenv("KRYSP_GATHER_HINT");
+        return e && std::atoi(e) != 0;
+    }();
+    const int64_t items = P->nchunk + P->nlng + (P->nmed + kAdNT / 32 - 1) / (kAdNT / 32) + P->nblk;
+    if (items == 0) {
+    } else if (hint) {
+        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel<true>, kAdNT, 0), items);
+        adaptive_kernel<true><<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
+                                                            P->nchunk, P->partials, x, y, accumulate ? 1 : 0);
+    } else {
+        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel<false>, kAdNT, 0), items);
+        adaptive_kernel<false><<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
+                                                             P->nchunk, P->partials, x, y, accumulate ? 1 : 0);
     }
-    const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel, kAdNT, 0), P->nblk);
-    adaptive_kernel<<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, x, y, accumulate ? 1 : 0);
     KG_LAUNCH(c);
     if (P->ngiant) {
         giant_fixup_kernel<<<grid_for(P->ngiant, 128, 1024), 128, 0, s>>>(P->giant, P->ngiant, P->partials, y,

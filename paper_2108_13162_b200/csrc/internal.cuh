@@ -99,8 +99,12 @@ struct CooView {
 // rows, and rows longer than kAdSplit split into kAdChunk-nnz chunks (partials + fixup).
 namespace kg {
 struct AdaptivePlan {
-    int32_t* blk = nullptr;    // nblk + 1 row boundaries
+    int32_t* blk = nullptr;    // (r0, r1) per stream block of short rows
     int64_t nblk = 0;
+    int32_t* med = nullptr;    // medium rows (a warp each)
+    int64_t nmed = 0;
+    int32_t* lng = nullptr;    // long rows (a CTA each)
+    int64_t nlng = 0;
     int32_t* chunk = nullptr;  // (row, k0, k1) per chunk of a giant row
     int64_t nchunk = 0;
     int32_t* giant = nullptr;  // (row, c0, c1) per giant row
