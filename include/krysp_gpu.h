@@ -314,6 +314,49 @@ krysp_status krysp_gpu_dist_solve(krysp_gpu_dist* d, int32_t method, const doubl
                                   double* h_history);
 krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d);
 
+/* ------------------------------------------------------------------ substructure.hpp */
+/* Algebraic sub-structuring (the paper's hybrid method, substructure.cpp).  The partition
+ * (partition_matrix, substructure.cpp:95-238) is built on the host from the global CSR and
+ * an assignment (one subdomain id per equation, -1 = explicitly shared; NULL = band rows
+ * over n_parts, band_row_assignment :20-31).  rank -1: every subdomain on ctx's GPU (the
+ * reference's one-thread-per-subdomain run); rank >= 0: subdomain `rank` on this GPU, NCCL
+ * between the subdomains' processes (world = number of subdomains, id from
+ * krysp_gpu_dist_unique_id).  Device vectors are per held subdomain (local numbering). */
+typedef struct krysp_gpu_sub krysp_gpu_sub;
+krysp_status krysp_gpu_band_row_assignment(int64_t n, int64_t n_parts, int64_t* assignment);
+/* read_assignment_file (substructure.cpp:244-266); out may be NULL (validation only) */
+krysp_status krysp_gpu_read_assignment_file(const char* path, int64_t expected_n, int64_t* out);
+krysp_status krysp_gpu_sub_create(krysp_gpu_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                  const double* values, const int64_t* assignment, int64_t n_parts, int32_t rank,
+                                  const uint8_t* nccl_id, krysp_gpu_sub** out);
+/* [n_subdomains, dof, nnz, n_interfaces, interface entries, owner entries (global)] */
+krysp_status krysp_gpu_sub_info(const krysp_gpu_sub* h, int64_t s, int64_t info[6]);
+/* LocalSystem s (substructure.hpp:34-38) on the host: local_to_global, K_local, weights */
+krysp_status krysp_gpu_sub_local(const krysp_gpu_sub* h, int64_t s, int64_t* l2g, int64_t* row_ptr,
+                                 int64_t* col_idx, double* values, double* weights);
+/* InterfaceDescriptor list of s (substructure.hpp:15-20): neighbours, offsets, equations */
+krysp_status krysp_gpu_sub_interfaces(const krysp_gpu_sub* h, int64_t s, int64_t* neighbors, int64_t* offsets,
+                                      int64_t* equations);
+krysp_status krysp_gpu_sub_owners(const krysp_gpu_sub* h, int64_t* ptr, int64_t* list);
+/* local_spmv_assemble (substructure.cpp:354-405) for every held subdomain */
+krysp_status krysp_gpu_sub_assemble_spmv(krysp_gpu_sub* h, const double* const* d_x, double* const* d_y,
+                                         const krysp_policy* policy, int32_t mode);
+/* distributed_dot (substructure.cpp:407-437) */
+krysp_status krysp_gpu_sub_dot(krysp_gpu_sub* h, const double* const* d_x, const double* const* d_y,
+                               const krysp_policy* policy, int32_t mode, double* out);
+/* solve_cg_substructured (substructure.cpp:445-583): b, x0, solution are GLOBAL host
+ * vectors (every rank passes the same b, x0 and receives the whole solution) */
+krysp_status krysp_gpu_sub_solve_cg(krysp_gpu_sub* h, const double* b, const double* x0,
+                                    const krysp_solver_cfg* cfg, krysp_report* report, double* h_history,
+                                    double* solution);
+krysp_status krysp_gpu_sub_destroy(krysp_gpu_sub* h);
+/* one-call solve_cg_substructured with all subdomains on ctx's GPU */
+krysp_status krysp_gpu_solve_cg_substructured_host(krysp_gpu_ctx* ctx, int64_t n, const int64_t* row_ptr,
+                                                   const int64_t* col_idx, const double* values, const double* b,
+                                                   const double* x0, const int64_t* assignment, int64_t n_parts,
+                                                   const krysp_solver_cfg* cfg, krysp_report* report,
+                                                   double* h_history, double* solution);
+
 /* ------------------------------------------------------------------ autotune.hpp:40-64 */
 /* tune_spmv autotune.cpp:136-177 with CUDA-event timing under the same protocol
  * (:37-87) and tie-break (:118-134).  grid may be NULL (= default_policy_grid, 72).

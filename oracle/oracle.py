@@ -250,8 +250,9 @@ class Ref:
 
     def from_csr(self, m: Csr) -> RefMat:
         h = _P()
-        self._chk(self.L.kref_mat_csr(_I(m.n_rows), _I(m.n_cols), _ptr(m.row_ptr),
-                                      _ptr(m.col_idx), _ptr(m.values), C.byref(h)))
+        rp, ci = np.ascontiguousarray(m.row_ptr, np.int64), np.ascontiguousarray(m.col_idx, np.int64)
+        va = np.ascontiguousarray(m.values, np.float64)
+        self._chk(self.L.kref_mat_csr(_I(m.n_rows), _I(m.n_cols), _ptr(rp), _ptr(ci), _ptr(va), C.byref(h)))
         return RefMat(self.L, h)
 
     def build_coo(self, n_rows, n_cols, r, c, v) -> RefMat:
@@ -377,4 +378,85 @@ class Ref:
     def band_row_assignment(self, n, parts):
         out = np.zeros(n, np.int64)
         self._chk(self.L.kref_band_row_assignment(_I(n), _I(parts), _ptr(out)))
+        return out
+
+    # ---- algebraic sub-structuring (substructure.hpp) ------------------------------------
+    def partition(self, m: RefMat, assignment, b=None) -> "RefPart":
+        a = np.ascontiguousarray(assignment, np.int64)
+        bb = None if b is None else np.ascontiguousarray(b, np.float64)
+        h = _P()
+        self._chk(self.L.kref_partition(m.h, _ptr(a), _ptr(bb) if bb is not None else None, C.byref(h)))
+        return RefPart(self, h, len(a))
+
+    def solve_cg_substructured(self, m: RefMat, b, x0, assignment, tol=1e-6, max_it=30000, jacobi=True,
+                               bs=256, tw=8, workers=0):
+        n = len(assignment)
+        b = np.ascontiguousarray(b, np.float64)
+        x0 = np.ascontiguousarray(x0, np.float64)
+        a = np.ascontiguousarray(assignment, np.int64)
+        rep, hist, sol = np.zeros(4), np.zeros(max_it), np.zeros(n)
+        rc = self.L.kref_solve_cg_substructured(m.h, _ptr(b), _ptr(x0), _ptr(a), _D(tol), _I(max_it),
+                                                C.c_int(1 if jacobi else 0), _I(bs), _I(tw), _I(workers),
+                                                _ptr(rep), _ptr(hist), _I(max_it), _ptr(sol))
+        it = int(rep[1])
+        out = dict(converged=bool(rep[0]), iterations=it, final_residual_measure=float(rep[2]),
+                   wall_time=float(rep[3]), residual_history=hist[:it].copy(), solution=sol, status=rc)
+        if rc != 0:
+            out["error"] = self.L.kref_last_error().decode()
+        return out
+
+
+class RefPart:
+    """PartitionResult of the reference (partition_matrix, substructure.cpp:95-238)."""
+
+    def __init__(self, ref: Ref, h, n):
+        self.ref, self.L, self.h, self.n = ref, ref.L, h, n
+        self.n_subdomains = self.info(0)["n_subdomains"]
+
+    def __del__(self):
+        try:
+            self.L.kref_part_free(self.h)
+        except Exception:
+            pass
+
+    def info(self, s):
+        a = np.zeros(6, np.int64)
+        self.ref._chk(self.L.kref_part_info(self.h, _I(s), _ptr(a)))
+        return dict(n_subdomains=int(a[0]), dof=int(a[1]), nnz=int(a[2]), n_interfaces=int(a[3]),
+                    interface_entries=int(a[4]), owner_entries=int(a[5]))
+
+    def local(self, s):
+        i = self.info(s)
+        d, z = i["dof"], i["nnz"]
+        l2g, rp, ci = np.zeros(d, np.int64), np.zeros(d + 1, np.int64), np.zeros(z, np.int64)
+        v, w, bl = np.zeros(z), np.zeros(d), np.zeros(d)
+        self.ref._chk(self.L.kref_part_local(self.h, _I(s), _ptr(l2g), _ptr(rp), _ptr(ci), _ptr(v), _ptr(w),
+                                             _ptr(bl)))
+        return dict(l2g=l2g, K=Csr(d, d, rp, ci, v), weights=w, b_local=bl)
+
+    def interfaces(self, s):
+        i = self.info(s)
+        nbr = np.zeros(i["n_interfaces"], np.int64)
+        off = np.zeros(i["n_interfaces"] + 1, np.int64)
+        eqs = np.zeros(i["interface_entries"], np.int64)
+        self.ref._chk(self.L.kref_part_interfaces(self.h, _I(s), _ptr(nbr), _ptr(off), _ptr(eqs)))
+        return [(int(nbr[k]), eqs[off[k]:off[k + 1]].copy()) for k in range(len(nbr))]
+
+    def owners(self):
+        tot = self.info(0)["owner_entries"]
+        ptr, lst = np.zeros(self.n + 1, np.int64), np.zeros(tot, np.int64)
+        self.ref._chk(self.L.kref_part_owners(self.h, _ptr(ptr), _ptr(lst)))
+        return [lst[ptr[e]:ptr[e + 1]].copy() for e in range(self.n)]
+
+    def assemble_spmv(self, x, bs=256, tw=8):
+        x = np.ascontiguousarray(x, np.float64)
+        dofs = [self.info(s)["dof"] for s in range(self.n_subdomains)]
+        y = np.zeros(sum(dofs))
+        self.ref._chk(self.L.kref_assemble_spmv(self.h, _ptr(x), _I(len(x)), _I(bs), _I(tw), _ptr(y)))
+        return np.split(y, np.cumsum(dofs)[:-1])
+
+    def distributed_dot(self, x, y, bs=256, tw=8):
+        x, y = np.ascontiguousarray(x, np.float64), np.ascontiguousarray(y, np.float64)
+        out = np.zeros(self.n_subdomains)
+        self.ref._chk(self.L.kref_distributed_dot(self.h, _ptr(x), _ptr(y), _I(len(x)), _I(bs), _I(tw), _ptr(out)))
         return out

@@ -353,4 +353,132 @@ int kref_band_row_assignment(int64_t n, int64_t parts, int64_t* out) {
     });
 }
 
+// ---- algebraic sub-structuring (substructure.hpp) ----------------------------------------
+struct kref_part {
+    PartitionResult pr;
+};
+
+void kref_part_free(kref_part* p) { delete p; }
+
+// partition_matrix(A, assignment, b) (substructure.cpp:95-238); b may be NULL
+int kref_partition(const kref_mat* m, const int64_t* assignment, const double* b, kref_part** out) {
+    return guard([&] {
+        CsrMatrix A = to_csr(m->m);
+        std::vector<index_t> a(assignment, assignment + A.n_rows);
+        std::span<const double> bs;
+        if (b) bs = std::span<const double>(b, static_cast<size_t>(A.n_rows));
+        *out = new kref_part{partition_matrix(A, a, bs)};
+    });
+}
+
+// [n_subdomains, dof(s), nnz(s), n_interfaces(s), interface entries(s), owner entries (all)]
+int kref_part_info(const kref_part* p, int64_t s, int64_t* info) {
+    return guard([&] {
+        const Partition& P = p->pr.partition;
+        info[0] = P.n_subdomains;
+        info[1] = static_cast<int64_t>(P.local_to_global[s].size());
+        info[2] = p->pr.locals[s].K_local.nnz();
+        info[3] = static_cast<int64_t>(P.interfaces[s].size());
+        int64_t e = 0;
+        for (const auto& f : P.interfaces[s]) e += static_cast<int64_t>(f.equation_list.size());
+        info[4] = e;
+        int64_t o = 0;
+        for (const auto& own : P.owners) o += static_cast<int64_t>(own.size());
+        info[5] = o;
+    });
+}
+
+// local system s: l2g[dof], K_local CSR, weights[dof], b_local[dof] (b_local may be empty)
+int kref_part_local(const kref_part* p, int64_t s, int64_t* l2g, int64_t* rp, int64_t* ci, double* v,
+                    double* w, double* b_local) {
+    return guard([&] {
+        const auto& l = p->pr.partition.local_to_global[s];
+        const LocalSystem& L = p->pr.locals[s];
+        std::memcpy(l2g, l.data(), l.size() * 8);
+        std::memcpy(rp, L.K_local.row_ptr.data(), L.K_local.row_ptr.size() * 8);
+        std::memcpy(ci, L.K_local.col_idx.data(), L.K_local.col_idx.size() * 8);
+        std::memcpy(v, L.K_local.values.data(), L.K_local.values.size() * 8);
+        std::memcpy(w, L.weights.data(), L.weights.size() * 8);
+        if (b_local && !L.b_local.empty()) std::memcpy(b_local, L.b_local.data(), L.b_local.size() * 8);
+    });
+}
+
+// interfaces of s: neighbor ids, offsets[n_if + 1], local equation lists
+int kref_part_interfaces(const kref_part* p, int64_t s, int64_t* nbr, int64_t* off, int64_t* eqs) {
+    return guard([&] {
+        int64_t k = 0, i = 0;
+        off[0] = 0;
+        for (const auto& f : p->pr.partition.interfaces[s]) {
+            nbr[i] = f.neighbor_id;
+            for (index_t e : f.equation_list) eqs[k++] = e;
+            off[++i] = k;
+        }
+    });
+}
+
+// owners per global equation: ptr[n + 1], list
+int kref_part_owners(const kref_part* p, int64_t* ptr, int64_t* list) {
+    return guard([&] {
+        int64_t k = 0, e = 0;
+        ptr[0] = 0;
+        for (const auto& own : p->pr.partition.owners) {
+            for (index_t s : own) list[k++] = s;
+            ptr[++e] = k;
+        }
+    });
+}
+
+// assemble_spmv_all on restrict_to_local(x): y locals concatenated in subdomain order
+int kref_assemble_spmv(const kref_part* p, const double* x, int64_t n, int64_t bs, int64_t tw, double* y_cat) {
+    return guard([&] {
+        std::vector<std::vector<double>> xl;
+        for (index_t s = 0; s < p->pr.partition.n_subdomains; ++s)
+            xl.push_back(restrict_to_local(p->pr, s, std::span<const double>(x, static_cast<size_t>(n))));
+        auto yl = assemble_spmv_all(p->pr, xl, policy_of(bs, tw, 0));
+        size_t k = 0;
+        for (const auto& y : yl) {
+            std::memcpy(y_cat + k, y.data(), y.size() * 8);
+            k += y.size();
+        }
+    });
+}
+
+// distributed_dot_all on the restrictions of x, y: one result per subdomain
+int kref_distributed_dot(const kref_part* p, const double* x, const double* y, int64_t n, int64_t bs, int64_t tw,
+                         double* out) {
+    return guard([&] {
+        std::vector<std::vector<double>> xl, yl;
+        for (index_t s = 0; s < p->pr.partition.n_subdomains; ++s) {
+            xl.push_back(restrict_to_local(p->pr, s, std::span<const double>(x, static_cast<size_t>(n))));
+            yl.push_back(restrict_to_local(p->pr, s, std::span<const double>(y, static_cast<size_t>(n))));
+        }
+        auto r = distributed_dot_all(p->pr, xl, yl, policy_of(bs, tw, 0));
+        std::memcpy(out, r.data(), r.size() * 8);
+    });
+}
+
+// solve_cg_substructured(A, b, x0, assignment, cfg) (substructure.cpp:445-583)
+// report: [converged, iterations, final_residual_measure, wall_time]
+int kref_solve_cg_substructured(const kref_mat* m, const double* b, const double* x0, const int64_t* assignment,
+                                double tol, int64_t max_it, int precond, int64_t bs, int64_t tw, int64_t workers,
+                                double* report, double* history, int64_t hist_cap, double* solution) {
+    return guard([&] {
+        SolverConfig cfg;
+        cfg.tolerance = tol;
+        cfg.max_iterations = max_it;
+        cfg.preconditioner = precond ? Preconditioner::Jacobi : Preconditioner::None;
+        cfg.policy = policy_of(bs, tw, workers);
+        size_t n = static_cast<size_t>(n_rows(m->m));
+        std::vector<index_t> a(assignment, assignment + n);
+        SolveReport r = solve_cg_substructured(m->m, std::span<const double>(b, n), std::span<const double>(x0, n), a, cfg);
+        report[0] = r.converged ? 1.0 : 0.0;
+        report[1] = static_cast<double>(r.iterations);
+        report[2] = r.final_residual_measure;
+        report[3] = r.wall_time;
+        size_t h = std::min(r.residual_history.size(), static_cast<size_t>(hist_cap));
+        if (history) std::memcpy(history, r.residual_history.data(), h * sizeof(double));
+        if (solution) std::memcpy(solution, r.solution.data(), n * sizeof(double));
+    });
+}
+
 }  // extern "C"

@@ -139,6 +139,9 @@ EXPORTS = [
     "krysp_gpu_dist_spmv", "krysp_gpu_dist_pcg_create", "krysp_gpu_dist_krylov_create", "krysp_gpu_dist_pcg_iterate", "krysp_gpu_dist_pcg_time",
     "krysp_gpu_dist_pcg_run", "krysp_gpu_dist_pcg_report", "krysp_gpu_dist_pcg_solution",
     "krysp_gpu_dist_kernels_per_iteration", "krysp_gpu_dist_solve", "krysp_gpu_dist_destroy",
+    "krysp_gpu_band_row_assignment", "krysp_gpu_read_assignment_file", "krysp_gpu_sub_create", "krysp_gpu_sub_info",
+    "krysp_gpu_sub_local", "krysp_gpu_sub_interfaces", "krysp_gpu_sub_owners", "krysp_gpu_sub_assemble_spmv",
+    "krysp_gpu_sub_dot", "krysp_gpu_sub_solve_cg", "krysp_gpu_sub_destroy", "krysp_gpu_solve_cg_substructured_host",
 ]
 
 _lib = None

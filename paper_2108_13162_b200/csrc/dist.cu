@@ -27,6 +27,7 @@
 #include <numeric>
 
 #include "engine.cuh"
+#include "nccl_api.cuh"
 #include "spmv_kernels.cuh"
 
 namespace kg {
@@ -34,67 +35,6 @@ namespace kg {
 krysp_gpu_mat* generate_rows(krysp_gpu_ctx*, const char*, int64_t, double, int64_t, int64_t);
 int64_t generator_dim(const char*, int64_t);
 krysp_gpu_mat* upload_csr(krysp_gpu_ctx*, int64_t, int64_t, const int64_t*, const int64_t*, const double*);
-
-// ------------------------------------------------------------------ NCCL (run-time loaded)
-struct NcclApi {
-    bool ok = false;
-    std::string err;
-    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
-    decltype(&ncclCommInitRank) CommInitRank = nullptr;
-    decltype(&ncclCommDestroy) CommDestroy = nullptr;
-    decltype(&ncclAllReduce) AllReduce = nullptr;
-    decltype(&ncclAllGather) AllGather = nullptr;
-    decltype(&ncclSend) Send = nullptr;
-    decltype(&ncclRecv) Recv = nullptr;
-    decltype(&ncclGroupStart) GroupStart = nullptr;
-    decltype(&ncclGroupEnd) GroupEnd = nullptr;
-    decltype(&ncclGetErrorString) GetErrorString = nullptr;
-
-    static NcclApi& get() {
-        static NcclApi a;
-        static bool tried = false;
-        if (!tried) {
-            tried = true;
-            a.load();
-        }
-        if (!a.ok) fail(KRYSP_NCCL_ERROR, "NCCL unavailable: %s", a.err.c_str());
-        return a;
-    }
-    void load() {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) {
-            const char* e = dlerror();
-            err = e ? e : "dlopen failed";
-            return;
-        }
-#define KG_SYM(name)                                                   \
-    name = reinterpret_cast<decltype(name)>(dlsym(h, "nccl" #name));   \
-    if (!name) {                                                       \
-        err = "libnccl.so.2 lacks nccl" #name;                         \
-        return;                                                        \
-    }
-        KG_SYM(GetUniqueId)
-        KG_SYM(CommInitRank)
-        KG_SYM(CommDestroy)
-        KG_SYM(AllReduce)
-        KG_SYM(AllGather)
-        KG_SYM(Send)
-        KG_SYM(Recv)
-        KG_SYM(GroupStart)
-        KG_SYM(GroupEnd)
-        KG_SYM(GetErrorString)
-#undef KG_SYM
-        ok = true;
-    }
-};
-
-#define KG_NCCL(call)                                                                                 \
-    do {                                                                                              \
-        ncclResult_t r_ = (call);                                                                     \
-        if (r_ != ncclSuccess)                                                                        \
-            ::kg::fail(KRYSP_NCCL_ERROR, "%s:%d %s: %s", __FILE__, __LINE__, #call,                 \
-                       ::kg::NcclApi::get().GetErrorString(r_));                                      \
-    } while (0)
 
 // band_row_assignment (substructure.cpp:20-31)
 void band_rows(int64_t n, int64_t parts, int64_t part, int64_t* lo, int64_t* hi) {
