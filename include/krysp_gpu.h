@@ -314,6 +314,22 @@ krysp_status krysp_gpu_dist_solve(krysp_gpu_dist* d, int32_t method, const doubl
                                   double* h_history);
 krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d);
 
+/* ------------------------------------------------------------------ matrix_market.hpp / build_coo */
+/* build_coo (formats.cpp:17-47) on the device: range check (IndexOutOfRange names the first
+ * offending triple), stable radix sort by (row, col), duplicates summed in input order.
+ * format: KRYSP_FMT_COO (canonical COO) or KRYSP_FMT_CSR (coo_to_csr). */
+krysp_status krysp_gpu_mat_build_coo(krysp_gpu_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                     const int64_t* row_idx, const int64_t* col_idx, const double* values,
+                                     int32_t format, krysp_gpu_mat** out);
+/* read_matrix_market (matrix_market.cpp:21-116): coordinate real|integer, general|symmetric;
+ * ParseError messages end in "(line N)" as the reference's.  Entry lines are tokenised by
+ * host threads, the COO is built on the device. */
+krysp_status krysp_gpu_read_matrix_market(krysp_gpu_ctx* ctx, const char* path, int32_t format, krysp_gpu_mat** out);
+krysp_status krysp_gpu_parse_matrix_market(krysp_gpu_ctx* ctx, const char* text, size_t len, int32_t format,
+                                           krysp_gpu_mat** out);
+/* write_matrix_market (matrix_market.cpp:119-141): coordinate real general, %.17g values */
+krysp_status krysp_gpu_write_matrix_market(const krysp_gpu_mat* m, const char* path);
+
 /* ------------------------------------------------------------------ substructure.hpp */
 /* Algebraic sub-structuring (the paper's hybrid method, substructure.cpp).  The partition
  * (partition_matrix, substructure.cpp:95-238) is built on the host from the global CSR and

@@ -388,6 +388,20 @@ class Ref:
         self._chk(self.L.kref_partition(m.h, _ptr(a), _ptr(bb) if bb is not None else None, C.byref(h)))
         return RefPart(self, h, len(a))
 
+    # ---- matrix_market.hpp -------------------------------------------------------------
+    def parse_matrix_market(self, text):
+        """read_matrix_market(std::istream&) on a text: (RefMat | None, status, message, line)."""
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        h = _P()
+        ln = C.c_int64()
+        rc = self.L.kref_parse_matrix_market(b, _I(len(b)), C.byref(h), C.byref(ln))
+        if rc:
+            return None, rc, self.L.kref_last_error().decode(), ln.value
+        return RefMat(self.L, h), 0, "", 0
+
+    def write_matrix_market(self, m: RefMat, path):
+        self._chk(self.L.kref_write_matrix_market(m.h, str(path).encode()))
+
     def solve_cg_substructured(self, m: RefMat, b, x0, assignment, tol=1e-6, max_it=30000, jacobi=True,
                                bs=256, tw=8, workers=0):
         n = len(assignment)
@@ -460,3 +474,4 @@ class RefPart:
         out = np.zeros(self.n_subdomains)
         self.ref._chk(self.L.kref_distributed_dot(self.h, _ptr(x), _ptr(y), _I(len(x)), _I(bs), _I(tw), _ptr(out)))
         return out
+

@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <string>
 #include <variant>
 #include <vector>
@@ -26,6 +27,7 @@
 #include "krysp/formats.hpp"
 #include "krysp/generators.hpp"
 #include "krysp/kernels.hpp"
+#include "krysp/matrix_market.hpp"
 #include "krysp/solvers.hpp"
 #include "krysp/stats.hpp"
 #include "krysp/substructure.hpp"
@@ -351,6 +353,28 @@ int kref_band_row_assignment(int64_t n, int64_t parts, int64_t* out) {
         auto a = band_row_assignment(n, parts);
         std::memcpy(out, a.data(), a.size() * sizeof(int64_t));
     });
+}
+
+// ---- matrix_market.hpp ------------------------------------------------------------------
+// read_matrix_market(std::istream&) on an in-memory text (matrix_market.cpp:21-108)
+int kref_parse_matrix_market(const char* text, int64_t len, kref_mat** out, int64_t* line_number) {
+    if (line_number) *line_number = 0;
+    try {
+        std::istringstream in(std::string(text, static_cast<size_t>(len)));
+        *out = new kref_mat{SparseMatrix(read_matrix_market(in))};
+        return 0;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        if (line_number) *line_number = e.line_number;
+        return code_of(e);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return code_of(e);
+    }
+}
+
+int kref_write_matrix_market(const kref_mat* m, const char* path) {
+    return guard([&] { write_matrix_market(std::string(path), csr_to_coo(to_csr(m->m))); });
 }
 
 // ---- algebraic sub-structuring (substructure.hpp) ----------------------------------------

@@ -35,6 +35,13 @@ class EllBlowup(Error):
 class ParseError(Error):
     code = 5
 
+    @property
+    def line_number(self):
+        """ParseError::line_number (types.hpp:26-30), from the "(line N)" suffix."""
+        import re
+        m = re.search(r"\(line (\d+)\)$", str(self))
+        return int(m.group(1)) if m else None
+
 
 class UnsupportedField(Error):
     code = 6
@@ -139,6 +146,8 @@ EXPORTS = [
     "krysp_gpu_dist_spmv", "krysp_gpu_dist_pcg_create", "krysp_gpu_dist_krylov_create", "krysp_gpu_dist_pcg_iterate", "krysp_gpu_dist_pcg_time",
     "krysp_gpu_dist_pcg_run", "krysp_gpu_dist_pcg_report", "krysp_gpu_dist_pcg_solution",
     "krysp_gpu_dist_kernels_per_iteration", "krysp_gpu_dist_solve", "krysp_gpu_dist_destroy",
+    "krysp_gpu_mat_build_coo", "krysp_gpu_read_matrix_market", "krysp_gpu_parse_matrix_market",
+    "krysp_gpu_write_matrix_market",
     "krysp_gpu_band_row_assignment", "krysp_gpu_read_assignment_file", "krysp_gpu_sub_create", "krysp_gpu_sub_info",
     "krysp_gpu_sub_local", "krysp_gpu_sub_interfaces", "krysp_gpu_sub_owners", "krysp_gpu_sub_assemble_spmv",
     "krysp_gpu_sub_dot", "krysp_gpu_sub_solve_cg", "krysp_gpu_sub_destroy", "krysp_gpu_solve_cg_substructured_host",

@@ -287,6 +287,30 @@ class Context:
         check(self.L.krysp_gpu_mat_generate(self.h, kind.encode(), n, pe, C.byref(h)))
         return DeviceMatrix(self, h)
 
+    # --- ingest (matrix_market.cpp, formats.cpp:17-63) -------------------------------
+    def build_coo(self, n_rows: int, n_cols: int, row_idx, col_idx, values, fmt: str = "coo") -> "DeviceMatrix":
+        """build_coo on the device (sorted, duplicates summed); fmt "coo" or "csr"."""
+        r, c, v = _i64(row_idx), _i64(col_idx), _f64(values)
+        if not (len(r) == len(c) == len(v)):
+            raise _lib.DimensionMismatch("triple arrays differ in length")
+        h = C.c_void_p()
+        check(self.L.krysp_gpu_mat_build_coo(self.h, C.c_int64(n_rows), C.c_int64(n_cols), C.c_int64(len(v)), _p(r),
+                                             _p(c), _p(v), C.c_int32(FORMATS[fmt]), C.byref(h)))
+        return DeviceMatrix(self, h)
+
+    def read_matrix_market(self, path: str, fmt: str = "coo") -> "DeviceMatrix":
+        """read_matrix_market (matrix_market.cpp:21-116) straight into a device matrix."""
+        h = C.c_void_p()
+        check(self.L.krysp_gpu_read_matrix_market(self.h, str(path).encode(), C.c_int32(FORMATS[fmt]), C.byref(h)))
+        return DeviceMatrix(self, h)
+
+    def parse_matrix_market(self, text, fmt: str = "coo") -> "DeviceMatrix":
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        h = C.c_void_p()
+        check(self.L.krysp_gpu_parse_matrix_market(self.h, b, C.c_size_t(len(b)), C.c_int32(FORMATS[fmt]),
+                                                   C.byref(h)))
+        return DeviceMatrix(self, h)
+
 
 class DeviceArray:
     """A float64 device buffer (the device-side std::span<double>)."""
@@ -367,6 +391,10 @@ class DeviceMatrix:
         h = C.c_void_p()
         check(self.ctx.L.krysp_gpu_mat_convert(self.h, FORMATS[fmt], hyb_width, slot_cap, C.byref(h)))
         return DeviceMatrix(self.ctx, h)
+
+    def write_matrix_market(self, path: str) -> None:
+        """write_matrix_market (matrix_market.cpp:119-141): coordinate real general, %.17g."""
+        check(self.ctx.L.krysp_gpu_write_matrix_market(self.h, str(path).encode()))
 
     def transpose(self) -> "DeviceMatrix":
         h = C.c_void_p()

@@ -648,7 +648,7 @@ krysp_status krysp_gpu_read_assignment_file(const char* path, int64_t expected_n
             std::istringstream is(line);
             long long id;
             if (!(is >> id) || (id < 0 && id != -1))
-                kg::fail(KRYSP_PARSE_ERROR, "line %ld: expected a subdomain id (or -1 for a shared equation)", line_no);
+                kg::fail(KRYSP_PARSE_ERROR, "expected a subdomain id (or -1 for a shared equation) (line %ld)", line_no);
             a.push_back(id);
         }
         if ((int64_t)a.size() != expected_n)
