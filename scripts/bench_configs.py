@@ -7,7 +7,8 @@ and parity against the reference on the B200.  One JSON object per line.
   C4  GCR(50) / BiCGStab(4) / tfQMR / BiCGStab on the 27-point stencil 320^3, HYB (auto width and
       w = 26): FAST it/s; parity at 80^3 vs the survey goldens
   C5  SpMV on power-law rows (1M-10M rows), CSR/HYB/COO + tune_spmv
-Usage: python scripts/bench_configs.py [C1 C2 C4 C5]
+  F1  sub-structured CG (1 and 8 subdomains) + EXACT bit-identity vs the reference
+Usage: python scripts/bench_configs.py [C1 C2 C4 C5 F1]
 """
 import json
 import os
@@ -159,12 +160,50 @@ def c5(ctx, R):
         emit(row)
 
 
+def f1(ctx, R):
+    """Sub-structured CG: 3D 7-pt 200^3 split into 1 and 8 subdomains (all on
+    this GPU), FAST device-resident throughput + roofline; EXACT bit-identity vs the reference
+    on 48^3 with 4 subdomains."""
+    from paper_2108_13162_b200 import substructure as ss
+    n = 200
+    A = ctx.generate("lap3d7", n).to_host()
+    N, nnz = A.n_rows, int(A.row_ptr[-1])
+    for parts in (1, 8):
+        t0 = time.perf_counter()
+        P = ss.Partition(ctx, A, n_parts=parts)
+        tp = time.perf_counter() - t0
+        dof = sum(P.info(s)["dof"] for s in range(parts))
+        knz = sum(P.info(s)["nnz"] for s in range(parts))
+        cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=1000, tolerance=1e-30)
+        P.solve_cg(np.ones(N), cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=20,
+                                                   tolerance=1e-30))  # module load + warm-up
+        r = P.solve_cg(np.ones(N), cfg=cfg)
+        # SpMV of every K_s + dot2 (4 streams) + update (9) + axpby (3) per iteration
+        B = 12 * knz + 4 * (dof + parts) + 16 * dof + 8 * dof * 16
+        t = r.device_time / r.iterations
+        emit({"config": "F1", "workload": f"sub-structured CG, lap3d7 {n}^3 ({N:,} rows), {parts} subdomain(s) on one "
+                                          f"GPU, FAST", "partition_s": tp, "dof_total": dof, "it_per_s": 1 / t,
+              "iterations": r.iterations, "bytes_per_iteration": B, "roofline_frac": B / t / 1e9 / PEAK})
+    if R:
+        m = 48
+        Am = ctx.generate("lap3d7", m).to_host()
+        Nm = Am.n_rows
+        a = ss.band_row_assignment(Nm, 4)
+        got = ss.solve_cg_substructured(ctx, Am, np.ones(Nm), np.zeros(Nm), a, kg.SolverConfig(mode="exact"))
+        rm = R.from_csr(Am)
+        want = R.solve_cg_substructured(rm, np.ones(Nm), np.zeros(Nm), a)
+        emit({"config": "F1", "check": f"EXACT sub-structured CG lap3d7 {m}^3, 4 subdomains vs reference",
+              "iterations": got.iterations, "ref_iterations": want["iterations"],
+              "bitwise_history": bool(np.array_equal(got.residual_history, want["residual_history"])),
+              "bitwise_solution": bool(np.array_equal(got.solution, want["solution"]))})
+
+
 def main():
-    which = sys.argv[1:] or ["C1", "C2", "C4", "C5"]
+    which = sys.argv[1:] or ["C1", "C2", "C4", "C5", "F1"]
     ctx = kg.Context(0)
     R = Ref() if os.path.exists(REF_SO) else None
     for w in which:
-        {"C1": c1, "C2": c2, "C4": c4, "C5": c5}[w](ctx, R)
+        {"C1": c1, "C2": c2, "C4": c4, "C5": c5, "F1": f1}[w](ctx, R)
 
 
 if __name__ == "__main__":

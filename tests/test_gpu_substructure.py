@@ -248,3 +248,24 @@ def test_nccl_single_subdomain(ctx, port, ref):
     np.testing.assert_array_equal(rep.residual_history, want["residual_history"])
     np.testing.assert_array_equal(rep.solution, want["solution"])
     P.close()
+
+
+@pytest.mark.parametrize("parts", [1, 3, 8])
+def test_fast_device_resident_matches_exact(ctx, port, ref, parts):
+    """FAST sub-structured CG (fused, device-resident) vs the reference trajectory."""
+    m = port.generate("poisson2d", 40)
+    A = csr_of(m)
+    n = 1600
+    b = np.random.default_rng(4).uniform(0.5, 1.5, n)
+    want = ref.solve_cg_substructured(ref.from_csr(m), b, np.zeros(n), ss.band_row_assignment(n, parts))
+    P = ss.Partition(ctx, A, n_parts=parts)
+    got = P.solve_cg(b, cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0)))
+    assert got.converged and abs(got.iterations - want["iterations"]) <= 1
+    k = min(got.iterations, want["iterations"])
+    np.testing.assert_allclose(got.residual_history[:k], want["residual_history"][:k], rtol=1e-8, atol=1e-12)
+    assert abs(got.final_residual_measure - want["final_residual_measure"]) <= 1e-10
+    np.testing.assert_allclose(got.solution, want["solution"], rtol=1e-6, atol=1e-9)
+    # bounded iteration budget: not converged, exactly max_iterations, same prefix
+    few = P.solve_cg(b, cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=5))
+    assert not few.converged and few.iterations == 5
+    np.testing.assert_allclose(few.residual_history, want["residual_history"][:5], rtol=1e-10)
