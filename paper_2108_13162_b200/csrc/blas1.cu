@@ -122,18 +122,12 @@ __global__ void __launch_bounds__(32 * kExactWarps)
     if (!out) return;  // partials only (k_chunk_partials)
     __threadfence();  // every lane wrote a partial (last_block fences thread 0 only)
     if (last_block(counter)) {
-        if (w == 0) {
-            // strict left-to-right fold (kernels.cpp:80-83)
-            double total = 0.0;
-            for (int64_t b = 0; b < n_chunks; b += 32) {
-                const double v = (b + lane < n_chunks) ? __ldcg(partials + b + lane) : 0.0;
-                const int cnt = (int)(n_chunks - b < 32 ? n_chunks - b : 32);
-                for (int q = 0; q < cnt; ++q) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, q));
-            }
-            if (lane == 0) {
-                *out = total;
-                *counter = 0;
-            }
+        // strict left-to-right fold (kernels.cpp:80-83): the block stages the partials in
+        // shared memory (coalesced), one thread runs the dependent add chain from registers
+        const double total = ordered_fold(partials, n_chunks, &tile[0][0][0]);
+        if (threadIdx.x == 0) {
+            *out = total;
+            *counter = 0;
         }
     }
 }

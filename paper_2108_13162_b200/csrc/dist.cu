@@ -1151,11 +1151,13 @@ __global__ void dot_fragments_kernel(const double* __restrict__ x, const double*
     }
 }
 
-// one warp: the reference fold over all ranks' records in global row order.  bands: 2P
-// int64 (lo, hi); each record starts at rank * cap.
-__global__ void dot_fold_kernel(const double* __restrict__ G, int64_t cap, const int64_t* __restrict__ bands, int P,
-                                int64_t bs, int64_t N, double* out) {
-    const int lane = threadIdx.x;
+// one block: the reference fold over all ranks' records in global row order.  bands: 2P
+// int64 (lo, hi); each record starts at rank * cap.  Thread 0 carries the chain; the whole
+// chunks are staged through shared memory tile by tile (as ordered_fold).
+__global__ void __launch_bounds__(256) dot_fold_kernel(const double* __restrict__ G, int64_t cap,
+                                                       const int64_t* __restrict__ bands, int P, int64_t bs,
+                                                       int64_t N, double* out) {
+    __shared__ double buf[kFoldTile];
     double total = 0.0, chunk = 0.0;
     for (int r = 0; r < P; ++r) {
         const int64_t lo = bands[2 * r], hi = bands[2 * r + 1];
@@ -1163,32 +1165,43 @@ __global__ void dot_fold_kernel(const double* __restrict__ G, int64_t cap, const
         const int64_t last = max(first, hi / bs * bs);
         const double* rec = G + (int64_t)r * cap;
         const int64_t H = first - lo, F = (last - first) / bs, T = hi - last;
-        // head products: rows lo .. first-1 (continue the chunk opened by the previous band)
-        for (int64_t i = 0; i < H; ++i) {
-            chunk = __dadd_rn(chunk, __ldcg(rec + i));
-            const int64_t g = lo + i + 1;
-            if (g % bs == 0 || g == N) {
-                total = __dadd_rn(total, chunk);
-                chunk = 0.0;
+        if (threadIdx.x == 0)  // head products: rows lo .. first-1 (continue the chunk opened before)
+            for (int64_t i = 0; i < H; ++i) {
+                chunk = __dadd_rn(chunk, __ldcg(rec + i));
+                const int64_t g = lo + i + 1;
+                if (g % bs == 0 || g == N) {
+                    total = __dadd_rn(total, chunk);
+                    chunk = 0.0;
+                }
+            }
+        for (int64_t b0 = 0; b0 < F; b0 += kFoldTile) {  // whole chunks, left to right
+            const int cnt = (int)(F - b0 < kFoldTile ? F - b0 : kFoldTile);
+            __syncthreads();
+            for (int i = threadIdx.x; i < cnt; i += blockDim.x) buf[i] = __ldcg(rec + H + b0 + i);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int i = 0;
+                for (; i + 16 <= cnt; i += 16) {
+                    double v[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) v[k] = buf[i + k];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) total = __dadd_rn(total, v[k]);
+                }
+                for (; i < cnt; ++i) total = __dadd_rn(total, buf[i]);
             }
         }
-        // whole chunks, folded left to right (warp-prefetched)
-        for (int64_t b0 = 0; b0 < F; b0 += 32) {
-            const double v = (b0 + lane < F) ? __ldcg(rec + H + b0 + lane) : 0.0;
-            const int cnt = (int)(F - b0 < 32 ? F - b0 : 32);
-            for (int q = 0; q < cnt; ++q) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, q));
-        }
-        // tail products: rows last .. hi-1 (a chunk the next band may continue)
-        for (int64_t i = 0; i < T; ++i) {
-            chunk = __dadd_rn(chunk, __ldcg(rec + H + F + i));
-            const int64_t g = last + i + 1;
-            if (g % bs == 0 || g == N) {
-                total = __dadd_rn(total, chunk);
-                chunk = 0.0;
+        if (threadIdx.x == 0)  // tail products: rows last .. hi-1 (a chunk the next band may continue)
+            for (int64_t i = 0; i < T; ++i) {
+                chunk = __dadd_rn(chunk, __ldcg(rec + H + F + i));
+                const int64_t g = last + i + 1;
+                if (g % bs == 0 || g == N) {
+                    total = __dadd_rn(total, chunk);
+                    chunk = 0.0;
+                }
             }
-        }
     }
-    if (lane == 0) *out = total;
+    if (threadIdx.x == 0) *out = total;
 }
 
 struct DistEngine : Engine {
@@ -1310,7 +1323,7 @@ struct DistEngine : Engine {
             }
             if (!d->emulated())
                 KG_NCCL(NcclApi::get().AllGather(rec, gathered, (size_t)cap, ncclDouble, d->comm, c->stream));
-            dot_fold_kernel<<<1, 32, 0, c->stream>>>(gathered, cap, d_bands, d->nparts, bs, N, c->d_scalars);
+            dot_fold_kernel<<<1, 256, 0, c->stream>>>(gathered, cap, d_bands, d->nparts, bs, N, c->d_scalars);
             KG_LAUNCH(c);
             KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
             stream_wait(c);

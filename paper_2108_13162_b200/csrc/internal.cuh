@@ -225,6 +225,33 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
     return s_last;
 }
 
+// The reference's strict left-to-right fold of n partials (kernels.cpp:80-83), total from
+// +0.0, by a whole block: tiles of kFoldTile partials are staged in shared memory `buf`
+// (>= kFoldTile doubles) with coalesced loads, then thread 0 runs the dependent add chain
+// from registers, 16 loads ahead.  Returns the total in thread 0 (other threads: 0.0).
+constexpr int kFoldTile = 4096;
+__device__ __forceinline__ double ordered_fold(const double* partials, int64_t n, double* buf) {
+    double total = 0.0;
+    for (int64_t b0 = 0; b0 < n; b0 += kFoldTile) {
+        const int cnt = (int)(n - b0 < kFoldTile ? n - b0 : kFoldTile);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) buf[i] = __ldcg(partials + b0 + i);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int i = 0;
+            for (; i + 16 <= cnt; i += 16) {
+                double v[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[k] = buf[i + k];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) total = __dadd_rn(total, v[k]);
+            }
+            for (; i < cnt; ++i) total = __dadd_rn(total, buf[i]);
+        }
+    }
+    return total;
+}
+
 // Same as block_sum for a runtime block size (multiple of 32, <= 1024).
 __device__ __forceinline__ double block_sum_dyn(double v, double* sh) {
     v = warp_sum(v);
