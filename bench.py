@@ -366,6 +366,9 @@ def run_ours_dist(args, dist):
     rep = D.pcg_report()
     assert rep.iterations == args.warmup + args.steps, f"converged inside the timed region ({rep.iterations})"
     kpi = D.kernels_per_iteration
+    # the halo-overlapped SpMV phase alone (CUDA events, eager iterations, max over ranks)
+    t_spmv_loc, _ = D.pcg_profile(min(20, max(1, GOLDEN_ITERS - rep.iterations - 5)))
+    t_spmv = dist.max(t_spmv_loc)
     # finish the solve for the parity check (same problem as the single-GPU golden)
     D.pcg_run()
     fin = D.pcg_report()
@@ -408,6 +411,10 @@ def run_ours_dist(args, dist):
                          "achieved": B_iter_gpu / t_it / 1e9, "peak": bw_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": B_iter_gpu / t_it / 1e9 / bw_peak, "traffic": None},
             "gpu_launches": kpi * args.steps, "clocks": ck,
+            "spmv_gflops": 2 * nnz_total / t_spmv / 1e9,
+            "spmv_phase": {"ms": t_spmv * 1e3, "what": "halo exchange (NCCL, overlapped) + interior / boundary "
+                                                       "row SpMV with the fused <p,Ap> partials, max over ranks",
+                           "frac": spmv_bytes(N, N, nnz_total) / dist.world / t_spmv / 1e9 / bw_peak},
             "bicgstab": {"value": bi_steps / t_bi, "unit": "iterations/s", "iterations_timed": bi_steps,
                          "converged_early": bi_ran < args.warmup + bi_steps, "kernels_per_iteration": bi_kpi,
                          "frac": (2 * spmv_bytes(N, N, nnz_total) + 136 * N) / dist.world / (t_bi / bi_steps) / 1e9

@@ -303,6 +303,9 @@ krysp_status krysp_gpu_dist_pcg_run(krysp_gpu_dist* d, double* seconds);
 krysp_status krysp_gpu_dist_pcg_report(krysp_gpu_dist* d, krysp_report* report, double* h_history);
 krysp_status krysp_gpu_dist_pcg_solution(krysp_gpu_dist* d, int32_t part, double* d_x);
 int32_t krysp_gpu_dist_kernels_per_iteration(const krysp_gpu_dist* d);
+/* n eagerly enqueued P-CG iterations timed with CUDA events: the mean halo-overlapped SpMV
+ * phase (halo + interior + boundary rows + fused <p, Ap> partials) and the mean iteration */
+krysp_status krysp_gpu_dist_pcg_profile(krysp_gpu_dist* d, int64_t n, double* spmv_seconds, double* iter_seconds);
 /* Any host-driven recurrence (PCG, CG_CLASSIC, GCR, BICGSTAB, BICGSTAB_L, TFQMR; not BICGCR)
  * over the partition, solve_* semantics (solvers.hpp:54-87) per held band: d_x holds x0 on
  * entry and the band of the solution on return.  KRYSP_MODE_EXACT replays the reference's

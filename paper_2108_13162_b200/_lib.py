@@ -145,7 +145,7 @@ EXPORTS = [
     "krysp_gpu_dist_generate", "krysp_gpu_dist_set_csr", "krysp_gpu_dist_setup", "krysp_gpu_dist_part_info",
     "krysp_gpu_dist_spmv", "krysp_gpu_dist_pcg_create", "krysp_gpu_dist_krylov_create", "krysp_gpu_dist_pcg_iterate", "krysp_gpu_dist_pcg_time",
     "krysp_gpu_dist_pcg_run", "krysp_gpu_dist_pcg_report", "krysp_gpu_dist_pcg_solution",
-    "krysp_gpu_dist_kernels_per_iteration", "krysp_gpu_dist_solve", "krysp_gpu_dist_destroy",
+    "krysp_gpu_dist_kernels_per_iteration", "krysp_gpu_dist_pcg_profile", "krysp_gpu_dist_solve", "krysp_gpu_dist_destroy",
     "krysp_gpu_mat_build_coo", "krysp_gpu_read_matrix_market", "krysp_gpu_parse_matrix_market",
     "krysp_gpu_write_matrix_market",
     "krysp_gpu_band_row_assignment", "krysp_gpu_read_assignment_file", "krysp_gpu_sub_create", "krysp_gpu_sub_info",

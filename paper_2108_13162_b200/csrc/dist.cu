@@ -875,7 +875,7 @@ void dist_iteration_bicg(krysp_gpu_dist* d) {
 }
 
 // one distributed P-CG iteration (all held parts), enqueued on ctx->stream
-void dist_iteration(krysp_gpu_dist* d) {
+void dist_iteration(krysp_gpu_dist* d, cudaEvent_t ev_spmv_done = nullptr) {
     krysp_gpu_ctx* c = d->ctx;
     cudaStream_t s = c->stream;
     const int64_t before = c->launches;
@@ -909,6 +909,7 @@ void dist_iteration(krysp_gpu_dist* d) {
                                        P.part_slot + 2 * kPartialCap, (int)gc[i]);
         KG_LAUNCH(c);
     }
+    if (ev_spmv_done) KG_CUDA(cudaEventRecord(ev_spmv_done, s));
     device_allreduce(d, offsetof(DistCgState, sigma_loc), offsetof(DistCgState, sigma), s);
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
@@ -1590,6 +1591,38 @@ krysp_status krysp_gpu_dist_pcg_solution(krysp_gpu_dist* d, int32_t part, double
 }
 
 int32_t krysp_gpu_dist_kernels_per_iteration(const krysp_gpu_dist* d) { return d ? d->kernels_per_iteration : 0; }
+
+krysp_status krysp_gpu_dist_pcg_profile(krysp_gpu_dist* d, int64_t n, double* spmv_seconds, double* iter_seconds) {
+    return guard([&] {
+        if (!d || !spmv_seconds || !iter_seconds) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (!d->pcg || d->method != KRYSP_PCG) kg::fail(KRYSP_ERROR, "no distributed P-CG (krysp_gpu_dist_pcg_create)");
+        if (n < 1) kg::fail(KRYSP_ERROR, "profile needs n >= 1");
+        cudaStream_t s = d->ctx->stream;
+        cudaEvent_t e[3];
+        for (auto& x : e) KG_CUDA(cudaEventCreate(&x));
+        double ts = 0.0, ti = 0.0;
+        std::exception_ptr err;
+        try {
+            for (int64_t i = 0; i < n; ++i) {
+                KG_CUDA(cudaEventRecord(e[0], s));
+                kg::dist_iteration(d, e[1]);
+                KG_CUDA(cudaEventRecord(e[2], s));
+                KG_CUDA(cudaEventSynchronize(e[2]));
+                float a = 0.f, b = 0.f;
+                KG_CUDA(cudaEventElapsedTime(&a, e[0], e[1]));
+                KG_CUDA(cudaEventElapsedTime(&b, e[0], e[2]));
+                ts += a * 1e-3;
+                ti += b * 1e-3;
+            }
+        } catch (...) {
+            err = std::current_exception();
+        }
+        for (auto& x : e) cudaEventDestroy(x);
+        if (err) std::rethrow_exception(err);
+        *spmv_seconds = ts / (double)n;
+        *iter_seconds = ti / (double)n;
+    });
+}
 
 krysp_status krysp_gpu_dist_solve(krysp_gpu_dist* d, int32_t method, const double* const* d_b, double* const* d_x,
                                   const krysp_solver_cfg* cfg, krysp_report* report, double* h_history) {

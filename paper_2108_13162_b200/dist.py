@@ -135,6 +135,12 @@ class DistSystem:
         check(self.L.krysp_gpu_dist_pcg_run(self.h, C.byref(t)))
         return t.value
 
+    def pcg_profile(self, n: int):
+        """(mean SpMV-phase seconds, mean iteration seconds) over n eager P-CG iterations."""
+        a, b = C.c_double(), C.c_double()
+        check(self.L.krysp_gpu_dist_pcg_profile(self.h, I64(n), C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def pcg_report(self) -> SolveReport:
         rep = _lib.Report()
         hist = np.zeros(max(self.cfg.max_iterations, 1))
