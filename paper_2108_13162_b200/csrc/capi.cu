@@ -501,7 +501,8 @@ krysp_status krysp_gpu_autotune_policy(const krysp_gpu_mat* m, krysp_policy* out
         krysp_policy p{256, 1, 0, 0};
         if (m->format == KRYSP_FMT_CSR && m->n_rows > 0) {
             const double mean = (double)m->nnz / (double)m->n_rows;
-            if (m->max_tile_nnz + 8 > 8192 || mean > 24.0) {
+            // irregular rows (power law) or long rows: vector kernel, tw ~ the mean row length
+            if (m->max_tile_nnz + 8 > 8192 || mean > 24.0 || csr_is_irregular(m)) {
                 int64_t tw = 1;
                 while (tw < 32 && (double)(tw * 2) <= mean * 1.5) tw *= 2;
                 p.workers_per_row = tw;

@@ -193,25 +193,24 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
         if (r < n) {
             const int32_t* jc = E.jcoef + r;
             const double* cf = E.coef + r;
-            int s = 0;
-            for (; s + 4 <= E.width; s += 4) {
-                int32_t c[4];
-                double v[4];
+            // 8 slots per batch: all column / value loads, then all x gathers in flight before
+            // the slot-ordered sum (the reference's sequential order, kernels.cpp:203-206)
+            for (int s = 0; s < E.width; s += 8) {
+                int32_t c[8];
+                double v[8], xv[8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    c[j] = __ldcs(jc + (int64_t)(s + j) * n);
-                    v[j] = __ldcs(cf + (int64_t)(s + j) * n);
+                for (int j = 0; j < 8; ++j) {
+                    c[j] = E.n_cols;
+                    if (s + j < E.width) {
+                        c[j] = __ldcs(jc + (int64_t)(s + j) * n);
+                        v[j] = __ldcs(cf + (int64_t)(s + j) * n);
+                    }
                 }
-                double xv[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
+                for (int j = 0; j < 8; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < 8; ++j)
                     if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
-            }
-            for (; s < E.width; ++s) {
-                const int32_t c = __ldcs(jc + (int64_t)s * n);
-                if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * n), __ldg(x + c));
             }
             epi.row(r, sum);
         }
