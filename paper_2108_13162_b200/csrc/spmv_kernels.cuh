@@ -19,6 +19,8 @@
 // by every thread of every block exactly once (block reductions live there); Epi::active()
 // is read once at entry and lets a converged solver's queued iterations exit immediately.
 #pragma once
+
+#include <type_traits>
 #include <unordered_map>
 
 #include "internal.cuh"
@@ -101,12 +103,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 struct TmaTileLayout {
-    int cap;  // entries per stage (>= max tile nnz + 8, multiple of 4)
+    int cap;     // entries per stage (>= max tile nnz + 8, multiple of 4)
+    int staged;  // per-row epilogue vectors moved with the tile (Epi::kStaged)
     __host__ __device__ int val_bytes() const { return (cap + 8) * 8; }
     __host__ __device__ int col_bytes() const { return (cap + 8) * 4; }
     __host__ __device__ int rp_bytes() const { return (kTileRows + 8) * 4; }
-    __host__ __device__ int stage_bytes() const { return val_bytes() + col_bytes() + rp_bytes(); }
+    __host__ __device__ int vec_bytes() const { return (kTileRows + 2) * 8; }
+    __host__ __device__ int stage_bytes() const { return val_bytes() + col_bytes() + rp_bytes() + staged * vec_bytes(); }
     __host__ __device__ int total_bytes() const { return 2 * stage_bytes() + 64; }
+};
+
+// Epilogues that read per-row vectors (Jacobi inverse, dot operands) declare them as
+// `static constexpr int kStaged` + `staged_src(k)`: the TMA producer bulk-copies the tile's
+// rows of each into shared memory with the matrix tile, and `row_staged(r, v, sv)` gets the
+// values from there instead of issuing latency-exposed loads after the sum.
+template <class E, class = void>
+struct epi_staged {
+    static constexpr int value = 0;
+};
+template <class E>
+struct epi_staged<E, std::void_t<decltype(E::kStaged)>> {
+    static constexpr int value = E::kStaged;
 };
 
 template <class Epi>
@@ -119,9 +136,13 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
     const int64_t n_tiles = ((int64_t)A.n_rows + kTileRows - 1) / kTileRows;
     const uint64_t pol = evict_first_policy();
 
+    constexpr int NS = epi_staged<Epi>::value;
     auto stage_ptr = [&](int s, int part) -> unsigned char* {
         unsigned char* b = stage_base + s * L.stage_bytes();
-        return part == 0 ? b : part == 1 ? b + L.val_bytes() : b + L.val_bytes() + L.col_bytes();
+        return part == 0   ? b
+               : part == 1 ? b + L.val_bytes()
+               : part == 2 ? b + L.val_bytes() + L.col_bytes()
+                           : b + L.val_bytes() + L.col_bytes() + L.rp_bytes() + (part - 3) * L.vec_bytes();
     };
     // thread 0: bulk-copy tile `t` into stage `s`
     auto issue = [&](int64_t t, int s) {
@@ -132,10 +153,22 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
         const int32_t ca = k0 & ~3, cb = (k1 + 3) & ~3;
         const uint32_t bv = (uint32_t)(vb - va) * 8u, bc = (uint32_t)(cb - ca) * 4u;
         const uint32_t brp = (uint32_t)(((r1 - r0 + 1) + 3) & ~3) * 4u;
-        mbar_arrive_expect_tx(&bars[s], bv + bc + brp);
+        const uint32_t bvec = (uint32_t)(((r1 - r0) + 1) & ~1) * 8u;  // padded vectors: +1 row is readable
+        uint32_t bst = 0;
+        if constexpr (NS > 0) {
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if (epi.staged_src(k)) bst += bvec;
+        }
+        mbar_arrive_expect_tx(&bars[s], bv + bc + brp + bst);
         bulk_g2s(stage_ptr(s, 2), A.row_ptr + r0, brp, &bars[s], pol);
         if (bv) bulk_g2s(stage_ptr(s, 0), A.val + va, bv, &bars[s], pol);
         if (bc) bulk_g2s(stage_ptr(s, 1), A.col + ca, bc, &bars[s], pol);
+        if constexpr (NS > 0) {
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if (epi.staged_src(k)) bulk_g2s(stage_ptr(s, 3 + k), epi.staged_src(k) + r0, bvec, &bars[s], pol);
+        }
     };
 
     if (threadIdx.x == 0) {
@@ -174,7 +207,14 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
 #pragma unroll 8
                 for (int j = 0; j < len; ++j) sum = madd(sum, s_val[av + j], __ldg(x + s_col[ac + j]));
             }
-            epi.row(r, sum);
+            if constexpr (NS > 0) {
+                double sv[NS > 0 ? NS : 1];
+#pragma unroll
+                for (int k = 0; k < NS; ++k) sv[k] = reinterpret_cast<const double*>(stage_ptr(s, 3 + k))[threadIdx.x];
+                epi.row_staged(r, sum, sv);
+            } else {
+                epi.row(r, sum);
+            }
         }
         __syncthreads();  // stage s is re-filled in the next-but-one iteration
     }
@@ -193,24 +233,48 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
         if (r < n) {
             const int32_t* jc = E.jcoef + r;
             const double* cf = E.coef + r;
-            // 8 slots per batch: all column / value loads, then all x gathers in flight before
-            // the slot-ordered sum (the reference's sequential order, kernels.cpp:203-206)
-            for (int s = 0; s < E.width; s += 8) {
-                int32_t c[8];
-                double v[8], xv[8];
+            if constexpr (std::is_same<Epi, EpiStore>::value) {
+                // plain store: 8 slots per batch — all column / value loads, then all x gathers
+                // in flight before the slot-ordered sum (kernels.cpp:203-206)
+                for (int s = 0; s < E.width; s += 8) {
+                    int32_t c[8];
+                    double v[8], xv[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    c[j] = E.n_cols;
-                    if (s + j < E.width) {
+                    for (int j = 0; j < 8; ++j) {
+                        c[j] = E.n_cols;
+                        if (s + j < E.width) {
+                            c[j] = __ldcs(jc + (int64_t)(s + j) * n);
+                            v[j] = __ldcs(cf + (int64_t)(s + j) * n);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
+                }
+            } else {
+                // solver epilogues (dot accumulators): 4-slot batches + a scalar tail keep the
+                // register count, hence the occupancy that overlaps the gathers
+                int s = 0;
+                for (; s + 4 <= E.width; s += 4) {
+                    int32_t c[4];
+                    double v[4], xv[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
                         c[j] = __ldcs(jc + (int64_t)(s + j) * n);
                         v[j] = __ldcs(cf + (int64_t)(s + j) * n);
                     }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
                 }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
+                for (; s < E.width; ++s) {
+                    const int32_t c = __ldcs(jc + (int64_t)s * n);
+                    if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * n), __ldg(x + c));
+                }
             }
             epi.row(r, sum);
         }
@@ -285,7 +349,7 @@ inline int64_t launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi,
     if (tiles == 0) return 0;
     int cap = (int)std::min<int64_t>(std::max<int64_t>(m->max_tile_nnz + 8, 64), kTileCapMax);
     cap = (cap + 3) & ~3;
-    const TmaTileLayout L{cap};
+    const TmaTileLayout L{cap, epi_staged<Epi>::value};
     const int smem = L.total_bytes();
     if (smem > 48 * 1024)
         KG_CUDA(cudaFuncSetAttribute(csr_tma_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
