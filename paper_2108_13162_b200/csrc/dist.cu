@@ -303,6 +303,19 @@ struct EpiBiPart {
         d2_add_prod(a0, w0 ? w0[r] : v, v);
         if (NACC == 2) d2_add_prod(a1, w1[r], v);
     }
+    // D^-1 and the dot operand ride with the TMA tile (views start at 256-row multiples)
+    static constexpr int kStaged = 2;
+    __device__ __forceinline__ const double* staged_src(int k) const { return k == 0 ? dinv : (NACC == 2 ? w1 : w0); }
+    __device__ __forceinline__ void row_staged(int64_t r, double v, const double* sv) {
+        if (dinv) v = __dmul_rn(v, sv[0]);
+        y[r] = v;
+        if (NACC == 2) {
+            d2_add_prod(a0, w0 ? w0[r] : v, v);
+            d2_add_prod(a1, sv[1], v);
+        } else {
+            d2_add_prod(a0, w0 ? sv[1] : v, v);
+        }
+    }
     __device__ __forceinline__ void finish() {
         __shared__ D2 sh[32];
         const D2 b0 = block_d2_dyn(a0, sh);
