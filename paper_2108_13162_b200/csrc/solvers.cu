@@ -619,6 +619,11 @@ struct EpiScale {
     const double* __restrict__ dinv;
     __device__ __forceinline__ bool active() const { return true; }
     __device__ __forceinline__ void row(int64_t r, double v) { y[r] = dinv ? __dmul_rn(v, dinv[r]) : v; }
+    static constexpr int kStaged = 1;  // D^-1 rides with the TMA tile
+    __device__ __forceinline__ const double* staged_src(int) const { return dinv; }
+    __device__ __forceinline__ void row_staged(int64_t r, double v, const double* sv) {
+        y[r] = dinv ? __dmul_rn(v, sv[0]) : v;
+    }
     __device__ __forceinline__ void finish() {}
 };
 
@@ -813,6 +818,19 @@ struct EpiTfqmrV {
         v[r] = vn;
         d2_add_prod(acc, vn, r0[r]);
     }
+    // D^-1, bu, v and r0 (all solver-owned, padded) ride with the TMA tile
+    static constexpr int kStaged = 4;
+    __device__ __forceinline__ const double* staged_src(int k) const {
+        return k == 0 ? dinv : k == 1 ? bu : k == 2 ? (const double*)v : r0;
+    }
+    __device__ __forceinline__ void row_staged(int64_t r, double val, const double* sv) {
+        const double bn = dinv ? __dmul_rn(val, sv[0]) : val;
+        bu_next[r] = bn;
+        const double vv = __dadd_rn(__dmul_rn(beta, sv[1]), __dmul_rn(beta2, sv[2]));
+        const double vn = __dadd_rn(__dmul_rn(1.0, bn), vv);
+        v[r] = vn;
+        d2_add_prod(acc, vn, sv[3]);
+    }
     __device__ __forceinline__ void finish() {
         __shared__ D2 sh[32];
         d2_grid_finish<1>(&acc, sh, partials, counter, out);
@@ -988,6 +1006,13 @@ struct EpiScaleDot {
         if (dinv) v = __dmul_rn(v, dinv[r]);
         y[r] = v;
         d2_add_prod(acc, w[r], v);
+    }
+    static constexpr int kStaged = 2;  // D^-1 and w ride with the TMA tile
+    __device__ __forceinline__ const double* staged_src(int k) const { return k == 0 ? dinv : w; }
+    __device__ __forceinline__ void row_staged(int64_t r, double v, const double* sv) {
+        if (dinv) v = __dmul_rn(v, sv[0]);
+        y[r] = v;
+        d2_add_prod(acc, sv[1], v);
     }
     __device__ __forceinline__ void finish() {
         __shared__ D2 sh[32];
