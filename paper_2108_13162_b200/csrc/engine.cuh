@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 
 #include "internal.cuh"
 
@@ -112,6 +113,21 @@ protected:
         }
     }
 };
+
+// Device-resident descent-form CG (descent.cu): FAST solve_cg_classic and
+// solve_cg_substructured.  apply_op computes kw = K w for every part (stream-ordered,
+// capturable); wt NULL = unit weights; comm: NCCL communicator across GPUs (one part per
+// process) or NULL (parts summed in order on this device).  Returns 0 or a kDescent* code.
+struct DescentPart {
+    int64_t n;
+    double *x, *g, *z, *w, *kw;
+    const double *inv, *wt;
+};
+enum { kDescentOk = 0, kDescentDenomNonFinite, kDescentBreakdown, kDescentRhoNonFinite, kDescentGammaNonFinite,
+       kDescentMeasureNonFinite };
+int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const std::function<void()>& apply_op,
+                  void* comm, double norm_g0, const krysp_solver_cfg& cfg, std::vector<double>& history,
+                  int64_t& iterations, double& measure);
 
 // The host-driven recurrences (pcg, cg_classic, gcr, bicgstab, bicgstab_l, tfqmr; FAST mode
 // uses the fused GCR / BiCGStab(l) / tfQMR variants) on an engine; report as krysp_report.

@@ -116,6 +116,28 @@ void cg_classic(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
     e.precond(g, z);
     e.copy(z, w);
     double measure = 1.0;
+    if (e.mode == KRYSP_MODE_FAST && e.A) {  // device-resident (descent.cu)
+        rep.mark(e.c->stream);
+        const DescentPart part{e.n, x, g, z, w, kw, e.jacobi ? (const double*)e.inv : nullptr, nullptr};
+        const double* wp = w;
+        double* kwp = kw;
+        auto op = [&]() { e.spmv(wp, kwp); };
+        int64_t its = 0;
+        const int st = fused_descent(e.c, {part}, op, nullptr, norm_g0, cfg, rep.history, its, measure);
+        rep.iterations = its;
+        rep.end(e.c->stream);
+        rep.final_measure = measure;
+        switch (st) {
+            case kDescentDenomNonFinite: fail(KRYSP_NON_FINITE, "descent denominator became non-finite");
+            case kDescentBreakdown: fail(KRYSP_BREAKDOWN, "cg: <Kw, w> vanished before convergence");
+            case kDescentRhoNonFinite: fail(KRYSP_NON_FINITE, "rho became non-finite");
+            case kDescentGammaNonFinite: fail(KRYSP_NON_FINITE, "gamma became non-finite");
+            case kDescentMeasureNonFinite: fail(KRYSP_NON_FINITE, "residual measure became non-finite");
+            default: break;
+        }
+        rep.converged = its > 0 && measure <= cfg.tolerance;
+        return;
+    }
     for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         e.spmv(w, kw);
         double denom = e.dot(kw, w);

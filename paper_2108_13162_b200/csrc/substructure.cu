@@ -29,6 +29,7 @@
 #include <sstream>
 #include <string>
 
+#include "engine.cuh"
 #include "nccl_api.cuh"
 #include "spmv_kernels.cuh"
 
@@ -502,236 +503,29 @@ struct SubVec {  // one device vector per held subdomain
 };
 
 // ------------------------------------------------------------------ FAST: device-resident loop
-// One iteration of the descent-form CG per subdomain, scalars and the convergence test on
-// the device, iterations CUDA-graph captured: SpMV of K_s + pack, the exchange, the interface
-// fold + both dots of the step length (<Kw, w>_W, <g, w>_W in one pass), a scalar kernel, the
-// x / g / z update fused with <z, Kw>_W and <g, g>_W, a scalar kernel, the direction update.
-// Dots are compensated (Dot2) per subdomain and summed over subdomains in order (emulation)
-// or by an NCCL allreduce of the (sum, compensation) pairs.
-struct SubCgState {
-    double red_loc[4];  // this subdomain's two dots, (sum, compensation) each
-    double red[4];      // summed over subdomains
-    double norm_g0, tol, denom, rho, gamma, measure;
-    long long iter, max_it;
-    int done, status;
-};
-enum { kScOk = 0, kScDenomNonFinite, kScBreakdown, kScRhoNonFinite, kScGammaNonFinite, kScMeasureNonFinite };
-
-__device__ __forceinline__ double sc_red(const SubCgState* st, int k) { return st->red[2 * k] + st->red[2 * k + 1]; }
-
-__device__ __forceinline__ void sc_finish2(D2 a0, D2 a1, D2* sh, double* partials, unsigned* counter, SubCgState* st) {
-    const D2 b0 = block_d2_dyn(a0, sh);
-    const D2 b1 = block_d2_dyn(a1, sh);
-    if (threadIdx.x == 0) {
-        double* q = partials + 4 * blockIdx.x;
-        q[0] = b0.s, q[1] = b0.c, q[2] = b1.s, q[3] = b1.c;
-    }
-    if (last_block(counter)) {
-        D2 t0{0.0, 0.0}, t1{0.0, 0.0};
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
-            const double* q = partials + 4 * i;
-            t0 = d2_merge(t0, D2{__ldcg(q), __ldcg(q + 1)});
-            t1 = d2_merge(t1, D2{__ldcg(q + 2), __ldcg(q + 3)});
-        }
-        t0 = block_d2_dyn(t0, sh);
-        t1 = block_d2_dyn(t1, sh);
-        if (threadIdx.x == 0) {
-            st->red_loc[0] = t0.s, st->red_loc[1] = t0.c, st->red_loc[2] = t1.s, st->red_loc[3] = t1.c;
-            *counter = 0;
-        }
-    }
-}
-
-// <Kw, w>_W and <g, w>_W (distributed_dot's weighted form: dot(x, fl(y * w)))
-__global__ void __launch_bounds__(kSubNT) sc_dot2_kernel(int64_t n, const double* __restrict__ kw,
-                                                          const double* __restrict__ w, const double* __restrict__ g,
-                                                          const double* __restrict__ wt, SubCgState* st,
-                                                          double* partials, unsigned* counter) {
-    if (*(volatile int*)&st->done) return;
-    __shared__ D2 sh[32];
-    D2 a0{0.0, 0.0}, a1{0.0, 0.0};
-    for (int64_t i = blockIdx.x * (int64_t)kSubNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kSubNT) {
-        const double ww = __dmul_rn(w[i], wt[i]);
-        d2_add_prod(a0, kw[i], ww);
-        d2_add_prod(a1, g[i], ww);
-    }
-    sc_finish2(a0, a1, sh, partials, counter, st);
-}
-
-// x += rho w; g += rho Kw; z = D^-1 g; <z, Kw>_W and <g, g>_W
-__global__ void __launch_bounds__(kSubNT) sc_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ g,
-                                                            double* __restrict__ z, const double* __restrict__ w,
-                                                            const double* __restrict__ kw,
-                                                            const double* __restrict__ inv,
-                                                            const double* __restrict__ wt, SubCgState* st,
-                                                            double* partials, unsigned* counter) {
-    if (*(volatile int*)&st->done) return;
-    __shared__ D2 sh[32];
-    const double rho = st->rho;
-    D2 a0{0.0, 0.0}, a1{0.0, 0.0};
-    for (int64_t i = blockIdx.x * (int64_t)kSubNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kSubNT) {
-        const double kwi = kw[i], wti = wt[i];
-        x[i] = __dadd_rn(__dmul_rn(rho, w[i]), x[i]);
-        const double gi = __dadd_rn(__dmul_rn(rho, kwi), g[i]);
-        g[i] = gi;
-        const double zi = inv ? __dmul_rn(gi, inv[i]) : gi;
-        z[i] = zi;
-        d2_add_prod(a0, zi, __dmul_rn(kwi, wti));
-        d2_add_prod(a1, gi, __dmul_rn(gi, wti));
-    }
-    sc_finish2(a0, a1, sh, partials, counter, st);
-}
-
-__device__ __forceinline__ void sc_fail(SubCgState* st, int code) {
-    st->status = code;
-    st->done = 1;
-}
-
-__global__ void sc_scalar1_kernel(SubCgState* st) {  // substructure.cpp:534-539
-    if (st->done) return;
-    const double denom = sc_red(st, 0);
-    if (!isfinite(denom)) return sc_fail(st, kScDenomNonFinite);
-    if (fabs(denom) < 1e-300) return sc_fail(st, kScBreakdown);
-    st->denom = denom;
-    st->rho = -sc_red(st, 1) / denom;
-    if (!isfinite(st->rho)) sc_fail(st, kScRhoNonFinite);
-}
-
-__global__ void sc_scalar2_kernel(SubCgState* st, double* history) {  // substructure.cpp:543-553
-    if (st->done) return;
-    st->gamma = -sc_red(st, 0) / st->denom;
-    if (!isfinite(st->gamma)) return sc_fail(st, kScGammaNonFinite);
-    const double measure = sqrt(sc_red(st, 1)) / st->norm_g0;
-    if (!isfinite(measure)) return sc_fail(st, kScMeasureNonFinite);
-    st->measure = measure;
-    history[st->iter] = measure;
-    st->iter += 1;
-    if (measure <= st->tol || st->iter >= st->max_it) st->done = 1;
-}
-
-// w = fl(1 * z) + fl(gamma * w) (axpby, kernels.cpp:109-118); skipped once converged
-__global__ void __launch_bounds__(kSubNT) sc_axpby_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ w,
-                                                           const SubCgState* st) {
-    if (*(volatile const int*)&st->done) return;
-    const double gamma = st->gamma;
-    for (int64_t i = blockIdx.x * (int64_t)kSubNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kSubNT)
-        w[i] = __dadd_rn(z[i], __dmul_rn(gamma, w[i]));
-}
-
-// the subdomain-order sum of the emulated subdomains' partial dots
-__global__ void sc_emu_reduce_kernel(SubCgState* sts, int ns) {
-    if (threadIdx.x != 0) return;
-    for (int k = 0; k < 4; ++k) {
-        double s = 0.0;
-        for (int j = 0; j < ns; ++j) s += sts[j].red_loc[k];
-        for (int j = 0; j < ns; ++j) sts[j].red[k] = s;
-    }
-}
-
-void sub_reduce(krysp_gpu_sub* h, SubCgState* d_st) {
-    if (h->emulated()) {
-        sc_emu_reduce_kernel<<<1, 32, 0, h->ctx->stream>>>(d_st, (int)h->held.size());
-        KG_LAUNCH(h->ctx);
-        return;
-    }
-    char* base = reinterpret_cast<char*>(d_st);
-    KG_NCCL(NcclApi::get().AllReduce(base + offsetof(SubCgState, red_loc), base + offsetof(SubCgState, red), 4,
-                                     ncclDouble, ncclSum, h->comm, h->ctx->stream));
-}
-
-// the FAST loop on device (setup — g, norm_g0, z, w — already done by the caller)
+// descent.cu's device-resident descent CG with the assembled product as the operator and the
+// weighted dots summed over subdomains (in order when emulated, NCCL allreduce otherwise).
 void fused_cg(krysp_gpu_sub* h, SubVec& x, SubVec& g, SubVec& z, SubVec& w, SubVec& kw, const SubVec* inv,
               double norm_g0, const krysp_solver_cfg& cfg, std::vector<double>& history, int64_t& iterations,
               double& measure) {
-    krysp_gpu_ctx* c = h->ctx;
-    cudaStream_t st = c->stream;
-    const size_t nh = h->held.size();
-    if ((int64_t)nh > kSlots) fail(KRYSP_ERROR, "FAST sub-structured CG holds at most %d subdomains per GPU", kSlots);
-    std::vector<SubCgState> init(nh);
-    for (auto& s0 : init) {
-        std::memset(&s0, 0, sizeof s0);
-        s0.norm_g0 = norm_g0;
-        s0.tol = cfg.tolerance;
-        s0.max_it = cfg.max_iterations;
-    }
-    SubCgState* d_st = dev_alloc<SubCgState>((int64_t)nh, false);
-    double* d_hist = dev_alloc<double>((int64_t)nh * cfg.max_iterations, false);
-    KG_CUDA(cudaMemcpyAsync(d_st, init.data(), sizeof(SubCgState) * nh, cudaMemcpyHostToDevice, st));
+    std::vector<DescentPart> parts;
+    for (size_t i = 0; i < h->held.size(); ++i)
+        parts.push_back({h->held[i].dof, x.v[i], g.v[i], z.v[i], w.v[i], kw.v[i],
+                         inv ? (const double*)inv->v[i] : nullptr, h->held[i].w});
     const krysp_policy auto_pol{0, 0, 0, 0};
-    auto grid = [&](int64_t n) { return grid_for(n, kSubNT, (int64_t)c->sm_count * 4); };
-    auto slot = [&](size_t i) { return c->d_partials + (int64_t)i * kPartialCap; };
-    auto cnt = [&](size_t i) { return c->d_counters + i; };
-    auto iteration = [&]() {
+    auto op = [&]() {
         sub_local_spmv(h, w.c(), kw.m(), auto_pol, KRYSP_MODE_FAST);
         sub_exchange(h);
-        for (size_t i = 0; i < nh; ++i) {
-            sub_fold(h, i, kw.v[i]);
-            const SubDev& D = h->held[i];
-            sc_dot2_kernel<<<grid(D.dof), kSubNT, 0, st>>>(D.dof, kw.v[i], w.v[i], g.v[i], D.w, d_st + i, slot(i), cnt(i));
-            KG_LAUNCH(c);
-        }
-        sub_reduce(h, d_st);
-        for (size_t i = 0; i < nh; ++i) {
-            sc_scalar1_kernel<<<1, 1, 0, st>>>(d_st + i);
-            KG_LAUNCH(c);
-            const SubDev& D = h->held[i];
-            sc_update_kernel<<<grid(D.dof), kSubNT, 0, st>>>(D.dof, x.v[i], g.v[i], z.v[i], w.v[i], kw.v[i],
-                                                             inv ? (const double*)inv->v[i] : nullptr, D.w, d_st + i,
-                                                             slot(i), cnt(i));
-            KG_LAUNCH(c);
-        }
-        sub_reduce(h, d_st);
-        for (size_t i = 0; i < nh; ++i) {
-            const SubDev& D = h->held[i];
-            sc_scalar2_kernel<<<1, 1, 0, st>>>(d_st + i, d_hist + (int64_t)i * cfg.max_iterations);
-            KG_LAUNCH(c);
-            sc_axpby_kernel<<<grid(D.dof), kSubNT, 0, st>>>(D.dof, z.v[i], w.v[i], d_st + i);
-            KG_LAUNCH(c);
-        }
+        for (size_t i = 0; i < h->held.size(); ++i) sub_fold(h, i, kw.v[i]);
     };
-    constexpr int kChunk = 8;
-    cudaGraphExec_t exec = nullptr;
-    std::exception_ptr err;
-    try {
-        cudaGraph_t graph = nullptr;
-        KG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        try {
-            for (int k = 0; k < kChunk; ++k) iteration();
-        } catch (...) {
-            cudaStreamEndCapture(st, &graph);
-            if (graph) cudaGraphDestroy(graph);
-            throw;
-        }
-        KG_CUDA(cudaStreamEndCapture(st, &graph));
-        KG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        cudaGraphDestroy(graph);
-        int done = 0;
-        while (!done) {
-            KG_CUDA(cudaGraphLaunch(exec, st));
-            KG_CUDA(cudaMemcpyAsync(c->h_pinned, &d_st[0].done, 4, cudaMemcpyDeviceToHost, st));
-            stream_wait(c);
-            std::memcpy(&done, c->h_pinned, 4);
-        }
-    } catch (...) {
-        err = std::current_exception();
-    }
-    if (exec) cudaGraphExecDestroy(exec);
-    SubCgState fin;
-    KG_CUDA(cudaMemcpyAsync(&fin, d_st, sizeof fin, cudaMemcpyDeviceToHost, st));
-    KG_CUDA(cudaStreamSynchronize(st));
-    iterations = fin.iter;
-    history.resize((size_t)fin.iter);
-    if (fin.iter) KG_CUDA(cudaMemcpy(history.data(), d_hist, 8 * (size_t)fin.iter, cudaMemcpyDeviceToHost));
-    if (fin.iter) measure = fin.measure;
-    dev_free(d_st);
-    dev_free(d_hist);
-    if (err) std::rethrow_exception(err);
-    switch (fin.status) {
-        case kScDenomNonFinite: fail(KRYSP_NON_FINITE, "descent denominator non-finite");
-        case kScBreakdown: fail(KRYSP_BREAKDOWN, "substructured cg: <Kw, w> vanished");
-        case kScRhoNonFinite: fail(KRYSP_NON_FINITE, "rho non-finite");
-        case kScGammaNonFinite: fail(KRYSP_NON_FINITE, "gamma non-finite");
-        case kScMeasureNonFinite: fail(KRYSP_NON_FINITE, "residual measure non-finite");
+    const int st = fused_descent(h->ctx, parts, op, h->emulated() ? nullptr : (void*)h->comm, norm_g0, cfg, history,
+                                 iterations, measure);
+    switch (st) {
+        case kDescentDenomNonFinite: fail(KRYSP_NON_FINITE, "descent denominator non-finite");
+        case kDescentBreakdown: fail(KRYSP_BREAKDOWN, "substructured cg: <Kw, w> vanished");
+        case kDescentRhoNonFinite: fail(KRYSP_NON_FINITE, "rho non-finite");
+        case kDescentGammaNonFinite: fail(KRYSP_NON_FINITE, "gamma non-finite");
+        case kDescentMeasureNonFinite: fail(KRYSP_NON_FINITE, "residual measure non-finite");
         default: break;
     }
 }

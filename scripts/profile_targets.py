@@ -32,3 +32,8 @@ elif target == "adaptive":
         kg.spmv_into(P, x, y, kg.ExecPolicy(0, 0), "fast")
     ctx.sync()
 print("ok", target)
+if target == "bicgstab_l":
+    A = ctx.generate("lap3d7", 400)
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=2, tolerance=1e-30, stab_l=4)
+    r = kg.solve(A, "bicgstab_l", np.ones(A.n_rows), cfg=cfg)
+    print("bicgstab_l", r.iterations)
