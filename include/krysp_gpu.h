@@ -348,6 +348,11 @@ krysp_status krysp_gpu_read_assignment_file(const char* path, int64_t expected_n
 krysp_status krysp_gpu_sub_create(krysp_gpu_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                                   const double* values, const int64_t* assignment, int64_t n_parts, int32_t rank,
                                   const uint8_t* nccl_id, krysp_gpu_sub** out);
+/* partition_matrix only, on the host (no device, no NCCL): the handle answers _info /
+ * _local / _interfaces / _owners; the device calls refuse it */
+krysp_status krysp_gpu_sub_partition_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                          const double* values, const int64_t* assignment, int64_t n_parts,
+                                          krysp_gpu_sub** out);
 /* [n_subdomains, dof, nnz, n_interfaces, interface entries, owner entries (global)] */
 krysp_status krysp_gpu_sub_info(const krysp_gpu_sub* h, int64_t s, int64_t info[6]);
 /* LocalSystem s (substructure.hpp:34-38) on the host: local_to_global, K_local, weights */

@@ -148,7 +148,7 @@ EXPORTS = [
     "krysp_gpu_dist_kernels_per_iteration", "krysp_gpu_dist_pcg_profile", "krysp_gpu_dist_solve", "krysp_gpu_dist_destroy",
     "krysp_gpu_mat_build_coo", "krysp_gpu_read_matrix_market", "krysp_gpu_parse_matrix_market",
     "krysp_gpu_write_matrix_market",
-    "krysp_gpu_band_row_assignment", "krysp_gpu_read_assignment_file", "krysp_gpu_sub_create", "krysp_gpu_sub_info",
+    "krysp_gpu_band_row_assignment", "krysp_gpu_read_assignment_file", "krysp_gpu_sub_partition_host", "krysp_gpu_sub_create", "krysp_gpu_sub_info",
     "krysp_gpu_sub_local", "krysp_gpu_sub_interfaces", "krysp_gpu_sub_owners", "krysp_gpu_sub_assemble_spmv",
     "krysp_gpu_sub_dot", "krysp_gpu_sub_solve_cg", "krysp_gpu_sub_destroy", "krysp_gpu_solve_cg_substructured_host",
 ]

@@ -705,25 +705,52 @@ krysp_status krysp_gpu_read_assignment_file(const char* path, int64_t expected_n
     });
 }
 
+namespace kg {
+namespace {
+// the host half of sub_create: validated partition_matrix (no device work)
+krysp_gpu_sub* partition_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                              const int64_t* assignment, int64_t n_parts) {
+    if (!row_ptr || (n > 0 && (!col_idx || !values))) fail(KRYSP_ERROR, "NULL argument");
+    std::vector<int64_t> a = assignment ? std::vector<int64_t>(assignment, assignment + n) : band_assignment(n, n_parts);
+    for (int64_t r = 0; r < n; ++r) {
+        if (row_ptr[r + 1] < row_ptr[r]) fail(KRYSP_ERROR, "row_ptr must be non-decreasing");
+        for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k)
+            if (col_idx[k] < 0 || col_idx[k] >= n)
+                fail(KRYSP_INDEX_OUT_OF_RANGE, "column %lld outside [0, %lld)", (long long)col_idx[k], (long long)n);
+    }
+    auto* h = new krysp_gpu_sub;
+    try {
+        build_partition(h->part, n, row_ptr, col_idx, values, a);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    return h;
+}
+}  // namespace
+}  // namespace kg
+
+// partition_matrix alone, on the host (no device, no collectives): every rank of a
+// multi-process run can build and inspect the identical split system
+krysp_status krysp_gpu_sub_partition_host(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                          const double* values, const int64_t* assignment, int64_t n_parts,
+                                          krysp_gpu_sub** out) {
+    return guard([&] {
+        if (!out) kg::fail(KRYSP_ERROR, "NULL argument");
+        *out = kg::partition_host(n, row_ptr, col_idx, values, assignment, n_parts);
+    });
+}
+
 krysp_status krysp_gpu_sub_create(krysp_gpu_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                                   const double* values, const int64_t* assignment, int64_t n_parts, int32_t rank,
                                   const uint8_t* nccl_id, krysp_gpu_sub** out) {
     return guard([&] {
-        if (!ctx || !row_ptr || !out || (n > 0 && (!col_idx || !values))) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (!ctx || !out) kg::fail(KRYSP_ERROR, "NULL argument");
         KG_CUDA(cudaSetDevice(ctx->device));
-        std::vector<int64_t> a = assignment ? std::vector<int64_t>(assignment, assignment + n)
-                                            : kg::band_assignment(n, n_parts);
-        for (int64_t r = 0; r < n; ++r) {
-            if (row_ptr[r + 1] < row_ptr[r]) kg::fail(KRYSP_ERROR, "row_ptr must be non-decreasing");
-            for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k)
-                if (col_idx[k] < 0 || col_idx[k] >= n)
-                    kg::fail(KRYSP_INDEX_OUT_OF_RANGE, "column %lld outside [0, %lld)", (long long)col_idx[k], (long long)n);
-        }
-        auto* h = new krysp_gpu_sub;
+        auto* h = kg::partition_host(n, row_ptr, col_idx, values, assignment, n_parts);
         try {
             h->ctx = ctx;
             h->rank = rank;
-            kg::build_partition(h->part, n, row_ptr, col_idx, values, a);
             if (rank >= 0) {
                 if (!nccl_id) kg::fail(KRYSP_ERROR, "NCCL mode needs the unique id");
                 if (rank >= h->part.nsub) kg::fail(KRYSP_ERROR, "rank %d has no subdomain (%lld subdomains)", rank,
@@ -793,6 +820,7 @@ krysp_status krysp_gpu_sub_assemble_spmv(krysp_gpu_sub* h, const double* const* 
                                          const krysp_policy* policy, int32_t mode) {
     return guard([&] {
         if (!h || !d_x || !d_y || !policy) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (!h->ctx) kg::fail(KRYSP_ERROR, "host-only partition (krysp_gpu_sub_partition_host): no device subdomains");
         if (policy->block_size) kg::check_policy(*policy);
         else if (mode != KRYSP_MODE_FAST) kg::fail(KRYSP_ERROR, "auto policy (block_size 0) requires FAST mode");
         std::vector<const double*> xs(d_x, d_x + h->held.size());
@@ -806,6 +834,7 @@ krysp_status krysp_gpu_sub_dot(krysp_gpu_sub* h, const double* const* d_x, const
                                const krysp_policy* policy, int32_t mode, double* out) {
     return guard([&] {
         if (!h || !d_x || !d_y || !policy || !out) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (!h->ctx) kg::fail(KRYSP_ERROR, "host-only partition (krysp_gpu_sub_partition_host): no device subdomains");
         if (policy->block_size) kg::check_policy(*policy);
         std::vector<const double*> xs(d_x, d_x + h->held.size()), ys(d_y, d_y + h->held.size());
         *out = kg::distributed_dot(h, xs, ys, *policy, mode);
@@ -816,6 +845,7 @@ krysp_status krysp_gpu_sub_solve_cg(krysp_gpu_sub* h, const double* b, const dou
                                     krysp_report* report, double* h_history, double* solution) {
     return guard([&] {
         if (!h || !b || !x0 || !cfg || !report) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (!h->ctx) kg::fail(KRYSP_ERROR, "host-only partition (krysp_gpu_sub_partition_host): no device subdomains");
         kg::solve_cg(h, b, x0, *cfg, report, h_history, solution);
     });
 }

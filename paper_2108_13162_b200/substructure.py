@@ -65,6 +65,30 @@ class Partition:
         self.held = list(range(self.n_subdomains)) if rank < 0 else [rank]
 
     @classmethod
+    def host(cls, A: CsrMatrix, assignment=None, n_parts: Optional[int] = None) -> "Partition":
+        """partition_matrix on the host only (krysp_gpu_sub_partition_host): the split system
+        without device subdomains — inspection, tests, or every rank's identical plan."""
+        self = cls.__new__(cls)
+        self.ctx, self.L = None, _lib.load()
+        if assignment is None and n_parts is None:
+            raise ValueError("need an assignment or n_parts")
+        self.n = A.n_rows
+        if A.n_rows != A.n_cols:
+            raise _lib.DimensionMismatch("partitioning expects a square matrix")
+        a = None if assignment is None else _i64(assignment)
+        if a is not None and len(a) != self.n:
+            raise _lib.DimensionMismatch(f"assignment covers {len(a)} equations, matrix has {self.n}")
+        rp, ci, va = _i64(A.row_ptr), _i64(A.col_idx), _f64(A.values)
+        h = C.c_void_p()
+        check(self.L.krysp_gpu_sub_partition_host(I64(self.n), _p(rp), _p(ci), _p(va), _p(a) if a is not None else None,
+                                                  I64(n_parts or 0), C.byref(h)))
+        self.h = h
+        self.rank = -1
+        self.n_subdomains = self.info(0)["n_subdomains"]
+        self.held = []
+        return self
+
+    @classmethod
     def nccl(cls, ctx: Context, A: CsrMatrix, rank: int, world: int, assignment=None, group=None) -> "Partition":
         from .dist import nccl_unique_id
         import torch.distributed as dist
