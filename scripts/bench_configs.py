@@ -111,8 +111,10 @@ def c4(ctx, R):
     for w in [-1, 26]:
         H = A.convert("hyb", hyb_width=w)
         hi = H.info
+        # V: vector streams per iteration (per cycle for BiCGStab(l): 5 l^2 + 11 l + 7 = 131 at
+        # l = 4 — the reference's MGS-ordered recurrence with the fusion of solvers.cu)
         for method, its, k, V, sl in [("bicgstab", 20, 2, 17, 1), ("tfqmr", 10, 3, 30, 1),
-                                      ("bicgstab_l", 4, 8, 60, 4), ("gcr", 20, 1, 12, 1)]:
+                                      ("bicgstab_l", 4, 8, 131, 4), ("gcr", 20, 1, 12, 1)]:
             r, got = rate(H, method, its, stab_l=sl)
             B = gcr_bytes(Bs, N, got) if method == "gcr" else k * Bs + 8 * N * V
             emit({"config": "C4", "format": f"hyb(w={hi['width']}, coo={hi['coo_nnz']})", "method": method,
