@@ -182,6 +182,31 @@ def cpu_reference_rate(m, iters: int, warm: int, bs: int, tw: int):
     return dict(value=done / dt if dt > 0 else None, cores=1, kind="port", seconds=t2 - t0, iterations=done)
 
 
+def cpu_model() -> str:
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_spmv_gflops(m):
+    """Reference SpMV at <1024,1> and <256,8> with its own timing protocol (autotune.cpp:37-87)."""
+    from oracle.oracle import REF_SO, Ref
+    if not os.path.exists(REF_SO):
+        return None
+    R = Ref()
+    rm = R.from_csr(m)
+    nnz = int(m.row_ptr[-1])
+    out = {}
+    for bs, tw in ((1024, 1), (256, 8)):
+        t = R.time_spmv(rm, bs=bs, tw=tw, min_reps=5)
+        out[f"<{bs},{tw}>"] = 2 * nnz / t["mean"] / 1e9
+    return out
+
+
 def oracle_csr(n):
     from oracle.oracle import Port
     return Port().generate("lap3d7", n)
@@ -329,10 +354,24 @@ def run_ours(args, dist):
     if dist.world == 1 and dist.rank == 0 and not args.no_cpu:
         hm = oracle_csr(args.n)
         os.environ["KRYSP_WORKERS"] = str(os.cpu_count())
-        r = cpu_reference_rate(hm, args.cpu_iters, 2, 1024, 1)
-        line["cpu_baseline"] = {"value": r["value"], "unit": "iterations/s", "cores": r["cores"], "kind": r["kind"],
+        # SURVEY §8(d) "CPU timing beside it": the tuned <1024,1> and the default <256,8>,
+        # median and min of 3 samples each, plus the reference's own SpMV timing protocol
+        runs = [cpu_reference_rate(hm, args.cpu_iters, 2, 1024, 1) for _ in range(3)]
+        dflt = [cpu_reference_rate(hm, max(2, args.cpu_iters // 4), 2, 256, 8) for _ in range(3)]
+        r = runs[0]
+        vals = sorted(x["value"] for x in runs if x["value"])
+        dvals = sorted(x["value"] for x in dflt if x["value"])
+        line["cpu_baseline"] = {"value": statistics.median(vals), "unit": "iterations/s", "cores": r["cores"],
+                                "kind": r["kind"], "cpu_model": cpu_model(),
                                 "sample": f"{r['iterations']} P-CG iterations of the same 400^3 problem, policy "
-                                          f"<1024,1> (difference of max_iterations 2+{args.cpu_iters} and 2)"}
+                                          f"<1024,1> (difference of max_iterations 2+{args.cpu_iters} and 2), "
+                                          f"median of 3 samples",
+                                "min_of_samples": vals[0], "default_policy_256_8": {
+                                    "median": statistics.median(dvals), "min": dvals[0],
+                                    "iterations": dflt[0]["iterations"]}}
+        spmv = cpu_spmv_gflops(hm)
+        if spmv:
+            line["cpu_baseline"]["spmv_gflops"] = spmv
     return line
 
 
