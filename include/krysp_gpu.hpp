@@ -9,11 +9,13 @@
 // value semantics); DeviceMatrix keeps a matrix resident across calls.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <variant>
 #include <vector>
 
@@ -340,6 +342,75 @@ inline TuneResult tune_spmv(const DeviceMatrix& m, const std::vector<ExecPolicy>
                            t.reps, t.total_time, t.mean_time, t.stddev_time});
     }
     return r;
+}
+
+// ------------------------------------------------------------------ formats.cpp:17-63, matrix_market.hpp
+using Triple = std::tuple<index_t, index_t, double>;
+// build_coo + coo_to_csr on the device (sort, duplicate sum), result kept on the device
+inline DeviceMatrix build_coo_device(const std::vector<Triple>& t, index_t n_rows, index_t n_cols,
+                                     Format out = Format::Coo, Context& ctx = Context::instance()) {
+    std::vector<int64_t> r, c;
+    std::vector<double> v;
+    for (const auto& [i, j, x] : t) r.push_back(i), c.push_back(j), v.push_back(x);
+    krysp_gpu_mat* o = nullptr;
+    check(krysp_gpu_mat_build_coo(ctx.get(), n_rows, n_cols, (int64_t)v.size(), r.data(), c.data(), v.data(),
+                                  (int32_t)out, &o));
+    return DeviceMatrix(o);
+}
+inline DeviceMatrix read_matrix_market_device(const std::string& path, Format out = Format::Coo,
+                                              Context& ctx = Context::instance()) {
+    krysp_gpu_mat* o = nullptr;
+    check(krysp_gpu_read_matrix_market(ctx.get(), path.c_str(), (int32_t)out, &o));
+    return DeviceMatrix(o);
+}
+inline void write_matrix_market(const std::string& path, const DeviceMatrix& m) {
+    check(krysp_gpu_write_matrix_market(m.get(), path.c_str()));
+}
+// stats.hpp compute_stats (density_percent = 100 * density)
+inline krysp_stats compute_stats(const DeviceMatrix& m) {
+    krysp_stats s{};
+    check(krysp_gpu_mat_stats(m.get(), &s));
+    return s;
+}
+
+// ------------------------------------------------------------------ substructure.hpp
+inline constexpr index_t kInterfaceEquation = -1;
+inline std::vector<index_t> band_row_assignment(index_t n, index_t n_parts) {
+    std::vector<index_t> a((size_t)n);
+    check(krysp_gpu_band_row_assignment(n, n_parts, a.data()));
+    return a;
+}
+inline std::vector<index_t> read_assignment_file(const std::string& path, index_t expected_n) {
+    std::vector<index_t> a((size_t)expected_n);
+    check(krysp_gpu_read_assignment_file(path.c_str(), expected_n, a.data()));
+    return a;
+}
+// solve_cg_substructured(A, b, x0, assignment, cfg) with every subdomain on the context's GPU
+inline SolveReport solve_cg_substructured(const CsrMatrix& A, std::span<const double> b, std::span<const double> x0,
+                                          const std::vector<index_t>& assignment, const SolverConfig& cfg,
+                                          Context& ctx = Context::instance()) {
+    if (A.n_rows != A.n_cols) throw DimensionMismatch("solver expects a square matrix");
+    if ((index_t)b.size() != A.n_rows || b.size() != x0.size())
+        throw DimensionMismatch("rhs / initial guess length does not match the matrix");
+    SolveReport r;
+    r.solution.resize(b.size());
+    std::vector<double> hist((size_t)std::max<index_t>(cfg.max_iterations, 1));
+    krysp_solver_cfg c = cfg.c();
+    krysp_report rep{};
+    check(krysp_gpu_solve_cg_substructured_host(ctx.get(), A.n_rows, A.row_ptr.data(), A.col_idx.data(),
+                                                A.values.data(), b.data(), x0.data(), assignment.data(), 0, &c, &rep,
+                                                hist.data(), r.solution.data()));
+    r.converged = rep.converged != 0;
+    r.iterations = rep.iterations;
+    r.final_residual_measure = rep.final_residual_measure;
+    r.wall_time = rep.wall_time;
+    r.device_time = rep.device_time;
+    r.residual_history.assign(hist.begin(), hist.begin() + rep.iterations);
+    return r;
+}
+inline SolveReport solve_cg_substructured(const CsrMatrix& A, std::span<const double> b, std::span<const double> x0,
+                                          index_t n_parts, const SolverConfig& cfg) {
+    return solve_cg_substructured(A, b, x0, band_row_assignment(A.n_rows, n_parts), cfg);
 }
 
 }  // namespace krysp_gpu

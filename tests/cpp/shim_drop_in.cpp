@@ -46,7 +46,27 @@ int main() {
         ok = false;
     } catch (const kr::EllBlowup&) {
     }
-    std::printf("pcg it=%lld fast it=%lld bicgstab it=%lld %s\n", (long long)r.iterations,
-                (long long)rf.iterations, (long long)rb.iterations, ok ? "shim ok" : "shim FAILED");
+    // matrix_market.hpp / build_coo / substructure.hpp / stats.hpp call shapes
+    std::vector<kr::Triple> t{{0, 0, 2.0}, {0, 2, -1.0}, {1, 1, 3.0}, {1, 2, -1.0}, {2, 0, -1.0}, {2, 1, -1.0},
+                              {2, 2, 4.0}, {2, 2, 0.0}};
+    kr::DeviceMatrix K = kr::build_coo_device(t, 3, 3, kr::Format::Csr);
+    ok = ok && K.info().nnz == 7;  // the duplicate (2, 2) folded
+    const char* mtx = "/tmp/krysp_gpu_shim_drop_in.mtx";
+    kr::write_matrix_market(mtx, dA);
+    kr::DeviceMatrix back = kr::read_matrix_market_device(mtx, kr::Format::Csr);
+    ok = ok && back.info().nnz == dA.info().nnz && kr::compute_stats(back).max_row == 5;
+    cfg.mode = kr::Mode::Exact;
+    cfg.preconditioner = kr::Preconditioner::None;
+    kr::SolveReport rs = kr::solve_cg_substructured(A, b, x0, kr::index_t(4), cfg);
+    kr::SolveReport rc = kr::solve_cg_classic(dA, b, x0, cfg);
+    ok = ok && rs.converged && rs.iterations == rc.iterations;  // acceptance.cpp:370-419
+    try {
+        kr::read_matrix_market_device("/nonexistent/krysp.mtx");
+        ok = false;
+    } catch (const kr::Error&) {
+    }
+    std::printf("pcg it=%lld fast it=%lld bicgstab it=%lld substructured it=%lld %s\n", (long long)r.iterations,
+                (long long)rf.iterations, (long long)rb.iterations, (long long)rs.iterations,
+                ok ? "shim ok" : "shim FAILED");
     return ok ? 0 : 1;
 }
