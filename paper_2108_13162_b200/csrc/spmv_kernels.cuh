@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
 
 // ------------------------------------------------------------------ ELL
 // Thread per row, column-major slab => every slot load is a coalesced 32-lane stream.
-template <class Epi>
+template <class Epi, int KB>
 __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
     if (!epi.active()) return;
     const int64_t n = E.n_rows;
@@ -233,9 +233,9 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
         if (r < n) {
             const int32_t* jc = E.jcoef + r;
             const double* cf = E.coef + r;
-            if constexpr (std::is_same<Epi, EpiStore>::value) {
-                // plain store: 8 slots per batch — all column / value loads, then all x gathers
-                // in flight before the slot-ordered sum (kernels.cpp:203-206)
+            if constexpr (KB == 8) {
+                // 8 slots per batch — all column / value loads, then all x gathers in flight
+                // before the slot-ordered sum (kernels.cpp:203-206)
                 for (int s = 0; s < E.width; s += 8) {
                     int32_t c[8];
                     double v[8], xv[8];
@@ -364,8 +364,15 @@ inline void launch_ell(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t
     krysp_gpu_ctx* c = m->ctx;
     const int64_t nvb = (m->n_rows + bs - 1) / bs;
     if (nvb == 0) return;
-    const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi>, (int)bs, 0), nvb);
-    ell_kernel<Epi><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+    // measured: 8-slot batches lose for the solver epilogues at any width (C2 w = 5, C4
+    // w = 27: register-limited occupancy), win for the plain store
+    if (std::is_same<Epi, EpiStore>::value) {
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 8><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+    } else {
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 4><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+    }
     KG_LAUNCH(c);
 }
 
