@@ -503,15 +503,15 @@ krysp_status krysp_gpu_autotune_policy(const krysp_gpu_mat* m, krysp_policy* out
             const double mean = (double)m->nnz / (double)m->n_rows;
             // irregular rows (power law) or long rows: vector kernel, tw ~ the mean row length
             // measured (profiles/r01_tuner_evidence.md, scripts/c4_probe.py): irregular rows want
-            // tw ~ the mean length (power law, mean 4.6: tw 4-8); long regular rows want
-            // tw ~ mean / 3 (27-point rows: tw = 8, 2x faster than tw = 32)
+            // tw ~ the mean length (power law, mean 4.6: tw 4-8, vector kernel); long regular
+            // rows want tw ~ mean / 6 on the TMA tile kernel (27-point rows: tw = 4, 5.8 TB/s)
             if (csr_is_irregular(m)) {
                 int64_t tw = 1;
                 while (tw < 32 && (double)(tw * 2) <= mean * 1.5) tw *= 2;
                 p.workers_per_row = tw;
             } else if (m->max_tile_nnz + 8 > 8192 || mean > 24.0) {
                 int64_t tw = 1;
-                while (tw < 32 && (double)(tw * 2) <= mean / 3.0 * 1.5) tw *= 2;
+                while (tw < 32 && (double)(tw * 2) <= mean / 5.0) tw *= 2;
                 p.workers_per_row = tw;
             }
         }

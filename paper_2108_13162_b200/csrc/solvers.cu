@@ -618,7 +618,7 @@ void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y,
     const bool irregular = e.auto_pol && ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) ||
                                           m->format == KRYSP_FMT_COO || (m->format == KRYSP_FMT_HYB && m->coo_nnz));
     if (!irregular && m->format == KRYSP_FMT_CSR) {
-        if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, x, epi, s);
+        if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, x, epi, s, e.pol.workers_per_row);
         else launch_csr_vector(m, x, epi, e.pol.block_size, e.pol.workers_per_row, s);
     } else if (!irregular && (m->format == KRYSP_FMT_ELL || (m->format == KRYSP_FMT_HYB && m->coo_nnz == 0))) {
         launch_ell(m, x, epi, e.pol.block_size, s);

@@ -39,8 +39,13 @@ void launch_coo_accumulate(const krysp_gpu_mat* m, const double* x, double* y, c
 
 // CSR kernel choice: the tile kernel realises the tw == 1 order with coalesced staging;
 // it is used when the policy asks tw == 1 (any mode) and tiles fit shared memory.
+// the TMA tile pipeline serves tw = 1, and any wider tw whose tiles (kTileRows / tw rows) fit
+// a stage on rows of even length; irregular rows (power law) stay on the vector kernel, whose
+// per-row segments do not wait for the longest row of a tile (tuner evidence: 4x)
 bool csr_use_tile(const krysp_gpu_mat* m, int64_t tw) {
-    return tw == 1 && m->max_tile_nnz >= 0 && m->max_tile_nnz + 8 <= kTileCapMax;
+    if (tw < 1 || tw > 32 || (tw & (tw - 1)) != 0) return false;
+    if (tw > 1 && csr_is_irregular(m)) return false;
+    return tile_nnz_bound(m, tw) + 8 <= kTileCapMax;
 }
 
 int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const krysp_policy& pol0,
@@ -71,7 +76,7 @@ int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const kr
     switch (m->format) {
         case KRYSP_FMT_CSR:
             if (csr_use_tile(m, pol.workers_per_row)) {
-                launch_csr_tile(m, x, epi, s);
+                launch_csr_tile(m, x, epi, s, pol.workers_per_row);
                 return kVarCsrTile;
             }
             launch_csr_vector(m, x, epi, pol.block_size, pol.workers_per_row, s);

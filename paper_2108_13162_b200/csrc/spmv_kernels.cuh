@@ -105,10 +105,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 struct TmaTileLayout {
     int cap;     // entries per stage (>= max tile nnz + 8, multiple of 4)
     int staged;  // per-row epilogue vectors moved with the tile (Epi::kStaged)
+    int rows;    // rows per tile (kTileRows / tw)
     __host__ __device__ int val_bytes() const { return (cap + 8) * 8; }
     __host__ __device__ int col_bytes() const { return (cap + 8) * 4; }
-    __host__ __device__ int rp_bytes() const { return (kTileRows + 8) * 4; }
-    __host__ __device__ int vec_bytes() const { return (kTileRows + 2) * 8; }
+    __host__ __device__ int rp_bytes() const { return (rows + 8) * 4; }
+    __host__ __device__ int vec_bytes() const { return (rows + 2) * 8; }
     __host__ __device__ int stage_bytes() const { return val_bytes() + col_bytes() + rp_bytes() + staged * vec_bytes(); }
     __host__ __device__ int total_bytes() const { return 2 * stage_bytes() + 64; }
 };
@@ -126,14 +127,19 @@ struct epi_staged<E, std::void_t<decltype(E::kStaged)>> {
     static constexpr int value = E::kStaged;
 };
 
-template <class Epi>
+// TW lanes per row (TW = 1: thread per row): a tile is kTileRows / TW rows; lane l of a row
+// sums entries l, l + TW, ... sequentially from 0.0 and the lanes fold with the shuffle tree
+// of csr_vector_kernel — the reference's tw-lane order (kernels.cpp:175-186), so any policy
+// with a tile that fits the stage runs on the TMA pipeline bit-identically.
+template <int TW, class Epi>
 __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const double* __restrict__ x, Epi epi,
                                                             TmaTileLayout L) {
     if (!epi.active()) return;
+    constexpr int TR = kTileRows / TW;
     extern __shared__ __align__(128) unsigned char smem_tma[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma);  // 2 mbarriers
     unsigned char* stage_base = smem_tma + 64;
-    const int64_t n_tiles = ((int64_t)A.n_rows + kTileRows - 1) / kTileRows;
+    const int64_t n_tiles = ((int64_t)A.n_rows + TR - 1) / TR;
     const uint64_t pol = evict_first_policy();
 
     constexpr int NS = epi_staged<Epi>::value;
@@ -146,8 +152,8 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
     };
     // thread 0: bulk-copy tile `t` into stage `s`
     auto issue = [&](int64_t t, int s) {
-        const int64_t r0 = t * kTileRows;
-        const int64_t r1 = (r0 + kTileRows < A.n_rows) ? r0 + kTileRows : (int64_t)A.n_rows;
+        const int64_t r0 = t * TR;
+        const int64_t r1 = (r0 + TR < A.n_rows) ? r0 + TR : (int64_t)A.n_rows;
         const int32_t k0 = __ldg(A.row_ptr + r0), k1 = __ldg(A.row_ptr + r1);
         const int32_t va = k0 & ~1, vb = (k1 + 1) & ~1;
         const int32_t ca = k0 & ~3, cb = (k1 + 3) & ~3;
@@ -189,13 +195,27 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
         const double* s_val = reinterpret_cast<const double*>(stage_ptr(s, 0));
         const int32_t* s_col = reinterpret_cast<const int32_t*>(stage_ptr(s, 1));
         const int32_t* s_rp = reinterpret_cast<const int32_t*>(stage_ptr(s, 2));
-        const int64_t r = tile * kTileRows + threadIdx.x;
+        const int tr = threadIdx.x / TW;  // row within the tile
+        const int lane = threadIdx.x & (TW - 1);
+        const int64_t r = tile * TR + tr;
         double sum = 0.0;
-        if (r < A.n_rows) {
+        if constexpr (TW > 1) {
+            if (r < A.n_rows) {
+                const int32_t k0 = s_rp[0];
+                const int32_t rb = s_rp[tr], re = s_rp[tr + 1];
+                const int av = rb - (k0 & ~1), ac = rb - (k0 & ~3), len = re - rb;
+#pragma unroll 4
+                for (int j = lane; j < len; j += TW) sum = madd(sum, s_val[av + j], __ldg(x + s_col[ac + j]));
+            }
+#pragma unroll
+            for (int off = TW / 2; off >= 1; off >>= 1) sum = __dadd_rn(sum, __shfl_down_sync(0xffffffffu, sum, off, TW));
+        }
+        if (r < A.n_rows && lane == 0) {
             const int32_t k0 = s_rp[0];
-            const int32_t rb = s_rp[threadIdx.x], re = s_rp[threadIdx.x + 1];
+            const int32_t rb = s_rp[tr], re = s_rp[tr + 1];
             const int av = rb - (k0 & ~1), ac = rb - (k0 & ~3), len = re - rb;
-            if (len <= 8) {
+            if constexpr (TW > 1) {
+            } else if (len <= 8) {
                 double xv[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -210,7 +230,7 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
             if constexpr (NS > 0) {
                 double sv[NS > 0 ? NS : 1];
 #pragma unroll
-                for (int k = 0; k < NS; ++k) sv[k] = reinterpret_cast<const double*>(stage_ptr(s, 3 + k))[threadIdx.x];
+                for (int k = 0; k < NS; ++k) sv[k] = reinterpret_cast<const double*>(stage_ptr(s, 3 + k))[tr];
                 epi.row_staged(r, sum, sv);
             } else {
                 epi.row(r, sum);
@@ -342,21 +362,40 @@ inline void launch_csr_vector(const krysp_gpu_mat* m, const double* x, Epi epi, 
 }
 
 // returns the grid size (number of per-CTA partials an epilogue writes)
-template <class Epi>
-inline int64_t launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s) {
+// entries a TR-row tile of m can hold at most (the cached 256-row maximum, or max_row * TR)
+inline int64_t tile_nnz_bound(const krysp_gpu_mat* m, int64_t tw) {
+    if (m->max_tile_nnz < 0 || m->max_row < 0) return INT64_MAX;
+    return tw == 1 ? m->max_tile_nnz : std::min<int64_t>(m->max_tile_nnz, m->max_row * (kTileRows / tw));
+}
+
+template <int TW, class Epi>
+inline int64_t launch_csr_tile_tw(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s) {
     krysp_gpu_ctx* c = m->ctx;
-    const int64_t tiles = (m->n_rows + kTileRows - 1) / kTileRows;
+    constexpr int TR = kTileRows / TW;
+    const int64_t tiles = (m->n_rows + TR - 1) / TR;
     if (tiles == 0) return 0;
-    int cap = (int)std::min<int64_t>(std::max<int64_t>(m->max_tile_nnz + 8, 64), kTileCapMax);
+    int cap = (int)std::min<int64_t>(std::max<int64_t>(tile_nnz_bound(m, TW) + 8, 64), kTileCapMax);
     cap = (cap + 3) & ~3;
-    const TmaTileLayout L{cap, epi_staged<Epi>::value};
+    const TmaTileLayout L{cap, epi_staged<Epi>::value, TR};
     const int smem = L.total_bytes();
-    if (smem > 48 * 1024)
-        KG_CUDA(cudaFuncSetAttribute(csr_tma_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t g = bounded_grid(c, resident_blocks(csr_tma_kernel<Epi>, kTileRows, smem), tiles);
-    csr_tma_kernel<Epi><<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, L);
+    auto k = csr_tma_kernel<TW, Epi>;
+    if (smem > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t g = bounded_grid(c, resident_blocks(k, kTileRows, smem), tiles);
+    k<<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, L);
     KG_LAUNCH(c);
     return g;
+}
+
+template <class Epi>
+inline int64_t launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s, int64_t tw = 1) {
+    switch (tw) {
+        case 2: return launch_csr_tile_tw<2>(m, x, epi, s);
+        case 4: return launch_csr_tile_tw<4>(m, x, epi, s);
+        case 8: return launch_csr_tile_tw<8>(m, x, epi, s);
+        case 16: return launch_csr_tile_tw<16>(m, x, epi, s);
+        case 32: return launch_csr_tile_tw<32>(m, x, epi, s);
+        default: return launch_csr_tile_tw<1>(m, x, epi, s);
+    }
 }
 
 template <class Epi>
