@@ -39,12 +39,12 @@ void launch_coo_accumulate(const krysp_gpu_mat* m, const double* x, double* y, c
 
 // CSR kernel choice: the tile kernel realises the tw == 1 order with coalesced staging;
 // it is used when the policy asks tw == 1 (any mode) and tiles fit shared memory.
-// the TMA tile pipeline serves tw = 1, and any wider tw whose tiles (kTileRows / tw rows) fit
-// a stage on rows of even length; irregular rows (power law) stay on the vector kernel, whose
-// per-row segments do not wait for the longest row of a tile (tuner evidence: 4x)
+// the TMA tile pipeline serves any tw whose tiles (kTileRows / tw rows) fit a stage, on rows
+// of even length; irregular rows (power law) stay on the vector kernel, whose per-row
+// segments do not wait for the longest row of a tile (tuner evidence: 4-8x)
 bool csr_use_tile(const krysp_gpu_mat* m, int64_t tw) {
     if (tw < 1 || tw > 32 || (tw & (tw - 1)) != 0) return false;
-    if (tw > 1 && csr_is_irregular(m)) return false;
+    if (csr_is_irregular(m)) return false;
     return tile_nnz_bound(m, tw) + 8 <= kTileCapMax;
 }
 

@@ -1,5 +1,6 @@
 """Auto-tuner evidence (north star item 5): every SpMV kernel variant the tuner can pick, on
-a regular stencil (C3-like 3D 7-pt, 300^3) and on power-law rows (C5, 10M rows, alpha 2),
+a regular stencil (C3-like 3D 7-pt, 300^3), the C4 27-point stencil (320^3, CSR and HYB) and
+on power-law rows (C5, 10M rows, alpha 2),
 timed with CUDA events (mean of 10) and the library's own choice marked.  Run it plain for
 the timing table, and under `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum` (each variant launches exactly twice: warm-up + measured) for the DRAM
@@ -21,6 +22,11 @@ cases.append(("lap3d7 300^3", A, [("csr", kg.ExecPolicy(256, tw), "exact") for t
               + [("csr", kg.ExecPolicy(0, 0), "fast")]))
 E = A.convert("ell", slot_cap=1 << 40)
 cases.append(("lap3d7 300^3", E, [("ell", kg.ExecPolicy(256, 1), "exact"), ("ell", kg.ExecPolicy(0, 0), "fast")]))
+F = ctx.generate("fem27", 320, 0.5)
+cases.append(("fem27 320^3", F, [("csr", kg.ExecPolicy(256, tw), "exact") for tw in (1, 2, 4, 8, 32)]
+              + [("csr", kg.ExecPolicy(0, 0), "fast")]))
+FH = F.convert("hyb")
+cases.append(("fem27 320^3", FH, [("hyb", kg.ExecPolicy(0, 0), "fast")]))
 P = ctx.upload(kg.generate_csr("powerlaw", 10_000_000, alpha=2.0, seed=2108))
 cases.append(("powerlaw 10M a=2", P, [("csr", kg.ExecPolicy(256, tw), "exact") for tw in (1, 2, 4, 8, 32)]
               + [("csr", kg.ExecPolicy(0, 0), "fast")]))

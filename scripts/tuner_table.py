@@ -17,6 +17,7 @@ for r in rows[1:]:
     seen[k][d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
 spmv = [l for l in launches if any(t in l["name"] for t in ("csr_tma_kernel", "csr_vector_kernel", "ell_kernel",
                                                              "adaptive_kernel"))]
+# HYB with an empty COO part launches only its ELL kernel; one SpMV = one launch here
 out = ["| matrix | format | policy <bs,tw> | mode | kernel | CUDA-event ms | algorithmic GB/s | ncu DRAM GB/launch | "
        "ncu DRAM GB/s | tuner |", "|---|---|---|---|---|---|---|---|---|---|"]
 for i, t in enumerate(timing):
