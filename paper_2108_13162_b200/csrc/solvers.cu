@@ -621,7 +621,17 @@ void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y,
         if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, x, epi, s, e.pol.workers_per_row);
         else launch_csr_vector(m, x, epi, e.pol.block_size, e.pol.workers_per_row, s);
     } else if (!irregular && (m->format == KRYSP_FMT_ELL || (m->format == KRYSP_FMT_HYB && m->coo_nnz == 0))) {
-        launch_ell(m, x, epi, e.pol.block_size, s);
+        if (m->width < 16) {  // narrow slabs (C2: 5, C3: 7): the fused epilogue wins (measured)
+            launch_ell(m, x, epi, e.pol.block_size, s);
+        } else {
+            // wide slabs (C4: 27 slots): the plain 8-slot kernel (gated on the solve's done
+            // flag) + a vector epilogue pass — faster than the fused epilogue kernels, whose dot
+            // accumulators cost the occupancy that hides the gathers (C4: 2.3-2.6 -> 1.9 ms)
+            launch_ell(m, x, EpiStoreGated<Epi>{y, epi}, e.pol.block_size, s);
+            vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y,
+                                                                                                       epi);
+            KG_LAUNCH(e.c);
+        }
     } else {
         spmv_launch(m, x, y, e.launch_pol(), e.mode, s);
         vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y, epi);

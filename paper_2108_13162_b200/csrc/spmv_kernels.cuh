@@ -20,6 +20,7 @@
 // is read once at entry and lets a converged solver's queued iterations exit immediately.
 #pragma once
 
+#include <cstdlib>
 #include <type_traits>
 #include <unordered_map>
 
@@ -37,6 +38,23 @@ struct EpiStore {
     __device__ __forceinline__ void row(int64_t r, double v) { y[r] = v; }
     __device__ __forceinline__ void finish() {}
 };
+
+// plain store that is skipped once another epilogue's solve has converged (its active())
+template <class Gate>
+struct EpiStoreGated {
+    double* __restrict__ y;
+    Gate gate;
+    __device__ __forceinline__ bool active() const { return gate.active(); }
+    __device__ __forceinline__ void row(int64_t r, double v) { y[r] = v; }
+    __device__ __forceinline__ void finish() {}
+};
+
+template <class E>
+struct epi_is_store : std::false_type {};
+template <>
+struct epi_is_store<EpiStore> : std::true_type {};
+template <class G>
+struct epi_is_store<EpiStoreGated<G>> : std::true_type {};
 
 // ------------------------------------------------------------------ CSR vector (paper)
 // One segment of TW lanes per row; virtual blocks of blockDim.x threads cover
@@ -405,7 +423,7 @@ inline void launch_ell(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t
     if (nvb == 0) return;
     // measured: 8-slot batches lose for the solver epilogues at any width (C2 w = 5, C4
     // w = 27: register-limited occupancy), win for the plain store
-    if (std::is_same<Epi, EpiStore>::value) {
+    if (epi_is_store<Epi>::value) {
         const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8>, (int)bs, 0), nvb);
         ell_kernel<Epi, 8><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
     } else {

@@ -37,3 +37,8 @@ if target == "bicgstab_l":
     cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=2, tolerance=1e-30, stab_l=4)
     r = kg.solve(A, "bicgstab_l", np.ones(A.n_rows), cfg=cfg)
     print("bicgstab_l", r.iterations)
+if target == "c4_bicgstab":
+    H = ctx.generate("fem27", 320, 0.5).convert("hyb")
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=3, tolerance=1e-30)
+    r = kg.solve(H, "bicgstab", np.ones(H.n_rows), cfg=cfg)
+    print("c4_bicgstab", r.iterations)
