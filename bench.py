@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=400, help="grid side (C3 = 400)")
     ap.add_argument("--format", default="csr", choices=["csr", "ell", "hyb"])
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=20)
@@ -332,6 +332,9 @@ def run_ours(args, dist):
         hsol = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
         e2e_cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0))
         its, secs, rep2 = 0, 0.0, None
+        # one untimed warm-up call (first-use module loading of the upload / build kernels),
+        # as the device-timed steps have their warm-up
+        kg.solve_csr_host(ctx, hm, "pcg", hb, hx0, e2e_cfg, fmt=args.format, out=hsol)
         dist.barrier()
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()
@@ -344,7 +347,7 @@ def run_ours(args, dist):
                        "d2h_bytes_per_step": 8 * n + 8 * rep2.iterations,
                        "what": "krysp_gpu_solve_csr_host: pinned int64 CSR + b + x0 upload, device CSR build, "
                                "FAST P-CG to convergence, solution download",
-                       "seconds_per_step": secs / args.e2e_steps}
+                       "seconds_per_step": secs / args.e2e_steps, "steps": args.e2e_steps, "warmup": 1}
         line["parity"] = {"iterations": rep2.iterations, "golden_iterations": GOLDEN_ITERS,
                           "final_residual_measure": rep2.final_residual_measure,
                           "golden_final_measure": GOLDEN_MEASURE,
