@@ -305,7 +305,8 @@ def run_ours(args, dist):
                                                 "nnz": nnz, "rows": n}),
             "roofline": {"bound": "hbm", "kernel": f"spmv_{args.format} + fused <p,Ap>",
                          "achieved": achieved, "peak": bw_peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / bw_peak, "traffic": ncu_traffic(),
+                         "frac": achieved / bw_peak, "frac_of_nominal_8tbs": achieved / 8000.0,
+                         "traffic": ncu_traffic(),
                          "algorithmic_bytes_per_launch": B_spmv,
                          "launch_ms": t_spmv * 1e3, "update_ms": t_upd * 1e3, "direction_ms": t_dir * 1e3},
             "spmv_gflops": 2 * nnz / t_spmv / 1e9,
