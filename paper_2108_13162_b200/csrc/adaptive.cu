@@ -49,44 +49,12 @@ struct RowsView {
     const double* __restrict__ val;
 };
 
-// L2 residency split for random gathers (opt-in, KRYSP_GATHER_HINT=1): x (read ~nnz/n times,
-// in random order) is loaded with an evict_last policy, the once-read column/value streams
-// with evict_first.  Measured on C5 it does not pay: x misses are dominated by capacity.
-struct L2Hints {
-    uint64_t keep, stream;
-};
-__device__ __forceinline__ L2Hints l2_hints() {
-    L2Hints h;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(h.keep));
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(h.stream));
-    return h;
-}
-__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
-    double v;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ int32_t ld_stream(const int32_t* p, uint64_t pol) {
-    int32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
-
 // a block's sum of one row strided by `nthreads` threads starting at `t`
-template <bool kHint>
 __device__ __forceinline__ double strided_row(RowsView A, const double* __restrict__ x, int64_t k0, int64_t k1,
-                                              int t, int nthreads, L2Hints h) {
+                                              int t, int nthreads) {
     double acc = 0.0;
 #pragma unroll 4
-    for (int64_t k = k0 + t; k < k1; k += nthreads) {
-        if constexpr (kHint) acc = fma(ld_stream(A.val + k, h.stream), ld_hint(x + ld_stream(A.col + k, h.stream), h.keep), acc);
-        else acc = fma(__ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)), acc);
-    }
+    for (int64_t k = k0 + t; k < k1; k += nthreads) acc = fma(__ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)), acc);
     return acc;
 }
 
@@ -98,7 +66,6 @@ __device__ __forceinline__ double strided_row(RowsView A, const double* __restri
 // strided by the whole CTA.
 constexpr int kAdPer = kAdTile / kAdNT;
 
-template <bool kHint>
 __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const int32_t* __restrict__ blk, int64_t nblk,
                                                           const int32_t* __restrict__ med, int64_t nmed,
                                                           const int32_t* __restrict__ lng, int64_t nlng,
@@ -109,19 +76,18 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
     __shared__ double sh[32];
     __shared__ double prod[kAdTile];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const L2Hints h = kHint ? l2_hints() : L2Hints{0, 0};
     const int64_t nmedg = (nmed + kAdNT / 32 - 1) / (kAdNT / 32);
     const int64_t items = nchunk + nlng + nmedg + nblk;
     for (int64_t bi = blockIdx.x; bi < items; bi += gridDim.x) {
         if (bi < nchunk) {  // a piece of a giant row (fixup kernel adds the pieces in order)
-            const double s = block_sum_dyn(strided_row<kHint>(A, x, chunk[3 * bi + 1], chunk[3 * bi + 2], tid, kAdNT, h), sh);
+            const double s = block_sum_dyn(strided_row(A, x, chunk[3 * bi + 1], chunk[3 * bi + 2], tid, kAdNT), sh);
             if (tid == 0) partials[bi] = s;
             continue;
         }
         const int64_t b = bi - nchunk;
         if (b < nlng) {  // long row: the whole CTA
             const int32_t r = lng[b];
-            const double s = block_sum_dyn(strided_row<kHint>(A, x, A.rp[r], A.rp[r + 1], tid, kAdNT, h), sh);
+            const double s = block_sum_dyn(strided_row(A, x, A.rp[r], A.rp[r + 1], tid, kAdNT), sh);
             if (tid == 0) y[r] = accumulate ? y[r] + s : s;
             continue;
         }
@@ -129,7 +95,7 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
             const int64_t i = (b - nlng) * (kAdNT / 32) + warp;
             if (i < nmed) {
                 const int32_t r = med[i];
-                double s = strided_row<kHint>(A, x, A.rp[r], A.rp[r + 1], lane, 32, h);
+                double s = strided_row(A, x, A.rp[r], A.rp[r + 1], lane, 32);
                 s = warp_sum(s);
                 if (lane == 0) y[r] = accumulate ? y[r] + s : s;
             }
@@ -145,19 +111,14 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
         for (int j = 0; j < kAdPer; ++j) {
             const int k = tid + j * kAdNT;
             if (k < nz) {
-                if constexpr (kHint) {
-                    cl[j] = ld_stream(A.col + k0 + k, h.stream);
-                    vl[j] = ld_stream(A.val + k0 + k, h.stream);
-                } else {
-                    cl[j] = __ldcs(A.col + k0 + k);
-                    vl[j] = __ldcs(A.val + k0 + k);
-                }
+                cl[j] = __ldcs(A.col + k0 + k);
+                vl[j] = __ldcs(A.val + k0 + k);
             }
         }
 #pragma unroll
         for (int j = 0; j < kAdPer; ++j) {
             const int k = tid + j * kAdNT;
-            if (k < nz) prod[k] = vl[j] * (kHint ? ld_hint(x + cl[j], h.keep) : __ldg(x + cl[j]));
+            if (k < nz) prod[k] = vl[j] * __ldg(x + cl[j]);
         }
         __syncthreads();
         for (int32_t row = r0 + tid; row < r1; row += kAdNT) {
@@ -287,23 +248,13 @@ void launch_adaptive(const krysp_gpu_mat* cm, bool coo_part, const double* x, do
         P = &m->ad_csr;
     }
     if (!P->built) build_plan(c, A.rp, m->n_rows, *P);
-    static const bool hint = [] {
-        // opt-in: measured slower (the policy registers spill under the 5-CTA register cap)
-        const char* e = std::getenv("KRYSP_GATHER_HINT");
-        return e && std::atoi(e) != 0;
-    }();
     const int64_t items = P->nchunk + P->nlng + (P->nmed + kAdNT / 32 - 1) / (kAdNT / 32) + P->nblk;
-    if (items == 0) {
-    } else if (hint) {
-        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel<true>, kAdNT, 0), items);
-        adaptive_kernel<true><<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
-                                                            P->nchunk, P->partials, x, y, accumulate ? 1 : 0);
-    } else {
-        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel<false>, kAdNT, 0), items);
-        adaptive_kernel<false><<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
-                                                             P->nchunk, P->partials, x, y, accumulate ? 1 : 0);
+    if (items) {
+        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel, kAdNT, 0), items);
+        adaptive_kernel<<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
+                                                      P->nchunk, P->partials, x, y, accumulate ? 1 : 0);
+        KG_LAUNCH(c);
     }
-    KG_LAUNCH(c);
     if (P->ngiant) {
         giant_fixup_kernel<<<grid_for(P->ngiant, 128, 1024), 128, 0, s>>>(P->giant, P->ngiant, P->partials, y,
                                                                          accumulate ? 1 : 0);

@@ -81,8 +81,6 @@ __global__ void csr_vector_kernel(CsrView A, const double* __restrict__ x, Epi e
 // ------------------------------------------------------------------ CSR tile (tw == 1 order)
 constexpr int kTileRows = 256;
 
-inline int tile_smem_bytes(int cap) { return (cap + 8) * 8 + (cap + 8) * 4; }
-
 // ------------------------------------------------------------------ CSR tile, TMA pipeline
 // Same tw == 1 order, but tiles are moved by the Tensor Memory Accelerator: one elected
 // thread issues 1-D bulk copies (cp.async.bulk, L2 evict-first) of the next tile's row
