@@ -670,17 +670,20 @@ int fused_grid_mult() {
 }
 
 // ------------------------------------------------------------------ fused GCR(m) kernels
-// Multi-dot: out[q] = <w, V_q> for q < k (k <= 8) in one pass over w (Dot2 compensated).
+// Multi-dot: out[q] = <w, V_q> for q < k (k <= 8) in one pass over w.  Plain FMA partial
+// sums in a fixed tree (deterministic): the Dot2 variant carried 16 more registers per thread
+// and ran this bandwidth-bound pass at 3 TB/s (GCR's orthogonalisation coefficients do not
+// need the compensation the BiCGStab breakdown tests do).
 constexpr int kMdNT = 256;
 constexpr int kMdG = 8;
 
 __global__ void __launch_bounds__(kMdNT) multidot_kernel(int64_t n, const double* __restrict__ w,
                                                           const double* const* __restrict__ vs, int k,
                                                           double* partials, unsigned* counter, double* out) {
-    __shared__ D2 sh[32];
-    D2 acc[kMdG];
+    __shared__ double sh[32];
+    double acc[kMdG];
 #pragma unroll
-    for (int q = 0; q < kMdG; ++q) acc[q] = D2{0.0, 0.0};
+    for (int q = 0; q < kMdG; ++q) acc[q] = 0.0;
     const double* v[kMdG];
 #pragma unroll
     for (int q = 0; q < kMdG; ++q) v[q] = q < k ? vs[q] : nullptr;
@@ -688,22 +691,18 @@ __global__ void __launch_bounds__(kMdNT) multidot_kernel(int64_t n, const double
         const double wi = w[i];
 #pragma unroll
         for (int q = 0; q < kMdG; ++q)
-            if (q < k) d2_add_prod(acc[q], wi, v[q][i]);
+            if (q < k) acc[q] = fma(wi, v[q][i], acc[q]);
     }
     for (int q = 0; q < k; ++q) {
-        const D2 b = block_d2_dyn(acc[q], sh);
-        if (threadIdx.x == 0) {
-            partials[2 * (blockIdx.x * kMdG + q)] = b.s;
-            partials[2 * (blockIdx.x * kMdG + q) + 1] = b.c;
-        }
+        const double b = block_sum_dyn(acc[q], sh);
+        if (threadIdx.x == 0) partials[blockIdx.x * kMdG + q] = b;
     }
     if (last_block(counter)) {
         for (int q = 0; q < k; ++q) {
-            D2 t{0.0, 0.0};
-            for (int i = threadIdx.x; i < (int)gridDim.x; i += kMdNT)
-                t = d2_merge(t, D2{__ldcg(partials + 2 * (i * kMdG + q)), __ldcg(partials + 2 * (i * kMdG + q) + 1)});
-            t = block_d2_dyn(t, sh);
-            if (threadIdx.x == 0) out[q] = __dadd_rn(t.s, t.c);
+            double t = 0.0;
+            for (int i = threadIdx.x; i < (int)gridDim.x; i += kMdNT) t += __ldcg(partials + i * kMdG + q);
+            t = block_sum_dyn(t, sh);
+            if (threadIdx.x == 0) out[q] = t;
         }
         if (threadIdx.x == 0) *counter = 0;
     }

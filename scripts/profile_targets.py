@@ -42,3 +42,8 @@ if target == "c4_bicgstab":
     cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=3, tolerance=1e-30)
     r = kg.solve(H, "bicgstab", np.ones(H.n_rows), cfg=cfg)
     print("c4_bicgstab", r.iterations)
+if target == "gcr":
+    A = ctx.generate("lap3d7", 300)
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=30, tolerance=1e-30)
+    r = kg.solve(A, "gcr", np.ones(A.n_rows), cfg=cfg)
+    print("gcr", r.iterations)
