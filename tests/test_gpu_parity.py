@@ -406,3 +406,31 @@ def test_cpp_shim_drop_in(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "shim ok" in out.stdout
+
+
+BREAKDOWN_CASES = {
+    "indefinite": (kg.CsrMatrix(2, 2, np.array([0, 1, 2]), np.array([0, 1]), np.array([1., -1.])), [1., 1.]),
+    "skew": (kg.CsrMatrix(2, 2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([0., 1., -1., 0.])), [1., 0.]),
+    "nan_rhs": (kg.CsrMatrix(3, 3, np.arange(4), np.arange(3), np.full(3, 2.)), [1., np.nan, 1.]),
+    "inf_rhs": (kg.CsrMatrix(3, 3, np.arange(4), np.arange(3), np.full(3, 2.)), [1., np.inf, 1.]),
+}
+
+
+@pytest.mark.parametrize("case", sorted(BREAKDOWN_CASES))
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_breakdown_and_non_finite_match_reference(ctx, ref, case, mode):
+    """Breakdown / NonFinite (test_solvers.cpp failure cases): same exception class as the
+    reference for every solver and mode, with the same message (same check, same point)."""
+    m, b = BREAKDOWN_CASES[case]
+    b = np.array(b)
+    rm = ref.from_csr(m)
+    A = ctx.upload(m)
+    for s in SOLVERS:
+        want = ref.solve(rm, s, b, jacobi=False, stab_l=2)
+        assert want["status"] in (kg.Breakdown.code, kg.NonFinite.code), (s, want)
+        cfg = kg.SolverConfig(mode=mode, preconditioner="none", stab_l=2,
+                              policy=kg.ExecPolicy(0, 0) if mode == "fast" else kg.ExecPolicy())
+        with pytest.raises(kg.Error) as ei:
+            kg.solve(A, s, b, cfg=cfg)
+        assert ei.value.code == want["status"], (s, mode, str(ei.value), want["error"])
+        assert str(ei.value) == want["error"], (s, mode, str(ei.value), want["error"])
