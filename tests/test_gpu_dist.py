@@ -224,3 +224,23 @@ def test_dist_solve_errors(ctx):
         D.solve("bicgcr", split(np.ones(N), N, 2))
     with pytest.raises(kg.Error):
         D.solve("pcg", split(np.ones(N), N, 2), cfg=kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(0, 0)))
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_dist_breakdown_matches_reference(ctx, ref, mode):
+    """Breakdown / NonFinite over the partition: same class and message as the reference."""
+    A = kg.CsrMatrix(4, 4, np.arange(5), np.arange(4), np.array([1., -1., 1., -1.]))
+    rm = ref.from_csr(A)
+    for rhs in ([1., 1., 1., 1.], [1., np.nan, 1., 1.]):
+        b = np.array(rhs)
+        for s in ["pcg", "cg_classic", "gcr", "bicgstab", "bicgstab_l", "tfqmr"]:
+            want = ref.solve(rm, s, b, jacobi=False, stab_l=2)
+            D = DistSystem.emulated(ctx, 2)
+            D.set_csr(0, 4, kg.CsrMatrix(2, 4, np.array([0, 1, 2]), np.array([0, 1]), np.array([1., -1.])))
+            D.set_csr(1, 4, kg.CsrMatrix(2, 4, np.array([0, 1, 2]), np.array([2, 3]), np.array([1., -1.])))
+            D.setup()
+            cfg = kg.SolverConfig(mode=mode, preconditioner="none", stab_l=2,
+                                  policy=kg.ExecPolicy(0, 0) if mode == "fast" else kg.ExecPolicy())
+            with pytest.raises(kg.Error) as ei:
+                D.solve(s, split(b, 4, 2), cfg=cfg)
+            assert ei.value.code == want["status"] and str(ei.value) == want["error"], (s, str(ei.value), want)
