@@ -27,12 +27,11 @@ struct NcclApi {
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
 
     static NcclApi& get() {
-        static NcclApi a;
-        static bool tried = false;
-        if (!tried) {
-            tried = true;
-            a.load();
-        }
+        static NcclApi a = [] {  // loaded once; thread-safe static initialisation
+            NcclApi x;
+            x.load();
+            return x;
+        }();
         if (!a.ok) fail(KRYSP_NCCL_ERROR, "NCCL unavailable: %s", a.err.c_str());
         return a;
     }

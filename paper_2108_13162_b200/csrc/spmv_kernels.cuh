@@ -337,7 +337,7 @@ inline int resident_blocks(K kernel, int threads, int smem) {
     struct H {
         size_t operator()(const Key& a) const { return std::hash<const void*>()(a.k) ^ ((size_t)a.t << 20) ^ a.s; }
     };
-    static std::unordered_map<Key, int, H> cache;
+    static thread_local std::unordered_map<Key, int, H> cache;  // per host thread: no locking
     const Key key{reinterpret_cast<const void*>(kernel), threads, smem};
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
