@@ -147,7 +147,7 @@ __global__ void diag_ell(EllView E, double* d, int64_t n) {
         double v = 0.0;
         if (r < E.n_rows)
             for (int32_t s = 0; s < E.width; ++s) {
-                const int64_t slot = (int64_t)s * E.n_rows + r;
+                const int64_t slot = (int64_t)s * E.ld + r;
                 if (E.jcoef[slot] == r) v = E.coef[slot];
             }
         d[r] = v;

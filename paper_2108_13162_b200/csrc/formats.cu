@@ -156,7 +156,7 @@ __global__ void csr_to_coo_rows(const int32_t* __restrict__ rp, int32_t n_rows, 
 // csr_to_ell fill (formats.cpp:94-103) and the ELL part of csr_to_hyb (:132-144): the first
 // min(width, len) entries of row r go to slots 0.., the rest of the slab is padding
 // (0.0, sentinel n_cols).  Overflow entries (HYB) are appended at coo_off[r].
-__global__ void csr_to_ell_fill(kg::CsrView A, int32_t width, double* __restrict__ coef,
+__global__ void csr_to_ell_fill(kg::CsrView A, int32_t width, int64_t ld, double* __restrict__ coef,
                                 int32_t* __restrict__ jcoef, const int64_t* __restrict__ coo_off,
                                 int32_t* __restrict__ co_r, int32_t* __restrict__ co_c,
                                 double* __restrict__ co_v) {
@@ -167,7 +167,7 @@ __global__ void csr_to_ell_fill(kg::CsrView A, int32_t width, double* __restrict
         int32_t len = e - b;
         int32_t in_ell = len < width ? len : width;
         for (int32_t s = 0; s < width; ++s) {
-            int64_t slot = (int64_t)s * n + r;
+            int64_t slot = (int64_t)s * ld + r;
             if (s < in_ell) {
                 coef[slot] = A.val[b + s];
                 jcoef[slot] = A.col[b + s];
@@ -222,7 +222,7 @@ __global__ void ell_row_count(kg::EllView E, const int64_t* __restrict__ extra,
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
          r += (int64_t)gridDim.x * blockDim.x) {
         int64_t c = 0;
-        for (int32_t s = 0; s < E.width; ++s) c += (E.jcoef[(int64_t)s * n + r] != E.n_cols);
+        for (int32_t s = 0; s < E.width; ++s) c += (E.jcoef[(int64_t)s * E.ld + r] != E.n_cols);
         cnt[r] = c + (extra ? extra[r] : 0);
     }
 }
@@ -242,7 +242,7 @@ __global__ void ell_to_csr_fill(kg::EllView E, const int64_t* __restrict__ off,
          r += (int64_t)gridDim.x * blockDim.x) {
         int64_t o = off[r];
         for (int32_t s = 0; s < E.width; ++s) {
-            int64_t slot = (int64_t)s * n + r;
+            int64_t slot = (int64_t)s * E.ld + r;
             int32_t c = E.jcoef[slot];
             if (c != E.n_cols) {
                 ci[o] = c;
@@ -819,8 +819,9 @@ static krysp_gpu_mat* csr_to_ell_hyb(const krysp_gpu_mat* a, bool hyb, int64_t w
     krysp_gpu_mat* m = mat_new(c, hyb ? KRYSP_FMT_HYB : KRYSP_FMT_ELL, n, a->n_cols);
     try {
         m->width = width;
-        m->coef = dev_alloc<double>(n * width + kPad, true, c->stream);
-        m->jcoef = dev_alloc<int32_t>(n * width + kPad, true, c->stream);
+        m->ell_ld = (n + 3) & ~int64_t(3);
+        m->coef = dev_alloc<double>(m->ell_ld * width + kPad, true, c->stream);
+        m->jcoef = dev_alloc<int32_t>(m->ell_ld * width + kPad, true, c->stream);
         int64_t* off = nullptr;
         int64_t o_nnz = 0;
         if (hyb) {
@@ -841,7 +842,7 @@ static krysp_gpu_mat* csr_to_ell_hyb(const krysp_gpu_mat* a, bool hyb, int64_t w
         m->co_v = dev_alloc<double>(o_nnz + kPad, true, c->stream);
         if (n) {
             csr_to_ell_fill<<<grid_for(n, kNT, cap_grid(c)), kNT, 0, c->stream>>>(
-                a->csr(), (int32_t)width, m->coef, m->jcoef, off, m->co_r, m->co_c, m->co_v);
+                a->csr(), (int32_t)width, m->ell_ld, m->coef, m->jcoef, off, m->co_r, m->co_c, m->co_v);
             KG_LAUNCH(c);
         }
         KG_CUDA(cudaStreamSynchronize(c->stream));
@@ -1020,10 +1021,16 @@ void download_csr(const krysp_gpu_mat* m, int64_t* rp, int64_t* ci, double* cv) 
 void download_ell(const krysp_gpu_mat* m, double* coef, int64_t* jcoef) {
     if (m->format != KRYSP_FMT_ELL && m->format != KRYSP_FMT_HYB) fail(KRYSP_ERROR, "matrix has no ELL part");
     cudaStream_t s = m->ctx->stream;
-    int64_t slots = m->n_rows * m->width;
-    widen(m->jcoef, jcoef, slots, s);
-    if (slots) KG_CUDA(cudaMemcpyAsync(coef, m->coef, 8 * slots, cudaMemcpyDeviceToHost, s));
+    // the device slab has slot stride ell_ld; the reference layout is stride n_rows
+    const int64_t n = m->n_rows, ld = m->ell().ld, w = m->width;
+    if (n == 0 || w == 0) return;
+    std::vector<int32_t> jc((size_t)(ld * w));
+    KG_CUDA(cudaMemcpyAsync(jc.data(), m->jcoef, 4 * (size_t)(ld * w), cudaMemcpyDeviceToHost, s));
+    KG_CUDA(cudaMemcpy2DAsync(coef, 8 * (size_t)n, m->coef, 8 * (size_t)ld, 8 * (size_t)n, (size_t)w,
+                              cudaMemcpyDeviceToHost, s));
     KG_CUDA(cudaStreamSynchronize(s));
+    for (int64_t sl = 0; sl < w; ++sl)
+        for (int64_t r = 0; r < n; ++r) jcoef[sl * n + r] = jc[(size_t)(sl * ld + r)];
 }
 
 void download_coo(const krysp_gpu_mat* m, int64_t* r, int64_t* ci, double* v) {

@@ -83,6 +83,7 @@ struct EllView {
     int32_t width;
     const int32_t* __restrict__ jcoef;  // column-major, sentinel = n_cols
     const double* __restrict__ coef;
+    int64_t ld;  // slot stride (>= n_rows, multiple of 4: 16-byte aligned slot columns)
 };
 struct CooView {
     int32_t n_rows, n_cols;
@@ -126,6 +127,7 @@ struct krysp_gpu_mat {
     double* cv = nullptr;
     // ELL (also the ELL part of HYB)
     int64_t width = 0;
+    int64_t ell_ld = 0;  // slot stride of the slab (n_rows rounded up to 4)
     int32_t* jcoef = nullptr;
     double* coef = nullptr;
     // COO (also the overflow part of HYB)
@@ -141,7 +143,9 @@ struct krysp_gpu_mat {
     kg::CsrView csr() const {
         return {(int32_t)n_rows, (int32_t)n_cols, nnz, rp, ci, cv};
     }
-    kg::EllView ell() const { return {(int32_t)n_rows, (int32_t)n_cols, (int32_t)width, jcoef, coef}; }
+    kg::EllView ell() const {
+        return {(int32_t)n_rows, (int32_t)n_cols, (int32_t)width, jcoef, coef, ell_ld ? ell_ld : n_rows};
+    }
     kg::CooView coo() const { return {(int32_t)n_rows, (int32_t)n_cols, coo_nnz, co_r, co_c, co_v}; }
 };
 

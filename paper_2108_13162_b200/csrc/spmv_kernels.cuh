@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
 template <class Epi, int KB>
 __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
     if (!epi.active()) return;
-    const int64_t n = E.n_rows;
+    const int64_t n = E.n_rows, ld = E.ld;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r - threadIdx.x < n;
          r += (int64_t)gridDim.x * blockDim.x) {
         double sum = 0.0;
@@ -279,8 +279,8 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
                     for (int j = 0; j < 8; ++j) {
                         c[j] = E.n_cols;
                         if (s + j < E.width) {
-                            c[j] = __ldcs(jc + (int64_t)(s + j) * n);
-                            v[j] = __ldcs(cf + (int64_t)(s + j) * n);
+                            c[j] = __ldcs(jc + (int64_t)(s + j) * ld);
+                            v[j] = __ldcs(cf + (int64_t)(s + j) * ld);
                         }
                     }
 #pragma unroll
@@ -298,8 +298,8 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
                     double v[4], xv[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        c[j] = __ldcs(jc + (int64_t)(s + j) * n);
-                        v[j] = __ldcs(cf + (int64_t)(s + j) * n);
+                        c[j] = __ldcs(jc + (int64_t)(s + j) * ld);
+                        v[j] = __ldcs(cf + (int64_t)(s + j) * ld);
                     }
 #pragma unroll
                     for (int j = 0; j < 4; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
@@ -308,8 +308,8 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
                         if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
                 }
                 for (; s < E.width; ++s) {
-                    const int32_t c = __ldcs(jc + (int64_t)s * n);
-                    if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * n), __ldg(x + c));
+                    const int32_t c = __ldcs(jc + (int64_t)s * ld);
+                    if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * ld), __ldg(x + c));
                 }
             }
             epi.row(r, sum);

@@ -47,3 +47,15 @@ if target == "gcr":
     cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=30, tolerance=1e-30)
     r = kg.solve(A, "gcr", np.ones(A.n_rows), cfg=cfg)
     print("gcr", r.iterations)
+if target == "c1":
+    A = ctx.generate("poisson2d", 1000)
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=40, tolerance=1e-30)
+    r = kg.solve(A, "pcg", np.ones(A.n_rows), cfg=cfg)
+    print("c1", r.iterations, r.device_time / r.iterations * 1e6, "us/it")
+if target == "c2_ell":
+    E = ctx.generate("convdiff2d", 4000, 0.5).convert("ell", slot_cap=1 << 40)
+    x, y = ctx.to_device(np.ones(E.n_cols)), ctx.empty(E.n_rows)
+    kg.spmv_into(E, x, y, kg.ExecPolicy(256, 1), "exact")
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=3, tolerance=1e-30)
+    r = kg.solve(E, "bicgstab", np.ones(E.n_rows), cfg=cfg)
+    print("c2_ell", r.iterations)
