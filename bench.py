@@ -29,6 +29,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the image sets NCCL_DEBUG=VERSION: keep NCCL's banner off stdout (one JSON line there)
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "FP64 CG iterations/sec and SpMV GFLOP/s (+% HBM roofline) at 1/2/4/8 B200"
 GOLDEN_ITERS, GOLDEN_MEASURE = 733, 9.650895609e-07  # SURVEY §6 / §8(a12), oracle at 400^3
