@@ -211,13 +211,7 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
         KG_CUDA(cudaStreamEndCapture(st, &graph));
         KG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         cudaGraphDestroy(graph);
-        int done = 0;
-        while (!done) {
-            KG_CUDA(cudaGraphLaunch(exec, st));
-            KG_CUDA(cudaMemcpyAsync(c->h_pinned, &d_st[0].done, 4, cudaMemcpyDeviceToHost, st));
-            stream_wait(c);
-            std::memcpy(&done, c->h_pinned, 4);
-        }
+        run_pipelined(c, &d_st[0].done, [&] { KG_CUDA(cudaGraphLaunch(exec, st)); });
     } catch (...) {
         err = std::current_exception();
     }

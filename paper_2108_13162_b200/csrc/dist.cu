@@ -1557,8 +1557,8 @@ krysp_status krysp_gpu_dist_pcg_time(krysp_gpu_dist* d, int64_t n, double* secon
 krysp_status krysp_gpu_dist_pcg_run(krysp_gpu_dist* d, double* seconds) {
     return guard([&] {
         auto t0 = std::chrono::steady_clock::now();
-        if (!d->done_at_setup)
-            while (!kg::pcg_done(d)) kg::pcg_enqueue(d, krysp_gpu_dist::kChunk);
+        if (!d->done_at_setup && !kg::pcg_done(d))  // same chunk count on every rank: the flag is allreduced
+            kg::run_pipelined(d->ctx, &d->parts[0].st->done, [&] { kg::pcg_enqueue(d, krysp_gpu_dist::kChunk); });
         if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
 }

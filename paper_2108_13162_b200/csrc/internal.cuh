@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <exception>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -374,6 +375,39 @@ inline void stream_wait(krysp_gpu_ctx* c) {
     while ((e = cudaEventQuery(c->sync_ev)) == cudaErrorNotReady) {
     }
     if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "stream wait: %s", cudaGetErrorString(e));
+}
+
+// Drive a device-resident solve to convergence with one chunk always queued ahead of the host's
+// look at the `done` flag: enqueue() queues a chunk of iterations, the flag is copied after
+// it, and the host waits for the copy of chunk k while chunk k+1 runs — the GPU never idles
+// on the host round trip.  A chunk queued past convergence costs only no-op kernels.
+template <class Enqueue>
+void run_pipelined(krysp_gpu_ctx* c, const int* d_done, Enqueue&& enqueue) {
+    cudaEvent_t ev[2];
+    for (auto& e : ev) KG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int* h = reinterpret_cast<int*>(c->h_pinned + 8);  // two flag slots
+    auto post = [&](int k) {
+        enqueue();
+        KG_CUDA(cudaMemcpyAsync(h + k, d_done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        KG_CUDA(cudaEventRecord(ev[k], c->stream));
+    };
+    std::exception_ptr err;
+    try {
+        post(0);
+        for (int k = 0;; k ^= 1) {
+            post(k ^ 1);
+            cudaError_t e;
+            while ((e = cudaEventQuery(ev[k])) == cudaErrorNotReady) {
+            }
+            if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "solve wait: %s", cudaGetErrorString(e));
+            if (*(volatile int*)(h + k)) break;
+        }
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+        err = std::current_exception();
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (err) std::rethrow_exception(err);
 }
 
 // KRYSP_TRACE=1: host wall-clock laps of the big C-ABI calls (stderr)

@@ -1519,7 +1519,7 @@ struct PcgSession {
         KG_CUDA(cudaEventCreate(&a));
         KG_CUDA(cudaEventCreate(&b));
         KG_CUDA(cudaEventRecord(a, c->stream));
-        while (!finished()) enqueue(kChunk);
+        if (!finished()) run_pipelined(c, &st->done, [&] { enqueue(kChunk); });
         KG_CUDA(cudaEventRecord(b, c->stream));
         KG_CUDA(cudaEventSynchronize(b));
         float ms = 0.f;
@@ -1910,7 +1910,7 @@ struct BicgstabSession {
         KG_CUDA(cudaEventCreate(&b));
         KG_CUDA(cudaEventRecord(a, e.c->stream));
         // one extra graph after `done` lets a pending half-step x update (K4) run
-        while (!finished()) enqueue(kChunk);
+        if (!finished()) run_pipelined(e.c, &st->done, [&] { enqueue(kChunk); });
         enqueue(1);
         KG_CUDA(cudaEventRecord(b, e.c->stream));
         KG_CUDA(cudaEventSynchronize(b));
