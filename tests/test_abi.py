@@ -30,7 +30,9 @@ def test_library_exports_every_header_symbol():
 def test_cpp_shim_declares_same_surface():
     text = open(os.path.join(ROOT, "include", "krysp_gpu.hpp")).read()
     for name in ["solve_pcg", "solve_bicgstab", "solve_tfqmr", "solve_gcr", "solve_bicgstab_l", "solve_bicgcr",
-                 "solve_cg_classic", "spmv_into", "csr_to_ell", "csr_to_hyb", "tune_spmv", "dot", "norm2"]:
+                 "solve_cg_classic", "spmv_into", "csr_to_ell", "csr_to_hyb", "tune_spmv", "dot", "norm2",
+                 "build_coo_device", "read_matrix_market_device", "write_matrix_market", "compute_stats",
+                 "band_row_assignment", "read_assignment_file", "solve_cg_substructured"]:
         assert re.search(r"\b" + name + r"\s*\(", text) or f"KRYSP_GPU_SOLVER({name}," in text, name
 
 
