@@ -11,6 +11,7 @@
 // captured in chunks and a converged solve turns the remaining kernels into no-ops.
 #include <cstring>
 
+#include "descent.cuh"
 #include "engine.cuh"
 #include "nccl_api.cuh"
 
@@ -18,39 +19,6 @@ namespace kg {
 namespace {
 
 constexpr int kDcNT = 256;
-
-struct SubCgState {
-    double red_loc[4];  // this subdomain's two dots, (sum, compensation) each
-    double red[4];      // summed over subdomains
-    double norm_g0, tol, denom, rho, gamma, measure;
-    long long iter, max_it;
-    int done, status;
-};
-
-__device__ __forceinline__ double sc_red(const SubCgState* st, int k) { return st->red[2 * k] + st->red[2 * k + 1]; }
-
-__device__ __forceinline__ void sc_finish2(D2 a0, D2 a1, D2* sh, double* partials, unsigned* counter, SubCgState* st) {
-    const D2 b0 = block_d2_dyn(a0, sh);
-    const D2 b1 = block_d2_dyn(a1, sh);
-    if (threadIdx.x == 0) {
-        double* q = partials + 4 * blockIdx.x;
-        q[0] = b0.s, q[1] = b0.c, q[2] = b1.s, q[3] = b1.c;
-    }
-    if (last_block(counter)) {
-        D2 t0{0.0, 0.0}, t1{0.0, 0.0};
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
-            const double* q = partials + 4 * i;
-            t0 = d2_merge(t0, D2{__ldcg(q), __ldcg(q + 1)});
-            t1 = d2_merge(t1, D2{__ldcg(q + 2), __ldcg(q + 3)});
-        }
-        t0 = block_d2_dyn(t0, sh);
-        t1 = block_d2_dyn(t1, sh);
-        if (threadIdx.x == 0) {
-            st->red_loc[0] = t0.s, st->red_loc[1] = t0.c, st->red_loc[2] = t1.s, st->red_loc[3] = t1.c;
-            *counter = 0;
-        }
-    }
-}
 
 // <Kw, w>_W and <g, w>_W (distributed_dot's weighted form: dot(x, fl(y * w)); W = I when wt is NULL)
 __global__ void __launch_bounds__(kDcNT) sc_dot2_kernel(int64_t n, const double* __restrict__ kw,
@@ -65,66 +33,92 @@ __global__ void __launch_bounds__(kDcNT) sc_dot2_kernel(int64_t n, const double*
         d2_add_prod(a0, kw[i], ww);
         d2_add_prod(a1, g[i], ww);
     }
-    sc_finish2(a0, a1, sh, partials, counter, st);
+    sc_finish2<false>(a0, a1, sh, partials, counter, st, [](SubCgState*) {});
 }
 
-// x += rho w; g += rho Kw; z = D^-1 g; <z, Kw>_W and <g, g>_W
-__global__ void __launch_bounds__(kDcNT) sc_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ g,
-                                                            double* __restrict__ z, const double* __restrict__ w,
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <bool kInv, bool kWt>
+__device__ __forceinline__ void sc_update_row(double rho, double& x, double& g, double& z, double w, double kw,
+                                              double inv, double wt, D2& a0, D2& a1) {
+    x = __dadd_rn(__dmul_rn(rho, w), x);
+    g = __dadd_rn(__dmul_rn(rho, kw), g);
+    z = kInv ? __dmul_rn(g, inv) : g;
+    d2_add_prod(a0, z, kWt ? __dmul_rn(kw, wt) : kw);
+    d2_add_prod(a1, g, kWt ? __dmul_rn(g, wt) : g);
+}
+
+// x += rho w; g += rho Kw; z = D^-1 g; <z, Kw>_W and <g, g>_W (kSingle: then gamma, the
+// measure and the convergence test in the last block).  vec: every vector 16-byte aligned —
+// the rows go in pairs (double2 loads and stores), the odd last row in the scalar loop.
+template <bool kSingle, bool kInv, bool kWt>
+__global__ void __launch_bounds__(kDcNT) sc_update_kernel(int64_t n, bool vec, double* __restrict__ x,
+                                                            double* __restrict__ g, double* __restrict__ z,
+                                                            const double* __restrict__ w,
                                                             const double* __restrict__ kw,
                                                             const double* __restrict__ inv,
                                                             const double* __restrict__ wt, SubCgState* st,
-                                                            double* partials, unsigned* counter) {
+                                                            double* partials, unsigned* counter, double* history) {
     if (*(volatile int*)&st->done) return;
     __shared__ D2 sh[32];
     const double rho = st->rho;
     D2 a0{0.0, 0.0}, a1{0.0, 0.0};
-    for (int64_t i = blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kDcNT) {
-        const double kwi = kw[i];
-        x[i] = __dadd_rn(__dmul_rn(rho, w[i]), x[i]);
-        const double gi = __dadd_rn(__dmul_rn(rho, kwi), g[i]);
-        g[i] = gi;
-        const double zi = inv ? __dmul_rn(gi, inv[i]) : gi;
-        z[i] = zi;
-        d2_add_prod(a0, zi, wt ? __dmul_rn(kwi, wt[i]) : kwi);
-        d2_add_prod(a1, gi, wt ? __dmul_rn(gi, wt[i]) : gi);
+    const int64_t n2 = vec ? n / 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * kDcNT;
+    for (int64_t i = blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n2; i += stride) {
+        double2 xv = reinterpret_cast<const double2*>(x)[i], gv = reinterpret_cast<const double2*>(g)[i], zv;
+        const double2 wv = reinterpret_cast<const double2*>(w)[i], kv = reinterpret_cast<const double2*>(kw)[i];
+        const double2 iv = kInv ? reinterpret_cast<const double2*>(inv)[i] : double2{0.0, 0.0};
+        const double2 tv = kWt ? reinterpret_cast<const double2*>(wt)[i] : double2{0.0, 0.0};
+        sc_update_row<kInv, kWt>(rho, xv.x, gv.x, zv.x, wv.x, kv.x, iv.x, tv.x, a0, a1);
+        sc_update_row<kInv, kWt>(rho, xv.y, gv.y, zv.y, wv.y, kv.y, iv.y, tv.y, a0, a1);
+        reinterpret_cast<double2*>(x)[i] = xv;
+        reinterpret_cast<double2*>(g)[i] = gv;
+        reinterpret_cast<double2*>(z)[i] = zv;
     }
-    sc_finish2(a0, a1, sh, partials, counter, st);
+    for (int64_t i = 2 * n2 + blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += stride) {
+        double xi = x[i], gi = g[i], zi;
+        sc_update_row<kInv, kWt>(rho, xi, gi, zi, w[i], kw[i], kInv ? inv[i] : 0.0, kWt ? wt[i] : 0.0, a0, a1);
+        x[i] = xi, g[i] = gi, z[i] = zi;
+    }
+    sc_finish2<kSingle>(a0, a1, sh, partials, counter, st, [history](SubCgState* s) { sc_scalar2(s, history); });
 }
 
-__device__ __forceinline__ void sc_fail(SubCgState* st, int code) {
-    st->status = code;
-    st->done = 1;
+template <bool kSingle>
+void launch_sc_update(unsigned grid, cudaStream_t s, const DescentPart& P, SubCgState* st, double* partials,
+                      unsigned* counter, double* history) {
+    auto al = [](const void* p) { return p == nullptr || aligned16(p); };
+    const bool vec = al(P.x) && al(P.g) && al(P.z) && al(P.w) && al(P.kw) && al(P.inv) && al(P.wt);
+#define KG_SCU(I, W)                                                                                                \
+    sc_update_kernel<kSingle, I, W><<<grid, kDcNT, 0, s>>>(P.n, vec, P.x, P.g, P.z, P.w, P.kw, P.inv, P.wt, st, \
+                                                           partials, counter, history)
+    if (P.inv && P.wt) KG_SCU(true, true);
+    else if (P.inv) KG_SCU(true, false);
+    else if (P.wt) KG_SCU(false, true);
+    else KG_SCU(false, false);
+#undef KG_SCU
 }
 
-__global__ void sc_scalar1_kernel(SubCgState* st) {  // solvers.cpp:220-225, substructure.cpp:534-539
-    if (st->done) return;
-    const double denom = sc_red(st, 0);
-    if (!isfinite(denom)) return sc_fail(st, kDescentDenomNonFinite);
-    if (fabs(denom) < 1e-300) return sc_fail(st, kDescentBreakdown);
-    st->denom = denom;
-    st->rho = -sc_red(st, 1) / denom;
-    if (!isfinite(st->rho)) sc_fail(st, kDescentRhoNonFinite);
-}
+__global__ void sc_scalar1_kernel(SubCgState* st) { sc_scalar1(st); }
 
-__global__ void sc_scalar2_kernel(SubCgState* st, double* history) {  // solvers.cpp:228-240, substructure.cpp:543-553
-    if (st->done) return;
-    st->gamma = -sc_red(st, 0) / st->denom;
-    if (!isfinite(st->gamma)) return sc_fail(st, kDescentGammaNonFinite);
-    const double measure = sqrt(sc_red(st, 1)) / st->norm_g0;
-    if (!isfinite(measure)) return sc_fail(st, kDescentMeasureNonFinite);
-    st->measure = measure;
-    history[st->iter] = measure;
-    st->iter += 1;
-    if (measure <= st->tol || st->iter >= st->max_it) st->done = 1;
-}
+__global__ void sc_scalar2_kernel(SubCgState* st, double* history) { sc_scalar2(st, history); }
 
-// w = fl(1 * z) + fl(gamma * w) (axpby, kernels.cpp:109-118); skipped once converged
-__global__ void __launch_bounds__(kDcNT) sc_axpby_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ w,
-                                                           const SubCgState* st) {
+// w = fl(1 * z) + fl(gamma * w) (axpby, kernels.cpp:109-118); skipped once converged; pairs
+// of rows when both vectors are 16-byte aligned
+__global__ void __launch_bounds__(kDcNT) sc_axpby_kernel(int64_t n, bool vec, const double* __restrict__ z,
+                                                           double* __restrict__ w, const SubCgState* st) {
     if (*(volatile const int*)&st->done) return;
     const double gamma = st->gamma;
-    for (int64_t i = blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kDcNT)
+    const int64_t n2 = vec ? n / 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * kDcNT;
+    for (int64_t i = blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n2; i += stride) {
+        const double2 zv = reinterpret_cast<const double2*>(z)[i];
+        double2 wv = reinterpret_cast<const double2*>(w)[i];
+        wv.x = __dadd_rn(zv.x, __dmul_rn(gamma, wv.x));
+        wv.y = __dadd_rn(zv.y, __dmul_rn(gamma, wv.y));
+        reinterpret_cast<double2*>(w)[i] = wv;
+    }
+    for (int64_t i = 2 * n2 + blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += stride)
         w[i] = __dadd_rn(z[i], __dmul_rn(gamma, w[i]));
 }
 
@@ -142,7 +136,7 @@ __global__ void sc_emu_reduce_kernel(SubCgState* sts, int ns) {
 
 int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const std::function<void()>& apply_op,
                   void* comm, double norm_g0, const krysp_solver_cfg& cfg, std::vector<double>& history,
-                  int64_t& iterations, double& measure) {
+                  int64_t& iterations, double& measure, const DescentFusedOp& fused_op) {
     cudaStream_t st = c->stream;
     const size_t nh = parts.size();
     if ((int64_t)nh > kSlots) fail(KRYSP_ERROR, "the fused descent CG holds at most %d parts per GPU", kSlots);
@@ -156,7 +150,7 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
     SubCgState* d_st = dev_alloc<SubCgState>((int64_t)nh, false);
     double* d_hist = dev_alloc<double>((int64_t)nh * cfg.max_iterations, false);
     KG_CUDA(cudaMemcpyAsync(d_st, init.data(), sizeof(SubCgState) * nh, cudaMemcpyHostToDevice, st));
-    auto grid = [&](int64_t n) { return grid_for(n, kDcNT, (int64_t)c->sm_count * 4); };
+    auto grid = [&](int64_t n) { return grid_for(n, kDcNT, (int64_t)c->sm_count * 8); };
     auto slot = [&](size_t i) { return c->d_partials + (int64_t)i * kPartialCap; };
     auto cnt = [&](size_t i) { return c->d_counters + i; };
     auto reduce = [&]() {
@@ -169,7 +163,19 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
         KG_NCCL(NcclApi::get().AllReduce(base + offsetof(SubCgState, red_loc), base + offsetof(SubCgState, red), 4,
                                          ncclDouble, ncclSum, (ncclComm_t)comm, st));
     };
+    // one part, one GPU, and an operator that fuses the step-length dots (EpiDescent): three
+    // kernels per iteration — SpMV + dots + rho, update + dots + gamma/measure, direction
+    const bool single = fused_op && nh == 1 && !comm;
     auto iteration = [&]() {
+        if (single) {
+            const DescentPart& P = parts[0];
+            fused_op(d_st, slot(0), cnt(0));
+            launch_sc_update<true>(grid(P.n), st, P, d_st, slot(0), cnt(0), d_hist);
+            KG_LAUNCH(c);
+            sc_axpby_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, aligned16(P.z) && aligned16(P.w), P.z, P.w, d_st);
+            KG_LAUNCH(c);
+            return;
+        }
         apply_op();
         for (size_t i = 0; i < nh; ++i) {
             const DescentPart& P = parts[i];
@@ -181,8 +187,7 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
             const DescentPart& P = parts[i];
             sc_scalar1_kernel<<<1, 1, 0, st>>>(d_st + i);
             KG_LAUNCH(c);
-            sc_update_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, P.x, P.g, P.z, P.w, P.kw, P.inv, P.wt, d_st + i,
-                                                         slot(i), cnt(i));
+            launch_sc_update<false>(grid(P.n), st, P, d_st + i, slot(i), cnt(i), nullptr);
             KG_LAUNCH(c);
         }
         reduce();
@@ -190,7 +195,7 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
             const DescentPart& P = parts[i];
             sc_scalar2_kernel<<<1, 1, 0, st>>>(d_st + i, d_hist + (int64_t)i * cfg.max_iterations);
             KG_LAUNCH(c);
-            sc_axpby_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, P.z, P.w, d_st + i);
+            sc_axpby_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, aligned16(P.z) && aligned16(P.w), P.z, P.w, d_st + i);
             KG_LAUNCH(c);
         }
     };

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <functional>
 
+#include "descent.cuh"
 #include "internal.cuh"
 
 namespace kg {
@@ -123,11 +124,12 @@ struct DescentPart {
     double *x, *g, *z, *w, *kw;
     const double *inv, *wt;
 };
-enum { kDescentOk = 0, kDescentDenomNonFinite, kDescentBreakdown, kDescentRhoNonFinite, kDescentGammaNonFinite,
-       kDescentMeasureNonFinite };
+// fused_op (optional, one part on one GPU): kw = K w plus the step-length dots and rho into
+// the device state (EpiDescent, descent.cuh), given the state, partials slot and counter.
+using DescentFusedOp = std::function<void(SubCgState*, double*, unsigned*)>;
 int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const std::function<void()>& apply_op,
                   void* comm, double norm_g0, const krysp_solver_cfg& cfg, std::vector<double>& history,
-                  int64_t& iterations, double& measure);
+                  int64_t& iterations, double& measure, const DescentFusedOp& fused_op = nullptr);
 
 // The host-driven recurrences (pcg, cg_classic, gcr, bicgstab, bicgstab_l, tfqmr; FAST mode
 // uses the fused GCR / BiCGStab(l) / tfQMR variants) on an engine; report as krysp_report.

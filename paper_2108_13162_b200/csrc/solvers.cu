@@ -103,6 +103,9 @@ void pcg(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
     rep.end(e.c->stream);
 }
 
+template <class Epi>
+void spmv_fused(Engine& e, const double* x, double* y, Epi epi);  // below, with the epilogues
+
 // solve_cg_classic solvers.cpp:193-250
 void cg_classic(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
     DVec g = e.vec(), z = e.vec(), w = e.vec(), kw = e.vec();
@@ -122,8 +125,12 @@ void cg_classic(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
         const double* wp = w;
         double* kwp = kw;
         auto op = [&]() { e.spmv(wp, kwp); };
+        const double* gp = g;
+        auto fused = [&](SubCgState* dst, double* pa, unsigned* ca) {
+            spmv_fused(e, wp, kwp, EpiDescent{kwp, wp, gp, dst, pa, ca, {0, 0}, {0, 0}});
+        };
         int64_t its = 0;
-        const int st = fused_descent(e.c, {part}, op, nullptr, norm_g0, cfg, rep.history, its, measure);
+        const int st = fused_descent(e.c, {part}, op, nullptr, norm_g0, cfg, rep.history, its, measure, fused);
         rep.iterations = its;
         rep.end(e.c->stream);
         rep.final_measure = measure;
