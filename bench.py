@@ -480,6 +480,11 @@ def run_ours_dist(args, dist):
 
 def main():
     args = parse()
+    # stdout carries exactly one JSON line: anything a library prints on fd 1 (NCCL's version
+    # banner under NCCL_DEBUG=VERSION, ...) goes to stderr; the line goes to the saved fd
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     dist = Dist()
     try:
         if args.impl == "reference":
@@ -489,7 +494,7 @@ def main():
         else:
             line = run_ours(args, dist)
         if dist.rank == 0 and line is not None:
-            print(json.dumps(line), flush=True)
+            os.write(json_fd, (json.dumps(line) + "\n").encode())
     finally:
         dist.close()
 
