@@ -684,28 +684,39 @@ int fused_grid_mult() {
 constexpr int kMdNT = 256;
 constexpr int kMdG = 8;
 
+// out[q] = <w, v_q> for the K vectors of vs (K a template argument: the vector pointers in
+// registers, every row pair's K + 1 loads issued before the FMAs)
+template <int K>
 __global__ void __launch_bounds__(kMdNT) multidot_kernel(int64_t n, const double* __restrict__ w,
-                                                          const double* const* __restrict__ vs, int k,
-                                                          double* partials, unsigned* counter, double* out) {
+                                                          const double* const* __restrict__ vs, double* partials,
+                                                          unsigned* counter, double* out) {
     __shared__ double sh[32];
-    double acc[kMdG];
+    double acc[K];
+    const double2* v[K];
 #pragma unroll
-    for (int q = 0; q < kMdG; ++q) acc[q] = 0.0;
-    const double* v[kMdG];
+    for (int q = 0; q < K; ++q) acc[q] = 0.0, v[q] = reinterpret_cast<const double2*>(vs[q]);
+    // rows in pairs (16-byte loads: every basis vector is a 256-byte aligned allocation)
+    const int64_t n2 = n / 2, stride = (int64_t)gridDim.x * kMdNT;
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n2; i += stride) {
+        const double2 wi = __ldg(w2 + i);
+        double2 vi[K];
 #pragma unroll
-    for (int q = 0; q < kMdG; ++q) v[q] = q < k ? vs[q] : nullptr;
-    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
-        const double wi = w[i];
+        for (int q = 0; q < K; ++q) vi[q] = __ldg(v[q] + i);
 #pragma unroll
-        for (int q = 0; q < kMdG; ++q)
-            if (q < k) acc[q] = fma(wi, v[q][i], acc[q]);
+        for (int q = 0; q < K; ++q) acc[q] = fma(wi.y, vi[q].y, fma(wi.x, vi[q].x, acc[q]));
     }
-    for (int q = 0; q < k; ++q) {
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc[q] = fma(w[n - 1], vs[q][n - 1], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
         const double b = block_sum_dyn(acc[q], sh);
         if (threadIdx.x == 0) partials[blockIdx.x * kMdG + q] = b;
     }
     if (last_block(counter)) {
-        for (int q = 0; q < k; ++q) {
+        for (int q = 0; q < K; ++q) {
             double t = 0.0;
             for (int i = threadIdx.x; i < (int)gridDim.x; i += kMdNT) t += __ldcg(partials + i * kMdG + q);
             t = block_sum_dyn(t, sh);
@@ -713,6 +724,15 @@ __global__ void __launch_bounds__(kMdNT) multidot_kernel(int64_t n, const double
         }
         if (threadIdx.x == 0) *counter = 0;
     }
+}
+
+template <int K>
+void launch_multidot(int k, unsigned g, cudaStream_t s, int64_t n, const double* w, const double* const* vs,
+                     double* partials, unsigned* counter, double* out) {
+    if constexpr (K > 1) {
+        if (k < K) return launch_multidot<K - 1>(k, g, s, n, w, vs, partials, counter, out);
+    }
+    multidot_kernel<K><<<g, kMdNT, 0, s>>>(n, w, vs, partials, counter, out);
 }
 
 // x += alpha p_j; r -= alpha ap_j (two daxpy, solvers.cpp:306-307) and ||r||^2
@@ -762,9 +782,10 @@ __global__ void __launch_bounds__(kMdNT) gcr_next_kernel(int64_t n, const double
         s_ap[i] = AP[i];
     }
     __syncthreads();
-    D2 acc{0.0, 0.0};
+    D2 acc{0.0, 0.0}, acc_r{0.0, 0.0};
     for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
-        double pn = r[e], an = w[e];
+        const double re = r[e];
+        double pn = re, an = w[e];
         for (int i = 0; i < k; ++i) {
             pn = __dadd_rn(__dmul_rn(s_mb[i], s_p[i][e]), pn);
             an = __dadd_rn(__dmul_rn(s_mb[i], s_ap[i][e]), an);
@@ -772,16 +793,27 @@ __global__ void __launch_bounds__(kMdNT) gcr_next_kernel(int64_t n, const double
         p_next[e] = pn;
         ap_next[e] = an;
         d2_add_prod(acc, an, an);
+        d2_add_prod(acc_r, re, an);
     }
-    const D2 b = block_d2_dyn(acc, sh);
+    // out[0] = <ap_next, ap_next>; out[1] = <r, ap_next>, the next step's alpha numerator
+    const D2 b0 = block_d2_dyn(acc, sh);
+    const D2 b1 = block_d2_dyn(acc_r, sh);
     if (threadIdx.x == 0) {
-        partials[2 * blockIdx.x] = b.s;
-        partials[2 * blockIdx.x + 1] = b.c;
+        double* q = partials + 4 * blockIdx.x;
+        q[0] = b0.s, q[1] = b0.c, q[2] = b1.s, q[3] = b1.c;
     }
     if (last_block(counter)) {
-        const D2 t = reduce_d2_partials(partials, gridDim.x, sh);
+        D2 t0{0.0, 0.0}, t1{0.0, 0.0};
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+            const double* q = partials + 4 * i;
+            t0 = d2_merge(t0, D2{__ldcg(q), __ldcg(q + 1)});
+            t1 = d2_merge(t1, D2{__ldcg(q + 2), __ldcg(q + 3)});
+        }
+        t0 = block_d2_dyn(t0, sh);
+        t1 = block_d2_dyn(t1, sh);
         if (threadIdx.x == 0) {
-            *out = __dadd_rn(t.s, t.c);
+            out[0] = __dadd_rn(t0.s, t0.c);
+            out[1] = __dadd_rn(t1.s, t1.c);
             *counter = 0;
         }
     }
@@ -1059,25 +1091,51 @@ struct EpiScaleDot {
 };
 
 // u_i = r_i - beta u_i for i < k (axpby(1, rr[i], -beta, uu[i]), solvers.cpp:497-499)
-__global__ void __launch_bounds__(kMdNT) bl_beta_kernel(int64_t n, int k, double beta, double* const* __restrict__ rr,
+// The BiCG-part vector kernels take the basis count as a template argument: the vector
+// pointers sit in registers and every element's loads are issued before its stores (the
+// stores may alias nothing the same element reads, but the compiler cannot know that).
+template <int K>
+__global__ void __launch_bounds__(kMdNT) bl_beta_kernel(int64_t n, double beta, double* const* __restrict__ rr,
                                                          double* const* __restrict__ uu) {
     const double mb = -beta;
-    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT)
-        for (int i = 0; i < k; ++i) uu[i][e] = __dadd_rn(__dmul_rn(1.0, rr[i][e]), __dmul_rn(mb, uu[i][e]));
+    const double* r[K];
+    double* u[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) r[i] = rr[i], u[i] = uu[i];
+    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
+        double rv[K], uv[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) rv[i] = r[i][e], uv[i] = u[i][e];
+#pragma unroll
+        for (int i = 0; i < K; ++i) u[i][e] = __dadd_rn(__dmul_rn(1.0, rv[i]), __dmul_rn(mb, uv[i]));
+    }
 }
 
 // r_i -= alpha u_{i+1} (i < k), x += alpha u_0, ||r_0||^2 (solvers.cpp:507-513)
-__global__ void __launch_bounds__(kMdNT) bl_alpha_kernel(int64_t n, int k, double alpha, double* const* __restrict__ rr,
+template <int K>
+__global__ void __launch_bounds__(kMdNT) bl_alpha_kernel(int64_t n, double alpha, double* const* __restrict__ rr,
                                                           double* const* __restrict__ uu, double* __restrict__ x,
                                                           double* partials, unsigned* counter, double* out) {
     __shared__ D2 sh[32];
     D2 acc{0.0, 0.0};
     const double ma = -alpha;
+    double* r[K];
+    const double* u[K + 1];
+#pragma unroll
+    for (int i = 0; i < K; ++i) r[i] = rr[i];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) u[i] = uu[i];
     for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
-        for (int i = 0; i < k; ++i) rr[i][e] = __dadd_rn(__dmul_rn(ma, uu[i + 1][e]), rr[i][e]);
-        x[e] = __dadd_rn(__dmul_rn(alpha, uu[0][e]), x[e]);
-        const double r0 = rr[0][e];
-        d2_add_prod(acc, r0, r0);
+        double rv[K], uv[K + 1];
+#pragma unroll
+        for (int i = 0; i < K; ++i) rv[i] = r[i][e];
+#pragma unroll
+        for (int i = 0; i <= K; ++i) uv[i] = u[i][e];
+        const double xe = x[e];
+#pragma unroll
+        for (int i = 0; i < K; ++i) r[i][e] = rv[i] = __dadd_rn(__dmul_rn(ma, uv[i + 1]), rv[i]);
+        x[e] = __dadd_rn(__dmul_rn(alpha, uv[0]), xe);
+        d2_add_prod(acc, rv[0], rv[0]);
     }
     d2_grid_finish<1>(&acc, sh, partials, counter, out);
 }
@@ -1111,38 +1169,82 @@ __global__ void __launch_bounds__(kMdNT) bl_mgs_kernel(int64_t n, double* __rest
 //   x += g[1] r_0 (old r_0); r_0 -= gp[L] r_L; u_0 -= g[L] u_L;
 //   for j in 1..L-1: u_0 -= g[j] u_j; x += gpp[j] r_j; r_0 -= gp[j] r_j
 // then ||r_0||^2 and <r_0, r_shadow>
-__global__ void __launch_bounds__(kMdNT) bl_final_kernel(int64_t n, int L, const double* __restrict__ coef,
+template <int L>
+__global__ void __launch_bounds__(kMdNT) bl_final_kernel(int64_t n, const double* __restrict__ coef,
                                                           double* const* __restrict__ rr, double* const* __restrict__ uu,
                                                           double* __restrict__ x, const double* __restrict__ rs,
                                                           double* partials, unsigned* counter, double* out) {
     // coef: g[0..L], gp[0..L], gpp[0..L] (3 (L+1) doubles)
-    __shared__ double s_c[3 * 10];
+    __shared__ double s_c[3 * (L + 1)];
     __shared__ D2 sh[32];
     for (int i = threadIdx.x; i < 3 * (L + 1); i += kMdNT) s_c[i] = coef[i];
     __syncthreads();
     const double* g = s_c;
     const double* gp = s_c + (L + 1);
     const double* gpp = s_c + 2 * (L + 1);
+    double* r[L + 1];
+    double* u[L + 1];
+#pragma unroll
+    for (int i = 0; i <= L; ++i) r[i] = rr[i], u[i] = uu[i];
     D2 acc[2] = {D2{0.0, 0.0}, D2{0.0, 0.0}};
     for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
-        const double r0o = rr[0][e];
-        double xe = __dadd_rn(__dmul_rn(g[1], r0o), x[e]);
-        double r0 = __dadd_rn(__dmul_rn(-gp[L], rr[L][e]), r0o);
-        double u0 = __dadd_rn(__dmul_rn(-g[L], uu[L][e]), uu[0][e]);
+        double rv[L + 1], uv[L + 1];
+#pragma unroll
+        for (int i = 0; i <= L; ++i) rv[i] = r[i][e], uv[i] = u[i][e];
+        const double x0 = x[e], rse = rs[e];
+        double xe = __dadd_rn(__dmul_rn(g[1], rv[0]), x0);
+        double r0 = __dadd_rn(__dmul_rn(-gp[L], rv[L]), rv[0]);
+        double u0 = __dadd_rn(__dmul_rn(-g[L], uv[L]), uv[0]);
+#pragma unroll
         for (int j = 1; j < L; ++j) {
-            const double rj = rr[j][e];
-            u0 = __dadd_rn(__dmul_rn(-g[j], uu[j][e]), u0);
-            xe = __dadd_rn(__dmul_rn(gpp[j], rj), xe);
-            r0 = __dadd_rn(__dmul_rn(-gp[j], rj), r0);
+            u0 = __dadd_rn(__dmul_rn(-g[j], uv[j]), u0);
+            xe = __dadd_rn(__dmul_rn(gpp[j], rv[j]), xe);
+            r0 = __dadd_rn(__dmul_rn(-gp[j], rv[j]), r0);
         }
         x[e] = xe;
-        rr[0][e] = r0;
-        uu[0][e] = u0;
+        r[0][e] = r0;
+        u[0][e] = u0;
         d2_add_prod(acc[0], r0, r0);
-        d2_add_prod(acc[1], r0, rs[e]);
+        d2_add_prod(acc[1], r0, rse);
     }
     d2_grid_finish<2>(acc, sh, partials, counter, out);
 }
+
+template <template <int> class F, class... A>
+void bl_dispatch(int k, A... a) {
+    switch (k) {
+        case 1: return F<1>::go(a...);
+        case 2: return F<2>::go(a...);
+        case 3: return F<3>::go(a...);
+        case 4: return F<4>::go(a...);
+        case 5: return F<5>::go(a...);
+        case 6: return F<6>::go(a...);
+        case 7: return F<7>::go(a...);
+        case 8: return F<8>::go(a...);
+        case 9: return F<9>::go(a...);
+        default: fail(KRYSP_ERROR, "BiCGStab(l) basis count %d out of range", k);
+    }
+}
+template <int K>
+struct BlBeta {
+    static void go(unsigned g, cudaStream_t s, int64_t n, double beta, double* const* rr, double* const* uu) {
+        bl_beta_kernel<K><<<g, kMdNT, 0, s>>>(n, beta, rr, uu);
+    }
+};
+template <int K>
+struct BlAlpha {
+    static void go(unsigned g, cudaStream_t s, int64_t n, double alpha, double* const* rr, double* const* uu,
+                   double* x, double* part, unsigned* cnt, double* out) {
+        bl_alpha_kernel<K><<<g, kMdNT, 0, s>>>(n, alpha, rr, uu, x, part, cnt, out);
+    }
+};
+template <int L>
+struct BlFinal {
+    static void go(unsigned g, cudaStream_t s, int64_t n, const double* coef, double* const* rr, double* const* uu,
+                   double* x, const double* rs, double* part, unsigned* cnt, double* out) {
+        bl_final_kernel<L><<<g, kMdNT, 0, s>>>(n, coef, rr, uu, x, rs, part, cnt, out);
+    }
+};
 
 // FAST BiCGStab(l) (solvers.cpp:444-572): the reference's recurrences and host scalar
 // algebra, vector work fused (the i-loops of the BiCG part in one pass each, MGS steps with
@@ -1199,7 +1301,7 @@ void bicgstab_l_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, do
                 const double beta = alpha * rho1 / rho0;
                 check_finite(beta, "beta");
                 rho0 = rho1;
-                bl_beta_kernel<<<g, kMdNT, 0, c->stream>>>(n, (int)(j + 1), beta, d_rr, d_uu);
+                bl_dispatch<BlBeta>((int)(j + 1), g, c->stream, n, beta, (double* const*)d_rr, (double* const*)d_uu);
                 KG_LAUNCH(c);
                 spmv_fused(e, uu[j], uu[j + 1], EpiScaleDot{uu[j + 1], dinv, rs, part, cnt, d_scal, D2{0.0, 0.0}});
                 double gd;
@@ -1207,7 +1309,8 @@ void bicgstab_l_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, do
                 if (vanishes(gd)) fail(KRYSP_BREAKDOWN, "bicgstab(l): <u, r_shadow> vanished");
                 alpha = rho0 / gd;
                 check_finite(alpha, "alpha");
-                bl_alpha_kernel<<<g, kMdNT, 0, c->stream>>>(n, (int)(j + 1), alpha, d_rr, d_uu, x, part, cnt, d_scal);
+                bl_dispatch<BlAlpha>((int)(j + 1), g, c->stream, n, alpha, (double* const*)d_rr, (double* const*)d_uu, x,
+                                     part, cnt, d_scal);
                 KG_LAUNCH(c);
                 spmv_fused(e, rr[j], rr[j + 1],
                            EpiScaleDot{rr[j + 1], dinv, rs, part, cnt, d_scal + 1, D2{0.0, 0.0}});
@@ -1268,7 +1371,8 @@ void bicgstab_l_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, do
             coef.insert(coef.end(), gp.begin(), gp.end());
             coef.insert(coef.end(), gpp.begin(), gpp.end());
             KG_CUDA(cudaMemcpyAsync(d_scal + 16, coef.data(), 8 * coef.size(), cudaMemcpyHostToDevice, c->stream));
-            bl_final_kernel<<<g, kMdNT, 0, c->stream>>>(n, (int)L, d_scal + 16, d_rr, d_uu, x, rs, part, cnt, d_scal);
+            bl_dispatch<BlFinal>((int)L, g, c->stream, n, (const double*)(d_scal + 16), (double* const*)d_rr,
+                                 (double* const*)d_uu, x, (const double*)rs, part, cnt, d_scal);
             KG_LAUNCH(c);
             double two[2];
             d2h(two, 2);
@@ -1304,13 +1408,21 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
         rep.converged = true;
         return;
     }
-    std::vector<DVec> P, AP;
+    // the basis: one allocation, vectors at a stride of ld doubles
+    const int64_t nb = std::min<int64_t>(m, cfg.max_iterations) + 1;
+    static const int64_t pad = [] {
+        const char* v = std::getenv("KRYSP_BASIS_PAD");
+        return v ? (int64_t)std::atoll(v) : (int64_t)0;
+    }();
+    const int64_t ld = (n + 31) / 32 * 32 + pad;
+    double* slab = dev_alloc<double>(2 * nb * ld, false);
+    std::vector<double*> P, AP;
     std::vector<double> dd((size_t)m + 1);
     const double** d_ptrs = reinterpret_cast<const double**>(dev_alloc<char>(8 * 2 * (m + 1), false));
-    double* d_scal = dev_alloc<double>(2 * (m + 2), true, c->stream);  // [0]: scalar out, [8..]: betas / nums
+    double* d_scal = dev_alloc<double>(8 + m + 2, true, c->stream);  // [0..1]: scalars out, [8..]: betas / nums
     std::vector<const double*> hp((size_t)(2 * (m + 1)), nullptr);
-    auto slot = [&](std::vector<DVec>& v, int64_t j) -> DVec& {
-        while ((int64_t)v.size() <= j) v.emplace_back(e.vec());
+    auto slot = [&](std::vector<double*>& v, int64_t j) -> double* {
+        while ((int64_t)v.size() <= j) v.push_back(slab + ((&v == &P ? 0 : nb) + (int64_t)v.size()) * ld);
         return v[(size_t)j];
     };
     auto sync_ptrs = [&]() {
@@ -1338,11 +1450,12 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
             spmv_fused(e, slot(P, 0), slot(AP, 0), EpiScale{slot(AP, 0), dinv});  // op(p_0)
             sync_ptrs();
             dd[0] = e.dot(AP[0], AP[0]);
+            double r_ap = 0.0;  // <r, ap_j> for j >= 1: produced by gcr_next_kernel
             for (int64_t j = 0; j < m; ++j) {
                 const double d = dd[(size_t)j];
                 check_finite(d, "direction norm");
                 if (vanishes(d)) fail(KRYSP_BREAKDOWN, "gcr: direction norm vanished");
-                const double alpha = e.dot(r, AP[(size_t)j]) / d;
+                const double alpha = (j == 0 ? e.dot(r, AP[0]) : r_ap) / d;
                 check_finite(alpha, "alpha");
                 gcr_xr_kernel<<<g, kMdNT, 0, c->stream>>>(n, alpha, P[(size_t)j], AP[(size_t)j], x, r, part, cnt, d_scal);
                 KG_LAUNCH(c);
@@ -1361,20 +1474,23 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
                 const int k = (int)(j + 1);
                 std::vector<double> nums((size_t)k), betas((size_t)k);
                 for (int q0 = 0; q0 < k; q0 += kMdG) {
-                    multidot_kernel<<<g, kMdNT, 0, c->stream>>>(n, w, d_ptrs + (m + 1) + q0, std::min(kMdG, k - q0),
-                                                                part, cnt, d_scal + 8 + q0);
+                    launch_multidot<kMdG>(std::min(kMdG, k - q0), g, c->stream, n, w, d_ptrs + (m + 1) + q0, part,
+                                          cnt, d_scal + 8 + q0);
                     KG_LAUNCH(c);
                 }
                 d2h(nums.data(), d_scal + 8, (size_t)k);
                 for (int i = 0; i < k; ++i) betas[(size_t)i] = nums[(size_t)i] / dd[(size_t)i];
                 KG_CUDA(cudaMemcpyAsync(d_scal + 8, betas.data(), 8 * (size_t)k, cudaMemcpyHostToDevice, c->stream));
-                DVec& pn = slot(P, j + 1);
-                DVec& apn = slot(AP, j + 1);
+                double* pn = slot(P, j + 1);
+                double* apn = slot(AP, j + 1);
                 sync_ptrs();
                 gcr_next_kernel<<<g, kMdNT, 0, c->stream>>>(n, r, w, d_ptrs, d_ptrs + (m + 1), d_scal + 8, k, pn, apn,
                                                             part, cnt, d_scal);
                 KG_LAUNCH(c);
-                d2h(&dd[(size_t)j + 1], d_scal, 1);
+                double nd[2];
+                d2h(nd, d_scal, 2);
+                dd[(size_t)j + 1] = nd[0];
+                r_ap = nd[1];
             }
         }
     } catch (...) {
@@ -1384,6 +1500,7 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
     stream_wait(c);
     dev_free(d_ptrs);
     dev_free(d_scal);
+    dev_free(slab);
     rep.final_measure = measure;
     if (err) std::rethrow_exception(err);
 }
