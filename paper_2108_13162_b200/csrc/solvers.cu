@@ -448,7 +448,10 @@ void tfqmr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, R
 }
 
 // solve_bicgcr solvers.cpp:702-787 (transpose built on device, formats.cpp:312-334)
+void bicgcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep);
+
 void bicgcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    if (e.mode == KRYSP_MODE_FAST && e.A) return bicgcr_fast(e, cfg, b, x, rep);
     DVec raw = e.vec(), z = e.vec(), zt = e.vec(), p = e.vec(), pt = e.vec(), bz = e.vec(), bp = e.vec(),
          btpt = e.vec();
     e.residual(b, x, raw);
@@ -1090,10 +1093,10 @@ struct EpiScaleDot {
     }
 };
 
-// u_i = r_i - beta u_i for i < k (axpby(1, rr[i], -beta, uu[i]), solvers.cpp:497-499)
 // The BiCG-part vector kernels take the basis count as a template argument: the vector
 // pointers sit in registers and every element's loads are issued before its stores (the
 // stores may alias nothing the same element reads, but the compiler cannot know that).
+// u_i = r_i - beta u_i for i < k (axpby(1, rr[i], -beta, uu[i]), solvers.cpp:497-499)
 template <int K>
 __global__ void __launch_bounds__(kMdNT) bl_beta_kernel(int64_t n, double beta, double* const* __restrict__ rr,
                                                          double* const* __restrict__ uu) {
@@ -1245,6 +1248,114 @@ struct BlFinal {
         bl_final_kernel<L><<<g, kMdNT, 0, s>>>(n, coef, rr, uu, x, rs, part, cnt, out);
     }
 };
+
+// BiCGCR vector steps (solvers.cpp:702-787) in the reference's element-wise order:
+// x += alpha p; z -= alpha Bp; z' -= alpha B'p' (three daxpy) and ||z||^2
+__global__ void __launch_bounds__(kMdNT) bicgcr_upd_kernel(int64_t n, double alpha, const double* __restrict__ p,
+                                                            const double* __restrict__ bp,
+                                                            const double* __restrict__ btpt, double* __restrict__ x,
+                                                            double* __restrict__ z, double* __restrict__ zt,
+                                                            double* partials, unsigned* counter, double* out) {
+    __shared__ D2 sh[32];
+    D2 acc{0.0, 0.0};
+    const double ma = -alpha;
+    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
+        const double pi = p[i], bpi = bp[i], bti = btpt[i], xi = x[i], zi0 = z[i], zti = zt[i];
+        x[i] = __dadd_rn(__dmul_rn(alpha, pi), xi);
+        const double zi = __dadd_rn(__dmul_rn(ma, bpi), zi0);
+        z[i] = zi;
+        zt[i] = __dadd_rn(__dmul_rn(ma, bti), zti);
+        d2_add_prod(acc, zi, zi);
+    }
+    d2_grid_finish<1>(&acc, sh, partials, counter, out);
+}
+
+// p = z + beta p; p' = z' + beta p'; Bp = Bz + beta Bp (three axpby(1, ., beta, .))
+__global__ void __launch_bounds__(kMdNT) bicgcr_dir_kernel(int64_t n, double beta, const double* __restrict__ z,
+                                                            const double* __restrict__ zt,
+                                                            const double* __restrict__ bz, double* __restrict__ p,
+                                                            double* __restrict__ pt, double* __restrict__ bp) {
+    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
+        const double zi = z[i], zti = zt[i], bzi = bz[i], pi = p[i], pti = pt[i], bpi = bp[i];
+        p[i] = __dadd_rn(__dmul_rn(1.0, zi), __dmul_rn(beta, pi));
+        pt[i] = __dadd_rn(__dmul_rn(1.0, zti), __dmul_rn(beta, pti));
+        bp[i] = __dadd_rn(__dmul_rn(1.0, bzi), __dmul_rn(beta, bpi));
+    }
+}
+
+// FAST BiCGCR: the reference's recurrence and host scalar algebra with four passes per
+// iteration — B' p' (transpose SpMV, Jacobi and <B'p', Bp> in the epilogue), the fused
+// daxpys with ||z||, B z (with <z', Bz>), the fused direction updates.
+void bicgcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep) {
+    krysp_gpu_ctx* c = e.c;
+    const int64_t n = e.n;
+    DVec raw = e.vec(), z = e.vec(), zt = e.vec(), p = e.vec(), pt = e.vec(), bz = e.vec(), bp = e.vec(),
+         btpt = e.vec();
+    e.residual(b, x, raw);
+    e.precond(raw, z);
+    const double norm_z0 = e.norm2(z);
+    if (norm_z0 == 0.0) {
+        rep.converged = true;
+        return;
+    }
+    const double* dinv = e.jacobi ? (const double*)e.inv : nullptr;
+    double* part = c->d_partials + 4 * kPartialCap;
+    unsigned* cnt = c->d_counters + 4;
+    double* d_scal = dev_alloc<double>(8, true, c->stream);
+    const unsigned g = grid_for(n, kMdNT, (int64_t)c->sm_count * fused_grid_mult());
+    auto d2h = [&](double* dst) {
+        KG_CUDA(cudaMemcpyAsync(dst, d_scal, 8, cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+    };
+    std::exception_ptr err;
+    double measure = 1.0;
+    try {
+        e.copy(z, zt);
+        e.copy(z, p);
+        e.copy(z, pt);
+        spmv_fused(e, z, bz, EpiScaleDot{bz, dinv, zt, part, cnt, d_scal, D2{0.0, 0.0}});  // Bz, <z', Bz>
+        e.copy(bz, bp);
+        double num;
+        d2h(&num);
+        for (rep.mark(c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
+            spmv_fused_m(e, e.At, pt, btpt, EpiScaleDot{btpt, dinv, bp, part, cnt, d_scal, D2{0.0, 0.0}});
+            double denom;
+            d2h(&denom);
+            check_finite(denom, "<B'p', Bp>");
+            if (vanishes(denom)) fail(KRYSP_BREAKDOWN, "bicgcr: direction denominator vanished");
+            const double alpha = num / denom;
+            check_finite(alpha, "alpha");
+            bicgcr_upd_kernel<<<g, kMdNT, 0, c->stream>>>(n, alpha, p, bp, btpt, x, z, zt, part, cnt, d_scal);
+            KG_LAUNCH(c);
+            double zz;
+            d2h(&zz);
+            measure = std::sqrt(zz) / norm_z0;
+            check_finite(measure, "residual measure");
+            rep.push(measure);
+            if (measure <= cfg.tolerance) {
+                rep.converged = true;
+                break;
+            }
+            spmv_fused(e, z, bz, EpiScaleDot{bz, dinv, zt, part, cnt, d_scal, D2{0.0, 0.0}});
+            double num_new;
+            d2h(&num_new);
+            check_finite(num_new, "<z', Bz>");
+            if (vanishes(num)) fail(KRYSP_BREAKDOWN, "bicgcr: <z', Bz> vanished");
+            const double beta = num_new / num;
+            check_finite(beta, "beta");
+            bicgcr_dir_kernel<<<g, kMdNT, 0, c->stream>>>(n, beta, z, zt, bz, p, pt, bp);
+            KG_LAUNCH(c);
+            num = num_new;
+        }
+    } catch (...) {
+        err = std::current_exception();
+    }
+    rep.end(c->stream);
+    stream_wait(c);
+    dev_free(d_scal);
+    rep.final_measure = measure;
+    if (err) std::rethrow_exception(err);
+}
 
 // FAST BiCGStab(l) (solvers.cpp:444-572): the reference's recurrences and host scalar
 // algebra, vector work fused (the i-loops of the BiCG part in one pass each, MGS steps with
