@@ -223,7 +223,7 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
     if (exec) cudaGraphExecDestroy(exec);
     SubCgState fin;
     KG_CUDA(cudaMemcpyAsync(&fin, d_st, sizeof fin, cudaMemcpyDeviceToHost, st));
-    KG_CUDA(cudaStreamSynchronize(st));
+    kg::wait_stream(c, st);
     iterations = fin.iter;
     history.resize((size_t)fin.iter);
     if (fin.iter) KG_CUDA(cudaMemcpy(history.data(), d_hist, 8 * (size_t)fin.iter, cudaMemcpyDeviceToHost));

@@ -24,7 +24,9 @@
 #include <cmath>
 #include <cstring>
 #include <cub/cub.cuh>
+#include <mutex>
 #include <numeric>
+#include <set>
 
 #include "engine.cuh"
 #include "nccl_api.cuh"
@@ -561,7 +563,7 @@ void localize(krysp_gpu_dist* d, DistPart& P) {
     }
     unsigned long long h_cnt = 0;
     KG_CUDA(cudaMemcpyAsync(&h_cnt, cnt, 8, cudaMemcpyDeviceToHost, c->stream));
-    KG_CUDA(cudaStreamSynchronize(c->stream));
+    kg::wait_stream(c, c->stream);
     P.ghosts.clear();
     int32_t* d_ghost = nullptr;
     if (h_cnt) {
@@ -580,7 +582,7 @@ void localize(krysp_gpu_dist* d, DistPart& P) {
         KG_LAUNCH(c);
         int nu = 0;
         KG_CUDA(cudaMemcpyAsync(&nu, n_unique, 4, cudaMemcpyDeviceToHost, c->stream));
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        kg::wait_stream(c, c->stream);
         std::vector<int32_t> hg((size_t)nu);
         KG_CUDA(cudaMemcpy(hg.data(), d_ghost, 4 * (size_t)nu, cudaMemcpyDeviceToHost));
         P.ghosts.assign(hg.begin(), hg.end());
@@ -619,7 +621,7 @@ void localize(krysp_gpu_dist* d, DistPart& P) {
         }
         std::vector<unsigned char> h((size_t)P.n_local);
         KG_CUDA(cudaMemcpyAsync(h.data(), fl, (size_t)P.n_local, cudaMemcpyDeviceToHost, c->stream));
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        kg::wait_stream(c, c->stream);
         dev_free(fl);
         int64_t best_a = 0, best_len = 0, run_a = 0;
         for (int64_t r = 0; r <= P.n_local; ++r) {
@@ -680,7 +682,7 @@ void build_send_plans(krysp_gpu_dist* d) {
     KG_NCCL(N.AllGather(d_row, d_all, (size_t)P, ncclInt64, d->comm, c->stream));
     std::vector<int64_t> all((size_t)P * P);
     KG_CUDA(cudaMemcpyAsync(all.data(), d_all, 8 * all.size(), cudaMemcpyDeviceToHost, c->stream));
-    KG_CUDA(cudaStreamSynchronize(c->stream));
+    kg::wait_stream(c, c->stream);
     // my ghost ids (int64) on device, grouped by owner
     int64_t* d_need = dev_alloc<int64_t>(Me.n_ghost + 1, false);
     if (Me.n_ghost) KG_CUDA(cudaMemcpy(d_need, Me.ghosts.data(), 8 * (size_t)Me.n_ghost, cudaMemcpyHostToDevice));
@@ -713,7 +715,7 @@ void build_send_plans(krysp_gpu_dist* d) {
         to_local_idx<<<grid_for(total, kNT, 4096), kNT, 0, c->stream>>>(d_req, Me.send_idx, total, Me.lo);
         KG_LAUNCH(c);
     }
-    KG_CUDA(cudaStreamSynchronize(c->stream));
+    kg::wait_stream(c, c->stream);
     for (void* q : {(void*)d_row, (void*)d_all, (void*)d_need, (void*)d_req}) dev_free(q);
 }
 
@@ -773,7 +775,7 @@ double allreduce_host(krysp_gpu_dist* d, const std::vector<double*>& d_vals) {
         for (double* p : d_vals) {
             double v;
             KG_CUDA(cudaMemcpyAsync(&v, p, 8, cudaMemcpyDeviceToHost, c->stream));
-            KG_CUDA(cudaStreamSynchronize(c->stream));
+            kg::wait_stream(c, c->stream);
             s += v;
         }
         return s;
@@ -781,7 +783,7 @@ double allreduce_host(krysp_gpu_dist* d, const std::vector<double*>& d_vals) {
     KG_NCCL(NcclApi::get().AllReduce(d_vals[0], d_vals[0], 1, ncclDouble, ncclSum, d->comm, c->stream));
     double v;
     KG_CUDA(cudaMemcpyAsync(&v, d_vals[0], 8, cudaMemcpyDeviceToHost, c->stream));
-    KG_CUDA(cudaStreamSynchronize(c->stream));
+    kg::wait_stream(c, c->stream);
     return v;
 }
 
@@ -1044,7 +1046,7 @@ void krylov_create(krysp_gpu_dist* d, int method, const double* const* bs, const
     std::vector<int> hz(d->parts.size(), INT32_MAX);
     if (cfg.preconditioner) {
         KG_CUDA(cudaMemcpyAsync(hz.data(), zr, 4 * hz.size(), cudaMemcpyDeviceToHost, s));
-        KG_CUDA(cudaStreamSynchronize(s));
+        kg::wait_stream(c, s);
     }
     for (size_t i = 0; i < d->parts.size(); ++i)
         KG_CUDA(cudaMemcpyAsync(d_dot + 2 * i + 1, hz[i] == INT32_MAX ? &kZero : &kOne, 8, cudaMemcpyHostToDevice, s));
@@ -1108,7 +1110,7 @@ void krylov_create(krysp_gpu_dist* d, int method, const double* const* bs, const
     }
     d->d_sts = reinterpret_cast<DistCgState**>(dev_alloc<char>(8 * (int64_t)sts.size(), false));
     KG_CUDA(cudaMemcpyAsync(d->d_sts, sts.data(), 8 * sts.size(), cudaMemcpyHostToDevice, s));
-    KG_CUDA(cudaStreamSynchronize(s));
+    kg::wait_stream(c, s);
     d->exec_chunk = capture(d, krysp_gpu_dist::kChunk);
     d->exec_one = capture(d, 1);
     d->pcg = true;
@@ -1124,7 +1126,7 @@ void pcg_enqueue(krysp_gpu_dist* d, int64_t n) {
 bool pcg_done(krysp_gpu_dist* d) {
     int v = 0;
     KG_CUDA(cudaMemcpyAsync(&v, &d->parts[0].st->done, 4, cudaMemcpyDeviceToHost, d->ctx->stream));
-    KG_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    kg::wait_stream(d->ctx, d->ctx->stream);
     return v != 0;
 }
 
@@ -1261,7 +1263,7 @@ struct DistEngine : Engine {
             KG_CUDA(cudaMemcpyAsync(d_bands, bands.data(), 8 * bands.size(), cudaMemcpyHostToDevice, c->stream));
         }
         if (cfg.preconditioner) make_dist_jacobi();
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        kg::wait_stream(c, c->stream);
     }
     ~DistEngine() override {
         if (c && c->stream) cudaStreamSynchronize(c->stream);
@@ -1363,6 +1365,49 @@ struct DistEngine : Engine {
 // ------------------------------------------------------------------ C-ABI
 using kg::guard;
 
+namespace kg {
+namespace {
+std::mutex g_aborted_mu;
+std::set<void*> g_aborted;
+double nccl_timeout_s() {
+    static const double v = [] {
+        const char* s = std::getenv("KRYSP_NCCL_TIMEOUT_S");
+        const double t = s ? std::atof(s) : 0.0;
+        return t > 0.0 ? t : 0.0;
+    }();
+    return v;
+}
+}  // namespace
+
+void comm_poll(krysp_gpu_ctx* c, double waited_s) {
+    ncclComm_t comm = (ncclComm_t)c->nccl_watch;
+    if (!comm) return;
+    NcclApi& N = NcclApi::get();
+    ncclResult_t async = ncclSuccess;
+    const ncclResult_t q = N.CommGetAsyncError(comm, &async);
+    const bool failed = q != ncclSuccess || (async != ncclSuccess && async != ncclInProgress);
+    const double limit = nccl_timeout_s();
+    if (!failed && (limit == 0.0 || waited_s < limit)) return;
+    {
+        std::lock_guard<std::mutex> lk(g_aborted_mu);
+        g_aborted.insert(comm);
+    }
+    c->nccl_watch = nullptr;
+    N.CommAbort(comm);
+    if (failed)
+        fail(KRYSP_NCCL_ERROR, "NCCL peer failure (communicator aborted): %s",
+             N.GetErrorString(q != ncclSuccess ? q : async));
+    fail(KRYSP_NCCL_ERROR, "NCCL collective made no progress for %.0f s (KRYSP_NCCL_TIMEOUT_S); communicator aborted",
+         waited_s);
+}
+
+bool comm_aborted(void* comm) {
+    std::lock_guard<std::mutex> lk(g_aborted_mu);
+    return g_aborted.count(comm) != 0;
+}
+}  // namespace kg
+
+
 extern "C" {
 
 krysp_status krysp_gpu_band_rows(int64_t n, int32_t nparts, int32_t part, int64_t* lo, int64_t* hi) {
@@ -1429,6 +1474,7 @@ krysp_status krysp_gpu_dist_create(krysp_gpu_ctx* ctx, int32_t nparts, int32_t r
                 ncclUniqueId u;
                 std::memcpy(&u, id, 128);
                 KG_NCCL(kg::NcclApi::get().CommInitRank(&d->comm, nparts, u, rank));
+                ctx->nccl_watch = d->comm;
                 d->parts.emplace_back();
                 d->parts.back().id = rank;
                 KG_CUDA(cudaStreamCreateWithFlags(&d->cstream, cudaStreamNonBlocking));
@@ -1512,7 +1558,7 @@ krysp_status krysp_gpu_dist_spmv(krysp_gpu_dist* d, const double* const* d_x, do
             krysp_policy pol{256, 1, 0, 0};
             kg::spmv_launch(d->parts[i].A, xs[i], d_y[i], pol, KRYSP_MODE_EXACT, c->stream);
         }
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        kg::wait_stream(c, c->stream);
     });
 }
 
@@ -1545,7 +1591,7 @@ krysp_status krysp_gpu_dist_pcg_time(krysp_gpu_dist* d, int64_t n, double* secon
         KG_CUDA(cudaEventRecord(a, s));
         kg::pcg_enqueue(d, n);
         KG_CUDA(cudaEventRecord(b, s));
-        KG_CUDA(cudaEventSynchronize(b));
+        kg::wait_event(d->ctx, b);
         float ms = 0.f;
         KG_CUDA(cudaEventElapsedTime(&ms, a, b));
         cudaEventDestroy(a);
@@ -1599,7 +1645,7 @@ krysp_status krysp_gpu_dist_pcg_solution(krysp_gpu_dist* d, int32_t part, double
         kg::DistPart& P = d->part(part);
         if (!P.x.p) kg::fail(KRYSP_ERROR, "no distributed solver");
         if (P.n_local) KG_CUDA(cudaMemcpyAsync(d_x, P.x, 8 * P.n_local, cudaMemcpyDeviceToDevice, d->ctx->stream));
-        KG_CUDA(cudaStreamSynchronize(d->ctx->stream));
+        kg::wait_stream(d->ctx, d->ctx->stream);
     });
 }
 
@@ -1620,7 +1666,7 @@ krysp_status krysp_gpu_dist_pcg_profile(krysp_gpu_dist* d, int64_t n, double* sp
                 KG_CUDA(cudaEventRecord(e[0], s));
                 kg::dist_iteration(d, e[1]);
                 KG_CUDA(cudaEventRecord(e[2], s));
-                KG_CUDA(cudaEventSynchronize(e[2]));
+                kg::wait_event(d->ctx, e[2]);
                 float a = 0.f, b = 0.f;
                 KG_CUDA(cudaEventElapsedTime(&a, e[0], e[1]));
                 KG_CUDA(cudaEventElapsedTime(&b, e[0], e[2]));
@@ -1659,7 +1705,7 @@ krysp_status krysp_gpu_dist_solve(krysp_gpu_dist* d, int32_t method, const doubl
             const int64_t nl = d->parts[i].n_local;
             if (nl) KG_CUDA(cudaMemcpyAsync(d_x[i], x + e.off[i], 8 * nl, cudaMemcpyDeviceToDevice, c->stream));
         }
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        kg::wait_stream(c, c->stream);
     });
 }
 
@@ -1670,7 +1716,8 @@ krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d) {
         cudaStreamSynchronize(d->ctx->stream);
         kg::pcg_release(d);
         for (auto& P : d->parts) P.release();
-        if (d->comm) kg::NcclApi::get().CommDestroy(d->comm);
+        if (d->comm && d->ctx->nccl_watch == (void*)d->comm) d->ctx->nccl_watch = nullptr;
+        if (d->comm && !kg::comm_aborted(d->comm)) kg::NcclApi::get().CommDestroy(d->comm);
         if (d->cstream) cudaStreamDestroy(d->cstream);
         if (d->ev_fork) cudaEventDestroy(d->ev_fork);
         if (d->ev_halo) cudaEventDestroy(d->ev_halo);

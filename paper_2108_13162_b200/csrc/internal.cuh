@@ -2,6 +2,8 @@
 // include/krysp_gpu.h.
 #pragma once
 
+#include <chrono>
+
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -59,6 +61,9 @@ struct krysp_gpu_ctx {
     double* d_scalars = nullptr;
     double* h_pinned = nullptr;
     cudaEvent_t sync_ev = nullptr;  // host waits on solver scalars (spin, see stream_wait)
+    // NCCL communicator whose health the host wait loops poll (set while a multi-GPU
+    // partition is alive on this context; see comm_poll in dist.cu)
+    void* nccl_watch = nullptr;
 };
 
 namespace kg {
@@ -369,11 +374,52 @@ krysp_status guard(F&& f) {
 // Wait for the context stream by spinning on an event: host-driven solvers round-trip a
 // scalar every few hundred microseconds, and a sleeping cudaStreamSynchronize can wake up
 // milliseconds late (measured: 4-11 ms of idle GPU per tfQMR iteration).
+// Failure detection for multi-GPU waits (NCCL async-error polling in place of
+// the reference's ChannelMesh timeout): while c->nccl_watch is set, a host spin that lasts
+// polls ncclCommGetAsyncError and, past KRYSP_NCCL_TIMEOUT_S seconds (0 / unset: no limit),
+// aborts the communicator and fails with KRYSP_NCCL_ERROR instead of hanging on a dead peer.
+void comm_poll(krysp_gpu_ctx* c, double waited_s);
+bool comm_aborted(void* comm);  // aborted by comm_poll: destroy must not touch it
+
+struct WaitWatch {
+    krysp_gpu_ctx* c;
+    unsigned spins = 0;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+    void tick() {  // a clock read every 1024 spins, a poll every 20 ms of waiting
+        if (!c->nccl_watch || (++spins & 0x3FF)) return;
+        const auto now = std::chrono::steady_clock::now();
+        if (now - last < std::chrono::milliseconds(20)) return;
+        last = now;
+        comm_poll(c, std::chrono::duration<double>(now - t0).count());
+    }
+};
+
+// blocking waits that may sit behind NCCL work: plain synchronisation, or a watched spin
+// while a communicator is registered on the context
+inline void wait_event(krysp_gpu_ctx* c, cudaEvent_t ev) {
+    if (!c->nccl_watch) {
+        KG_CUDA(cudaEventSynchronize(ev));
+        return;
+    }
+    cudaError_t e;
+    WaitWatch w{c};
+    while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) w.tick();
+    if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "wait: %s", cudaGetErrorString(e));
+}
+inline void wait_stream(krysp_gpu_ctx* c, cudaStream_t s) {
+    if (!c->nccl_watch) {
+        KG_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    KG_CUDA(cudaEventRecord(c->sync_ev, s));
+    wait_event(c, c->sync_ev);
+}
+
 inline void stream_wait(krysp_gpu_ctx* c) {
     KG_CUDA(cudaEventRecord(c->sync_ev, c->stream));
     cudaError_t e;
-    while ((e = cudaEventQuery(c->sync_ev)) == cudaErrorNotReady) {
-    }
+    WaitWatch w{c};
+    while ((e = cudaEventQuery(c->sync_ev)) == cudaErrorNotReady) w.tick();
     if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "stream wait: %s", cudaGetErrorString(e));
 }
 
@@ -397,8 +443,8 @@ void run_pipelined(krysp_gpu_ctx* c, const int* d_done, Enqueue&& enqueue) {
         for (int k = 0;; k ^= 1) {
             post(k ^ 1);
             cudaError_t e;
-            while ((e = cudaEventQuery(ev[k])) == cudaErrorNotReady) {
-            }
+            WaitWatch w{c};
+            while ((e = cudaEventQuery(ev[k])) == cudaErrorNotReady) w.tick();
             if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "solve wait: %s", cudaGetErrorString(e));
             if (*(volatile int*)(h + k)) break;
         }

@@ -25,6 +25,8 @@ struct NcclApi {
     decltype(&ncclGroupStart) GroupStart = nullptr;
     decltype(&ncclGroupEnd) GroupEnd = nullptr;
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+    decltype(&ncclCommAbort) CommAbort = nullptr;
 
     static NcclApi& get() {
         static NcclApi a = [] {  // loaded once; thread-safe static initialisation
@@ -58,6 +60,8 @@ struct NcclApi {
         KG_SYM(GroupStart)
         KG_SYM(GroupEnd)
         KG_SYM(GetErrorString)
+        KG_SYM(CommGetAsyncError)
+        KG_SYM(CommAbort)
 #undef KG_SYM
         ok = true;
     }

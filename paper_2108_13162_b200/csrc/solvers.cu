@@ -1521,11 +1521,7 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
     }
     // the basis: one allocation, vectors at a stride of ld doubles
     const int64_t nb = std::min<int64_t>(m, cfg.max_iterations) + 1;
-    static const int64_t pad = [] {
-        const char* v = std::getenv("KRYSP_BASIS_PAD");
-        return v ? (int64_t)std::atoll(v) : (int64_t)0;
-    }();
-    const int64_t ld = (n + 31) / 32 * 32 + pad;
+    const int64_t ld = (n + 31) / 32 * 32;  // 256-byte aligned vectors
     double* slab = dev_alloc<double>(2 * nb * ld, false);
     std::vector<double*> P, AP;
     std::vector<double> dd((size_t)m + 1);

@@ -396,7 +396,7 @@ void setup_device(krysp_gpu_sub* h) {
         h->held.push_back(std::move(D));
     }
     if (!h->emulated()) h->d_dots = dev_alloc<double>(P.nsub, true, c->stream);
-    KG_CUDA(cudaStreamSynchronize(c->stream));
+    kg::wait_stream(c, c->stream);
 }
 
 // local_spmv_assemble (substructure.cpp:354-405), in three stream-ordered phases
@@ -564,7 +564,7 @@ void solve_cg(krysp_gpu_sub* h, const double* b, const double* x0, const krysp_s
             tmp.resize(l2g.size());
             for (size_t k = 0; k < l2g.size(); ++k) tmp[k] = global[l2g[k]];
             KG_CUDA(cudaMemcpyAsync(out.v[i], tmp.data(), 8 * tmp.size(), cudaMemcpyHostToDevice, st));
-            KG_CUDA(cudaStreamSynchronize(st));
+            kg::wait_stream(c, st);
         }
     };
     restrict_up(x0, x);
@@ -630,7 +630,7 @@ void solve_cg(krysp_gpu_sub* h, const double* b, const double* x0, const krysp_s
         err = std::current_exception();
     }
     KG_CUDA(cudaEventRecord(e1, st));
-    KG_CUDA(cudaEventSynchronize(e1));
+    kg::wait_event(c, e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
@@ -758,6 +758,7 @@ krysp_status krysp_gpu_sub_create(krysp_gpu_ctx* ctx, int64_t n, const int64_t* 
                 ncclUniqueId id;
                 std::memcpy(&id, nccl_id, sizeof id);
                 KG_NCCL(kg::NcclApi::get().CommInitRank(&h->comm, (int)h->part.nsub, id, rank));
+                ctx->nccl_watch = h->comm;
             }
             kg::setup_device(h);
         } catch (...) {
@@ -826,7 +827,7 @@ krysp_status krysp_gpu_sub_assemble_spmv(krysp_gpu_sub* h, const double* const* 
         std::vector<const double*> xs(d_x, d_x + h->held.size());
         std::vector<double*> ys(d_y, d_y + h->held.size());
         kg::assemble_spmv(h, xs, ys, *policy, mode);
-        KG_CUDA(cudaStreamSynchronize(h->ctx->stream));
+        kg::wait_stream(h->ctx, h->ctx->stream);
     });
 }
 
@@ -859,7 +860,8 @@ krysp_status krysp_gpu_sub_destroy(krysp_gpu_sub* h) {
         }
         for (auto& D : h->held) D.release();
         kg::dev_free(h->d_dots);
-        if (h->comm) kg::NcclApi::get().CommDestroy(h->comm);
+        if (h->comm && h->ctx && h->ctx->nccl_watch == (void*)h->comm) h->ctx->nccl_watch = nullptr;
+        if (h->comm && !kg::comm_aborted(h->comm)) kg::NcclApi::get().CommDestroy(h->comm);
         delete h;
     });
 }

@@ -244,3 +244,39 @@ def test_dist_breakdown_matches_reference(ctx, ref, mode):
             with pytest.raises(kg.Error) as ei:
                 D.solve(s, split(b, 4, 2), cfg=cfg)
             assert ei.value.code == want["status"] and str(ei.value) == want["error"], (s, str(ei.value), want)
+
+
+_WATCH_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2108_13162_b200 as kg
+from paper_2108_13162_b200 import _lib
+from paper_2108_13162_b200.dist import DistSystem, nccl_unique_id
+ctx = kg.Context(0)
+D = DistSystem(ctx, 1, 0, nccl_unique_id())
+D.generate("lap3d7", 200)
+D.setup()
+N = 200 ** 3
+D.pcg_create([ctx.to_device(np.ones(N))], [ctx.to_device(np.zeros(N))], kg.SolverConfig(mode="fast"))
+try:
+    D.pcg_time(300)
+    print("NO-ERROR", flush=True)
+except _lib.NcclError as e:
+    print("NCCL-ERROR", e, flush=True)
+"""
+
+
+def test_nccl_watch_timeout_aborts():
+    """Failure detection: with KRYSP_NCCL_TIMEOUT_S set, a host wait on a
+    multi-GPU solve that exceeds it aborts the communicator and raises NcclError instead of
+    hanging (run in a child process: the aborted communicator poisons its context)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KRYSP_NCCL_TIMEOUT_S="0.001")
+    r = subprocess.run([sys.executable, "-c", _WATCH_SCRIPT, root], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert "NCCL-ERROR" in r.stdout, (r.stdout, r.stderr[-2000:])
+    assert "no progress" in r.stdout
