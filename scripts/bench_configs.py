@@ -6,7 +6,7 @@ and parity against the reference on the B200.  One JSON object per line.
       50 iterations bit-identical to the reference library at <256,8>
   C4  GCR(50) / BiCGStab(4) / tfQMR / BiCGStab on the 27-point stencil 320^3, HYB (auto width and
       w = 26): FAST it/s; parity at 80^3 vs the survey goldens
-  C5  SpMV on power-law rows (1M-10M rows), CSR/HYB/COO + tune_spmv
+  C5  SpMV on power-law rows (1M, 10M rows and ~100M nnz), CSR/HYB/COO + tune_spmv
   F1  sub-structured CG (1 and 8 subdomains) + EXACT bit-identity vs the reference
 Usage: python scripts/bench_configs.py [C1 C2 C4 C5 F1]
 """
@@ -136,7 +136,9 @@ def c4(ctx, R):
 
 
 def c5(ctx, R):
-    for n, alpha in [(1_000_000, 2.0), (1_000_000, 1.5), (10_000_000, 2.0), (10_000_000, 1.5)]:
+    # n = 1M and 10M rows, then ~100M nnz ("scale n up to reach 10 M and 100 M nnz")
+    for n, alpha in [(1_000_000, 2.0), (1_000_000, 1.5), (10_000_000, 2.0), (10_000_000, 1.5), (21_850_000, 2.0),
+                     (15_170_000, 1.5)]:
         t0 = time.perf_counter()
         m = kg.generate_csr("powerlaw", n, alpha=alpha, seed=2108)
         gen = time.perf_counter() - t0
