@@ -34,6 +34,7 @@ os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "FP64 CG iterations/sec and SpMV GFLOP/s (+% HBM roofline) at 1/2/4/8 B200"
 GOLDEN_ITERS, GOLDEN_MEASURE = 733, 9.650895609e-07  # SURVEY §6 / §8(a12), oracle at 400^3
+TIMED_TOL = 1e-300  # timed steps: no convergence stop (see run_ours)
 
 
 def parse():
@@ -259,7 +260,11 @@ def run_ours(args, dist):
     n, nnz = info["n_rows"], info["nnz"]
     b = ctx.to_device(np.ones(n))
     x0 = ctx.to_device(np.zeros(n))
-    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), tolerance=1e-6, max_iterations=30000)
+    # timed sessions never stop on convergence (tolerance 1e-300): every one of the W + K steps
+    # is a full P-CG iteration on the C3 system whatever K the driver picks; the converged
+    # solve (tol 1e-6, the golden 733 iterations) is the e2e / parity run below
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), tolerance=TIMED_TOL,
+                          max_iterations=args.warmup + args.steps + 1000)
     solver = kg.PcgSolver(A, b, x0, cfg)
     solver.time(args.warmup)
     clocks = Clocks(dist.local)
@@ -273,8 +278,7 @@ def run_ours(args, dist):
     rep = solver.report()
     ran = rep.iterations
     assert ran == args.warmup + args.steps, f"solve converged inside the timed region ({ran} iterations)"
-    prof_n = min(20, max(1, GOLDEN_ITERS - ran - 5))
-    t_spmv, t_upd, t_dir = solver.profile(prof_n)
+    t_spmv, t_upd, t_dir = solver.profile(20)
     kpi = solver.kernels_per_iteration
     solver.close()
     # BiCGStab on the same system (north-star target: CG and BiCGStab >= 70% of the roofline)
@@ -400,7 +404,8 @@ def run_ours_dist(args, dist):
     N = args.n ** 3
     b = ctx.to_device(np.ones(n_loc))
     x0 = ctx.to_device(np.zeros(n_loc))
-    D.pcg_create([b], [x0], kg.SolverConfig(mode="fast", tolerance=1e-6, max_iterations=30000))
+    timed = kg.SolverConfig(mode="fast", tolerance=TIMED_TOL, max_iterations=args.warmup + args.steps + 1000)
+    D.pcg_create([b], [x0], timed)  # no convergence stop in the timed steps (see run_ours)
     D.pcg_time(args.warmup)
     clocks = Clocks(dist.local)
     dist.barrier()
@@ -414,14 +419,11 @@ def run_ours_dist(args, dist):
     assert rep.iterations == args.warmup + args.steps, f"converged inside the timed region ({rep.iterations})"
     kpi = D.kernels_per_iteration
     # the halo-overlapped SpMV phase alone (CUDA events, eager iterations, max over ranks)
-    t_spmv_loc, _ = D.pcg_profile(min(20, max(1, GOLDEN_ITERS - rep.iterations - 5)))
+    t_spmv_loc, _ = D.pcg_profile(20)
     t_spmv = dist.max(t_spmv_loc)
-    # finish the solve for the parity check (same problem as the single-GPU golden)
-    D.pcg_run()
-    fin = D.pcg_report()
-    # partitioned BiCGStab on the same bands (bounded: it converges in ~700 iterations)
+    # partitioned BiCGStab on the same bands
     bi_steps = min(args.steps, 100)
-    D.krylov_create("bicgstab", [b], [x0], kg.SolverConfig(mode="fast", tolerance=1e-6, max_iterations=30000))
+    D.krylov_create("bicgstab", [b], [x0], timed)
     D.pcg_time(args.warmup)
     dist.barrier()
     t_bi = dist.max(D.pcg_time(bi_steps))
@@ -439,6 +441,7 @@ def run_ours_dist(args, dist):
     e2e_rep = D.pcg_report()
     sol = D.pcg_solution(dist.rank)
     e2e_s = dist.max(time.perf_counter() - t0)
+    fin = e2e_rep  # the converged solve is the parity check (same problem as the single-GPU golden)
     D.close()
     nnz_total = 7 * N - 6 * args.n ** 2
     bw_peak, peak_kind = peaks()
