@@ -685,6 +685,7 @@ int fused_grid_mult() {
 // and ran this bandwidth-bound pass at 3 TB/s (GCR's orthogonalisation coefficients do not
 // need the compensation the BiCGStab breakdown tests do).
 constexpr int kMdNT = 256;
+constexpr int kVu = 2;  // rows per thread whose loads are issued together in the fused vector kernels
 constexpr int kMdG = 8;
 
 // out[q] = <w, v_q> for the K vectors of vs (K a template argument: the vector pointers in
@@ -746,11 +747,24 @@ __global__ void __launch_bounds__(kMdNT) gcr_xr_kernel(int64_t n, double alpha, 
     __shared__ D2 sh[32];
     D2 acc{0.0, 0.0};
     const double ma = -alpha;
-    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
-        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
-        const double ri = __dadd_rn(__dmul_rn(ma, ap[i]), r[i]);
-        r[i] = ri;
-        d2_add_prod(acc, ri, ri);
+    const int64_t stride = (int64_t)gridDim.x * kMdNT;
+    for (int64_t i0 = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double pv[kVu], av[kVu], xv[kVu], rv[kVu];  // every load of kVu rows before any store
+#pragma unroll
+        for (int u = 0; u < kVu; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i < n) pv[u] = p[i], av[u] = ap[i], xv[u] = x[i], rv[u] = r[i];
+        }
+#pragma unroll
+        for (int u = 0; u < kVu; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i < n) {
+                x[i] = __dadd_rn(__dmul_rn(alpha, pv[u]), xv[u]);
+                const double ri = __dadd_rn(__dmul_rn(ma, av[u]), rv[u]);
+                r[i] = ri;
+                d2_add_prod(acc, ri, ri);
+            }
+        }
     }
     const D2 b = block_d2_dyn(acc, sh);
     if (threadIdx.x == 0) {
@@ -912,7 +926,8 @@ struct EpiTfqmrV {
 
 // even: u_next = u - alpha v (copy + daxpy); both: w -= alpha bu; d = u + scale d;
 // ||w||^2 and (odd) <w, r0>
-__global__ void __launch_bounds__(kMdNT) tfqmr_wd_kernel(int64_t n, int even, double alpha, double scale,
+template <bool kEven>
+__global__ void __launch_bounds__(kMdNT) tfqmr_wd_kernel(int64_t n, double alpha, double scale,
                                                           const double* __restrict__ u, const double* __restrict__ v,
                                                           double* __restrict__ u_next, const double* __restrict__ bu,
                                                           double* __restrict__ w, double* __restrict__ d,
@@ -921,26 +936,59 @@ __global__ void __launch_bounds__(kMdNT) tfqmr_wd_kernel(int64_t n, int even, do
     __shared__ D2 sh[32];
     D2 acc[2] = {D2{0.0, 0.0}, D2{0.0, 0.0}};
     const double ma = -alpha;
-    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
-        const double ui = u[i];
-        if (even) u_next[i] = __dadd_rn(__dmul_rn(ma, v[i]), ui);
-        const double wi = __dadd_rn(__dmul_rn(ma, bu[i]), w[i]);
-        w[i] = wi;
-        d[i] = __dadd_rn(__dmul_rn(1.0, ui), __dmul_rn(scale, d[i]));
-        d2_add_prod(acc[0], wi, wi);
-        if (!even) d2_add_prod(acc[1], wi, r0[i]);
+    const int64_t stride = (int64_t)gridDim.x * kMdNT;
+    for (int64_t i0 = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double uv[kVu], vv[kVu], bv[kVu], wv[kVu], dv[kVu], rv[kVu];  // loads first
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                uv[q] = u[i], bv[q] = bu[i], wv[q] = w[i], dv[q] = d[i];
+                if (kEven) vv[q] = v[i];
+                else rv[q] = r0[i];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                if (kEven) u_next[i] = __dadd_rn(__dmul_rn(ma, vv[q]), uv[q]);
+                const double wi = __dadd_rn(__dmul_rn(ma, bv[q]), wv[q]);
+                w[i] = wi;
+                d[i] = __dadd_rn(__dmul_rn(1.0, uv[q]), __dmul_rn(scale, dv[q]));
+                d2_add_prod(acc[0], wi, wi);
+                if (!kEven) d2_add_prod(acc[1], wi, rv[q]);
+            }
+        }
     }
     d2_grid_finish<2>(acc, sh, partials, counter, out);
 }
 
 // x += eta d; (odd, after rho) u_next = w + beta u (copy(w) + daxpy(beta, u))
+template <bool kOdd>
 __global__ void __launch_bounds__(kMdNT) tfqmr_xu_kernel(int64_t n, double eta, const double* __restrict__ d,
-                                                          double* __restrict__ x, int odd, double beta,
+                                                          double* __restrict__ x, double beta,
                                                           const double* __restrict__ w, const double* __restrict__ u,
                                                           double* __restrict__ u_next) {
-    for (int64_t i = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMdNT) {
-        x[i] = __dadd_rn(__dmul_rn(eta, d[i]), x[i]);
-        if (odd) u_next[i] = __dadd_rn(__dmul_rn(beta, u[i]), w[i]);
+    const int64_t stride = (int64_t)gridDim.x * kMdNT;
+    for (int64_t i0 = blockIdx.x * (int64_t)kMdNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double dv[kVu], xv[kVu], uv[kVu], wv[kVu];  // loads first
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                dv[q] = d[i], xv[q] = x[i];
+                if (kOdd) uv[q] = u[i], wv[q] = w[i];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                x[i] = __dadd_rn(__dmul_rn(eta, dv[q]), xv[q]);
+                if (kOdd) u_next[i] = __dadd_rn(__dmul_rn(beta, uv[q]), wv[q]);
+            }
+        }
     }
 }
 
@@ -996,8 +1044,12 @@ void tfqmr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
             }
             const double scale = (theta * theta * eta) / alpha;
             check_finite(scale, "direction scale");
-            tfqmr_wd_kernel<<<g, kMdNT, 0, c->stream>>>(n, even ? 1 : 0, alpha, scale, u, v, un, bu, w, d, r0, part, cnt,
-                                                         d_scal);
+            if (even)
+                tfqmr_wd_kernel<true><<<g, kMdNT, 0, c->stream>>>(n, alpha, scale, u, v, un, bu, w, d, r0, part, cnt,
+                                                                  d_scal);
+            else
+                tfqmr_wd_kernel<false><<<g, kMdNT, 0, c->stream>>>(n, alpha, scale, u, v, un, bu, w, d, r0, part, cnt,
+                                                                   d_scal);
             KG_LAUNCH(c);
             double red[2];
             d2h(red, 2);
@@ -1011,7 +1063,7 @@ void tfqmr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
             if (!even) {
                 const double rho_new = red[1];
                 if (vanishes(rho_new)) {  // after x += eta d, as the reference (x is updated first)
-                    tfqmr_xu_kernel<<<g, kMdNT, 0, c->stream>>>(n, eta, d, x, 0, 0.0, w, u, un);
+                    tfqmr_xu_kernel<false><<<g, kMdNT, 0, c->stream>>>(n, eta, d, x, 0.0, w, u, un);
                     KG_LAUNCH(c);
                     if (bound <= cfg.tolerance) {
                         measure = true_measure();
@@ -1027,7 +1079,8 @@ void tfqmr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
             }
             // x += eta d (+ odd: u_next = w + beta u, which needs beta: checked below as the
             // reference does, after the true-residual test)
-            tfqmr_xu_kernel<<<g, kMdNT, 0, c->stream>>>(n, eta, d, x, even ? 0 : 1, beta, w, u, un);
+            if (even) tfqmr_xu_kernel<false><<<g, kMdNT, 0, c->stream>>>(n, eta, d, x, beta, w, u, un);
+            else tfqmr_xu_kernel<true><<<g, kMdNT, 0, c->stream>>>(n, eta, d, x, beta, w, u, un);
             KG_LAUNCH(c);
             if (bound <= cfg.tolerance) {
                 measure = true_measure();
@@ -1152,17 +1205,34 @@ __global__ void __launch_bounds__(kMdNT) bl_mgs_kernel(int64_t n, double* __rest
     __shared__ D2 sh[32];
     D2 acc[2] = {D2{0.0, 0.0}, D2{0.0, 0.0}};
     const double mt = -tau;
-    for (int64_t e = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e < n; e += (int64_t)gridDim.x * kMdNT) {
-        double v = rj[e];
-        if (ri) {
-            v = __dadd_rn(__dmul_rn(mt, ri[e]), v);
-            rj[e] = v;
+    const int64_t stride = (int64_t)gridDim.x * kMdNT;
+    for (int64_t e0 = blockIdx.x * (int64_t)kMdNT + threadIdx.x; e0 < n; e0 += kVu * stride) {
+        double jv[kVu], iv[kVu], ov[kVu];  // loads first
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t e = e0 + q * stride;
+            if (e < n) {
+                jv[q] = rj[e];
+                iv[q] = ri ? ri[e] : 0.0;
+                ov[q] = rnext ? rnext[e] : r0[e];
+            }
         }
-        if (rnext) {
-            d2_add_prod(acc[0], v, rnext[e]);
-        } else {
-            d2_add_prod(acc[0], v, v);
-            d2_add_prod(acc[1], r0[e], v);
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t e = e0 + q * stride;
+            if (e < n) {
+                double v = jv[q];
+                if (ri) {
+                    v = __dadd_rn(__dmul_rn(mt, iv[q]), v);
+                    rj[e] = v;
+                }
+                if (rnext) {
+                    d2_add_prod(acc[0], v, ov[q]);
+                } else {
+                    d2_add_prod(acc[0], v, v);
+                    d2_add_prod(acc[1], ov[q], v);
+                }
+            }
         }
     }
     d2_grid_finish<2>(acc, sh, partials, counter, out);
@@ -1920,10 +1990,19 @@ __global__ void __launch_bounds__(kBiNT) bi_s_kernel(int64_t n, double* __restri
     __shared__ D2 sh[32];
     const double ma = -st->alpha;
     D2 acc{0.0, 0.0};
-    for (int64_t i = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBiNT) {
-        const double si = __dadd_rn(__dmul_rn(ma, v[i]), r[i]);
-        s[i] = si;
-        d2_add_prod(acc, si, si);
+    const int64_t stride = (int64_t)gridDim.x * kBiNT;
+    for (int64_t i0 = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double vv[kVu], rv[kVu];  // loads of kVu rows before any store
+#pragma unroll
+        for (int q = 0; q < kVu; ++q)
+            if (i0 + q * stride < n) vv[q] = v[i0 + q * stride], rv[q] = r[i0 + q * stride];
+#pragma unroll
+        for (int q = 0; q < kVu; ++q)
+            if (i0 + q * stride < n) {
+                const double si = __dadd_rn(__dmul_rn(ma, vv[q]), rv[q]);
+                s[i0 + q * stride] = si;
+                d2_add_prod(acc, si, si);
+            }
     }
     const D2 b = block_d2_dyn(acc, sh);
     if (threadIdx.x == 0) {
@@ -1968,13 +2047,25 @@ __global__ void __launch_bounds__(kBiNT) bi_update_kernel(int64_t n, double* __r
     __shared__ D2 sh[32];
     const double om = st->omega, mom = -om;
     D2 a0{0.0, 0.0}, a1{0.0, 0.0};
-    for (int64_t i = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBiNT) {
-        const double si = s[i];
-        x[i] = __dadd_rn(__dmul_rn(om, si), __dadd_rn(__dmul_rn(alpha, p[i]), x[i]));
-        const double ri = __dadd_rn(__dmul_rn(mom, t[i]), si);
-        r[i] = ri;
-        d2_add_prod(a0, ri, ri);
-        d2_add_prod(a1, rh[i], ri);
+    const int64_t stride = (int64_t)gridDim.x * kBiNT;
+    for (int64_t i0 = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double sv[kVu], pv[kVu], xv[kVu], tv[kVu], hv[kVu];  // loads first
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) sv[q] = s[i], pv[q] = p[i], xv[q] = x[i], tv[q] = t[i], hv[q] = rh[i];
+        }
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                x[i] = __dadd_rn(__dmul_rn(om, sv[q]), __dadd_rn(__dmul_rn(alpha, pv[q]), xv[q]));
+                const double ri = __dadd_rn(__dmul_rn(mom, tv[q]), sv[q]);
+                r[i] = ri;
+                d2_add_prod(a0, ri, ri);
+                d2_add_prod(a1, hv[q], ri);
+            }
+        }
     }
     const D2 b0 = block_d2_dyn(a0, sh);
     const D2 b1 = block_d2_dyn(a1, sh);
@@ -2021,9 +2112,22 @@ __global__ void __launch_bounds__(kBiNT) bi_p_kernel(int64_t n, double* __restri
                                                       const double* __restrict__ v, const BiState* st) {
     if (*(volatile const int*)&st->done) return;
     const double mom = -st->omega, beta = st->beta;
-    for (int64_t i = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBiNT) {
-        const double pi = __dadd_rn(__dmul_rn(mom, v[i]), p[i]);
-        p[i] = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(beta, pi));
+    const int64_t stride = (int64_t)gridDim.x * kBiNT;
+    for (int64_t i0 = blockIdx.x * (int64_t)kBiNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double vv[kVu], pv[kVu], rv[kVu];  // loads first
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) vv[q] = v[i], pv[q] = p[i], rv[q] = r[i];
+        }
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                const double pi = __dadd_rn(__dmul_rn(mom, vv[q]), pv[q]);
+                p[i] = __dadd_rn(__dmul_rn(1.0, rv[q]), __dmul_rn(beta, pi));
+            }
+        }
     }
 }
 
