@@ -106,6 +106,7 @@ krysp_status krysp_gpu_ctx_destroy(krysp_gpu_ctx* c) {
         if (c->h_pinned) cudaFreeHost(c->h_pinned);
         if (c->sync_ev) cudaEventDestroy(c->sync_ev);
         if (c->own_stream) cudaStreamDestroy(c->own_stream);
+        kg::dev_cache_trim(c->device);
         delete c;
     });
 }

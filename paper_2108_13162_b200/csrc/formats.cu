@@ -13,14 +13,118 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <thread>
+#include <unordered_map>
 
 #include "internal.cuh"
 
 namespace kg {
 
+namespace {
+struct CachedBlock {
+    int device;
+    size_t bytes;
+};
+constexpr size_t kCacheMin = size_t(1) << 20, kCacheGran = size_t(2) << 20;
+std::mutex g_cache_mu;
+std::unordered_map<void*, CachedBlock> g_live;              // cache-managed blocks in use
+std::multimap<std::pair<int, size_t>, void*> g_free_blocks;  // (device, bytes) -> block
+size_t g_cached_bytes = 0;
+
+size_t cache_cap() {  // a quarter of the device memory, at most 48 GB
+    static const size_t cap = [] {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+            cudaGetLastError();
+            return size_t(0);
+        }
+        return std::min(tot / 4, size_t(48) << 30);
+    }();
+    return cap;
+}
+}  // namespace
+
+void* dev_alloc_bytes(size_t bytes) {
+    void* p = nullptr;
+    if (bytes < kCacheMin) {
+        KG_CUDA(cudaMalloc(&p, bytes));
+        return p;
+    }
+    const size_t r = (bytes + kCacheGran - 1) / kCacheGran * kCacheGran;
+    int dev = 0;
+    KG_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto it = g_free_blocks.find({dev, r});
+        if (it != g_free_blocks.end()) {
+            p = it->second;
+            g_free_blocks.erase(it);
+            g_cached_bytes -= r;
+            g_live[p] = {dev, r};
+            return p;
+        }
+    }
+    cudaError_t e = cudaMalloc(&p, r);
+    if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+        cudaGetLastError();
+        dev_cache_trim(dev);
+        e = cudaMalloc(&p, r);
+    }
+    if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "cudaMalloc(%zu): %s", r, cudaGetErrorString(e));
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_live[p] = {dev, r};
+    return p;
+}
+
 void dev_free(void* p) {
-    if (p) cudaFree(p);
+    if (!p) return;
+    CachedBlock b{};
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto it = g_live.find(p);
+        if (it == g_live.end()) {
+            cudaFree(p);
+            return;
+        }
+        b = it->second;
+        g_live.erase(it);
+        if (g_cached_bytes + b.bytes > cache_cap()) {
+            cudaFree(p);
+            return;
+        }
+    }
+    // the implicit synchronisation of cudaFree: no queued work may still use the block
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != b.device) cudaSetDevice(b.device);
+    cudaDeviceSynchronize();
+    if (cur != b.device) cudaSetDevice(cur);
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_free_blocks.insert({{b.device, b.bytes}, p});
+    g_cached_bytes += b.bytes;
+}
+
+void dev_cache_trim(int device) {
+    std::vector<void*> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto it = g_free_blocks.begin(); it != g_free_blocks.end();) {
+            if (it->first.first == device) {
+                drop.push_back(it->second);
+                g_cached_bytes -= it->first.second;
+                it = g_free_blocks.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    for (void* q : drop) cudaFree(q);
+    if (cur != device) cudaSetDevice(cur);
 }
 
 void mat_free_arrays(krysp_gpu_mat* m) {

@@ -158,15 +158,21 @@ struct krysp_gpu_mat {
 namespace kg {
 
 // ---------------------------------------------------------------- memory helpers
+// Device allocations go through a block cache (formats.cu): blocks of >= 1 MiB are rounded to
+// 2 MiB, kept on release and handed back to the next request of the same size on the same
+// device, so repeated solves (work vectors, staging of host uploads) skip cudaMalloc /
+// cudaFree, whose cost on GB-sized blocks varies from milliseconds to a tenth of a second.
+void* dev_alloc_bytes(size_t bytes);
+void dev_free(void* p);
+void dev_cache_trim(int device);  // release the cached (free) blocks of one device
+
 template <typename T>
 T* dev_alloc(int64_t count, bool zero = true, cudaStream_t s = nullptr) {
-    T* p = nullptr;
-    size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
-    KG_CUDA(cudaMalloc(&p, bytes));
+    const size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
+    T* p = static_cast<T*>(dev_alloc_bytes(bytes));
     if (zero) KG_CUDA(cudaMemsetAsync(p, 0, bytes, s));
     return p;
 }
-void dev_free(void* p);
 
 // RAII device vector of doubles
 struct DVec {
@@ -423,15 +429,17 @@ inline void stream_wait(krysp_gpu_ctx* c) {
     if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "stream wait: %s", cudaGetErrorString(e));
 }
 
-// Drive a device-resident solve to convergence with one chunk always queued ahead of the host's
-// look at the `done` flag: enqueue() queues a chunk of iterations, the flag is copied after
-// it, and the host waits for the copy of chunk k while chunk k+1 runs — the GPU never idles
-// on the host round trip.  A chunk queued past convergence costs only no-op kernels.
+// Drive a device-resident solve to convergence with chunks queued ahead of the host's look
+// at the `done` flag: enqueue() queues a chunk of iterations, the flag is copied after it,
+// and the host waits for the copy of chunk k while chunks k+1 and k+2 are queued behind it —
+// a host stall shorter than two chunks never idles the GPU.  Chunks queued past convergence
+// cost only no-op kernels (every kernel returns on the device flag).
 template <class Enqueue>
 void run_pipelined(krysp_gpu_ctx* c, const int* d_done, Enqueue&& enqueue) {
-    cudaEvent_t ev[2];
+    constexpr int kAhead = 3;
+    cudaEvent_t ev[kAhead];
     for (auto& e : ev) KG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    int* h = reinterpret_cast<int*>(c->h_pinned + 8);  // two flag slots
+    int* h = reinterpret_cast<int*>(c->h_pinned + 8);  // kAhead flag slots
     auto post = [&](int k) {
         enqueue();
         KG_CUDA(cudaMemcpyAsync(h + k, d_done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -439,16 +447,16 @@ void run_pipelined(krysp_gpu_ctx* c, const int* d_done, Enqueue&& enqueue) {
     };
     std::exception_ptr err;
     try {
-        post(0);
-        for (int k = 0;; k ^= 1) {
-            post(k ^ 1);
+        for (int k = 0; k < kAhead - 1; ++k) post(k);
+        for (int k = 0;; k = (k + 1) % kAhead) {
+            post((k + kAhead - 1) % kAhead);
             cudaError_t e;
             WaitWatch w{c};
             while ((e = cudaEventQuery(ev[k])) == cudaErrorNotReady) w.tick();
             if (e != cudaSuccess) fail(KRYSP_CUDA_ERROR, "solve wait: %s", cudaGetErrorString(e));
             if (*(volatile int*)(h + k)) break;
         }
-        KG_CUDA(cudaStreamSynchronize(c->stream));
+        wait_stream(c, c->stream);
     } catch (...) {
         err = std::current_exception();
     }

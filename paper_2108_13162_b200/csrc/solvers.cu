@@ -2285,10 +2285,16 @@ namespace {
 
 void pcg_fused(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep,
                bool trace, double* device_seconds) {
-    PcgSession s(A, cfg, b, x, trace);
-    if (!s.done_at_setup) *device_seconds = s.run_to_convergence();
-    if (A->n_rows) KG_CUDA(cudaMemcpyAsync(x, s.x, 8 * A->n_rows, cudaMemcpyDeviceToDevice, A->ctx->stream));
-    s.finish(rep, trace);
+    {
+        PcgSession s(A, cfg, b, x, trace);
+        trace_lap(A->ctx, "pcg_fused", "session");
+        if (!s.done_at_setup) *device_seconds = s.run_to_convergence();
+        trace_lap(A->ctx, "pcg_fused", "run");
+        if (A->n_rows) KG_CUDA(cudaMemcpyAsync(x, s.x, 8 * A->n_rows, cudaMemcpyDeviceToDevice, A->ctx->stream));
+        s.finish(rep, trace);
+        trace_lap(A->ctx, "pcg_fused", "finish");
+    }
+    trace_lap(A->ctx, "pcg_fused", "release");
 }
 
 void bicgstab_fused(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg, const double* b, double* x, Report& rep,

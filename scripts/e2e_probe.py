@@ -12,7 +12,8 @@ print("host gen+pin %.2f s" % (time.perf_counter() - t0), flush=True)
 N = hm.n_rows
 hb = torch.ones(N, dtype=torch.float64, pin_memory=True).numpy()
 hx0 = torch.zeros(N, dtype=torch.float64, pin_memory=True).numpy()
-for i in range(2):
+hs = torch.empty(N, dtype=torch.float64, pin_memory=True).numpy()
+for i in range(4):
     t0 = time.perf_counter()
-    r = kg.solve_csr_host(ctx, hm, "pcg", hb, hx0, kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0)))
+    r = kg.solve_csr_host(ctx, hm, "pcg", hb, hx0, kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0)), out=hs)
     print("e2e %.3f s  iterations %d  device_time %.3f s" % (time.perf_counter() - t0, r.iterations, r.device_time), flush=True)
