@@ -242,7 +242,9 @@ def run_reference(args, dist):
             "ms_per_step": 1e3 / r["value"] if r["value"] else None, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic 3D 7-point Laplacian)",
-            "config": config_block(args, dist, {"policy": "<1024,1> (reference tuned winner, SURVEY §6)"}),
+            "config": config_block(args, dist, {"policy": "<1024,1> (reference tuned winner, SURVEY §6)",
+                                                "parallelism": f"reference solve_pcg on {ncores} host threads "
+                                                               "(rank 0 only)"}),
             "cpu_baseline": {"value": r["value"], "unit": "iterations/s", "cores": r["cores"], "kind": r["kind"],
                              "sample": f"{r['iterations']} P-CG iterations of the full 400^3 problem "
                                        f"(solve_pcg max_iterations {args.warmup}+{args.steps} minus "
