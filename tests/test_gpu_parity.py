@@ -434,3 +434,23 @@ def test_breakdown_and_non_finite_match_reference(ctx, ref, case, mode):
             kg.solve(A, s, b, cfg=cfg)
         assert ei.value.code == want["status"], (s, mode, str(ei.value), want["error"])
         assert str(ei.value) == want["error"], (s, mode, str(ei.value), want["error"])
+
+
+def test_block_cache_reuses_solver_memory():
+    """The device block cache (formats.cu dev_alloc_bytes / dev_free): repeated solves of one
+    size reuse the cached work vectors — device free memory does not shrink from solve to
+    solve — and destroying the context hands the cached blocks back."""
+    import torch
+    c2 = kg.Context(0)
+    A = c2.generate("lap3d7", 64)
+    b = np.ones(A.n_rows)
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0))
+    first = kg.solve(A, "pcg", b, cfg=cfg)
+    free_after_first = torch.cuda.mem_get_info(0)[0]
+    for _ in range(3):
+        r = kg.solve(A, "pcg", b, cfg=cfg)
+        assert r.iterations == first.iterations
+        assert np.array_equal(r.solution, first.solution)
+    assert torch.cuda.mem_get_info(0)[0] >= free_after_first - (8 << 20)
+    del A
+    c2.close()
