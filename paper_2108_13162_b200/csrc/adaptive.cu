@@ -19,6 +19,12 @@
 
 namespace kg {
 
+// y is written once per SpMV: a streaming store (evict-first) keeps L2 for the gathered x
+__device__ __forceinline__ void ystore(double* p, double s, bool accumulate) {
+    if (accumulate) *p += s;
+    else __stcs(p, s);
+}
+
 constexpr int kAdNT = 256;
 constexpr int64_t kAdTile = 2048;
 constexpr int64_t kAdSplit = 4096;  // longer rows are cut into kAdChunk pieces
@@ -88,7 +94,7 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
         if (b < nlng) {  // long row: the whole CTA
             const int32_t r = lng[b];
             const double s = block_sum_dyn(strided_row(A, x, A.rp[r], A.rp[r + 1], tid, kAdNT), sh);
-            if (tid == 0) y[r] = accumulate ? y[r] + s : s;
+            if (tid == 0) ystore(y + r, s, accumulate);
             continue;
         }
         if (b < nlng + nmedg) {  // medium rows: one warp each
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
                 const int32_t r = med[i];
                 double s = strided_row(A, x, A.rp[r], A.rp[r + 1], lane, 32);
                 s = warp_sum(s);
-                if (lane == 0) y[r] = accumulate ? y[r] + s : s;
+                if (lane == 0) ystore(y + r, s, accumulate);
             }
             continue;
         }
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
             const int e0 = (int)(A.rp[row] - k0), e1 = (int)(A.rp[row + 1] - k0);
             double s = 0.0;
             for (int k = e0; k < e1; ++k) s += prod[k];
-            y[row] = accumulate ? y[row] + s : s;
+            ystore(y + row, s, accumulate);
         }
         __syncthreads();
     }
@@ -137,7 +143,7 @@ __global__ void giant_fixup_kernel(const int32_t* __restrict__ giant, int64_t ng
         const int32_t row = giant[3 * g], c0 = giant[3 * g + 1], c1 = giant[3 * g + 2];
         double s = 0.0;
         for (int32_t c = c0; c < c1; ++c) s += partials[c];
-        y[row] = accumulate ? y[row] + s : s;
+        ystore(y + row, s, accumulate);
     }
 }
 
