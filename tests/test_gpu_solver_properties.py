@@ -1,7 +1,7 @@
 """Solver properties the reference's own unit and acceptance tests assert, on the device.
 
 Mirrors of /root/reference/proj/tests (names and line numbers cited per test):
-test_solvers.cpp (GCR monotone residual :235-263, BiCGStab vs tfQMR :265-282, BiCGStab(1) =
+test_solvers.cpp (finite termination :128-143, descent CG = P-CG on the 2x2 :145-156, GCR monotone residual :235-263, BiCGStab vs tfQMR :265-282, BiCGStab(1) =
 BiCGStab :284-296, l = 8 <= l = 1 cycles :320-331, BiCGCR tracks CG :350-360, report invariants
 :362-393), acceptance.cpp criterion 6 (BiCGStab(l) trend on convdiff2d(32), :336-365) and
 criterion 8 (tuner winner <= 1.05x the default policy on poisson2d(128), :426-460).  Each is
@@ -134,3 +134,29 @@ def test_tuner_winner_within_default(ctx, port):
     default = min(v for k, v in by.items() if k[0] == 256 and k[1] == 8)
     assert best <= 1.05 * default
     assert tr.speedup_vs_default >= 1 / 1.05
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_cg_finite_termination_on_tridiagonals(ctx, port, mode):
+    """CG finite termination within the dimension bound (test_solvers.cpp:128-143): P-CG and
+    descent CG without preconditioning, tol 1e-10, converge in <= n iterations."""
+    for n in (10, 25, 50):
+        _, A = _dev(ctx, port, "laplace1d", n)
+        b = np.ones(n)
+        for method in ("pcg", "cg_classic"):
+            r = kg.solve(A, method, b, cfg=_cfg(mode, preconditioner="none", tolerance=1e-10))
+            assert r.converged and r.iterations <= n, (method, n, r.iterations)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_descent_cg_agrees_with_pcg_on_2x2(ctx, mode):
+    """Classic descent CG agrees with P-CG (no preconditioner) on the 2x2 SPD example
+    (test_solvers.cpp:145-156): same iteration count, solutions within 1e-12."""
+    A = ctx.upload(kg.CsrMatrix(2, 2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), np.array([4.0, 1, 1, 3])))
+    b = np.array([1.0, 2.0])
+    cfg = _cfg(mode, preconditioner="none", tolerance=1e-13)
+    d = kg.solve(A, "cg_classic", b, cfg=cfg)
+    p = kg.solve(A, "pcg", b, cfg=cfg)
+    assert d.iterations == p.iterations
+    assert np.max(np.abs(d.solution - p.solution)) <= 1e-12
+    assert abs(p.solution[0] - 1 / 11) < 1e-12 and abs(p.solution[1] - 7 / 11) < 1e-12
