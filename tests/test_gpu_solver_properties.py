@@ -1,12 +1,13 @@
 """Solver properties the reference's own unit and acceptance tests assert, on the device.
 
 Mirrors of /root/reference/proj/tests (names and line numbers cited per test):
-test_solvers.cpp (finite termination :128-143, descent CG = P-CG on the 2x2 :145-156, GCR monotone residual :235-263, BiCGStab vs tfQMR :265-282, BiCGStab(1) =
-BiCGStab :284-296, l = 8 <= l = 1 cycles :320-331, BiCGCR tracks CG :350-360, report invariants
-:362-393), acceptance.cpp criterion 6 (BiCGStab(l) trend on convdiff2d(32), :336-365) and
-criterion 8 (tuner winner <= 1.05x the default policy on poisson2d(128), :426-460).  Each is
-run in both modes; where the reference library is built (`oracle/_ref`) the EXACT iteration
-counts are also compared with it one for one.
+test_solvers.cpp (finite termination :128-143, descent CG = P-CG on the 2x2 :145-156, GCR
+monotone residual :235-263, BiCGStab vs tfQMR :265-282, BiCGStab(1) = BiCGStab :284-296,
+l = 8 <= l = 1 cycles :320-331, BiCGCR tracks CG :350-360, report invariants :362-393),
+acceptance.cpp criterion 6 (BiCGStab(l) trend on convdiff2d(32), :336-365) and criterion 8
+(tuner winner <= 1.05x the default policy on poisson2d(128), :426-460).  Each is run in both
+modes; where the reference library is built (`oracle/_ref`) the EXACT iteration counts are
+also compared with it one for one.
 """
 import numpy as np
 import pytest
