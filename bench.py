@@ -142,9 +142,15 @@ def spmv_bytes(n_rows, n_cols, nnz):
     return 12 * nnz + 4 * (n_rows + 1) + 8 * n_cols + 8 * n_rows
 
 
-def iter_bytes(n_rows, n_cols, nnz):
-    # P-CG: k_spmv = 1, V = 11 vector streams
-    return spmv_bytes(n_rows, n_cols, nnz) + 8 * n_rows * 11
+PCG_V = 10  # vector streams per P-CG iteration as implemented (below)
+
+
+def iter_bytes(n_rows, n_cols, nnz, v=PCG_V):
+    """P-CG: k_spmv = 1 plus V vector streams.  SURVEY §8(d) counts V = 11 (update: x, p, r, Ap,
+    D^-1 -> x, r; direction: r, D^-1, p -> p); the FAST kernels defer x += alpha p into the
+    direction pass, which reads p anyway (update: r, Ap, D^-1 -> r; direction: x, p, r, D^-1 ->
+    x, p), so the algorithmic minimum of this schedule is V = 10."""
+    return spmv_bytes(n_rows, n_cols, nnz) + 8 * n_rows * v
 
 
 def ncu_traffic():
@@ -322,8 +328,11 @@ def run_ours(args, dist):
                          "algorithmic_bytes_per_launch": B_spmv,
                          "launch_ms": t_spmv * 1e3, "update_ms": t_upd * 1e3, "direction_ms": t_dir * 1e3},
             "spmv_gflops": 2 * nnz / t_spmv / 1e9,
-            "iteration_roofline": {"bytes": B_iter, "achieved_gbs": B_iter / (t_max / args.steps) / 1e9,
-                                   "frac": B_iter / (t_max / args.steps) / 1e9 / bw_peak},
+            "iteration_roofline": {"bytes": B_iter, "v_streams": PCG_V,
+                                   "achieved_gbs": B_iter / (t_max / args.steps) / 1e9,
+                                   "frac": B_iter / (t_max / args.steps) / 1e9 / bw_peak,
+                                   "frac_survey_v11": iter_bytes(n, info["n_cols"], nnz, 11) / (t_max / args.steps)
+                                                      / 1e9 / bw_peak},
             "gpu_launches": kpi * args.steps,
             "clocks": ck,
             "pcg_ell": {"value": ell_rate, "unit": "iterations/s",

@@ -62,6 +62,7 @@ struct DistCgState {
     double omega;
     double red_loc[4], red[4];  // (sum, compensation) pairs
     int half;
+    int x_pending;  // P-CG: the last iteration's deferred x += alpha p still to apply
 };
 enum : int {
     kDsBreakdownSigma = 1, kDsNonFiniteSigma = 2, kDsNonFiniteAlpha = 3, kDsNonFiniteRho = 4,
@@ -223,8 +224,8 @@ __global__ void __launch_bounds__(kNT) dist_update_kernel(int64_t n, double* __r
     __shared__ double sh[32];
     const double alpha = st->alpha, malpha = -alpha;
     double acc = 0.0;
+    // x += alpha p is deferred to dist_direction_kernel, which reads p anyway
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
-        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
         const double ri = __dadd_rn(__dmul_rn(malpha, ap[i]), r[i]);
         r[i] = ri;
         const double zi = inv ? __dmul_rn(ri, inv[i]) : ri;
@@ -247,6 +248,7 @@ __global__ void converge_kernel(DistCgState* st, double* history) {
     const double rho_new = st->rho_new;
     if (!isfinite(rho_new)) {
         st->status = kDsNonFiniteRho;
+        st->x_pending = 1;
         st->done = 1;
         return;
     }
@@ -257,17 +259,35 @@ __global__ void converge_kernel(DistCgState* st, double* history) {
     st->rho_1 = st->rho;
     st->beta = rho_new / st->rho;
     st->rho = rho_new;
-    if (measure <= st->tol || it + 1 >= st->max_it) st->done = 1;
+    if (measure <= st->tol || it + 1 >= st->max_it) {
+        st->x_pending = 1;
+        st->done = 1;
+    }
 }
 
+// the deferred x += alpha p, then p = D^-1 r + beta p; after the iteration that ends the
+// solve only the x update runs, once (x_pending)
 __global__ void __launch_bounds__(kNT) dist_direction_kernel(int64_t n, double* __restrict__ p,
                                                               const double* __restrict__ r,
-                                                              const double* __restrict__ inv, const DistCgState* st) {
-    if (*(volatile const int*)&st->done) return;
-    const double beta = st->beta;
+                                                              const double* __restrict__ inv, double* __restrict__ x,
+                                                              DistCgState* st, unsigned* counter) {
+    const int done = *(volatile const int*)&st->done;
+    if (done && !*(volatile const int*)&st->x_pending) return;
+    const double alpha = st->alpha, beta = st->beta;
+    if (done) {
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT)
+            x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        if (last_block(counter) && threadIdx.x == 0) {
+            *counter = 0;
+            st->x_pending = 0;
+        }
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+        const double pi = p[i];
+        x[i] = __dadd_rn(__dmul_rn(alpha, pi), x[i]);
         const double zi = inv ? __dmul_rn(r[i], inv[i]) : r[i];
-        p[i] = __dadd_rn(__dmul_rn(beta, p[i]), zi);
+        p[i] = __dadd_rn(__dmul_rn(beta, pi), zi);
     }
 }
 
@@ -942,7 +962,7 @@ void dist_iteration(krysp_gpu_dist* d, cudaEvent_t ev_spmv_done = nullptr) {
         KG_LAUNCH(c);
         const unsigned g = grid_for(P.n_local, kNT, (int64_t)c->sm_count * 8);
         dist_direction_kernel<<<g, kNT, 0, s>>>(P.n_local, P.p, P.r, d->cfg.preconditioner ? (const double*)P.inv : nullptr,
-                                                 P.st);
+                                                 P.x, P.st, c->d_counters + 4 + (i % 4));
         KG_LAUNCH(c);
     }
     d->kernels_per_iteration = (int)(c->launches - before);

@@ -504,6 +504,7 @@ struct CgState {
     double rho, rho_1, sigma, alpha, beta, norm_r0, tol;
     long long iter, max_it;
     int done, status;
+    int x_pending;  // the last iteration's x += alpha p still to apply (deferred update)
 };
 
 enum : int { kStRunning = 0, kStBreakdownSigma = 1, kStNonFiniteSigma = 2, kStNonFiniteAlpha = 3, kStNonFiniteRho = 4 };
@@ -563,8 +564,8 @@ __global__ void __launch_bounds__(kFusedNT) cg_update_kernel(int64_t n, double* 
     __shared__ double sh[32];
     const double alpha = st->alpha, malpha = -alpha;
     double acc = 0.0;
+    // x += alpha p is deferred to the direction kernel, which reads p anyway (8n bytes fewer)
     for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kFusedNT) {
-        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
         const double ri = __dadd_rn(__dmul_rn(malpha, ap[i]), r[i]);
         r[i] = ri;
         const double zi = kJacobi ? __dmul_rn(ri, inv[i]) : ri;
@@ -586,6 +587,7 @@ __global__ void __launch_bounds__(kFusedNT) cg_update_kernel(int64_t n, double* 
             }
             if (!isfinite(rho_new)) {
                 st->status = kStNonFiniteRho;
+                st->x_pending = 1;
                 st->done = 1;
                 return;
             }
@@ -595,21 +597,41 @@ __global__ void __launch_bounds__(kFusedNT) cg_update_kernel(int64_t n, double* 
             st->rho_1 = st->rho;
             st->beta = rho_new / st->rho;
             st->rho = rho_new;
-            if (measure <= st->tol || it + 1 >= st->max_it) st->done = 1;
+            if (measure <= st->tol || it + 1 >= st->max_it) {
+                st->x_pending = 1;
+                st->done = 1;
+            }
         }
     }
 }
 
-// p = D^-1 r + beta p (solvers.cpp:154-157: z += beta p, then p <- z)
+// x += alpha p (the update phase's, solvers.cpp:167, deferred here where p is read anyway),
+// then p = D^-1 r + beta p (solvers.cpp:154-157: z += beta p, then p <- z).  After the
+// iteration that ends the solve only the x update runs, once (x_pending).
 template <bool kJacobi>
 __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, double* __restrict__ p,
                                                                  const double* __restrict__ r,
-                                                                 const double* __restrict__ inv, const CgState* st) {
-    if (*(volatile const int*)&st->done) return;
-    const double beta = st->beta;
+                                                                 const double* __restrict__ inv,
+                                                                 double* __restrict__ x, CgState* st,
+                                                                 unsigned* counter) {
+    const int done = *(volatile const int*)&st->done;
+    if (done && !*(volatile const int*)&st->x_pending) return;
+    const double alpha = st->alpha, beta = st->beta;
+    if (done) {
+        for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kFusedNT)
+            x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        __syncthreads();
+        if (last_block(counter) && threadIdx.x == 0) {
+            *counter = 0;
+            st->x_pending = 0;
+        }
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kFusedNT) {
+        const double pi = p[i];
+        x[i] = __dadd_rn(__dmul_rn(alpha, pi), x[i]);
         const double zi = kJacobi ? __dmul_rn(r[i], inv[i]) : r[i];
-        p[i] = __dadd_rn(__dmul_rn(beta, p[i]), zi);
+        p[i] = __dadd_rn(__dmul_rn(beta, pi), zi);
     }
 }
 
@@ -1774,8 +1796,9 @@ struct PcgSession {
             cg_update_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, x, r, p, ap, nullptr, st, part_b, cnt_b, hist, d_trace);
         KG_LAUNCH(c);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
-        if (e.jacobi) cg_direction_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, e.inv, st);
-        else cg_direction_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, nullptr, st);
+        unsigned* cnt_c = c->d_counters + 5;
+        if (e.jacobi) cg_direction_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, e.inv, x, st, cnt_c);
+        else cg_direction_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, nullptr, x, st, cnt_c);
         KG_LAUNCH(c);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[3], c->stream, cudaEventRecordExternal));
         kernels_per_iteration = (int)(c->launches - before);
