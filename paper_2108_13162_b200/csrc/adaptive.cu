@@ -19,10 +19,12 @@
 
 namespace kg {
 
-// y is written once per SpMV: a streaming store (evict-first) keeps L2 for the gathered x
+// y row result (accumulate: HYB's COO part adds onto the ELL rows).  A streaming store
+// (evict-first) here won 2% on C5 at 100M nnz but cost 20% on C4 HYB with COO overflow, whose
+// accumulate pass re-reads y: plain stores.
 __device__ __forceinline__ void ystore(double* p, double s, bool accumulate) {
     if (accumulate) *p += s;
-    else __stcs(p, s);
+    else *p = s;
 }
 
 constexpr int kAdNT = 256;
@@ -78,7 +80,8 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
                                                           const int32_t* __restrict__ chunk, int64_t nchunk,
                                                           double* __restrict__ partials,
                                                           const double* __restrict__ x, double* __restrict__ y,
-                                                          int accumulate) {
+                                                          int accumulate, const int* gate) {
+    if (gate && *(volatile const int*)gate) return;  // the owning solve has finished
     __shared__ double sh[32];
     __shared__ double prod[kAdTile];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -138,7 +141,9 @@ __global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const in
 }
 
 __global__ void giant_fixup_kernel(const int32_t* __restrict__ giant, int64_t ngiant,
-                                   const double* __restrict__ partials, double* __restrict__ y, int accumulate) {
+                                   const double* __restrict__ partials, double* __restrict__ y, int accumulate,
+                                   const int* gate) {
+    if (gate && *(volatile const int*)gate) return;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngiant; g += (int64_t)gridDim.x * blockDim.x) {
         const int32_t row = giant[3 * g], c0 = giant[3 * g + 1], c1 = giant[3 * g + 2];
         double s = 0.0;
@@ -240,7 +245,7 @@ int32_t* ensure_coo_rp(const krysp_gpu_mat* cm) {
 }  // namespace
 
 void launch_adaptive(const krysp_gpu_mat* cm, bool coo_part, const double* x, double* y, bool accumulate,
-                     cudaStream_t s) {
+                     cudaStream_t s, const int* gate) {
     auto* m = const_cast<krysp_gpu_mat*>(cm);
     krysp_gpu_ctx* c = m->ctx;
     if (m->n_rows == 0) return;
@@ -258,12 +263,12 @@ void launch_adaptive(const krysp_gpu_mat* cm, bool coo_part, const double* x, do
     if (items) {
         const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel, kAdNT, 0), items);
         adaptive_kernel<<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
-                                                      P->nchunk, P->partials, x, y, accumulate ? 1 : 0);
+                                                      P->nchunk, P->partials, x, y, accumulate ? 1 : 0, gate);
         KG_LAUNCH(c);
     }
     if (P->ngiant) {
         giant_fixup_kernel<<<grid_for(P->ngiant, 128, 1024), 128, 0, s>>>(P->giant, P->ngiant, P->partials, y,
-                                                                         accumulate ? 1 : 0);
+                                                                         accumulate ? 1 : 0, gate);
         KG_LAUNCH(c);
     }
 }

@@ -29,6 +29,7 @@ struct Engine {
     bool jacobi = false;
     DVec tmp;
     bool auto_pol = false;  // FAST + library's kernel choice (load-balanced kernels for irregular rows)
+    const int* gate = nullptr;  // device-resident sessions: their `done` flag, gating raw SpMVs
 
     Engine(const krysp_gpu_mat* A_, const krysp_solver_cfg& cfg)
         : c(A_->ctx), A(A_), pol(cfg.policy), mode(cfg.mode), n(A_->n_rows), tmp(A_->n_rows, A_->ctx->stream) {

@@ -482,8 +482,9 @@ krysp_gpu_mat* convert_to_csr(const krysp_gpu_mat* m);
 void adaptive_free(AdaptivePlan& p);
 bool csr_is_irregular(const krysp_gpu_mat* m);
 // y (=|+=) A x over the CSR arrays (or the COO part via coo_rp) with the load-balanced plan
+// gate: optional device flag (a device-resident solve's `done`); set -> the kernels return
 void launch_adaptive(const krysp_gpu_mat* m, bool coo_part, const double* x, double* y, bool accumulate,
-                     cudaStream_t s);
+                     cudaStream_t s, const int* gate = nullptr);
 
 // spmv.cu
 enum SpmvVariant : int32_t {
@@ -496,8 +497,11 @@ enum SpmvVariant : int32_t {
     kVarHybAdaptive = 6,  // FAST: ELL + load-balanced COO overflow
     kVarCooAdaptive = 7,  // FAST: load-balanced COO
 };
+// gate (FAST auto policy on irregular rows, the load-balanced kernels): an optional device
+// flag that turns the launch into a no-op once set — a device-resident solve's `done`, so
+// chunks queued past convergence cost nothing
 int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const krysp_policy& pol,
-                    int32_t mode, cudaStream_t s);
+                    int32_t mode, cudaStream_t s, const int* gate = nullptr);
 void check_policy(const krysp_policy& pol);
 
 // blas1.cu

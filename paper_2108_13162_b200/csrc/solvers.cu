@@ -127,6 +127,7 @@ void cg_classic(Engine& e, const krysp_solver_cfg& cfg, const double* b, double*
         auto op = [&]() { e.spmv(wp, kwp); };
         const double* gp = g;
         auto fused = [&](SubCgState* dst, double* pa, unsigned* ca) {
+            e.gate = &dst->done;
             spmv_fused(e, wp, kwp, EpiDescent{kwp, wp, gp, dst, pa, ca, {0, 0}, {0, 0}});
         };
         int64_t its = 0;
@@ -665,7 +666,7 @@ void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y,
             KG_LAUNCH(e.c);
         }
     } else {
-        spmv_launch(m, x, y, e.launch_pol(), e.mode, s);
+        spmv_launch(m, x, y, e.launch_pol(), e.mode, s, e.gate);
         vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y, epi);
         KG_LAUNCH(e.c);
     }
@@ -1748,6 +1749,7 @@ struct PcgSession {
                 h.done = 1;
             }
             st = dev_alloc<CgState>(1, false);
+            e.gate = &st->done;
             hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
             if (trace) d_trace = dev_alloc<double>(4 * cfg.max_iterations, true, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
@@ -2191,6 +2193,7 @@ struct BicgstabSession {
                 h.rho = e.dot(rh, r);
             }
             st = dev_alloc<BiState>(1, false);
+            e.gate = &st->done;
             hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
             stream_wait(c);

@@ -49,7 +49,7 @@ bool csr_use_tile(const krysp_gpu_mat* m, int64_t tw) {
 }
 
 int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const krysp_policy& pol0,
-                    int32_t mode, cudaStream_t s) {
+                    int32_t mode, cudaStream_t s, const int* gate) {
     krysp_policy pol = pol0;
     const bool auto_pol = pol.block_size == 0;
     if (auto_pol) {
@@ -60,16 +60,16 @@ int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const kr
     EpiStore epi{y};
     if (auto_pol) {  // FAST, library's choice: load-balanced kernels for irregular rows
         if (m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) {
-            launch_adaptive(m, false, x, y, false, s);
+            launch_adaptive(m, false, x, y, false, s, gate);
             return kVarCsrAdaptive;
         }
         if (m->format == KRYSP_FMT_HYB && m->coo_nnz) {
-            launch_ell(m, x, epi, pol.block_size, s);
-            launch_adaptive(m, true, x, y, true, s);
+            launch_ell(m, x, EpiStoreGated<FlagGate>{y, FlagGate{gate}}, pol.block_size, s);
+            launch_adaptive(m, true, x, y, true, s, gate);
             return kVarHybAdaptive;
         }
         if (m->format == KRYSP_FMT_COO) {
-            launch_adaptive(m, true, x, y, false, s);
+            launch_adaptive(m, true, x, y, false, s, gate);
             return kVarCooAdaptive;
         }
     }

@@ -39,6 +39,12 @@ struct EpiStore {
     __device__ __forceinline__ void finish() {}
 };
 
+// gate on a device flag (NULL: always active)
+struct FlagGate {
+    const int* f;
+    __device__ __forceinline__ bool active() const { return !f || !*(volatile const int*)f; }
+};
+
 // plain store that is skipped once another epilogue's solve has converged (its active())
 template <class Gate>
 struct EpiStoreGated {
