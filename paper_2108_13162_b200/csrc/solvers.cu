@@ -511,6 +511,7 @@ struct CgState {
 enum : int { kStRunning = 0, kStBreakdownSigma = 1, kStNonFiniteSigma = 2, kStNonFiniteAlpha = 3, kStNonFiniteRho = 4 };
 
 constexpr int kFusedNT = 256;
+constexpr int kVu = 2;  // rows per thread whose loads are issued together in the fused vector kernels
 
 // Epilogue of the SpMV: Ap[r] = (A p)[r], partial <p, Ap>; the last block forms sigma and
 // alpha = rho / sigma with the reference's checks (solvers.cpp:160-166).
@@ -628,11 +629,23 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
         }
         return;
     }
-    for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kFusedNT) {
-        const double pi = p[i];
-        x[i] = __dadd_rn(__dmul_rn(alpha, pi), x[i]);
-        const double zi = kJacobi ? __dmul_rn(r[i], inv[i]) : r[i];
-        p[i] = __dadd_rn(__dmul_rn(beta, pi), zi);
+    const int64_t stride = (int64_t)gridDim.x * kFusedNT;
+    for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double pv[kVu], xv[kVu], rv[kVu], iv[kVu];  // loads of kVu rows before any store
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) pv[q] = p[i], xv[q] = x[i], rv[q] = r[i], iv[q] = kJacobi ? inv[i] : 1.0;
+        }
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                x[i] = __dadd_rn(__dmul_rn(alpha, pv[q]), xv[q]);
+                const double zi = kJacobi ? __dmul_rn(rv[q], iv[q]) : rv[q];
+                p[i] = __dadd_rn(__dmul_rn(beta, pv[q]), zi);
+            }
+        }
     }
 }
 
@@ -708,7 +721,6 @@ int fused_grid_mult() {
 // and ran this bandwidth-bound pass at 3 TB/s (GCR's orthogonalisation coefficients do not
 // need the compensation the BiCGStab breakdown tests do).
 constexpr int kMdNT = 256;
-constexpr int kVu = 2;  // rows per thread whose loads are issued together in the fused vector kernels
 constexpr int kMdG = 8;
 
 // out[q] = <w, v_q> for the K vectors of vs (K a template argument: the vector pointers in
