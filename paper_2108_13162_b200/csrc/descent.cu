@@ -39,23 +39,21 @@ __global__ void __launch_bounds__(kDcNT) sc_dot2_kernel(int64_t n, const double*
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <bool kInv, bool kWt>
-__device__ __forceinline__ void sc_update_row(double rho, double& x, double& g, double& z, double w, double kw,
-                                              double inv, double wt, D2& a0, D2& a1) {
-    x = __dadd_rn(__dmul_rn(rho, w), x);
+__device__ __forceinline__ void sc_update_row(double rho, double& g, double& z, double kw, double inv, double wt,
+                                              D2& a0, D2& a1) {
     g = __dadd_rn(__dmul_rn(rho, kw), g);
     z = kInv ? __dmul_rn(g, inv) : g;
     d2_add_prod(a0, z, kWt ? __dmul_rn(kw, wt) : kw);
     d2_add_prod(a1, g, kWt ? __dmul_rn(g, wt) : g);
 }
 
-// x += rho w; g += rho Kw; z = D^-1 g; <z, Kw>_W and <g, g>_W (kSingle: then gamma, the
-// measure and the convergence test in the last block).  vec: every vector 16-byte aligned —
-// the rows go in pairs (double2 loads and stores), the odd last row in the scalar loop.
+// g += rho Kw; z = D^-1 g; <z, Kw>_W and <g, g>_W (kSingle: then gamma, the measure and the
+// convergence test in the last block); x += rho w is deferred to sc_axpby_kernel, which reads
+// w anyway.  vec: every vector 16-byte aligned — the rows go in pairs (double2 loads and
+// stores), the odd last row in the scalar loop.
 template <bool kSingle, bool kInv, bool kWt>
-__global__ void __launch_bounds__(kDcNT) sc_update_kernel(int64_t n, bool vec, double* __restrict__ x,
-                                                            double* __restrict__ g, double* __restrict__ z,
-                                                            const double* __restrict__ w,
-                                                            const double* __restrict__ kw,
+__global__ void __launch_bounds__(kDcNT) sc_update_kernel(int64_t n, bool vec, double* __restrict__ g,
+                                                            double* __restrict__ z, const double* __restrict__ kw,
                                                             const double* __restrict__ inv,
                                                             const double* __restrict__ wt, SubCgState* st,
                                                             double* partials, unsigned* counter, double* history) {
@@ -66,20 +64,19 @@ __global__ void __launch_bounds__(kDcNT) sc_update_kernel(int64_t n, bool vec, d
     const int64_t n2 = vec ? n / 2 : 0;
     const int64_t stride = (int64_t)gridDim.x * kDcNT;
     for (int64_t i = blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n2; i += stride) {
-        double2 xv = reinterpret_cast<const double2*>(x)[i], gv = reinterpret_cast<const double2*>(g)[i], zv;
-        const double2 wv = reinterpret_cast<const double2*>(w)[i], kv = reinterpret_cast<const double2*>(kw)[i];
+        double2 gv = reinterpret_cast<const double2*>(g)[i], zv;
+        const double2 kv = reinterpret_cast<const double2*>(kw)[i];
         const double2 iv = kInv ? reinterpret_cast<const double2*>(inv)[i] : double2{0.0, 0.0};
         const double2 tv = kWt ? reinterpret_cast<const double2*>(wt)[i] : double2{0.0, 0.0};
-        sc_update_row<kInv, kWt>(rho, xv.x, gv.x, zv.x, wv.x, kv.x, iv.x, tv.x, a0, a1);
-        sc_update_row<kInv, kWt>(rho, xv.y, gv.y, zv.y, wv.y, kv.y, iv.y, tv.y, a0, a1);
-        reinterpret_cast<double2*>(x)[i] = xv;
+        sc_update_row<kInv, kWt>(rho, gv.x, zv.x, kv.x, iv.x, tv.x, a0, a1);
+        sc_update_row<kInv, kWt>(rho, gv.y, zv.y, kv.y, iv.y, tv.y, a0, a1);
         reinterpret_cast<double2*>(g)[i] = gv;
         reinterpret_cast<double2*>(z)[i] = zv;
     }
     for (int64_t i = 2 * n2 + blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += stride) {
-        double xi = x[i], gi = g[i], zi;
-        sc_update_row<kInv, kWt>(rho, xi, gi, zi, w[i], kw[i], kInv ? inv[i] : 0.0, kWt ? wt[i] : 0.0, a0, a1);
-        x[i] = xi, g[i] = gi, z[i] = zi;
+        double gi = g[i], zi;
+        sc_update_row<kInv, kWt>(rho, gi, zi, kw[i], kInv ? inv[i] : 0.0, kWt ? wt[i] : 0.0, a0, a1);
+        g[i] = gi, z[i] = zi;
     }
     sc_finish2<kSingle>(a0, a1, sh, partials, counter, st, [history](SubCgState* s) { sc_scalar2(s, history); });
 }
@@ -88,10 +85,10 @@ template <bool kSingle>
 void launch_sc_update(unsigned grid, cudaStream_t s, const DescentPart& P, SubCgState* st, double* partials,
                       unsigned* counter, double* history) {
     auto al = [](const void* p) { return p == nullptr || aligned16(p); };
-    const bool vec = al(P.x) && al(P.g) && al(P.z) && al(P.w) && al(P.kw) && al(P.inv) && al(P.wt);
-#define KG_SCU(I, W)                                                                                                \
-    sc_update_kernel<kSingle, I, W><<<grid, kDcNT, 0, s>>>(P.n, vec, P.x, P.g, P.z, P.w, P.kw, P.inv, P.wt, st, \
-                                                           partials, counter, history)
+    const bool vec = al(P.g) && al(P.z) && al(P.kw) && al(P.inv) && al(P.wt);
+#define KG_SCU(I, W)                                                                                         \
+    sc_update_kernel<kSingle, I, W><<<grid, kDcNT, 0, s>>>(P.n, vec, P.g, P.z, P.kw, P.inv, P.wt, st, partials, \
+                                                           counter, history)
     if (P.inv && P.wt) KG_SCU(true, true);
     else if (P.inv) KG_SCU(true, false);
     else if (P.wt) KG_SCU(false, true);
@@ -103,23 +100,41 @@ __global__ void sc_scalar1_kernel(SubCgState* st) { sc_scalar1(st); }
 
 __global__ void sc_scalar2_kernel(SubCgState* st, double* history) { sc_scalar2(st, history); }
 
-// w = fl(1 * z) + fl(gamma * w) (axpby, kernels.cpp:109-118); skipped once converged; pairs
-// of rows when both vectors are 16-byte aligned
+// the deferred x += rho w (solvers.cpp:226, substructure.cpp:540), then w = fl(1 * z) +
+// fl(gamma * w) (axpby, kernels.cpp:109-118); after the iteration that ends the solve only the
+// x update runs, once (x_pending).  Pairs of rows when the vectors are 16-byte aligned.
 __global__ void __launch_bounds__(kDcNT) sc_axpby_kernel(int64_t n, bool vec, const double* __restrict__ z,
-                                                           double* __restrict__ w, const SubCgState* st) {
-    if (*(volatile const int*)&st->done) return;
-    const double gamma = st->gamma;
+                                                           double* __restrict__ w, double* __restrict__ x,
+                                                           SubCgState* st, unsigned* counter) {
+    const int done = *(volatile const int*)&st->done;
+    if (done && !*(volatile const int*)&st->x_pending) return;
+    const double rho = st->rho, gamma = st->gamma;
     const int64_t n2 = vec ? n / 2 : 0;
     const int64_t stride = (int64_t)gridDim.x * kDcNT;
+    if (done) {
+        for (int64_t i = blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += stride)
+            x[i] = __dadd_rn(__dmul_rn(rho, w[i]), x[i]);
+        if (last_block(counter) && threadIdx.x == 0) {
+            *counter = 0;
+            st->x_pending = 0;
+        }
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n2; i += stride) {
         const double2 zv = reinterpret_cast<const double2*>(z)[i];
-        double2 wv = reinterpret_cast<const double2*>(w)[i];
+        double2 wv = reinterpret_cast<const double2*>(w)[i], xv = reinterpret_cast<const double2*>(x)[i];
+        xv.x = __dadd_rn(__dmul_rn(rho, wv.x), xv.x);
+        xv.y = __dadd_rn(__dmul_rn(rho, wv.y), xv.y);
         wv.x = __dadd_rn(zv.x, __dmul_rn(gamma, wv.x));
         wv.y = __dadd_rn(zv.y, __dmul_rn(gamma, wv.y));
+        reinterpret_cast<double2*>(x)[i] = xv;
         reinterpret_cast<double2*>(w)[i] = wv;
     }
-    for (int64_t i = 2 * n2 + blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += stride)
-        w[i] = __dadd_rn(z[i], __dmul_rn(gamma, w[i]));
+    for (int64_t i = 2 * n2 + blockIdx.x * (int64_t)kDcNT + threadIdx.x; i < n; i += stride) {
+        const double wi = w[i];
+        x[i] = __dadd_rn(__dmul_rn(rho, wi), x[i]);
+        w[i] = __dadd_rn(z[i], __dmul_rn(gamma, wi));
+    }
 }
 
 // the part-order sum of the parts' partial dots (one device; a single part copies through)
@@ -172,7 +187,8 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
             fused_op(d_st, slot(0), cnt(0));
             launch_sc_update<true>(grid(P.n), st, P, d_st, slot(0), cnt(0), d_hist);
             KG_LAUNCH(c);
-            sc_axpby_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, aligned16(P.z) && aligned16(P.w), P.z, P.w, d_st);
+            sc_axpby_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, aligned16(P.z) && aligned16(P.w) && aligned16(P.x),
+                                                         P.z, P.w, P.x, d_st, cnt(0));
             KG_LAUNCH(c);
             return;
         }
@@ -195,7 +211,8 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
             const DescentPart& P = parts[i];
             sc_scalar2_kernel<<<1, 1, 0, st>>>(d_st + i, d_hist + (int64_t)i * cfg.max_iterations);
             KG_LAUNCH(c);
-            sc_axpby_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, aligned16(P.z) && aligned16(P.w), P.z, P.w, d_st + i);
+            sc_axpby_kernel<<<grid(P.n), kDcNT, 0, st>>>(P.n, aligned16(P.z) && aligned16(P.w) && aligned16(P.x),
+                                                         P.z, P.w, P.x, d_st + i, cnt(i));
             KG_LAUNCH(c);
         }
     };

@@ -12,6 +12,7 @@ struct SubCgState {
     double norm_g0, tol, denom, rho, gamma, measure;
     long long iter, max_it;
     int done, status;
+    int x_pending;  // the last iteration's x += rho w (deferred to the direction pass) still to apply
 };
 
 enum { kDescentOk = 0, kDescentDenomNonFinite, kDescentBreakdown, kDescentRhoNonFinite, kDescentGammaNonFinite,
@@ -36,16 +37,26 @@ __device__ __forceinline__ void sc_scalar1(SubCgState* st) {
 }
 
 // gamma = -<z,Kw>/<Kw,w>; measure; convergence (solvers.cpp:228-240, substructure.cpp:543-553)
+// (every exit that ends the solve here leaves this iteration's deferred x update pending)
 __device__ __forceinline__ void sc_scalar2(SubCgState* st, double* history) {
     if (st->done) return;
     st->gamma = -sc_red(st, 0) / st->denom;
-    if (!isfinite(st->gamma)) return sc_fail(st, kDescentGammaNonFinite);
+    if (!isfinite(st->gamma)) {
+        st->x_pending = 1;
+        return sc_fail(st, kDescentGammaNonFinite);
+    }
     const double measure = sqrt(sc_red(st, 1)) / st->norm_g0;
-    if (!isfinite(measure)) return sc_fail(st, kDescentMeasureNonFinite);
+    if (!isfinite(measure)) {
+        st->x_pending = 1;
+        return sc_fail(st, kDescentMeasureNonFinite);
+    }
     st->measure = measure;
     history[st->iter] = measure;
     st->iter += 1;
-    if (measure <= st->tol || st->iter >= st->max_it) st->done = 1;
+    if (measure <= st->tol || st->iter >= st->max_it) {
+        st->x_pending = 1;
+        st->done = 1;
+    }
 }
 
 // Grid finish of two compensated dots: block partials, then the last block merges them into

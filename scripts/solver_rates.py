@@ -14,7 +14,7 @@ if fmt != "csr":
 i = A.info
 N, nnz = i["n_rows"], i["nnz"]
 Bs = 12 * nnz + 4 * (N + 1) + 16 * N
-V = {"pcg": (1, 10), "bicgstab": (2, 17), "cg_classic": (1, 12), "tfqmr": (3, 30), "gcr": (1, 12), "bicgstab_l": (8, 131), "bicgcr": (2, 20)}
+V = {"pcg": (1, 10), "bicgstab": (2, 17), "cg_classic": (1, 11), "tfqmr": (3, 30), "gcr": (1, 12), "bicgstab_l": (8, 131), "bicgcr": (2, 20)}
 b = np.ones(N)
 peak = 6541.8
 for m in sys.argv[5].split(",") if len(sys.argv) > 5 else ["pcg", "bicgstab"]:
