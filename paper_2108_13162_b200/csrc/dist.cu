@@ -62,7 +62,6 @@ struct DistCgState {
     double omega;
     double red_loc[4], red[4];  // (sum, compensation) pairs
     int half;
-    int x_pending;  // P-CG: the last iteration's deferred x += alpha p still to apply
 };
 enum : int {
     kDsBreakdownSigma = 1, kDsNonFiniteSigma = 2, kDsNonFiniteAlpha = 3, kDsNonFiniteRho = 4,
@@ -198,33 +197,33 @@ __global__ void sum_partials(DistCgState* st, const double* a, int na, const dou
     if (threadIdx.x == 0) st->sigma_loc = t;
 }
 
-__global__ void alpha_kernel(DistCgState* st) {
-    if (st->done) return;
-    const double sigma = st->sigma;
-    if (!isfinite(sigma)) {
-        st->status = kDsNonFiniteSigma;
-        st->done = 1;
-    } else if (fabs(sigma) < 1e-300) {
-        st->status = kDsBreakdownSigma;
-        st->done = 1;
-    } else {
-        st->alpha = st->rho / sigma;
-        if (!isfinite(st->alpha)) {
-            st->status = kDsNonFiniteAlpha;
-            st->done = 1;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kNT) dist_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
-                                                           const double* __restrict__ p, const double* __restrict__ ap,
+// P-CG vector passes of the partitioned solve, each with the scalar step of the reference
+// folded into its prologue (every block derives the same scalars from the allreduced values;
+// the last block to finish — after every other block has read them — writes the state):
+//   update:    alpha = rho / sigma with the checks of solvers.cpp:160-166; r -= alpha Ap;
+//              local <r, D^-1 r>
+//   direction: convergence on the allreduced rho (solvers.cpp:174-181); the deferred
+//              x += alpha p; unless the solve ends here, p = D^-1 r + beta p
+__global__ void __launch_bounds__(kNT) dist_update_kernel(int64_t n, double* __restrict__ r,
+                                                           const double* __restrict__ ap,
                                                            const double* __restrict__ inv, DistCgState* st,
                                                            double* partials, unsigned* counter) {
     if (*(volatile int*)&st->done) return;
+    const double sigma = st->sigma, alpha = st->rho / sigma;
+    int bad = 0;
+    if (!isfinite(sigma)) bad = kDsNonFiniteSigma;
+    else if (fabs(sigma) < 1e-300) bad = kDsBreakdownSigma;
+    else if (!isfinite(alpha)) bad = kDsNonFiniteAlpha;
+    if (bad) {  // every block sees the same sigma: all return, block 0 records it
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->status = bad;
+            st->done = 1;
+        }
+        return;
+    }
     __shared__ double sh[32];
-    const double alpha = st->alpha, malpha = -alpha;
+    const double malpha = -alpha;
     double acc = 0.0;
-    // x += alpha p is deferred to dist_direction_kernel, which reads p anyway
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
         const double ri = __dadd_rn(__dmul_rn(malpha, ap[i]), r[i]);
         r[i] = ri;
@@ -236,58 +235,47 @@ __global__ void __launch_bounds__(kNT) dist_update_kernel(int64_t n, double* __r
     if (last_block(counter)) {
         const double t = reduce_partials<kNT>(partials, gridDim.x, sh);
         if (threadIdx.x == 0) {
+            st->alpha = alpha;
             st->rho_loc = t;
             *counter = 0;
         }
     }
 }
 
-// convergence test on the reduced rho (solvers.cpp:174-181)
-__global__ void converge_kernel(DistCgState* st, double* history) {
-    if (st->done) return;
-    const double rho_new = st->rho_new;
-    if (!isfinite(rho_new)) {
-        st->status = kDsNonFiniteRho;
-        st->x_pending = 1;
-        st->done = 1;
-        return;
-    }
-    const long long it = st->iter;
-    const double measure = rho_new / st->norm_r0;
-    if (history) history[it] = measure;
-    st->iter = it + 1;
-    st->rho_1 = st->rho;
-    st->beta = rho_new / st->rho;
-    st->rho = rho_new;
-    if (measure <= st->tol || it + 1 >= st->max_it) {
-        st->x_pending = 1;
-        st->done = 1;
-    }
-}
-
-// the deferred x += alpha p, then p = D^-1 r + beta p; after the iteration that ends the
-// solve only the x update runs, once (x_pending)
 __global__ void __launch_bounds__(kNT) dist_direction_kernel(int64_t n, double* __restrict__ p,
                                                               const double* __restrict__ r,
                                                               const double* __restrict__ inv, double* __restrict__ x,
-                                                              DistCgState* st, unsigned* counter) {
-    const int done = *(volatile const int*)&st->done;
-    if (done && !*(volatile const int*)&st->x_pending) return;
-    const double alpha = st->alpha, beta = st->beta;
-    if (done) {
+                                                              DistCgState* st, double* history, unsigned* counter) {
+    if (*(volatile const int*)&st->done) return;
+    const double rho_new = st->rho_new, rho = st->rho, alpha = st->alpha;
+    const long long it = st->iter;
+    const double measure = rho_new / st->norm_r0, beta = rho_new / rho;
+    const bool bad = !isfinite(rho_new);
+    const bool stop = bad || measure <= st->tol || it + 1 >= st->max_it;
+    if (stop) {  // the reference updated x before its rho test: only x += alpha p remains
         for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT)
             x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
-        if (last_block(counter) && threadIdx.x == 0) {
-            *counter = 0;
-            st->x_pending = 0;
+    } else {
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+            const double pi = p[i];
+            x[i] = __dadd_rn(__dmul_rn(alpha, pi), x[i]);
+            const double zi = inv ? __dmul_rn(r[i], inv[i]) : r[i];
+            p[i] = __dadd_rn(__dmul_rn(beta, pi), zi);
         }
-        return;
     }
-    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
-        const double pi = p[i];
-        x[i] = __dadd_rn(__dmul_rn(alpha, pi), x[i]);
-        const double zi = inv ? __dmul_rn(r[i], inv[i]) : r[i];
-        p[i] = __dadd_rn(__dmul_rn(beta, pi), zi);
+    if (last_block(counter) && threadIdx.x == 0) {
+        *counter = 0;
+        if (bad) {
+            st->status = kDsNonFiniteRho;
+            st->done = 1;
+            return;
+        }
+        if (history) history[it] = measure;
+        st->iter = it + 1;
+        st->rho_1 = rho;
+        st->beta = beta;
+        st->rho = rho_new;
+        if (stop) st->done = 1;
     }
 }
 
@@ -948,21 +936,17 @@ void dist_iteration(krysp_gpu_dist* d, cudaEvent_t ev_spmv_done = nullptr) {
     device_allreduce(d, offsetof(DistCgState, sigma_loc), offsetof(DistCgState, sigma), s);
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
-        alpha_kernel<<<1, 1, 0, s>>>(P.st);
-        KG_LAUNCH(c);
         const unsigned g = grid_for(P.n_local, kNT, (int64_t)c->sm_count * 8);
-        dist_update_kernel<<<g, kNT, 0, s>>>(P.n_local, P.x, P.r, P.p, P.ap, d->cfg.preconditioner ? (const double*)P.inv : nullptr,
+        dist_update_kernel<<<g, kNT, 0, s>>>(P.n_local, P.r, P.ap, d->cfg.preconditioner ? (const double*)P.inv : nullptr,
                                               P.st, c->d_partials + (4 + (i % 4)) * kPartialCap, c->d_counters + 4 + (i % 4));
         KG_LAUNCH(c);
     }
     device_allreduce(d, offsetof(DistCgState, rho_loc), offsetof(DistCgState, rho_new), s);
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
-        converge_kernel<<<1, 1, 0, s>>>(P.st, P.hist);
-        KG_LAUNCH(c);
         const unsigned g = grid_for(P.n_local, kNT, (int64_t)c->sm_count * 8);
         dist_direction_kernel<<<g, kNT, 0, s>>>(P.n_local, P.p, P.r, d->cfg.preconditioner ? (const double*)P.inv : nullptr,
-                                                 P.x, P.st, c->d_counters + 4 + (i % 4));
+                                                 P.x, P.st, P.hist, c->d_counters + 4 + (i % 4));
         KG_LAUNCH(c);
     }
     d->kernels_per_iteration = (int)(c->launches - before);
