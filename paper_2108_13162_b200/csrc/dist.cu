@@ -365,22 +365,38 @@ __global__ void sum_d2_partials(DistCgState* st, const double* a, int na, const 
     }
 }
 
-__global__ void db_alpha_kernel(DistCgState* st) {  // solvers.cpp:379-385
-    if (st->done) return;
+// The scalar steps of the reference are folded into the prologues of the vector passes: every
+// block derives the same scalars from the allreduced values, a failure is recorded by block 0
+// (all blocks return), and the last block to finish — after every other block has read the
+// state — writes it.
+__device__ __forceinline__ int db_alpha(const DistCgState* st, double& alpha) {  // solvers.cpp:379-385
     const double denom = red_val(st, 0);
-    if (!isfinite(denom)) return db_fail(st, kDbNonFiniteDenom);
-    if (fabs(denom) < 1e-300) return db_fail(st, kDbBreakdownDenom);
-    st->alpha = st->rho / denom;
-    if (!isfinite(st->alpha)) db_fail(st, kDsNonFiniteAlpha);
+    if (!isfinite(denom)) return kDbNonFiniteDenom;
+    if (fabs(denom) < 1e-300) return kDbBreakdownDenom;
+    alpha = st->rho / denom;
+    return isfinite(alpha) ? 0 : kDsNonFiniteAlpha;
 }
 
-// s = r - alpha v and ||s||^2 (solvers.cpp:387-389)
+__device__ __forceinline__ int db_omega(const DistCgState* st, double& omega) {  // solvers.cpp:400-408
+    const double tt = red_val(st, 0), ts = red_val(st, 1);
+    if (fabs(tt) < 1e-300) return kDbBreakdownTT;
+    omega = ts / tt;
+    if (!isfinite(omega)) return kDbNonFiniteOmega;
+    return fabs(omega) < 1e-300 ? kDbBreakdownOmega : 0;
+}
+
+// alpha; s = r - alpha v and ||s||^2 (solvers.cpp:379-389)
 __global__ void __launch_bounds__(kNT) db_s_kernel(int64_t n, double* __restrict__ s, const double* __restrict__ r,
                                                     const double* __restrict__ v, DistCgState* st, double* partials,
                                                     unsigned* counter) {
     if (*(volatile int*)&st->done) return;
+    double alpha = 0.0;
+    if (const int bad = db_alpha(st, alpha)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) db_fail(st, bad);
+        return;
+    }
     __shared__ D2 sh[32];
-    const double ma = -st->alpha;
+    const double ma = -alpha;
     D2 acc{0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
         const double si = __dadd_rn(__dmul_rn(ma, v[i]), r[i]);
@@ -395,6 +411,7 @@ __global__ void __launch_bounds__(kNT) db_s_kernel(int64_t n, double* __restrict
     if (last_block(counter)) {
         const D2 t = reduce_d2_partials(partials, gridDim.x, sh);
         if (threadIdx.x == 0) {
+            st->alpha = alpha;
             st->red_loc[0] = t.s;
             st->red_loc[1] = t.c;
             *counter = 0;
@@ -414,16 +431,7 @@ __global__ void db_half_kernel(DistCgState* st, double* history) {  // solvers.c
     }
 }
 
-__global__ void db_omega_kernel(DistCgState* st) {  // solvers.cpp:400-408
-    if (st->done) return;
-    const double tt = red_val(st, 0), ts = red_val(st, 1);
-    if (fabs(tt) < 1e-300) return db_fail(st, kDbBreakdownTT);
-    st->omega = ts / tt;
-    if (!isfinite(st->omega)) return db_fail(st, kDbNonFiniteOmega);
-    if (fabs(st->omega) < 1e-300) db_fail(st, kDbBreakdownOmega);
-}
-
-// x += alpha p; x += omega s; r = s - omega t; ||r||^2, <r^, r> (solvers.cpp:410-415)
+// omega; x += alpha p; x += omega s; r = s - omega t; ||r||^2, <r^, r> (solvers.cpp:400-415)
 __global__ void __launch_bounds__(kNT) db_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                                                          const double* __restrict__ p, const double* __restrict__ s,
                                                          const double* __restrict__ t, const double* __restrict__ rh,
@@ -440,8 +448,13 @@ __global__ void __launch_bounds__(kNT) db_update_kernel(int64_t n, double* __res
         }
         return;
     }
+    double om = 0.0;
+    if (const int bad = db_omega(st, om)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) db_fail(st, bad);
+        return;
+    }
     __shared__ D2 sh[32];
-    const double om = st->omega, mom = -om;
+    const double mom = -om;
     D2 a0{0.0, 0.0}, a1{0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
         const double si = s[i];
@@ -470,6 +483,7 @@ __global__ void __launch_bounds__(kNT) db_update_kernel(int64_t n, double* __res
         t0 = block_d2_dyn(t0, sh);
         t1 = block_d2_dyn(t1, sh);
         if (threadIdx.x == 0) {
+            st->omega = om;
             st->red_loc[0] = t0.s;
             st->red_loc[1] = t0.c;
             st->red_loc[2] = t1.s;
@@ -479,34 +493,44 @@ __global__ void __launch_bounds__(kNT) db_update_kernel(int64_t n, double* __res
     }
 }
 
-__global__ void db_converge_kernel(DistCgState* st, double* history) {  // solvers.cpp:415-432
-    if (st->done) return;
-    const double measure = sqrt(red_val(st, 0)) / st->norm_r0;
-    if (!isfinite(measure)) return db_fail(st, kDbNonFiniteMeasure);
-    const long long it = st->iter;
-    history[it] = measure;
-    st->iter = it + 1;
-    if (measure <= st->tol) {
-        st->done = 1;
-        return;
-    }
-    const double rho_new = red_val(st, 1);
-    if (fabs(rho_new) < 1e-300) return db_fail(st, kDbBreakdownRho);
-    const double beta = (rho_new / st->rho) * (st->alpha / st->omega);
-    if (!isfinite(beta)) return db_fail(st, kDbNonFiniteBeta);
-    st->beta = beta;
-    st->rho = rho_new;
-    if (it + 1 >= st->max_it) st->done = 1;
-}
-
+// the convergence test, beta (solvers.cpp:415-432); unless the solve ends here,
 // p = r + beta (p - omega v) (solvers.cpp:430-431)
 __global__ void __launch_bounds__(kNT) db_p_kernel(int64_t n, double* __restrict__ p, const double* __restrict__ r,
-                                                    const double* __restrict__ v, const DistCgState* st) {
+                                                    const double* __restrict__ v, DistCgState* st, double* history,
+                                                    unsigned* counter) {
     if (*(volatile const int*)&st->done) return;
-    const double mom = -st->omega, beta = st->beta;
-    for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
-        const double pi = __dadd_rn(__dmul_rn(mom, v[i]), p[i]);
-        p[i] = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(beta, pi));
+    const double measure = sqrt(red_val(st, 0)) / st->norm_r0;
+    if (!isfinite(measure)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) db_fail(st, kDbNonFiniteMeasure);
+        return;
+    }
+    const long long it = st->iter;
+    const double rho = st->rho, rho_new = red_val(st, 1), omega = st->omega;
+    const double beta = (rho_new / rho) * (st->alpha / omega);
+    int bad = 0;
+    bool stop = measure <= st->tol;
+    if (!stop) {
+        if (fabs(rho_new) < 1e-300) bad = kDbBreakdownRho;
+        else if (!isfinite(beta)) bad = kDbNonFiniteBeta;
+        stop = bad || it + 1 >= st->max_it;
+    }
+    if (!stop) {
+        const double mom = -omega;
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+            const double pi = __dadd_rn(__dmul_rn(mom, v[i]), p[i]);
+            p[i] = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(beta, pi));
+        }
+    }
+    if (last_block(counter) && threadIdx.x == 0) {
+        *counter = 0;
+        history[it] = measure;
+        st->iter = it + 1;
+        if (bad) return db_fail(st, bad);
+        if (measure > st->tol) {
+            st->beta = beta;
+            st->rho = rho_new;
+        }
+        if (stop) st->done = 1;
     }
 }
 
@@ -866,8 +890,6 @@ void dist_iteration_bicg(krysp_gpu_dist* d) {
     bi_spmv<1>(d, ps, vs, rhs, nul);  // v = op(p), <r^, v>
     for (size_t i = 0; i < np; ++i) {
         DistPart& P = d->parts[i];
-        db_alpha_kernel<<<1, 1, 0, s>>>(P.st);
-        KG_LAUNCH(c);
         db_s_kernel<<<g_of(P), kNT, 0, s>>>(P.n_local, P.sx, P.r, P.ap, P.st, c->d_partials + (4 + (i % 4)) * kPartialCap,
                                              c->d_counters + 4 + (i % 4));
         KG_LAUNCH(c);
@@ -880,8 +902,6 @@ void dist_iteration_bicg(krysp_gpu_dist* d) {
     bi_spmv<2>(d, ss, ts, nul, sws);  // t = op(s), <t, t>, <t, s>
     for (size_t i = 0; i < np; ++i) {
         DistPart& P = d->parts[i];
-        db_omega_kernel<<<1, 1, 0, s>>>(P.st);
-        KG_LAUNCH(c);
         db_update_kernel<<<g_of(P), kNT, 0, s>>>(P.n_local, P.x, P.r, P.p, P.sx, P.t, P.rh, P.st,
                                                   c->d_partials + (4 + (i % 4)) * kPartialCap, c->d_counters + 4 + (i % 4));
         KG_LAUNCH(c);
@@ -889,9 +909,7 @@ void dist_iteration_bicg(krysp_gpu_dist* d) {
     device_allreduce(d, offsetof(DistCgState, red_loc), offsetof(DistCgState, red), s, 4);
     for (size_t i = 0; i < np; ++i) {
         DistPart& P = d->parts[i];
-        db_converge_kernel<<<1, 1, 0, s>>>(P.st, P.hist);
-        KG_LAUNCH(c);
-        db_p_kernel<<<g_of(P), kNT, 0, s>>>(P.n_local, P.p, P.r, P.ap, P.st);
+        db_p_kernel<<<g_of(P), kNT, 0, s>>>(P.n_local, P.p, P.r, P.ap, P.st, P.hist, c->d_counters + 4 + (i % 4));
         KG_LAUNCH(c);
     }
     d->kernels_per_iteration = (int)(c->launches - before);

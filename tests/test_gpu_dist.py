@@ -246,6 +246,63 @@ def test_dist_breakdown_matches_reference(ctx, ref, mode):
             assert ei.value.code == want["status"] and str(ei.value) == want["error"], (s, str(ei.value), want)
 
 
+def _two_band(ctx, d):
+    D = DistSystem.emulated(ctx, 2)
+    D.set_csr(0, 4, kg.CsrMatrix(2, 4, np.array([0, 1, 2]), np.array([0, 1]), np.array(d[:2])))
+    D.set_csr(1, 4, kg.CsrMatrix(2, 4, np.array([0, 1, 2]), np.array([2, 3]), np.array(d[2:])))
+    D.setup()
+    return D
+
+
+@pytest.mark.parametrize("method", ["pcg", "bicgstab"])
+def test_fused_breakdown_matches_reference(ctx, ref, method):
+    """The fused partitioned solvers (scalar steps folded into the vector passes) report the
+    reference's error class and message on breakdown / non-finite values."""
+    d = [1., -1., 1., -1.]
+    rm = ref.from_csr(kg.CsrMatrix(4, 4, np.arange(5), np.arange(4), np.array(d)))
+    for rhs in ([1., 1., 1., 1.], [1., np.nan, 1., 1.]):
+        b = np.array(rhs)
+        want = ref.solve(rm, method, b, jacobi=False)
+        assert want["status"] != 0
+        D = _two_band(ctx, d)
+        with pytest.raises(kg.Error) as ei:  # at setup (non-finite b) or in the iteration
+            D.krylov_create(method, [ctx.to_device(v) for v in split(b, 4, 2)],
+                            [ctx.to_device(np.zeros(2)) for _ in range(2)],
+                            kg.SolverConfig(mode="fast", preconditioner="none"))
+            D.pcg_run()
+            D.pcg_report()
+        assert ei.value.code == want["status"] and str(ei.value) == want["error"], (method, rhs, str(ei.value))
+
+
+def test_fused_bicgstab_half_step_and_max_iterations(ctx, ref):
+    """Half-step convergence (s = 0 after the first BiCG step: x += alpha p only) and the
+    max-iteration stop of the fused partitioned BiCGStab, against the reference."""
+    d = [2., 3., 4., 5.]
+    rm = ref.from_csr(kg.CsrMatrix(4, 4, np.arange(5), np.arange(4), np.array(d)))
+    b = np.array(d)  # Jacobi: D^-1 A = I, D^-1 b = 1: alpha = 1 and s = 0 exactly
+    want = ref.solve(rm, "bicgstab", b)
+    assert want["iterations"] == 1 and want["converged"]
+    D = _two_band(ctx, d)
+    D.krylov_create("bicgstab", [ctx.to_device(v) for v in split(b, 4, 2)],
+                    [ctx.to_device(np.zeros(2)) for _ in range(2)], kg.SolverConfig(mode="fast"))
+    D.pcg_run()
+    rep = D.pcg_report()
+    assert rep.converged and rep.iterations == want["iterations"]
+    np.testing.assert_array_equal(np.concatenate([D.pcg_solution(p) for p in range(2)]), want["solution"])
+    np.testing.assert_array_equal(rep.residual_history, want["residual_history"])
+    # max-iteration stop: 7 iterations of a 20 x 20 convection-diffusion system
+    for method in ["pcg", "bicgstab"]:
+        D = DistSystem.emulated(ctx, 2)
+        D.generate("convdiff2d" if method == "bicgstab" else "poisson2d", 20, 0.5)
+        D.setup()
+        D.krylov_create(method, [ctx.to_device(np.ones(200)) for _ in range(2)],
+                        [ctx.to_device(np.zeros(200)) for _ in range(2)],
+                        kg.SolverConfig(mode="fast", max_iterations=7))
+        D.pcg_run()
+        rep = D.pcg_report()
+        assert not rep.converged and rep.iterations == 7 and len(rep.residual_history) == 7
+
+
 _WATCH_SCRIPT = r"""
 import sys
 import numpy as np
