@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Internal header of libkrysp_gpu.so (sm_100a).  Not installed; the public surface is
 // include/krysp_gpu.h.
 #pragma once
@@ -228,6 +229,33 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // last.  Partials written before the call are visible to that block.
 // Only thread 0 may have written the block's partials (the callers' convention), so only
 // it needs the release fence before arriving.
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl() may start while
+// its predecessor drains; pdl_wait() blocks until the predecessor grid has completed and its
+// writes are visible (a no-op for a normally launched kernel); pdl_trigger() lets the successor
+// launch early (a no-op when the successor is not launched with PDL).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("KRYSP_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ bool last_block(unsigned* counter) {
     __shared__ bool s_last;
     __syncthreads();

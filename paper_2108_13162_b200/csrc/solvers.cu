@@ -562,6 +562,8 @@ __global__ void __launch_bounds__(kFusedNT) cg_update_kernel(int64_t n, double* 
                                                               const double* __restrict__ inv, CgState* st,
                                                               double* partials, unsigned* counter,
                                                               double* history, double* trace) {
+    pdl_wait();
+    pdl_trigger();
     if (*(volatile int*)&st->done) return;
     __shared__ double sh[32];
     const double alpha = st->alpha, malpha = -alpha;
@@ -616,6 +618,7 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
                                                                  const double* __restrict__ inv,
                                                                  double* __restrict__ x, CgState* st,
                                                                  unsigned* counter) {
+    pdl_wait();
     const int done = *(volatile const int*)&st->done;
     if (done && !*(volatile const int*)&st->x_pending) return;
     const double alpha = st->alpha, beta = st->beta;
@@ -1804,15 +1807,16 @@ struct PcgSession {
         EpiCgSigma epi{ap, p, part_a, cnt_a, st, 0.0};
         spmv_fused(e, p, ap, epi);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
-        if (e.jacobi)
-            cg_update_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, x, r, p, ap, e.inv, st, part_b, cnt_b, hist, d_trace);
-        else
-            cg_update_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, x, r, p, ap, nullptr, st, part_b, cnt_b, hist, d_trace);
+        // update and direction passes by programmatic dependent launch: each grid is resident
+        // while its predecessor's tail drains and waits in pdl_wait() for its results
+        KG_CUDA(launch_pdl(e.jacobi ? cg_update_kernel<true> : cg_update_kernel<false>, g_vec, kFusedNT, c->stream,
+                           n, (double*)x, (double*)r, (const double*)p, (const double*)ap, (e.jacobi ? (const double*)e.inv : nullptr),
+                           st, part_b, cnt_b, hist, d_trace));
         KG_LAUNCH(c);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
         unsigned* cnt_c = c->d_counters + 5;
-        if (e.jacobi) cg_direction_kernel<true><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, e.inv, x, st, cnt_c);
-        else cg_direction_kernel<false><<<g_vec, kFusedNT, 0, c->stream>>>(n, p, r, nullptr, x, st, cnt_c);
+        KG_CUDA(launch_pdl(e.jacobi ? cg_direction_kernel<true> : cg_direction_kernel<false>, g_vec, kFusedNT,
+                           c->stream, n, (double*)p, (const double*)r, (e.jacobi ? (const double*)e.inv : nullptr), (double*)x, st, cnt_c));
         KG_LAUNCH(c);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[3], c->stream, cudaEventRecordExternal));
         kernels_per_iteration = (int)(c->launches - before);

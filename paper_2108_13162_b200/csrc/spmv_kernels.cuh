@@ -67,6 +67,7 @@ struct epi_is_store<EpiStoreGated<G>> : std::true_type {};
 // blockDim.x / TW rows each.  Every lane participates in the shuffles.
 template <int TW, class Epi>
 __global__ void csr_vector_kernel(CsrView A, const double* __restrict__ x, Epi epi, int64_t n_vblocks) {
+    pdl_trigger();
     if (!epi.active()) return;
     const int lane = threadIdx.x & (TW - 1);
     for (int64_t vb = blockIdx.x; vb < n_vblocks; vb += gridDim.x) {
@@ -156,6 +157,7 @@ struct epi_staged<E, std::void_t<decltype(E::kStaged)>> {
 template <int TW, class Epi>
 __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const double* __restrict__ x, Epi epi,
                                                             TmaTileLayout L) {
+    pdl_trigger();
     if (!epi.active()) return;
     constexpr int TR = kTileRows / TW;
     extern __shared__ __align__(128) unsigned char smem_tma[];
@@ -267,6 +269,7 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
 // Thread per row, column-major slab => every slot load is a coalesced 32-lane stream.
 template <class Epi, int KB>
 __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
+    pdl_trigger();
     if (!epi.active()) return;
     const int64_t n = E.n_rows, ld = E.ld;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r - threadIdx.x < n;
