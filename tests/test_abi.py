@@ -3,6 +3,7 @@ host-only entry points (grid arithmetic, policies, host generators) match the or
 import ctypes as C
 import os
 import re
+import subprocess
 
 import numpy as np
 import pytest
@@ -97,3 +98,21 @@ def test_no_gpu_context_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(kg.Error):
         kg.Context(0)
+
+
+def test_reference_typed_binding_compiles_against_reference_headers(tmp_path):
+    """include/krysp_gpu_ref.hpp takes the reference's own types: it must compile inside the
+    reference tree (-I proj/include) and its symbols must be the reference's signatures."""
+    inc = "/root/reference/proj/include"
+    if not os.path.isdir(inc):
+        pytest.skip("reference headers absent (GPU box)")
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "krysp_gpu_ref.hpp"\n'
+                   "using namespace krysp;\n"
+                   "static_assert(std::is_same_v<decltype(gpu::solve_bicgstab(std::declval<const SparseMatrix&>(),\n"
+                   "    std::span<const double>{}, std::span<const double>{}, SolverConfig{})), SolveReport>);\n"
+                   "static_assert(std::is_same_v<decltype(gpu::csr_to_hyb(std::declval<const CsrMatrix&>())), HybMatrix>);\n"
+                   "static_assert(std::is_base_of_v<Error, gpu::CudaError>);\n"
+                   "int main() { return 0; }\n")
+    subprocess.check_call(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Werror", "-I", inc, "-I",
+                           os.path.join(ROOT, "include"), str(src)])
