@@ -225,15 +225,14 @@ def oracle_csr(n):
     return Port().generate("lap3d7", n)
 
 
-def config_block(args, dist, extra=None):
-    c = {"workload": f"C3: P-CG + Jacobi, 3D 7-point Laplacian {args.n}^3 "
-                     f"({args.n ** 3:,} rows), {args.format.upper()}, FP64, b=1, x0=0, tol 1e-6",
-         "matrix": f"lap3d7 n={args.n}", "format": args.format, "solver": "pcg", "preconditioner": "jacobi",
-         "parallelism": f"replicas{dist.world}" if dist.world > 1 else "single-gpu",
-         "l2": "inputs larger than L2 (12.3 GB touched per iteration vs 126 MB L2)"}
-    if extra:
-        c.update(extra)
-    return c
+def config_block(args):
+    """The workload, identical in both arms (how each arm runs it goes under "arm")."""
+    n = args.n
+    return {"workload": f"C3: P-CG + Jacobi, 3D 7-point Laplacian {n}^3 "
+                        f"({n ** 3:,} rows), {args.format.upper()}, FP64, b=1, x0=0, tol 1e-6",
+            "matrix": f"lap3d7 n={n}", "format": args.format, "solver": "pcg", "preconditioner": "jacobi",
+            "rows": n ** 3, "nnz": 7 * n ** 3 - 6 * n ** 2,
+            "l2": "inputs larger than L2 (12.3 GB touched per iteration vs 126 MB L2)"}
 
 
 def run_reference(args, dist):
@@ -248,9 +247,9 @@ def run_reference(args, dist):
             "ms_per_step": 1e3 / r["value"] if r["value"] else None, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic 3D 7-point Laplacian)",
-            "config": config_block(args, dist, {"policy": "<1024,1> (reference tuned winner, SURVEY §6)",
-                                                "parallelism": f"reference solve_pcg on {ncores} host threads "
-                                                               "(rank 0 only)"}),
+            "config": config_block(args),
+            "arm": {"policy": "<1024,1> (reference tuned winner, SURVEY §6)",
+                    "parallelism": f"reference solve_pcg on {ncores} host threads (rank 0 only)"},
             "cpu_baseline": {"value": r["value"], "unit": "iterations/s", "cores": r["cores"], "kind": r["kind"],
                              "sample": f"{r['iterations']} P-CG iterations of the full 400^3 problem "
                                        f"(solve_pcg max_iterations {args.warmup}+{args.steps} minus "
@@ -319,8 +318,8 @@ def run_ours(args, dist):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic 3D 7-point Laplacian, generated on device)",
-            "config": config_block(args, dist, {"policy": "auto (FAST mode)", "mode": "fast", "step": STEP_NOTE,
-                                                "nnz": nnz, "rows": n}),
+            "config": config_block(args),
+            "arm": {"policy": "auto (FAST mode)", "mode": "fast", "parallelism": "single-gpu", "step": STEP_NOTE},
             "roofline": {"bound": "hbm", "kernel": f"spmv_{args.format} + fused <p,Ap>",
                          "achieved": achieved, "peak": bw_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / bw_peak, "frac_of_nominal_8tbs": achieved / 8000.0,
@@ -444,18 +443,26 @@ def run_ours_dist(args, dist):
     t_bi = dist.max(D.pcg_time(bi_steps))
     bi_ran = D.pcg_report().iterations
     bi_kpi = D.kernels_per_iteration
-    # e2e: a whole partitioned solve from pinned host b / x0 to the host solution
+    # e2e, the same thing as at N = 1: each rank's band CSR (int64, as the reference holds it),
+    # b and x0 from pinned host memory, uploaded inside the timed call; band build + halo plan,
+    # FAST P-CG to convergence, the solution band back to the host
     import torch
+    lo, hi = info["lo"], info["hi"]
+    hband = kg.generate_csr_rows("lap3d7", args.n, lo, hi, pinned=True)
     hb = torch.ones(n_loc, dtype=torch.float64, pin_memory=True).numpy()
     hx0 = torch.zeros(n_loc, dtype=torch.float64, pin_memory=True).numpy()
     dist.barrier()
+    ctx.sync()
     t0 = time.perf_counter()
+    D.set_csr(dist.rank, N, hband)
+    D.setup()
     db, dx0 = ctx.to_device(hb), ctx.to_device(hx0)
     D.pcg_create([db], [dx0], kg.SolverConfig(mode="fast", tolerance=1e-6, max_iterations=30000))
     D.pcg_run()
     e2e_rep = D.pcg_report()
     sol = D.pcg_solution(dist.rank)
     e2e_s = dist.max(time.perf_counter() - t0)
+    h2d_e2e = int(hband.row_ptr.nbytes + hband.col_idx.nbytes + hband.values.nbytes + hb.nbytes + hx0.nbytes)
     fin = e2e_rep  # the converged solve is the parity check (same problem as the single-GPU golden)
     D.close()
     nnz_total = 7 * N - 6 * args.n ** 2
@@ -466,12 +473,10 @@ def run_ours_dist(args, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_it, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic 3D 7-point Laplacian, each band generated on its GPU)",
-            "config": {"workload": f"C3: P-CG + Jacobi, 3D 7-point Laplacian {args.n}^3 ({N:,} rows) row-partitioned "
-                                   f"over {dist.world} GPUs, CSR, FP64, b=1, x0=0, tol 1e-6",
-                       "matrix": f"lap3d7 n={args.n}", "format": "csr", "solver": "pcg", "mode": "fast",
-                       "parallelism": f"band-rows{dist.world} (NCCL x-halo overlapped with interior SpMV, "
-                                      "NCCL allreduce of the 2 scalars)",
-                       "l2": "inputs larger than L2", "rows_per_gpu": n_loc, "step": STEP_NOTE},
+            "config": config_block(args),
+            "arm": {"policy": "auto (FAST mode)", "mode": "fast", "step": STEP_NOTE, "rows_per_gpu": n_loc,
+                    "parallelism": f"band-rows{dist.world}: the 400^3 problem row-partitioned over {dist.world} GPUs "
+                                   "(NCCL x-halo overlapped with the interior-row SpMV, NCCL allreduce of the scalars)"},
             "roofline": {"bound": "hbm", "kernel": "whole P-CG iteration per GPU (B_iter / N)",
                          "achieved": B_iter_gpu / t_it / 1e9, "peak": bw_peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": B_iter_gpu / t_it / 1e9 / bw_peak, "traffic": None},
@@ -487,9 +492,10 @@ def run_ours_dist(args, dist):
                          "what": "row-partitioned FAST BiCGStab (2 halo-overlapped SpMVs, 3 NCCL allreduces "
                                  "/ iteration, CUDA graphs), CUDA events, max over ranks"},
             "e2e": {"value": e2e_rep.iterations / e2e_s, "unit": "iterations/s",
-                    "h2d_bytes_per_step": int(hb.nbytes + hx0.nbytes), "d2h_bytes_per_step": int(sol.nbytes),
-                    "what": "krysp_gpu_dist_pcg_create/run/solution from pinned host b, x0 to the host solution "
-                            "(per rank; the band matrix stays device-resident, generated on its GPU)",
+                    "h2d_bytes_per_step": h2d_e2e, "d2h_bytes_per_step": int(sol.nbytes),
+                    "what": "per rank: krysp_gpu_dist_set_csr (pinned int64 band CSR upload + device build), "
+                            "_setup (halo plan), _pcg_create/_run (FAST P-CG to convergence), _pcg_solution "
+                            "(band of the solution to the host); bytes are rank 0's",
                     "seconds_per_step": e2e_s},
             "parity": {"iterations": fin.iterations, "golden_iterations": GOLDEN_ITERS if args.n == 400 else None,
                        "final_residual_measure": fin.final_residual_measure,
@@ -505,6 +511,12 @@ def main():
     sys.stdout.flush()
     json_fd = os.dup(1)
     os.dup2(2, 1)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":
+        # a rank mismatch or deadlock fails in minutes, not at the driver's limit; NCCL's INIT
+        # lines (nranks, NVLS/P2P transport) go to stderr for the record
+        os.environ.setdefault("KRYSP_NCCL_TIMEOUT_S", "120")
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
     dist = Dist()
     try:
         if args.impl == "reference":

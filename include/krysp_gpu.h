@@ -180,12 +180,18 @@ krysp_status krysp_gpu_gen_nnz(const char* kind, int64_t n, double pe, double al
 krysp_status krysp_gpu_gen_csr_host(const char* kind, int64_t n, double pe, double alpha,
                                     uint64_t seed, int64_t* row_ptr, int64_t* col_idx,
                                     double* values);
+/* Rows [row_lo, row_hi) of a stencil generator (not powerlaw): local row_ptr (row_ptr[0] = 0,
+ * row_hi - row_lo + 1 entries), global column indices — the band one rank of the band-row
+ * partition (substructure.cpp:20-31) holds.  col_idx = values = NULL: fill row_ptr only (sizing). */
+krysp_status krysp_gpu_gen_csr_rows_host(const char* kind, int64_t n, double pe, int64_t row_lo,
+                                         int64_t row_hi, int64_t* row_ptr, int64_t* col_idx,
+                                         double* values);
 /* convert formats.cpp:273-286 / csr_to_ell :80-104 (slot_cap, EllBlowup) /
  * csr_to_hyb :123-153 (hyb_width -1 = auto ⅔ rule :109-119) / csr_to_coo :65-78 /
  * ell_to_csr :155-182 / hyb_to_csr :184-202 — all on device, bit-exact. */
 krysp_status krysp_gpu_mat_convert(const krysp_gpu_mat* m, int32_t format, int64_t hyb_width,
                                    int64_t slot_cap, krysp_gpu_mat** out);
-/* csr_transpose formats.cpp:312-334 (device stable counting sort) */
+/* csr_transpose formats.cpp:312-334 (device stable sort by column: CUB DeviceRadixSort) */
 krysp_status krysp_gpu_mat_transpose(const krysp_gpu_mat* m, krysp_gpu_mat** out);
 krysp_status krysp_gpu_mat_info(const krysp_gpu_mat* m, krysp_mat_info* info);
 /* Downloads widen int32 back to int64 (ELL padding = sentinel n_cols, formats.hpp:45). */
@@ -319,7 +325,8 @@ krysp_status krysp_gpu_dist_destroy(krysp_gpu_dist* d);
 
 /* ------------------------------------------------------------------ matrix_market.hpp / build_coo */
 /* build_coo (formats.cpp:17-47) on the device: range check (IndexOutOfRange names the first
- * offending triple), stable radix sort by (row, col), duplicates summed in input order.
+ * offending triple), stable radix sort by (row, col) (CUB DeviceRadixSort), duplicates summed in
+ * input order.
  * format: KRYSP_FMT_COO (canonical COO) or KRYSP_FMT_CSR (coo_to_csr). */
 krysp_status krysp_gpu_mat_build_coo(krysp_gpu_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
                                      const int64_t* row_idx, const int64_t* col_idx, const double* values,

@@ -132,6 +132,7 @@ EXPORTS = [
     "krysp_gpu_launch_count", "krysp_gpu_grid_spmv_blocks", "krysp_gpu_grid_vector_blocks",
     "krysp_gpu_compute_grid", "krysp_gpu_validate_policy", "krysp_gpu_mat_upload_csr",
     "krysp_gpu_mat_upload_coo", "krysp_gpu_mat_generate", "krysp_gpu_gen_nnz", "krysp_gpu_gen_csr_host",
+    "krysp_gpu_gen_csr_rows_host",
     "krysp_gpu_mat_convert", "krysp_gpu_mat_transpose", "krysp_gpu_mat_info", "krysp_gpu_mat_download_csr",
     "krysp_gpu_mat_download_ell", "krysp_gpu_mat_download_coo", "krysp_gpu_mat_destroy", "krysp_gpu_mat_stats",
     "krysp_gpu_spmv", "krysp_gpu_spmv_host", "krysp_gpu_daxpy", "krysp_gpu_scal_elementwise", "krysp_gpu_copy",
@@ -183,6 +184,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.krysp_gpu_mat_generate.argtypes = [P, C.c_char_p, I64, D, C.POINTER(P)]
     L.krysp_gpu_gen_nnz.argtypes = [C.c_char_p, I64, D, D, C.c_uint64, C.POINTER(I64), C.POINTER(I64)]
     L.krysp_gpu_gen_csr_host.argtypes = [C.c_char_p, I64, D, D, C.c_uint64, P, P, P]
+    L.krysp_gpu_gen_csr_rows_host.argtypes = [C.c_char_p, I64, D, I64, I64, P, P, P]
     L.krysp_gpu_mat_convert.argtypes = [P, I32, I64, I64, C.POINTER(P)]
     L.krysp_gpu_mat_upload_csr.argtypes = [P, I64, I64, P, P, P, C.POINTER(P)]
     L.krysp_gpu_mat_upload_coo.argtypes = [P, I64, I64, I64, P, P, P, C.POINTER(P)]

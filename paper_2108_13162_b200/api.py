@@ -224,6 +224,27 @@ def generate_csr(kind: str, n: int, pe: float = 0.5, alpha: float = 2.0, seed: i
     return CsrMatrix(nr.value, nr.value, rp, ci, va)
 
 
+def generate_csr_rows(kind: str, n: int, lo: int, hi: int, pe: float = 0.5, pinned: bool = False) -> CsrMatrix:
+    """Rows [lo, hi) of a stencil generator as a band CSR (local row_ptr, global columns):
+    what one rank of the band-row partition holds, built without the rest of the matrix."""
+    L = _lib.load()
+    nr, tot = C.c_int64(), C.c_int64()
+    check(L.krysp_gpu_gen_nnz(kind.encode(), n, pe, 2.0, 2108, C.byref(nr), C.byref(tot)))
+    m = hi - lo
+
+    def buf(k, dt):
+        if pinned:
+            import torch
+            return torch.empty(k, dtype=torch.int64 if dt == np.int64 else torch.float64, pin_memory=True).numpy()
+        return np.empty(k, dt)
+    rp = buf(m + 1, np.int64)
+    check(L.krysp_gpu_gen_csr_rows_host(kind.encode(), n, pe, lo, hi, _p(rp), None, None))
+    nnz = int(rp[-1])
+    ci, va = buf(nnz, np.int64), buf(nnz, np.float64)
+    check(L.krysp_gpu_gen_csr_rows_host(kind.encode(), n, pe, lo, hi, _p(rp), _p(ci), _p(va)))
+    return CsrMatrix(m, nr.value, rp, ci, va)
+
+
 # ----------------------------------------------------------------------------- device objects
 class Context:
     """One device: stream + reduction scratch (krysp_gpu_ctx)."""

@@ -45,6 +45,7 @@ krysp_gpu_mat* upload_coo(krysp_gpu_ctx*, int64_t, int64_t, int64_t, const int64
 krysp_gpu_mat* generate(krysp_gpu_ctx*, const char*, int64_t, double);
 void gen_nnz_host(const char*, int64_t, double, double, uint64_t, int64_t*, int64_t*);
 void gen_csr_host(const char*, int64_t, double, double, uint64_t, int64_t*, int64_t*, double*);
+void gen_csr_rows_host(const char*, int64_t, double, int64_t, int64_t, int64_t*, int64_t*, double*);
 krysp_gpu_mat* convert(const krysp_gpu_mat*, int32_t, int64_t, int64_t);
 krysp_gpu_mat* transpose(const krysp_gpu_mat*);
 void download_csr(const krysp_gpu_mat*, int64_t*, int64_t*, double*);
@@ -242,6 +243,15 @@ krysp_status krysp_gpu_gen_csr_host(const char* kind, int64_t n, double pe, doub
     return guard([&] {
         need(kind, "kind");
         gen_csr_host(kind, n, pe, alpha, seed, rp, ci, cv);
+    });
+}
+
+krysp_status krysp_gpu_gen_csr_rows_host(const char* kind, int64_t n, double pe, int64_t row_lo, int64_t row_hi,
+                                         int64_t* rp, int64_t* ci, double* cv) {
+    return guard([&] {
+        need(kind, "kind");
+        need(rp, "row_ptr");
+        gen_csr_rows_host(kind, n, pe, row_lo, row_hi, rp, ci, cv);
     });
 }
 

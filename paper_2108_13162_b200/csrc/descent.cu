@@ -162,8 +162,9 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
         s0.tol = cfg.tolerance;
         s0.max_it = cfg.max_iterations;
     }
-    SubCgState* d_st = dev_alloc<SubCgState>((int64_t)nh, false);
-    double* d_hist = dev_alloc<double>((int64_t)nh * cfg.max_iterations, false);
+    DevBuf<SubCgState> d_st((int64_t)nh, false);
+    DevBuf<double> d_hist;
+    d_hist.p = dev_alloc_records<double>((int64_t)nh * cfg.max_iterations, st);
     KG_CUDA(cudaMemcpyAsync(d_st, init.data(), sizeof(SubCgState) * nh, cudaMemcpyHostToDevice, st));
     auto grid = [&](int64_t n) { return grid_for(n, kDcNT, (int64_t)c->sm_count * 8); };
     auto slot = [&](size_t i) { return c->d_partials + (int64_t)i * kPartialCap; };
@@ -174,7 +175,7 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
             KG_LAUNCH(c);
             return;
         }
-        char* base = reinterpret_cast<char*>(d_st);
+        char* base = reinterpret_cast<char*>(d_st.p);
         KG_NCCL(NcclApi::get().AllReduce(base + offsetof(SubCgState, red_loc), base + offsetof(SubCgState, red), 4,
                                          ncclDouble, ncclSum, (ncclComm_t)comm, st));
     };
@@ -238,6 +239,19 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
         err = std::current_exception();
     }
     if (exec) cudaGraphExecDestroy(exec);
+    if (err) {
+        // best effort: the state as far as it got, without masking the original error
+        SubCgState fin{};
+        if (cudaMemcpyAsync(&fin, d_st, sizeof fin, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+            cudaStreamSynchronize(st) == cudaSuccess && fin.iter > 0 && fin.iter <= cfg.max_iterations) {
+            iterations = fin.iter;
+            history.resize((size_t)fin.iter);
+            if (cudaMemcpy(history.data(), d_hist, 8 * (size_t)fin.iter, cudaMemcpyDeviceToHost) != cudaSuccess)
+                history.clear();
+        }
+        cudaGetLastError();
+        std::rethrow_exception(err);
+    }
     SubCgState fin;
     KG_CUDA(cudaMemcpyAsync(&fin, d_st, sizeof fin, cudaMemcpyDeviceToHost, st));
     kg::wait_stream(c, st);
@@ -245,9 +259,6 @@ int fused_descent(krysp_gpu_ctx* c, const std::vector<DescentPart>& parts, const
     history.resize((size_t)fin.iter);
     if (fin.iter) KG_CUDA(cudaMemcpy(history.data(), d_hist, 8 * (size_t)fin.iter, cudaMemcpyDeviceToHost));
     if (fin.iter) measure = fin.measure;
-    dev_free(d_st);
-    dev_free(d_hist);
-    if (err) std::rethrow_exception(err);
     return fin.status;
 }
 

@@ -109,7 +109,6 @@ struct DistPart {
 namespace {
 
 constexpr int kNT = 256;
-const double kZero = 0.0, kOne = 1.0;
 
 __global__ void count_ghosts(CsrView A, int64_t lo, int64_t hi, unsigned long long* cnt) {
     unsigned long long local = 0;
@@ -1031,7 +1030,7 @@ void krylov_create(krysp_gpu_dist* d, int method, const double* const* bs, const
     cudaStream_t s = c->stream;
     d->cfg = cfg;
     std::vector<double*> xs, dots;
-    double* d_dot = dev_alloc<double>((int64_t)d->parts.size() * 2, true, s);
+    DevBuf<double> d_dot((int64_t)d->parts.size() * 2, true, s);
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
         P.x = DVec(P.n_local, s);
@@ -1044,41 +1043,42 @@ void krylov_create(krysp_gpu_dist* d, int method, const double* const* bs, const
             P.t = DVec(P.n_local, s);
         }
         P.part_slot = dev_alloc<double>(3 * (int64_t)kPartialCap, true, s);
-        P.hist = dev_alloc<double>(cfg.max_iterations, true, s);
+        P.hist = dev_alloc_records<double>(cfg.max_iterations, s);
         P.st = dev_alloc<DistCgState>(1, true, s);
         if (P.n_local) KG_CUDA(cudaMemcpyAsync(P.p, x0s[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, s));
         if (P.n_local) KG_CUDA(cudaMemcpyAsync(P.x, x0s[i], 8 * P.n_local, cudaMemcpyDeviceToDevice, s));
         xs.push_back(P.p);
         dots.push_back(d_dot + 2 * i);
     }
-    // Jacobi first (zero diagonal anywhere -> Breakdown on every rank)
-    int* zr = dev_alloc<int>((int64_t)d->parts.size(), false);
-    for (size_t i = 0; i < d->parts.size(); ++i) {
-        DistPart& P = d->parts[i];
-        if (cfg.preconditioner) {
+    // Jacobi first: a zero diagonal anywhere stops every rank with Breakdown naming the same
+    // (global, smallest) row, the reference's message (solvers.cpp:106-109)
+    if (cfg.preconditioner) {
+        DevBuf<int> zr((int64_t)d->parts.size(), false);
+        std::vector<int> big(d->parts.size(), INT32_MAX), hz(d->parts.size());
+        KG_CUDA(cudaMemcpyAsync(zr, big.data(), 4 * big.size(), cudaMemcpyHostToDevice, s));
+        for (size_t i = 0; i < d->parts.size(); ++i) {
+            DistPart& P = d->parts[i];
             P.inv = DVec(P.n_local, s);
             krysp_gpu_mat v = *P.A;
             v.n_cols = P.n_local;  // diagonal of the owned block
             k_diagonal(&v, P.inv);
-            int big = INT32_MAX;
-            KG_CUDA(cudaMemcpyAsync(zr + i, &big, 4, cudaMemcpyHostToDevice, s));
             k_invert_diag(c, P.n_local, P.inv, zr + i);
         }
-    }
-    std::vector<int> hz(d->parts.size(), INT32_MAX);
-    if (cfg.preconditioner) {
         KG_CUDA(cudaMemcpyAsync(hz.data(), zr, 4 * hz.size(), cudaMemcpyDeviceToHost, s));
         kg::wait_stream(c, s);
-    }
-    for (size_t i = 0; i < d->parts.size(); ++i)
-        KG_CUDA(cudaMemcpyAsync(d_dot + 2 * i + 1, hz[i] == INT32_MAX ? &kZero : &kOne, 8, cudaMemcpyHostToDevice, s));
-    std::vector<double*> zflags;
-    for (size_t i = 0; i < d->parts.size(); ++i) zflags.push_back(d_dot + 2 * i + 1);
-    const double n_zero = allreduce_host(d, zflags);
-    dev_free(zr);
-    if (n_zero > 0.0) {
-        dev_free(d_dot);
-        fail(KRYSP_BREAKDOWN, "zero diagonal entry; Jacobi preconditioner undefined");
+        double bad = (double)INT64_MAX;
+        for (size_t i = 0; i < d->parts.size(); ++i)
+            if (hz[i] != INT32_MAX) bad = std::min(bad, (double)(d->parts[i].lo + hz[i]));
+        if (!d->emulated() && d->nparts > 1) {
+            c->h_pinned[0] = bad;
+            KG_CUDA(cudaMemcpyAsync(c->d_scalars, c->h_pinned, 8, cudaMemcpyHostToDevice, s));
+            KG_NCCL(NcclApi::get().AllReduce(c->d_scalars, c->d_scalars, 1, ncclDouble, ncclMin, d->comm, s));
+            KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, 8, cudaMemcpyDeviceToHost, s));
+            kg::wait_stream(c, s);
+            bad = c->h_pinned[0];
+        }
+        if (bad < (double)INT64_MAX)
+            fail(KRYSP_BREAKDOWN, "zero diagonal entry at row %lld; Jacobi preconditioner undefined", (long long)bad);
     }
     // r = b - A x0 (spmv, scale(-1), daxpy(1, b)) with a halo of x0
     halo(d, xs, s);
@@ -1119,7 +1119,6 @@ void krylov_create(krysp_gpu_dist* d, int method, const double* const* bs, const
             rho = allreduce_host(d, dots);
         }
     }
-    dev_free(d_dot);
     h.rho = rho;
     h.norm_r0 = norm_r0;
     h.tol = cfg.tolerance;

@@ -865,6 +865,28 @@ void gen_csr_host(const char* kind, int64_t n, double pe, double alpha, uint64_t
     });
 }
 
+// rows [lo, hi) of a stencil generator: local row_ptr (rp[0] = 0), global columns — one band of
+// band_row_assignment (substructure.cpp:20-31) as a rank would hold it; nnz = rp[hi - lo]
+void gen_csr_rows_host(const char* kind, int64_t n, double pe, int64_t lo, int64_t hi, int64_t* rp, int64_t* ci,
+                       double* cv) {
+    int k = kind_id(kind);
+    if (k == 5) fail(KRYSP_ERROR, "gen_csr_rows: powerlaw rows depend on every earlier row (use gen_csr_host)");
+    if (n < 2) fail(KRYSP_ERROR, "generator needs n >= 2");
+    const int64_t dim = kind_dim(k, n);
+    if (lo < 0 || hi < lo || hi > dim) fail(KRYSP_INDEX_OUT_OF_RANGE, "row range [%lld, %lld) outside [0, %lld)",
+                                            (long long)lo, (long long)hi, (long long)dim);
+    const int64_t m = hi - lo;
+    parallel_rows(m, [&](int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; ++r) rp[r + 1] = host_row(k, n, pe, lo + r, nullptr, nullptr);
+    });
+    rp[0] = 0;
+    for (int64_t r = 0; r < m; ++r) rp[r + 1] += rp[r];
+    if (!ci) return;  // sizing pass
+    parallel_rows(m, [&](int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; ++r) host_row(k, n, pe, lo + r, ci + rp[r], cv + rp[r]);
+    });
+}
+
 // ------------------------------------------------------------------ conversions (public)
 static krysp_gpu_mat* csr_to_coo(const krysp_gpu_mat* a) {
     krysp_gpu_ctx* c = a->ctx;

@@ -1,4 +1,3 @@
-#include <cstdlib>
 // Internal header of libkrysp_gpu.so (sm_100a).  Not installed; the public surface is
 // include/krysp_gpu.h.
 #pragma once
@@ -10,6 +9,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <exception>
 #include <stdexcept>
 #include <string>
@@ -175,6 +175,32 @@ T* dev_alloc(int64_t count, bool zero = true, cudaStream_t s = nullptr) {
     return p;
 }
 
+// Per-iteration record buffers of the device-resident solvers (residual history, P-CG trace)
+// are sized by cfg.max_iterations up front, because the kernels write them without a host
+// round trip.  A max_iterations whose records would not fit the device fails here with a
+// clear message instead of a CUDA out-of-memory from deep inside the setup.
+template <typename T>
+T* dev_alloc_records(int64_t count, cudaStream_t s) {
+    size_t free_b = 0, total_b = 0;
+    const size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && bytes > free_b / 4)
+        fail(KRYSP_ERROR, "max_iterations = %lld needs %.2f GB of device iteration records (%.2f GB free); "
+             "lower max_iterations", (long long)count, bytes / 1e9, free_b / 1e9);
+    return dev_alloc<T>(count, true, s);
+}
+
+// RAII owner of one dev_alloc block: setup scratch that must not leak when a call throws
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    DevBuf() = default;
+    explicit DevBuf(int64_t count, bool zero = true, cudaStream_t s = nullptr) : p(dev_alloc<T>(count, zero, s)) {}
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { dev_free(p); }
+    operator T*() const { return p; }
+};
+
 // RAII device vector of doubles
 struct DVec {
     double* p = nullptr;
@@ -225,10 +251,6 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return r;
 }
 
-// Arrival on a grid-wide counter; returns true in every thread of the block that arrives
-// last.  Partials written before the call are visible to that block.
-// Only thread 0 may have written the block's partials (the callers' convention), so only
-// it needs the release fence before arriving.
 // Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl() may start while
 // its predecessor drains; pdl_wait() blocks until the predecessor grid has completed and its
 // writes are visible (a no-op for a normally launched kernel); pdl_trigger() lets the successor
@@ -258,6 +280,10 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// Arrival on a grid-wide counter; returns true in every thread of the block that arrives
+// last.  Partials written before the call are visible to that block.
+// Only thread 0 may have written the block's partials (the callers' convention), so only
+// it needs the release fence before arriving.
 __device__ __forceinline__ bool last_block(unsigned* counter) {
     __shared__ bool s_last;
     __syncthreads();

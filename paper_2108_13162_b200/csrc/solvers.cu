@@ -1765,8 +1765,8 @@ struct PcgSession {
             }
             st = dev_alloc<CgState>(1, false);
             e.gate = &st->done;
-            hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
-            if (trace) d_trace = dev_alloc<double>(4 * cfg.max_iterations, true, c->stream);
+            hist = dev_alloc_records<double>(cfg.max_iterations, c->stream);
+            if (trace) d_trace = dev_alloc_records<double>(4 * cfg.max_iterations, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
             stream_wait(c);
             trace_lap(c, "pcg_session", "setup kernels");
@@ -2211,7 +2211,7 @@ struct BicgstabSession {
             }
             st = dev_alloc<BiState>(1, false);
             e.gate = &st->done;
-            hist = dev_alloc<double>(cfg.max_iterations, true, c->stream);
+            hist = dev_alloc_records<double>(cfg.max_iterations, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
             stream_wait(c);
             exec_chunk = capture(kChunk);

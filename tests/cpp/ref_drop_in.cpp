@@ -26,7 +26,7 @@ using namespace krysp;
 
 namespace {
 
-int checks = 0, failures = 0;
+int checks = 0, failures = 0, solved = 0, raised = 0;
 
 void expect(bool ok, const std::string& what) {
     ++checks;
@@ -53,15 +53,6 @@ SolveReport run_solver(const std::string& method, const SparseMatrix& A, const s
     if (method == "bicgstab") return solve_bicgstab(A, b, x0, cfg);
     if (method == "bicgstabl") return solve_bicgstab_l(A, b, x0, cfg);
     throw Error("unknown method '" + method + "'");
-}
-
-void same_report(const SolveReport& h, const SolveReport& d, const std::string& tag) {
-    expect(h.converged == d.converged, tag + " converged");
-    expect(h.iterations == d.iterations,
-           tag + " iterations " + std::to_string(h.iterations) + " vs " + std::to_string(d.iterations));
-    expect(same_bits(h.final_residual_measure, d.final_residual_measure), tag + " final measure");
-    expect(same_bits(h.residual_history, d.residual_history), tag + " residual history");
-    expect(same_bits(h.solution, d.solution), tag + " solution");
 }
 
 // the exception class (most-derived krysp type) and message of a call
@@ -92,13 +83,33 @@ void same_outcome(const std::function<void()>& host, const std::function<void()>
     expect(a == b && (a != "ok" || !must_throw), tag + ": host '" + a + "' device '" + b + "'");
 }
 
+void same_report(const SolveReport& h, const SolveReport& d, const std::string& tag) {
+    expect(h.converged == d.converged, tag + " converged");
+    expect(h.iterations == d.iterations,
+           tag + " iterations " + std::to_string(h.iterations) + " vs " + std::to_string(d.iterations));
+    expect(same_bits(h.final_residual_measure, d.final_residual_measure), tag + " final measure");
+    expect(same_bits(h.residual_history, d.residual_history), tag + " residual history");
+    expect(same_bits(h.solution, d.solution), tag + " solution");
+}
+
+// both solves: the same report bit for bit, or the same exception class and message (the
+// reference itself stops some of these solves with NonFinite / Breakdown)
+void same_solve(const std::function<SolveReport()>& host, const std::function<SolveReport()>& dev,
+                const std::string& tag) {
+    SolveReport h, d;
+    const std::string a = outcome([&] { h = host(); }), b = outcome([&] { d = dev(); });
+    expect(a == b, tag + ": host '" + a + "' device '" + b + "'");
+    if (a == "ok" && b == "ok") same_report(h, d, tag);
+    ++(a == "ok" ? solved : raised);
+}
+
 CsrMatrix csr_of(const std::vector<Triple>& t, index_t n_rows, index_t n_cols) {
     return coo_to_csr(build_coo(t, n_rows, n_cols));
 }
 
 }  // namespace
 
-int main() {
+int run() {
     namespace g = krysp::gpu;
     const CsrMatrix spd = coo_to_csr(poisson2d(40));       // generators.cpp:15-32
     const CsrMatrix ns = coo_to_csr(convdiff2d(40, 0.5));  // generators.cpp:46-68
@@ -120,8 +131,9 @@ int main() {
             const CsrMatrix& A = std::string(m) == "cg" ? spd : ns;
             for (Format f : {Format::Csr, Format::Ell, Format::Hyb, Format::Coo}) {
                 const SparseMatrix M = convert(SparseMatrix(A), f);
-                same_report(run_solver(m, M, b, x0, c, false), run_solver(m, M, b, x0, c, true),
-                            std::string(m) + " fmt " + std::to_string((int)f) + " " + ptag);
+                same_solve([&] { return run_solver(m, M, b, x0, c, false); },
+                           [&] { return run_solver(m, M, b, x0, c, true); },
+                           std::string(m) + " fmt " + std::to_string((int)f) + " " + ptag);
             }
         }
         // P-CG trace (solvers.hpp:43-56) and the descent CG
@@ -134,15 +146,15 @@ int main() {
             tr = same_bits(th[k].rho, td[k].rho) && same_bits(th[k].beta, td[k].beta) &&
                  same_bits(th[k].sigma, td[k].sigma) && same_bits(th[k].alpha, td[k].alpha);
         expect(tr, "CgTrace " + ptag);
-        same_report(solve_cg_classic(SparseMatrix(spd), b, x0, cfg), g::solve_cg_classic(SparseMatrix(spd), b, x0, cfg),
-                    "cg_classic " + ptag);
+        same_solve([&] { return solve_cg_classic(SparseMatrix(spd), b, x0, cfg); },
+                   [&] { return g::solve_cg_classic(SparseMatrix(spd), b, x0, cfg); }, "cg_classic " + ptag);
         // non-zero x0, no preconditioner
         std::vector<double> x1(n);
         for (index_t i = 0; i < n; ++i) x1[i] = 0.25 * std::sin(0.1 * (double)i);
         SolverConfig c2 = cfg;
         c2.preconditioner = Preconditioner::None;
-        same_report(solve_bicgstab(SparseMatrix(ns), b, x1, c2), g::solve_bicgstab(SparseMatrix(ns), b, x1, c2),
-                    "bicgstab x0 none " + ptag);
+        same_solve([&] { return solve_bicgstab(SparseMatrix(ns), b, x1, c2); },
+                   [&] { return g::solve_bicgstab(SparseMatrix(ns), b, x1, c2); }, "bicgstab x0 none " + ptag);
     }
 
     // ---- FAST mode through the same binding: the gates of SURVEY §8(d)
@@ -246,7 +258,17 @@ int main() {
         expect(bench_table_csv(t.table).rfind("kernel,matrix,block_size", 0) == 0, "tune table CSV (reference writer)");
     }
 
-    std::printf("ref drop-in: %d checks, %d failures\n", checks, failures);
+    std::printf("ref drop-in: %d checks, %d failures (%d solves compared bit for bit, %d raised on both sides)\n",
+                checks, failures, solved, raised);
     if (failures == 0) std::printf("ref drop-in ok\n");
     return failures == 0 ? 0 : 1;
+}
+
+int main() {
+    try {
+        return run();
+    } catch (const std::exception& e) {
+        std::printf("FAIL uncaught exception: %s\nref drop-in: %d checks, %d failures\n", e.what(), checks, failures);
+        return 1;
+    }
 }

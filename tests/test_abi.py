@@ -116,3 +116,22 @@ def test_reference_typed_binding_compiles_against_reference_headers(tmp_path):
                    "int main() { return 0; }\n")
     subprocess.check_call(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Werror", "-I", inc, "-I",
                            os.path.join(ROOT, "include"), str(src)])
+
+
+def test_band_rows_host_generator_matches_full_matrix():
+    """krysp_gpu_gen_csr_rows_host: one band of the band-row partition equals the rows of the
+    full generator (local row_ptr, global columns)."""
+    from paper_2108_13162_b200.dist import band_rows
+    for kind, n in [("lap3d7", 12), ("fem27", 7), ("convdiff2d", 30), ("poisson2d", 17), ("laplace1d", 50)]:
+        full = kg.generate_csr(kind, n)
+        for parts in (1, 3, 8):
+            for p in range(parts):
+                lo, hi = band_rows(full.n_rows, parts, p)
+                band = kg.generate_csr_rows(kind, n, lo, hi)
+                a, b = full.row_ptr[lo], full.row_ptr[hi]
+                assert band.n_rows == hi - lo and band.n_cols == full.n_cols
+                np.testing.assert_array_equal(band.row_ptr, full.row_ptr[lo:hi + 1] - a)
+                np.testing.assert_array_equal(band.col_idx, full.col_idx[a:b])
+                np.testing.assert_array_equal(band.values, full.values[a:b])
+    with pytest.raises(kg.IndexOutOfRange):
+        kg.generate_csr_rows("lap3d7", 4, 0, 65)

@@ -272,6 +272,17 @@ def test_fused_breakdown_matches_reference(ctx, ref, method):
             D.pcg_run()
             D.pcg_report()
         assert ei.value.code == want["status"] and str(ei.value) == want["error"], (method, rhs, str(ei.value))
+    # Jacobi on a zero diagonal in the second band: the reference names the global row
+    # (solvers.cpp:106-109) and so does every rank of the partitioned solver
+    z = [1., 2., 3., 0.]
+    rz = ref.from_csr(kg.CsrMatrix(4, 4, np.arange(5), np.arange(4), np.array(z)))
+    want = ref.solve(rz, method, np.ones(4))
+    assert want["status"] == kg.Breakdown.code and "row 3" in want["error"]
+    D = _two_band(ctx, z)
+    with pytest.raises(kg.Breakdown) as ei:
+        D.krylov_create(method, [ctx.to_device(np.ones(2)) for _ in range(2)],
+                        [ctx.to_device(np.zeros(2)) for _ in range(2)], kg.SolverConfig(mode="fast"))
+    assert str(ei.value) == want["error"]
 
 
 def test_fused_bicgstab_half_step_and_max_iterations(ctx, ref):
