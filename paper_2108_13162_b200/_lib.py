@@ -132,7 +132,7 @@ EXPORTS = [
     "krysp_gpu_launch_count", "krysp_gpu_grid_spmv_blocks", "krysp_gpu_grid_vector_blocks",
     "krysp_gpu_compute_grid", "krysp_gpu_validate_policy", "krysp_gpu_mat_upload_csr",
     "krysp_gpu_mat_upload_coo", "krysp_gpu_mat_generate", "krysp_gpu_gen_nnz", "krysp_gpu_gen_csr_host",
-    "krysp_gpu_gen_csr_rows_host",
+    "krysp_gpu_gen_csr_rows_host", "krysp_gpu_mat_column_slices",
     "krysp_gpu_mat_convert", "krysp_gpu_mat_transpose", "krysp_gpu_mat_info", "krysp_gpu_mat_download_csr",
     "krysp_gpu_mat_download_ell", "krysp_gpu_mat_download_coo", "krysp_gpu_mat_destroy", "krysp_gpu_mat_stats",
     "krysp_gpu_spmv", "krysp_gpu_spmv_host", "krysp_gpu_daxpy", "krysp_gpu_scal_elementwise", "krysp_gpu_copy",

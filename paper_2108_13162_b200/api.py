@@ -678,6 +678,13 @@ def solve_csr_host(ctx: Context, m: CsrMatrix, method: str, b, x0=None, cfg: Opt
 
 
 # ----------------------------------------------------------------------------- autotune.hpp
+def column_slices(A: DeviceMatrix) -> int:
+    """Column slices of the FAST irregular-CSR SpMV of A (1 = unsliced; builds them)."""
+    k = C.c_int64()
+    check(A.ctx.L.krysp_gpu_mat_column_slices(A.h, C.byref(k)))
+    return int(k.value)
+
+
 def time_spmv(A: DeviceMatrix, policy: ExecPolicy, mode: str = "exact",
               protocol: TimingProtocol = TimingProtocol(), matrix_name: str = "") -> BenchRecord:
     r = _lib.BenchRecord()

@@ -242,7 +242,141 @@ int32_t* ensure_coo_rp(const krysp_gpu_mat* cm) {
     return rp;
 }
 
+// ---- column slices ------------------------------------------------------------------
+// Power-law x gathers are random: once x outgrows L2 (C5 at 100 M nnz: 175 MB of x against
+// 126 MB of L2) most gathers miss and each miss moves a whole DRAM burst for one double
+// (ncu: 4.2x the algorithmic bytes).  Cutting the columns into slices of <= KRYSP_SLICE_MB of
+// x and running the SpMV slice by slice (y accumulating) keeps each slice's x resident while
+// the slice's nonzeros stream past it (evict-first loads); the price is one extra row
+// pointer and one y read + write per additional slice.
+
+// per row: entries of slice k = [lower_bound(slice k start), lower_bound(slice k+1 start))
+__global__ void slice_count_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t n,
+                                   int64_t slice_cols, int K, int32_t* __restrict__ cnt) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        int32_t pos = rp[r];
+        const int32_t end = rp[r + 1];
+        for (int k = 0; k < K; ++k) {
+            int32_t lo = pos, hi = end;  // first entry with column >= (k + 1) * slice_cols
+            const int64_t bound = (int64_t)(k + 1) * slice_cols;
+            while (lo < hi) {
+                const int32_t mid = lo + ((hi - lo) >> 1);
+                if ((int64_t)ci[mid] < bound) lo = mid + 1;
+                else hi = mid;
+            }
+            cnt[(int64_t)k * n + r] = lo - pos;
+            pos = lo;
+        }
+    }
+}
+
+__global__ void slice_copy_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ cv, int64_t n, int K, int32_t* const* __restrict__ rps,
+                                  int32_t* const* __restrict__ cis, double* const* __restrict__ cvs) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        int32_t pos = rp[r];
+        for (int k = 0; k < K; ++k) {
+            const int32_t d0 = rps[k][r], len = rps[k][r + 1] - d0;
+            for (int32_t j = 0; j < len; ++j) {
+                cis[k][d0 + j] = ci[pos + j];
+                cvs[k][d0 + j] = cv[pos + j];
+            }
+            pos += len;
+        }
+    }
+}
+
+int64_t slice_bytes() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("KRYSP_SLICE_MB");
+        const long long mb = e ? std::atoll(e) : 48;
+        return mb > 0 ? (int64_t)mb << 20 : (int64_t)0;
+    }();
+    return v;
+}
+
+void build_slices(krysp_gpu_mat* m) {
+    krysp_gpu_ctx* c = m->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t n = m->n_rows, cols_per = std::max<int64_t>(slice_bytes() / 8, 1024);
+    const int K = (int)((m->n_cols + cols_per - 1) / cols_per);
+    auto* S = new ColumnSlices;
+    S->slice_cols = (m->n_cols + K - 1) / K;  // equal slices
+    S->s.resize((size_t)K);
+    DevBuf<int32_t> cnt((int64_t)K * n + 1, false);
+    const unsigned g = grid_for(n, 256, (int64_t)c->sm_count * 16);
+    slice_count_kernel<<<g, 256, 0, s>>>(m->rp, m->ci, n, S->slice_cols, K, cnt);
+    KG_LAUNCH(c);
+    std::vector<int32_t*> rps((size_t)K), cis((size_t)K);
+    std::vector<double*> cvs((size_t)K);
+    size_t tmp = 0;
+    KG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt.p, cnt.p, (int)n, s));
+    DevBuf<char> d_tmp((int64_t)tmp + 1, false);
+    for (int k = 0; k < K; ++k) {
+        ColumnSlice& q = S->s[(size_t)k];
+        q.rp = dev_alloc<int32_t>(n + 1 + kPad, true, s);
+        KG_CUDA(cub::DeviceScan::InclusiveSum(d_tmp.p, tmp, cnt.p + (int64_t)k * n, q.rp + 1, (int)n, s));
+        int32_t nz = 0;
+        KG_CUDA(cudaMemcpyAsync(&nz, q.rp + n, 4, cudaMemcpyDeviceToHost, s));
+        KG_CUDA(cudaStreamSynchronize(s));
+        q.nnz = nz;
+        q.ci = dev_alloc<int32_t>(nz + kPad, false);
+        q.cv = dev_alloc<double>(nz + kPad, false);
+        rps[(size_t)k] = q.rp;
+        cis[(size_t)k] = q.ci;
+        cvs[(size_t)k] = q.cv;
+    }
+    DevBuf<int32_t*> d_rps(K, false), d_cis(K, false);
+    DevBuf<double*> d_cvs(K, false);
+    KG_CUDA(cudaMemcpyAsync(d_rps.p, rps.data(), 8 * (size_t)K, cudaMemcpyHostToDevice, s));
+    KG_CUDA(cudaMemcpyAsync(d_cis.p, cis.data(), 8 * (size_t)K, cudaMemcpyHostToDevice, s));
+    KG_CUDA(cudaMemcpyAsync(d_cvs.p, cvs.data(), 8 * (size_t)K, cudaMemcpyHostToDevice, s));
+    slice_copy_kernel<<<g, 256, 0, s>>>(m->rp, m->ci, m->cv, n, K, d_rps, d_cis, d_cvs);
+    KG_LAUNCH(c);
+    for (auto& q : S->s) build_plan(c, q.rp, n, q.plan);  // synchronises the stream
+    m->slices = S;
+}
+
+void run_plan(krysp_gpu_ctx* c, RowsView A, AdaptivePlan* P, const double* x, double* y, bool accumulate,
+              cudaStream_t s, const int* gate) {
+    const int64_t items = P->nchunk + P->nlng + (P->nmed + kAdNT / 32 - 1) / (kAdNT / 32) + P->nblk;
+    if (items) {
+        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel, kAdNT, 0), items);
+        adaptive_kernel<<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
+                                                      P->nchunk, P->partials, x, y, accumulate ? 1 : 0, gate);
+        KG_LAUNCH(c);
+    }
+    if (P->ngiant) {
+        giant_fixup_kernel<<<grid_for(P->ngiant, 128, 1024), 128, 0, s>>>(P->giant, P->ngiant, P->partials, y,
+                                                                         accumulate ? 1 : 0, gate);
+        KG_LAUNCH(c);
+    }
+}
+
 }  // namespace
+
+void slices_free(krysp_gpu_mat* m) {
+    if (!m->slices) return;
+    for (auto& q : m->slices->s) {
+        dev_free(q.rp);
+        dev_free(q.ci);
+        dev_free(q.cv);
+        adaptive_free(q.plan);
+    }
+    delete m->slices;
+    m->slices = nullptr;
+    m->slices_checked = false;
+}
+
+int64_t csr_column_slices(const krysp_gpu_mat* cm) {
+    auto* m = const_cast<krysp_gpu_mat*>(cm);  // derived, cached acceleration structure
+    if (!m->slices_checked) {
+        m->slices_checked = true;
+        const int64_t sb = slice_bytes();
+        if (m->format == KRYSP_FMT_CSR && sb > 0 && 8 * m->n_cols > sb && m->nnz > 0) build_slices(m);
+    }
+    return m->slices ? (int64_t)m->slices->s.size() : 1;
+}
 
 void launch_adaptive(const krysp_gpu_mat* cm, bool coo_part, const double* x, double* y, bool accumulate,
                      cudaStream_t s, const int* gate) {
@@ -258,19 +392,16 @@ void launch_adaptive(const krysp_gpu_mat* cm, bool coo_part, const double* x, do
         A = {m->rp, m->ci, m->cv};
         P = &m->ad_csr;
     }
+    if (!coo_part && csr_column_slices(m) > 1) {  // slice by slice, y accumulating
+        bool acc = accumulate;
+        for (auto& q : m->slices->s) {
+            run_plan(c, RowsView{q.rp, q.ci, q.cv}, &q.plan, x, y, acc, s, gate);
+            acc = true;
+        }
+        return;
+    }
     if (!P->built) build_plan(c, A.rp, m->n_rows, *P);
-    const int64_t items = P->nchunk + P->nlng + (P->nmed + kAdNT / 32 - 1) / (kAdNT / 32) + P->nblk;
-    if (items) {
-        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel, kAdNT, 0), items);
-        adaptive_kernel<<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
-                                                      P->nchunk, P->partials, x, y, accumulate ? 1 : 0, gate);
-        KG_LAUNCH(c);
-    }
-    if (P->ngiant) {
-        giant_fixup_kernel<<<grid_for(P->ngiant, 128, 1024), 128, 0, s>>>(P->giant, P->ngiant, P->partials, y,
-                                                                         accumulate ? 1 : 0, gate);
-        KG_LAUNCH(c);
-    }
+    run_plan(c, A, P, x, y, accumulate, s, gate);
 }
 
 }  // namespace kg

@@ -505,6 +505,15 @@ krysp_status krysp_gpu_solve_csr_host(krysp_gpu_ctx* c, int64_t n_rows, const in
 // Heuristic policy from the row-length statistics: short rows (a 256-row tile fits shared
 // memory) -> thread per row (tw = 1, staged tile kernel); otherwise tw = the power of two
 // nearest the mean row length, clipped to [1, 32].
+krysp_status krysp_gpu_mat_column_slices(const krysp_gpu_mat* m, int64_t* n_slices) {
+    return guard([&] {
+        need(m, "mat");
+        need(n_slices, "n_slices");
+        set_dev(m->ctx);
+        *n_slices = (m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) ? csr_column_slices(m) : 1;
+    });
+}
+
 krysp_status krysp_gpu_autotune_policy(const krysp_gpu_mat* m, krysp_policy* out) {
     return guard([&] {
         need(m, "mat");

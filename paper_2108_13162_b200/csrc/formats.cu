@@ -141,6 +141,7 @@ void mat_free_arrays(krysp_gpu_mat* m) {
     m->cv = m->coef = m->co_v = nullptr;
     adaptive_free(m->ad_csr);
     adaptive_free(m->ad_coo);
+    slices_free(m);
 }
 
 krysp_gpu_mat* mat_new(krysp_gpu_ctx* ctx, int32_t fmt, int64_t n_rows, int64_t n_cols) {

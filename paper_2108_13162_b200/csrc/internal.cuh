@@ -120,12 +120,29 @@ struct AdaptivePlan {
     double* partials = nullptr;
     bool built = false;
 };
+
+// Column slices of an irregular CSR (adaptive.cu): the same rows restricted to consecutive
+// column ranges whose x segment stays resident in L2 while the slice's nonzeros stream past
+// it; y accumulates slice by slice.  Each slice is a CSR of its own with its own plan.
+struct ColumnSlice {
+    int32_t* rp = nullptr;
+    int32_t* ci = nullptr;
+    double* cv = nullptr;
+    int64_t nnz = 0;
+    AdaptivePlan plan;
+};
+struct ColumnSlices {
+    int64_t slice_cols = 0;  // columns per slice (the last one may be shorter)
+    std::vector<ColumnSlice> s;
+};
 }  // namespace kg
 
 struct krysp_gpu_mat {
     krysp_gpu_ctx* ctx = nullptr;
     kg::AdaptivePlan ad_csr, ad_coo;  // FAST irregular-row plans (CSR rows / COO overflow rows)
     int32_t* coo_rp = nullptr;        // row pointer over the COO entries (FAST COO / HYB)
+    kg::ColumnSlices* slices = nullptr;  // FAST irregular CSR with x larger than an L2 slice
+    bool slices_checked = false;
     int32_t format = KRYSP_FMT_CSR;
     int64_t n_rows = 0, n_cols = 0, nnz = 0;
     // CSR
@@ -541,6 +558,9 @@ bool csr_is_irregular(const krysp_gpu_mat* m);
 // gate: optional device flag (a device-resident solve's `done`); set -> the kernels return
 void launch_adaptive(const krysp_gpu_mat* m, bool coo_part, const double* x, double* y, bool accumulate,
                      cudaStream_t s, const int* gate = nullptr);
+void slices_free(krysp_gpu_mat* m);
+// number of column slices the FAST irregular CSR SpMV of m runs (1: unsliced); builds them
+int64_t csr_column_slices(const krysp_gpu_mat* m);
 
 // spmv.cu
 enum SpmvVariant : int32_t {
