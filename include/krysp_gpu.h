@@ -399,7 +399,7 @@ krysp_status krysp_gpu_tune_spmv(const krysp_gpu_mat* m, const krysp_policy* gri
 /* Heuristic choice from row-length statistics (no timing): FAST-mode policy. */
 krysp_status krysp_gpu_autotune_policy(const krysp_gpu_mat* m, krysp_policy* out);
 /* Column slices the FAST auto-policy SpMV of an irregular CSR runs (x cut into L2-sized
- * slices, KRYSP_SLICE_MB, default 48; y accumulates slice by slice); 1 = unsliced.  Builds
+ * slices, KRYSP_SLICE_MB, default 64; y accumulates slice by slice); 1 = unsliced.  Builds
  * the slices (a one-time plan cached on the matrix) when they apply. */
 krysp_status krysp_gpu_mat_column_slices(const krysp_gpu_mat* m, int64_t* n_slices);
 /* Time one SpMV (CUDA events, protocol as above); record filled. */

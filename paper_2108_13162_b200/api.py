@@ -25,7 +25,7 @@ FORMAT_NAMES = {v: k for k, v in FORMATS.items()}
 MODES = {"exact": 0, "fast": 1}
 METHODS = {"pcg": 0, "cg_classic": 1, "gcr": 2, "bicgstab": 3, "bicgstab_l": 4, "tfqmr": 5, "bicgcr": 6}
 VARIANTS = {0: "csr_vector", 1: "csr_tile", 2: "ell", 3: "hyb", 4: "coo", 5: "csr_adaptive", 6: "hyb_adaptive",
-            7: "coo_adaptive"}
+            7: "coo_adaptive", 8: "hyb_tail"}
 kDefaultEllSlotCap = 1 << 26  # formats.hpp:78
 kHybAutoWidth = -1            # formats.hpp:82
 

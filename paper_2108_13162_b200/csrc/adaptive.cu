@@ -152,6 +152,14 @@ __global__ void giant_fixup_kernel(const int32_t* __restrict__ giant, int64_t ng
     }
 }
 
+__global__ void row_max_kernel(const int32_t* __restrict__ cnt, int64_t n, int32_t* out) {
+    int32_t mx = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        mx = max(mx, cnt[i]);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
 __global__ void coo_count_rows(const int32_t* __restrict__ row, int64_t nnz, int32_t* cnt) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(cnt + row[k], 1);
@@ -218,30 +226,6 @@ void build_plan(krysp_gpu_ctx* c, const int32_t* d_rp, int64_t n, AdaptivePlan& 
     P.built = true;
 }
 
-int32_t* ensure_coo_rp(const krysp_gpu_mat* cm) {
-    auto* m = const_cast<krysp_gpu_mat*>(cm);  // derived, cached acceleration structure
-    if (m->coo_rp) return m->coo_rp;
-    krysp_gpu_ctx* c = m->ctx;
-    const int64_t n = m->n_rows;
-    int32_t* cnt = dev_alloc<int32_t>(n + 1, true, c->stream);
-    int32_t* rp = dev_alloc<int32_t>(n + 1 + kPad, true, c->stream);
-    if (m->coo_nnz) {
-        coo_count_rows<<<grid_for(m->coo_nnz, 256, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(m->co_r,
-                                                                                                   m->coo_nnz, cnt);
-        KG_LAUNCH(c);
-    }
-    size_t tmp = 0;
-    KG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt, rp + 1, (int)n, c->stream));
-    void* d_tmp = dev_alloc<char>((int64_t)tmp + 1, false);
-    if (n) KG_CUDA(cub::DeviceScan::InclusiveSum(d_tmp, tmp, cnt, rp + 1, (int)n, c->stream));
-    KG_LAUNCH(c);
-    KG_CUDA(cudaStreamSynchronize(c->stream));
-    dev_free(d_tmp);
-    dev_free(cnt);
-    m->coo_rp = rp;
-    return rp;
-}
-
 // ---- column slices ------------------------------------------------------------------
 // Power-law x gathers are random: once x outgrows L2 (C5 at 100 M nnz: 175 MB of x against
 // 126 MB of L2) most gathers miss and each miss moves a whole DRAM burst for one double
@@ -289,7 +273,7 @@ __global__ void slice_copy_kernel(const int32_t* __restrict__ rp, const int32_t*
 int64_t slice_bytes() {
     static const int64_t v = [] {
         const char* e = std::getenv("KRYSP_SLICE_MB");
-        const long long mb = e ? std::atoll(e) : 48;
+        const long long mb = e ? std::atoll(e) : 64;
         return mb > 0 ? (int64_t)mb << 20 : (int64_t)0;
     }();
     return v;
@@ -354,6 +338,49 @@ void run_plan(krysp_gpu_ctx* c, RowsView A, AdaptivePlan* P, const double* x, do
 }
 
 }  // namespace
+
+int32_t* ensure_coo_rp(const krysp_gpu_mat* cm) {
+    auto* m = const_cast<krysp_gpu_mat*>(cm);  // derived, cached acceleration structure
+    if (m->coo_rp) return m->coo_rp;
+    krysp_gpu_ctx* c = m->ctx;
+    const int64_t n = m->n_rows;
+    int32_t* cnt = dev_alloc<int32_t>(n + 1, true, c->stream);
+    int32_t* rp = dev_alloc<int32_t>(n + 1 + kPad, true, c->stream);
+    if (m->coo_nnz) {
+        coo_count_rows<<<grid_for(m->coo_nnz, 256, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(m->co_r,
+                                                                                                   m->coo_nnz, cnt);
+        KG_LAUNCH(c);
+    }
+    size_t tmp = 0;
+    KG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt, rp + 1, (int)n, c->stream));
+    void* d_tmp = dev_alloc<char>((int64_t)tmp + 1, false);
+    if (n) KG_CUDA(cub::DeviceScan::InclusiveSum(d_tmp, tmp, cnt, rp + 1, (int)n, c->stream));
+    KG_LAUNCH(c);
+    int32_t* d_max = dev_alloc<int32_t>(1, true, c->stream);
+    if (n) {
+        row_max_kernel<<<grid_for(n, 256, (int64_t)c->sm_count * 8), 256, 0, c->stream>>>(cnt, n, d_max);
+        KG_LAUNCH(c);
+    }
+    int32_t h_max = 0;
+    KG_CUDA(cudaMemcpyAsync(&h_max, d_max, 4, cudaMemcpyDeviceToHost, c->stream));
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    dev_free(d_max);
+    dev_free(d_tmp);
+    dev_free(cnt);
+    m->coo_max_row = h_max;
+    m->coo_rp = rp;
+    return rp;
+}
+
+// measured (C4 fem27 320^3, w = 26, one overflow entry per row): finishing the overflow in
+// the ELL kernel beats the separate load-balanced COO pass; rows with longer overflow
+// segments (C5's power-law tails) keep the load-balanced kernel
+bool hyb_tail_fusable(const krysp_gpu_mat* m) {
+    if (m->format != KRYSP_FMT_HYB || m->coo_nnz == 0) return false;
+    ensure_coo_rp(m);
+    return m->coo_max_row <= 4;
+}
+
 
 void slices_free(krysp_gpu_mat* m) {
     if (!m->slices) return;

@@ -91,6 +91,11 @@ struct EllView {
     const int32_t* __restrict__ jcoef;  // column-major, sentinel = n_cols
     const double* __restrict__ coef;
     int64_t ld;  // slot stride (>= n_rows, multiple of 4: 16-byte aligned slot columns)
+    // optional COO tail (HYB overflow, FAST): row r continues its ELL sum with the COO
+    // entries [trp[r], trp[r+1]) in column order — the reference's coo_accumulate order
+    const int32_t* __restrict__ trp = nullptr;
+    const int32_t* __restrict__ tcol = nullptr;
+    const double* __restrict__ tval = nullptr;
 };
 struct CooView {
     int32_t n_rows, n_cols;
@@ -141,6 +146,7 @@ struct krysp_gpu_mat {
     krysp_gpu_ctx* ctx = nullptr;
     kg::AdaptivePlan ad_csr, ad_coo;  // FAST irregular-row plans (CSR rows / COO overflow rows)
     int32_t* coo_rp = nullptr;        // row pointer over the COO entries (FAST COO / HYB)
+    int64_t coo_max_row = -1;         // longest COO row segment (with coo_rp)
     kg::ColumnSlices* slices = nullptr;  // FAST irregular CSR with x larger than an L2 slice
     bool slices_checked = false;
     int32_t format = KRYSP_FMT_CSR;
@@ -559,6 +565,10 @@ bool csr_is_irregular(const krysp_gpu_mat* m);
 void launch_adaptive(const krysp_gpu_mat* m, bool coo_part, const double* x, double* y, bool accumulate,
                      cudaStream_t s, const int* gate = nullptr);
 void slices_free(krysp_gpu_mat* m);
+// row pointer over the COO entries (built once, cached; coo_max_row filled)
+int32_t* ensure_coo_rp(const krysp_gpu_mat* m);
+// HYB whose COO overflow rows are short enough for the ELL kernel to finish them in place
+bool hyb_tail_fusable(const krysp_gpu_mat* m);
 // number of column slices the FAST irregular CSR SpMV of m runs (1: unsliced); builds them
 int64_t csr_column_slices(const krysp_gpu_mat* m);
 
@@ -572,6 +582,7 @@ enum SpmvVariant : int32_t {
     kVarCsrAdaptive = 5,  // FAST: load-balanced row blocks (irregular rows)
     kVarHybAdaptive = 6,  // FAST: ELL + load-balanced COO overflow
     kVarCooAdaptive = 7,  // FAST: load-balanced COO
+    kVarHybTail = 8,      // FAST: ELL slots + short COO overflow rows in one kernel
 };
 // gate (FAST auto policy on irregular rows, the load-balanced kernels): an optional device
 // flag that turns the launch into a no-op once set — a device-resident solve's `done`, so

@@ -664,9 +664,20 @@ __global__ void __launch_bounds__(1024) vec_epi_kernel(int64_t n, const double* 
 template <class Epi>
 void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y, Epi epi) {
     cudaStream_t s = e.c->stream;
-    const bool irregular = e.auto_pol && ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) ||
-                                          m->format == KRYSP_FMT_COO || (m->format == KRYSP_FMT_HYB && m->coo_nnz));
-    if (!irregular && m->format == KRYSP_FMT_CSR) {
+    const bool tail = e.auto_pol && hyb_tail_fusable(m);  // HYB overflow finished inside the ELL pass
+    const bool irregular = e.auto_pol && !tail &&
+                           ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) || m->format == KRYSP_FMT_COO ||
+                            (m->format == KRYSP_FMT_HYB && m->coo_nnz));
+    if (tail) {
+        if (m->width < 16) {
+            launch_ell_tail(m, x, epi, e.pol.block_size, s);
+        } else {
+            launch_ell_tail(m, x, EpiStoreGated<Epi>{y, epi}, e.pol.block_size, s);
+            vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y,
+                                                                                                       epi);
+            KG_LAUNCH(e.c);
+        }
+    } else if (!irregular && m->format == KRYSP_FMT_CSR) {
         if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, x, epi, s, e.pol.workers_per_row);
         else launch_csr_vector(m, x, epi, e.pol.block_size, e.pol.workers_per_row, s);
     } else if (!irregular && (m->format == KRYSP_FMT_ELL || (m->format == KRYSP_FMT_HYB && m->coo_nnz == 0))) {
@@ -1720,6 +1731,249 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
     if (err) std::rethrow_exception(err);
 }
 
+// ------------------------------------------------------------------ persistent P-CG
+// Small systems (C1: 1 M rows, 80 MB of matrix + 40 MB of vectors, about the size of L2) spend
+// a third of each 3-launch iteration in grid ramp-up / tail.  Here one cooperative grid runs
+// the whole solve: the same three phases (SpMV + <p,Ap>; r update + <r,z> and the convergence
+// test; x and direction update) separated by grid barriers, each CTA owning a contiguous row
+// range, the scalars formed redundantly (and identically) by every CTA from the same
+// partials in the same order — so no broadcast step.  Same recurrence, checks, history and
+// trace as the 3-kernel iteration (cg_update_kernel / cg_direction_kernel), so the two paths
+// share CgState and can alternate.
+constexpr int kPcNT = 512;
+constexpr int kPcRows = 4;  // rows per thread whose loads are issued together
+
+// sense-free grid barrier: arrival counter reset by the last arriver, which then bumps the
+// generation the others spin on (counter reset before the bump: no early re-arrival race)
+__device__ __forceinline__ void pc_grid_sync(unsigned* count, unsigned* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = *(volatile unsigned*)gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*(volatile unsigned*)gen == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// every CTA: the grid total of partials[0..gridDim) in one fixed order (warp 0 strided sums,
+// then the warp tree) — bit-identical in all CTAs
+__device__ __forceinline__ double pc_grid_total(const double* partials, double* sh) {
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += __ldcg(partials + i);
+        t = warp_sum(t);
+        if (threadIdx.x == 0) sh[0] = t;
+    }
+    __syncthreads();
+    const double v = sh[0];
+    __syncthreads();
+    return v;
+}
+
+template <bool kJacobi>
+__global__ void __launch_bounds__(kPcNT, 1) pcg_persistent_kernel(CsrView A, double* __restrict__ x, double* __restrict__ r,
+                                                               double* __restrict__ p, double* __restrict__ ap,
+                                                               const double* __restrict__ inv, CgState* st,
+                                                               double* part_s, double* part_r, unsigned* bar,
+                                                               double* history, double* trace, long long budget) {
+    __shared__ double sh[32];
+    // snapshot of the state before anyone may change it
+    struct {
+        double rho, rho_1, alpha, beta, norm_r0, tol;
+        long long iter, max_it;
+        int done, x_pending;
+    } h0;
+    h0.rho = __ldcg(&st->rho);
+    h0.rho_1 = __ldcg(&st->rho_1);
+    h0.alpha = __ldcg(&st->alpha);
+    h0.beta = __ldcg(&st->beta);
+    h0.norm_r0 = __ldcg(&st->norm_r0);
+    h0.tol = __ldcg(&st->tol);
+    h0.iter = __ldcg(&st->iter);
+    h0.max_it = __ldcg(&st->max_it);
+    h0.done = __ldcg(&st->done);
+    h0.x_pending = __ldcg(&st->x_pending);
+    pc_grid_sync(bar, bar + 1);
+    if (h0.done && !h0.x_pending) return;
+    const int64_t n = A.n_rows;
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = min(n, (int64_t)blockIdx.x * per), hi = min(n, lo + per);
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    double rho = h0.rho, rho_prev = h0.rho_1, alpha = h0.alpha, beta = h0.beta;
+    long long it = h0.iter;
+    if (h0.done) {  // the iteration that ended the solve left x += alpha p pending
+        for (int64_t i = lo + threadIdx.x; i < hi; i += kPcNT) x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        if (lead) st->x_pending = 0;
+        return;
+    }
+    for (long long k = 0; k < budget; ++k) {
+        // SpMV + <p, Ap> (solvers.cpp:158-166)
+        double acc = 0.0;
+        for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kPcRows * kPcNT) {
+            // kPcRows rows per thread at once: their entry, gather and p loads all in flight
+            int32_t b[kPcRows], e[kPcRows];
+            double v[kPcRows], pd[kPcRows];
+            int32_t len = 0;
+#pragma unroll
+            for (int q = 0; q < kPcRows; ++q) {
+                const int64_t i = i0 + q * kPcNT;
+                b[q] = e[q] = 0;
+                v[q] = pd[q] = 0.0;
+                if (i < hi) {
+                    b[q] = A.row_ptr[i];
+                    e[q] = A.row_ptr[i + 1];
+                    pd[q] = p[i];
+                }
+                len = max(len, e[q] - b[q]);
+            }
+            for (int32_t j = 0; j < len; ++j) {
+#pragma unroll
+                for (int q = 0; q < kPcRows; ++q)
+                    if (b[q] + j < e[q]) v[q] = fma(__ldg(A.val + b[q] + j), p[__ldg(A.col + b[q] + j)], v[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < kPcRows; ++q) {
+                const int64_t i = i0 + q * kPcNT;
+                if (i < hi) {
+                    ap[i] = v[q];
+                    acc = fma(pd[q], v[q], acc);
+                }
+            }
+        }
+        acc = block_sum<kPcNT>(acc, sh);
+        if (threadIdx.x == 0) part_s[blockIdx.x] = acc;
+        pc_grid_sync(bar, bar + 1);
+        const double sigma = pc_grid_total(part_s, sh);
+        int status = kStRunning;
+        if (!isfinite(sigma)) status = kStNonFiniteSigma;
+        else if (fabs(sigma) < kBreakdownEps) status = kStBreakdownSigma;
+        else {
+            alpha = rho / sigma;
+            if (!isfinite(alpha)) status = kStNonFiniteAlpha;
+        }
+        if (status != kStRunning) {
+            if (lead) {
+                st->sigma = sigma;
+                st->status = status;
+                st->done = 1;
+            }
+            return;
+        }
+        // r -= alpha Ap; rho = <r, D^-1 r> (solvers.cpp:167-181); x += alpha p deferred
+        acc = 0.0;
+        for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kPcRows * kPcNT) {
+            double av[kPcRows], rv[kPcRows], iv[kPcRows];
+#pragma unroll
+            for (int q = 0; q < kPcRows; ++q) {
+                const int64_t i = i0 + q * kPcNT;
+                if (i < hi) av[q] = ap[i], rv[q] = r[i], iv[q] = kJacobi ? inv[i] : 1.0;
+            }
+#pragma unroll
+            for (int q = 0; q < kPcRows; ++q) {
+                const int64_t i = i0 + q * kPcNT;
+                if (i < hi) {
+                    const double ri = __dadd_rn(__dmul_rn(-alpha, av[q]), rv[q]);
+                    r[i] = ri;
+                    acc = fma(ri, kJacobi ? __dmul_rn(ri, iv[q]) : ri, acc);
+                }
+            }
+        }
+        acc = block_sum<kPcNT>(acc, sh);
+        if (threadIdx.x == 0) part_r[blockIdx.x] = acc;
+        pc_grid_sync(bar, bar + 1);
+        const double rho_new = pc_grid_total(part_r, sh);
+        if (lead && trace) {
+            double* t = trace + 4 * it;
+            t[0] = rho;
+            t[1] = beta;
+            t[2] = sigma;
+            t[3] = alpha;
+        }
+        bool stop = false;
+        if (!isfinite(rho_new)) {
+            if (lead) {
+                st->sigma = sigma;
+                st->alpha = alpha;
+                st->status = kStNonFiniteRho;
+            }
+            stop = true;
+        } else {
+            const double measure = rho_new / h0.norm_r0;
+            if (lead) history[it] = measure;
+            ++it;
+            beta = rho_new / rho;
+            rho_prev = rho;
+            rho = rho_new;
+            stop = measure <= h0.tol || it >= h0.max_it;
+        }
+        if (stop) {  // x += alpha p for the own rows, then the solve is over
+            for (int64_t i = lo + threadIdx.x; i < hi; i += kPcNT) x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+            if (lead) {
+                st->iter = it;
+                st->rho_1 = rho_prev;
+                st->rho = rho;
+                st->beta = beta;
+                st->sigma = sigma;
+                st->alpha = alpha;
+                st->x_pending = 0;
+                st->done = 1;
+            }
+            return;
+        }
+        // x += alpha p; p = D^-1 r + beta p (solvers.cpp:154-157)
+        for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kPcRows * kPcNT) {
+            double pv[kPcRows], rv[kPcRows], xv[kPcRows], iv[kPcRows];
+#pragma unroll
+            for (int q = 0; q < kPcRows; ++q) {
+                const int64_t i = i0 + q * kPcNT;
+                if (i < hi) pv[q] = p[i], rv[q] = r[i], xv[q] = x[i], iv[q] = kJacobi ? inv[i] : 1.0;
+            }
+#pragma unroll
+            for (int q = 0; q < kPcRows; ++q) {
+                const int64_t i = i0 + q * kPcNT;
+                if (i < hi) {
+                    x[i] = __dadd_rn(__dmul_rn(alpha, pv[q]), xv[q]);
+                    p[i] = __dadd_rn(__dmul_rn(beta, pv[q]), kJacobi ? __dmul_rn(rv[q], iv[q]) : rv[q]);
+                }
+            }
+        }
+        if (k + 1 == budget) {
+            if (lead) {
+                st->iter = it;
+                st->rho_1 = rho_prev;
+                st->rho = rho;
+                st->beta = beta;
+                st->sigma = sigma;
+                st->alpha = alpha;
+            }
+            return;
+        }
+        pc_grid_sync(bar, bar + 1);
+    }
+}
+
+// KRYSP_PERSIST=0 turns the persistent path off; KRYSP_PERSIST_MB bounds the working set
+// (matrix + 6 vectors) it takes (default 160 MB: up to about C1's size class)
+bool pcg_persistent_eligible(const krysp_gpu_mat* m) {
+    static const int64_t cap = [] {
+        const char* e = std::getenv("KRYSP_PERSIST");
+        if (e && e[0] == '0') return (int64_t)0;
+        const char* mb = std::getenv("KRYSP_PERSIST_MB");
+        return (int64_t)(mb ? std::atoll(mb) : 160) << 20;
+    }();
+    if (m->format != KRYSP_FMT_CSR || m->n_rows == 0 || csr_is_irregular(m) || m->max_row > 32) return false;
+    const int64_t bytes = 12 * m->nnz + 4 * (m->n_rows + 1) + 48 * m->n_rows;
+    return bytes <= cap;
+}
+
 }  // namespace
 
 // Device-resident FAST P-CG session: setup once, then iterations are enqueued as CUDA-graph
@@ -1739,6 +1993,11 @@ struct PcgSession {
     cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr, exec_prof = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int kernels_per_iteration = 0;
+    // persistent cooperative path (pcg_persistent_kernel) for systems of C1's size class
+    bool persistent = false;
+    unsigned* bar = nullptr;
+    unsigned pc_grid = 0;
+    int64_t launches_total = 0;
 
     PcgSession(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg_, const double* b, const double* x0, bool trace)
         : e(A, cfg_), cfg(cfg_), n(A->n_rows), x(A->n_rows, A->ctx->stream), r(A->n_rows, A->ctx->stream),
@@ -1771,9 +2030,12 @@ struct PcgSession {
             stream_wait(c);
             trace_lap(c, "pcg_session", "setup kernels");
             for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
-            exec_chunk = capture(kChunk, false);
-            exec_one = capture(1, false);
-            trace_lap(c, "pcg_session", "graph capture");
+            setup_persistent();
+            if (!persistent) {
+                exec_chunk = capture(kChunk, false);
+                exec_one = capture(1, false);
+                trace_lap(c, "pcg_session", "graph capture");
+            }
         } catch (...) {
             release();
             throw;
@@ -1791,8 +2053,54 @@ struct PcgSession {
         dev_free(st);
         dev_free(hist);
         dev_free(d_trace);
+        dev_free(bar);
         st = nullptr;
+        bar = nullptr;
         hist = d_trace = nullptr;
+    }
+
+    void setup_persistent() {
+        krysp_gpu_ctx* c = e.c;
+        if (!pcg_persistent_eligible(e.A)) return;
+        int coop = 0;
+        KG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
+        int per_sm = 0;
+        auto* k = e.jacobi ? pcg_persistent_kernel<true> : pcg_persistent_kernel<false>;
+        KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPcNT, 0));
+        if (!coop || per_sm < 1) return;
+        // one CTA per SM: the barrier's arrivals scale with the grid, and C1's 1 M rows give
+        // every thread of 148 x 512 about 13 rows
+        const int64_t want = std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, pc_ctas_per_sm()),
+                                               (n + kPcNT - 1) / kPcNT);
+        pc_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, kPartialCap));
+        bar = dev_alloc<unsigned>(2, true, c->stream);
+        persistent = true;
+        kernels_per_iteration = 1;  // one launch per enqueue (covering all its iterations)
+    }
+
+    static int pc_ctas_per_sm() {
+        static const int v = [] {
+            const char* e = std::getenv("KRYSP_PERSIST_CTAS");
+            const int k = e ? std::atoi(e) : 1;
+            return k >= 1 && k <= 4 ? k : 1;
+        }();
+        return v;
+    }
+
+    void launch_persistent(int64_t budget) {
+        krysp_gpu_ctx* c = e.c;
+        if (budget <= 0) return;
+        CsrView A = e.A->csr();
+        double *px = x, *pr = r, *pp = p, *pap = ap;
+        const double* inv = e.jacobi ? (const double*)e.inv : nullptr;
+        double* part_s = c->d_partials + 2 * kPartialCap;
+        double* part_r = c->d_partials + 3 * kPartialCap;
+        long long bud = budget;
+        void* args[] = {&A, &px, &pr, &pp, &pap, &inv, &st, &part_s, &part_r, &bar, &hist, &d_trace, &bud};
+        auto* k = e.jacobi ? pcg_persistent_kernel<true> : pcg_persistent_kernel<false>;
+        KG_CUDA(cudaLaunchCooperativeKernel((void*)k, dim3(pc_grid), dim3(kPcNT), args, 0, c->stream));
+        KG_LAUNCH(c);
+        ++launches_total;
     }
 
     void iteration(bool events) {
@@ -1844,6 +2152,7 @@ struct PcgSession {
     // enqueue n iterations (kernels of a finished solve exit on entry)
     void enqueue(int64_t iters) {
         krysp_gpu_ctx* c = e.c;
+        if (persistent) return launch_persistent(iters);
         for (int64_t i = 0; i + kChunk <= iters; i += kChunk) KG_CUDA(cudaGraphLaunch(exec_chunk, c->stream));
         for (int64_t i = 0; i < iters % kChunk; ++i) KG_CUDA(cudaGraphLaunch(exec_one, c->stream));
     }
@@ -1862,7 +2171,8 @@ struct PcgSession {
         KG_CUDA(cudaEventCreate(&a));
         KG_CUDA(cudaEventCreate(&b));
         KG_CUDA(cudaEventRecord(a, c->stream));
-        if (!finished()) run_pipelined(c, &st->done, [&] { enqueue(kChunk); });
+        if (persistent) launch_persistent(cfg.max_iterations);  // one grid for the whole solve
+        else if (!finished()) run_pipelined(c, &st->done, [&] { enqueue(kChunk); });
         KG_CUDA(cudaEventRecord(b, c->stream));
         KG_CUDA(cudaEventSynchronize(b));
         float ms = 0.f;

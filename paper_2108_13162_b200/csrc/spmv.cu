@@ -63,6 +63,10 @@ int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const kr
             launch_adaptive(m, false, x, y, false, s, gate);
             return kVarCsrAdaptive;
         }
+        if (hyb_tail_fusable(m)) {
+            launch_ell_tail(m, x, EpiStoreGated<FlagGate>{y, FlagGate{gate}}, pol.block_size, s);
+            return kVarHybTail;
+        }
         if (m->format == KRYSP_FMT_HYB && m->coo_nnz) {
             launch_ell(m, x, EpiStoreGated<FlagGate>{y, FlagGate{gate}}, pol.block_size, s);
             launch_adaptive(m, true, x, y, true, s, gate);

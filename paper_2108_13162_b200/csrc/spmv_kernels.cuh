@@ -321,6 +321,9 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
                     if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * ld), __ldg(x + c));
                 }
             }
+            if (E.trp)  // HYB overflow of this row, continuing the sum in column order
+                for (int32_t k = E.trp[r], e = E.trp[r + 1]; k < e; ++k)
+                    sum = madd(sum, __ldcs(E.tval + k), __ldg(x + __ldcs(E.tcol + k)));
             epi.row(r, sum);
         }
     }
@@ -436,6 +439,27 @@ inline void launch_ell(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t
     } else {
         const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4>, (int)bs, 0), nvb);
         ell_kernel<Epi, 4><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+    }
+    KG_LAUNCH(c);
+}
+
+// HYB with short COO overflow rows (hyb_tail_fusable): ELL slots + the row's COO tail in one
+// kernel, one write of y
+template <class Epi>
+inline void launch_ell_tail(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
+    krysp_gpu_ctx* c = m->ctx;
+    const int64_t nvb = (m->n_rows + bs - 1) / bs;
+    if (nvb == 0) return;
+    EllView E = m->ell();
+    E.trp = ensure_coo_rp(m);
+    E.tcol = m->co_c;
+    E.tval = m->co_v;
+    if (epi_is_store<Epi>::value) {
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 8><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
+    } else {
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 4><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
     }
     KG_LAUNCH(c);
 }

@@ -20,8 +20,8 @@ def rel_err(got, want):
 
 
 def test_sliced_spmv_default_slices_at_scale(ctx):
-    # 7 M rows: 56 MB of x > the 48 MB default slice -> two slices
-    m = kg.generate_csr("powerlaw", 7_000_000, alpha=2.0, seed=2108)
+    # 9 M rows: 72 MB of x > the 64 MB default slice -> two slices
+    m = kg.generate_csr("powerlaw", 9_000_000, alpha=2.0, seed=2108)
     A = ctx.upload(m)
     assert kg.column_slices(A) == 2
     x = np.random.default_rng(1).uniform(-1, 1, m.n_cols)
