@@ -1740,8 +1740,6 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
 // partials in the same order — so no broadcast step.  Same recurrence, checks, history and
 // trace as the 3-kernel iteration (cg_update_kernel / cg_direction_kernel), so the two paths
 // share CgState and can alternate.
-constexpr int kPcNT = 512;
-constexpr int kPcRows = 4;  // rows per thread whose loads are issued together
 
 // sense-free grid barrier: arrival counter reset by the last arriver, which then bumps the
 // generation the others spin on (counter reset before the bump: no early re-arrival race)
@@ -1778,38 +1776,41 @@ __device__ __forceinline__ double pc_grid_total(const double* partials, double* 
     return v;
 }
 
-template <bool kJacobi>
-__global__ void __launch_bounds__(kPcNT, 1) pcg_persistent_kernel(CsrView A, double* __restrict__ x, double* __restrict__ r,
+// kPcNT threads per CTA, kPcRows rows per thread whose loads are issued together, kPcMin CTAs
+// per SM the register budget is sized for
+template <bool kJacobi, int kPcNT, int kPcRows, int kPcMin>
+__global__ void __launch_bounds__(kPcNT, kPcMin) pcg_persistent_kernel(CsrView A, double* __restrict__ x, double* __restrict__ r,
                                                                double* __restrict__ p, double* __restrict__ ap,
                                                                const double* __restrict__ inv, CgState* st,
                                                                double* part_s, double* part_r, unsigned* bar,
                                                                double* history, double* trace, long long budget) {
     __shared__ double sh[32];
-    // snapshot of the state before anyone may change it
-    struct {
-        double rho, rho_1, alpha, beta, norm_r0, tol;
-        long long iter, max_it;
-        int done, x_pending;
-    } h0;
-    h0.rho = __ldcg(&st->rho);
-    h0.rho_1 = __ldcg(&st->rho_1);
-    h0.alpha = __ldcg(&st->alpha);
-    h0.beta = __ldcg(&st->beta);
-    h0.norm_r0 = __ldcg(&st->norm_r0);
-    h0.tol = __ldcg(&st->tol);
-    h0.iter = __ldcg(&st->iter);
-    h0.max_it = __ldcg(&st->max_it);
-    h0.done = __ldcg(&st->done);
-    h0.x_pending = __ldcg(&st->x_pending);
+    // snapshot of the state (shared: the uniform scalars stay out of the registers) before
+    // anyone may change it
+    __shared__ double s_rho, s_rho_1, s_alpha, s_beta, s_norm_r0, s_tol;
+    __shared__ long long s_iter, s_max_it;
+    __shared__ int s_done, s_x_pending;
+    if (threadIdx.x == 0) {
+        s_rho = __ldcg(&st->rho);
+        s_rho_1 = __ldcg(&st->rho_1);
+        s_alpha = __ldcg(&st->alpha);
+        s_beta = __ldcg(&st->beta);
+        s_norm_r0 = __ldcg(&st->norm_r0);
+        s_tol = __ldcg(&st->tol);
+        s_iter = __ldcg(&st->iter);
+        s_max_it = __ldcg(&st->max_it);
+        s_done = __ldcg(&st->done);
+        s_x_pending = __ldcg(&st->x_pending);
+    }
     pc_grid_sync(bar, bar + 1);
-    if (h0.done && !h0.x_pending) return;
+    if (s_done && !s_x_pending) return;
     const int64_t n = A.n_rows;
     const int64_t per = (n + gridDim.x - 1) / gridDim.x;
     const int64_t lo = min(n, (int64_t)blockIdx.x * per), hi = min(n, lo + per);
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-    double rho = h0.rho, rho_prev = h0.rho_1, alpha = h0.alpha, beta = h0.beta;
-    long long it = h0.iter;
-    if (h0.done) {  // the iteration that ended the solve left x += alpha p pending
+    double rho = s_rho, alpha = s_alpha, beta = s_beta;
+    long long it = s_iter;
+    if (s_done) {  // the iteration that ended the solve left x += alpha p pending
         for (int64_t i = lo + threadIdx.x; i < hi; i += kPcNT) x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
         if (lead) st->x_pending = 0;
         return;
@@ -1906,19 +1907,21 @@ __global__ void __launch_bounds__(kPcNT, 1) pcg_persistent_kernel(CsrView A, dou
             }
             stop = true;
         } else {
-            const double measure = rho_new / h0.norm_r0;
-            if (lead) history[it] = measure;
+            const double measure = rho_new / s_norm_r0;
+            if (lead) {
+                history[it] = measure;
+                s_rho_1 = rho;  // only the lead reports it
+            }
             ++it;
             beta = rho_new / rho;
-            rho_prev = rho;
             rho = rho_new;
-            stop = measure <= h0.tol || it >= h0.max_it;
+            stop = measure <= s_tol || it >= s_max_it;
         }
         if (stop) {  // x += alpha p for the own rows, then the solve is over
             for (int64_t i = lo + threadIdx.x; i < hi; i += kPcNT) x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
             if (lead) {
                 st->iter = it;
-                st->rho_1 = rho_prev;
+                st->rho_1 = s_rho_1;
                 st->rho = rho;
                 st->beta = beta;
                 st->sigma = sigma;
@@ -1948,7 +1951,7 @@ __global__ void __launch_bounds__(kPcNT, 1) pcg_persistent_kernel(CsrView A, dou
         if (k + 1 == budget) {
             if (lead) {
                 st->iter = it;
-                st->rho_1 = rho_prev;
+                st->rho_1 = s_rho_1;
                 st->rho = rho;
                 st->beta = beta;
                 st->sigma = sigma;
@@ -1960,12 +1963,13 @@ __global__ void __launch_bounds__(kPcNT, 1) pcg_persistent_kernel(CsrView A, dou
     }
 }
 
-// KRYSP_PERSIST=0 turns the persistent path off; KRYSP_PERSIST_MB bounds the working set
-// (matrix + 6 vectors) it takes (default 160 MB: up to about C1's size class)
+// KRYSP_PERSIST=1 turns the persistent path on (measured on C1: 23.7-27.4 k it/s against the
+// 3-kernel graph's 28.8-29.2 k, profiles/r02_c1_persistent.jsonl — off by default);
+// KRYSP_PERSIST_MB bounds the working set (matrix + 6 vectors) it takes (default 160 MB)
 bool pcg_persistent_eligible(const krysp_gpu_mat* m) {
     static const int64_t cap = [] {
         const char* e = std::getenv("KRYSP_PERSIST");
-        if (e && e[0] == '0') return (int64_t)0;
+        if (!e || e[0] != '1') return (int64_t)0;
         const char* mb = std::getenv("KRYSP_PERSIST_MB");
         return (int64_t)(mb ? std::atoll(mb) : 160) << 20;
     }();
@@ -1997,6 +2001,8 @@ struct PcgSession {
     bool persistent = false;
     unsigned* bar = nullptr;
     unsigned pc_grid = 0;
+    void* pc_kernel = nullptr;
+    int pc_nt = 512, pc_min = 1;
     int64_t launches_total = 0;
 
     PcgSession(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg_, const double* b, const double* x0, bool trace)
@@ -2065,26 +2071,42 @@ struct PcgSession {
         int coop = 0;
         KG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
         int per_sm = 0;
-        auto* k = e.jacobi ? pcg_persistent_kernel<true> : pcg_persistent_kernel<false>;
-        KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPcNT, 0));
+        pc_kernel = pick_persistent(e.jacobi, pc_nt, pc_min);
+        KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pc_kernel, pc_nt, 0));
         if (!coop || per_sm < 1) return;
-        // one CTA per SM: the barrier's arrivals scale with the grid, and C1's 1 M rows give
-        // every thread of 148 x 512 about 13 rows
-        const int64_t want = std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, pc_ctas_per_sm()),
-                                               (n + kPcNT - 1) / kPcNT);
+        const int64_t want = std::min<int64_t>((int64_t)c->sm_count * std::min(per_sm, pc_min),
+                                               (n + pc_nt - 1) / pc_nt);
         pc_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, kPartialCap));
         bar = dev_alloc<unsigned>(2, true, c->stream);
         persistent = true;
         kernels_per_iteration = 1;  // one launch per enqueue (covering all its iterations)
     }
 
-    static int pc_ctas_per_sm() {
-        static const int v = [] {
-            const char* e = std::getenv("KRYSP_PERSIST_CTAS");
-            const int k = e ? std::atoi(e) : 1;
-            return k >= 1 && k <= 4 ? k : 1;
+    // KRYSP_PERSIST_CFG = <threads>x<rows>x<ctas per SM> (tuning; default below)
+    static void* pick_persistent(bool jacobi, int& nt, int& min_ctas) {
+        static const int cfg = [] {
+            const char* e = std::getenv("KRYSP_PERSIST_CFG");
+            if (!e) return 0;
+            const std::string v(e);
+            if (v == "512x4x1") return 0;
+            if (v == "1024x2x1") return 1;
+            if (v == "256x4x2") return 2;
+            if (v == "512x2x2") return 3;
+            if (v == "256x2x4") return 4;
+            return 0;
         }();
-        return v;
+        switch (cfg) {
+            case 1: nt = 1024, min_ctas = 1;
+                return jacobi ? (void*)pcg_persistent_kernel<true, 1024, 2, 1> : (void*)pcg_persistent_kernel<false, 1024, 2, 1>;
+            case 2: nt = 256, min_ctas = 2;
+                return jacobi ? (void*)pcg_persistent_kernel<true, 256, 4, 2> : (void*)pcg_persistent_kernel<false, 256, 4, 2>;
+            case 3: nt = 512, min_ctas = 2;
+                return jacobi ? (void*)pcg_persistent_kernel<true, 512, 2, 2> : (void*)pcg_persistent_kernel<false, 512, 2, 2>;
+            case 4: nt = 256, min_ctas = 4;
+                return jacobi ? (void*)pcg_persistent_kernel<true, 256, 2, 4> : (void*)pcg_persistent_kernel<false, 256, 2, 4>;
+            default: nt = 512, min_ctas = 1;
+                return jacobi ? (void*)pcg_persistent_kernel<true, 512, 4, 1> : (void*)pcg_persistent_kernel<false, 512, 4, 1>;
+        }
     }
 
     void launch_persistent(int64_t budget) {
@@ -2097,8 +2119,7 @@ struct PcgSession {
         double* part_r = c->d_partials + 3 * kPartialCap;
         long long bud = budget;
         void* args[] = {&A, &px, &pr, &pp, &pap, &inv, &st, &part_s, &part_r, &bar, &hist, &d_trace, &bud};
-        auto* k = e.jacobi ? pcg_persistent_kernel<true> : pcg_persistent_kernel<false>;
-        KG_CUDA(cudaLaunchCooperativeKernel((void*)k, dim3(pc_grid), dim3(kPcNT), args, 0, c->stream));
+        KG_CUDA(cudaLaunchCooperativeKernel(pc_kernel, dim3(pc_grid), dim3(pc_nt), args, 0, c->stream));
         KG_LAUNCH(c);
         ++launches_total;
     }

@@ -1,7 +1,8 @@
 """C1 (P-CG + Jacobi, poisson2d 1000, 1 M rows, CSR) FAST rate: iterations / device seconds of
 full tol-1e-6 solves (CUDA events around the iteration loop), median of 5, plus the parity
 numbers against the reference golden (1422 iterations, 8.653095e-07).
-Env: KRYSP_PERSIST=0 selects the 3-kernel graph path instead of the persistent grid."""
+Env: KRYSP_PERSIST=1 (+ KRYSP_PERSIST_CFG) selects the persistent cooperative grid instead of the
+3-kernel graph path."""
 import json
 import os
 import statistics
