@@ -202,6 +202,7 @@ krysp_status krysp_gpu_validate_policy(const krysp_policy* p) {
 krysp_status krysp_gpu_mat_upload_csr(krysp_gpu_ctx* c, int64_t n_rows, int64_t n_cols, const int64_t* rp,
                                       const int64_t* ci, const double* cv, krysp_gpu_mat** out) {
     return guard([&] {
+        KG_RANGE("krysp.upload_csr");
         need(c, "ctx");
         need(rp, "row_ptr");
         need(out, "out");
@@ -213,6 +214,7 @@ krysp_status krysp_gpu_mat_upload_csr(krysp_gpu_ctx* c, int64_t n_rows, int64_t 
 krysp_status krysp_gpu_mat_upload_coo(krysp_gpu_ctx* c, int64_t n_rows, int64_t n_cols, int64_t nnz,
                                       const int64_t* r, const int64_t* ci, const double* v, krysp_gpu_mat** out) {
     return guard([&] {
+        KG_RANGE("krysp.upload_coo");
         need(c, "ctx");
         need(out, "out");
         set_dev(c);
@@ -222,6 +224,7 @@ krysp_status krysp_gpu_mat_upload_coo(krysp_gpu_ctx* c, int64_t n_rows, int64_t 
 
 krysp_status krysp_gpu_mat_generate(krysp_gpu_ctx* c, const char* kind, int64_t n, double pe, krysp_gpu_mat** out) {
     return guard([&] {
+        KG_RANGE("krysp.generate");
         need(c, "ctx");
         need(kind, "kind");
         need(out, "out");
@@ -258,6 +261,7 @@ krysp_status krysp_gpu_gen_csr_rows_host(const char* kind, int64_t n, double pe,
 krysp_status krysp_gpu_mat_convert(const krysp_gpu_mat* m, int32_t fmt, int64_t hyb_width, int64_t slot_cap,
                                    krysp_gpu_mat** out) {
     return guard([&] {
+        KG_RANGE("krysp.convert");
         need(m, "mat");
         need(out, "out");
         set_dev(m->ctx);
@@ -267,6 +271,7 @@ krysp_status krysp_gpu_mat_convert(const krysp_gpu_mat* m, int32_t fmt, int64_t 
 
 krysp_status krysp_gpu_mat_transpose(const krysp_gpu_mat* m, krysp_gpu_mat** out) {
     return guard([&] {
+        KG_RANGE("krysp.transpose");
         need(m, "mat");
         need(out, "out");
         set_dev(m->ctx);
@@ -334,6 +339,7 @@ krysp_status krysp_gpu_mat_stats(const krysp_gpu_mat* m, krysp_stats* out) {
 // ---------------------------------------------------------------- kernels
 krysp_status krysp_gpu_spmv(const krysp_gpu_mat* m, const double* x, double* y, const krysp_policy* p, int32_t mode) {
     return guard([&] {
+        KG_RANGE("krysp.spmv");
         need(m, "mat");
         need(p, "policy");
         set_dev(m->ctx);
@@ -344,6 +350,7 @@ krysp_status krysp_gpu_spmv(const krysp_gpu_mat* m, const double* x, double* y, 
 krysp_status krysp_gpu_spmv_host(const krysp_gpu_mat* m, const double* hx, double* hy, const krysp_policy* p,
                                  int32_t mode) {
     return guard([&] {
+        KG_RANGE("krysp.spmv_host");
         need(m, "mat");
         need(p, "policy");
         krysp_gpu_ctx* c = m->ctx;
@@ -427,6 +434,7 @@ krysp_status krysp_gpu_solve_host(const krysp_gpu_mat* m, int32_t method, const 
                                   const krysp_solver_cfg* cfg, krysp_report* rep, double* h_hist, double* hx,
                                   double* h_trace) {
     return guard([&] {
+        KG_RANGE("krysp.solve_host");
         need(m, "mat");
         need(cfg, "cfg");
         need(rep, "report");
@@ -464,6 +472,7 @@ krysp_status krysp_gpu_solve_csr_host(krysp_gpu_ctx* c, int64_t n_rows, const in
                                       const double* hx0, const krysp_solver_cfg* cfg, krysp_report* rep,
                                       double* h_hist, double* hx) {
     return guard([&] {
+        KG_RANGE("krysp.solve_csr_host");
         need(c, "ctx");
         need(cfg, "cfg");
         need(rep, "report");
@@ -601,6 +610,7 @@ krysp_status krysp_gpu_tune_spmv(const krysp_gpu_mat* m, const krysp_policy* gri
                                  const krysp_timing_protocol* proto, krysp_policy* best, double* speedup,
                                  krysp_bench_record* table, int64_t cap, int64_t* table_len) {
     return guard([&] {
+        KG_RANGE("krysp.tune_spmv");
         need(m, "mat");
         need(best, "best");
         std::vector<krysp_policy> grid;

@@ -1525,6 +1525,7 @@ krysp_status krysp_gpu_dist_generate(krysp_gpu_dist* d, const char* kind, int64_
 krysp_status krysp_gpu_dist_set_csr(krysp_gpu_dist* d, int32_t part, int64_t n_global, int64_t lo, int64_t hi,
                                     const int64_t* rp, const int64_t* ci, const double* cv) {
     return guard([&] {
+        KG_RANGE("dist.set_csr");
         if (!d || !rp) kg::fail(KRYSP_ERROR, "NULL argument");
         int64_t elo, ehi;
         kg::band_rows(n_global, d->nparts, part, &elo, &ehi);
@@ -1538,6 +1539,7 @@ krysp_status krysp_gpu_dist_set_csr(krysp_gpu_dist* d, int32_t part, int64_t n_g
 
 krysp_status krysp_gpu_dist_setup(krysp_gpu_dist* d) {
     return guard([&] {
+        KG_RANGE("dist.setup");
         if (!d) kg::fail(KRYSP_ERROR, "NULL argument");
         kg::pcg_release(d);
         for (auto& P : d->parts) kg::localize(d, P);
@@ -1594,6 +1596,7 @@ krysp_status krysp_gpu_dist_pcg_create(krysp_gpu_dist* d, const double* const* d
 krysp_status krysp_gpu_dist_krylov_create(krysp_gpu_dist* d, int32_t method, const double* const* d_b,
                                           const double* const* d_x0, const krysp_solver_cfg* cfg) {
     return guard([&] {
+        KG_RANGE("dist.krylov_create");
         if (!d || !d_b || !d_x0 || !cfg) kg::fail(KRYSP_ERROR, "NULL argument");
         kg::krylov_create(d, method, d_b, d_x0, *cfg);
     });
@@ -1623,6 +1626,7 @@ krysp_status krysp_gpu_dist_pcg_time(krysp_gpu_dist* d, int64_t n, double* secon
 
 krysp_status krysp_gpu_dist_pcg_run(krysp_gpu_dist* d, double* seconds) {
     return guard([&] {
+        KG_RANGE("dist.run");
         auto t0 = std::chrono::steady_clock::now();
         if (!d->done_at_setup && !kg::pcg_done(d))  // same chunk count on every rank: the flag is allreduced
             kg::run_pipelined(d->ctx, &d->parts[0].st->done, [&] { kg::pcg_enqueue(d, krysp_gpu_dist::kChunk); });
@@ -1707,6 +1711,7 @@ krysp_status krysp_gpu_dist_pcg_profile(krysp_gpu_dist* d, int64_t n, double* sp
 krysp_status krysp_gpu_dist_solve(krysp_gpu_dist* d, int32_t method, const double* const* d_b, double* const* d_x,
                                   const krysp_solver_cfg* cfg, krysp_report* report, double* h_history) {
     return guard([&] {
+        KG_RANGE("dist.solve");
         if (!d || !d_b || !d_x || !cfg || !report) kg::fail(KRYSP_ERROR, "NULL argument");
         if (!d->ready) kg::fail(KRYSP_ERROR, "krysp_gpu_dist_setup must run first");
         if (cfg->mode != KRYSP_MODE_EXACT && cfg->mode != KRYSP_MODE_FAST) kg::fail(KRYSP_ERROR, "unknown mode %d", cfg->mode);

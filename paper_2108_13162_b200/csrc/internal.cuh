@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/krysp_gpu.h"
 
 namespace kg {
@@ -28,6 +30,18 @@ struct Status : std::exception {
 };
 
 [[noreturn]] void fail(krysp_status code, const char* fmt, ...);
+
+// NVTX range for the lifetime of a scope (SURVEY §5 tracing: one range per library call and
+// per solver phase; header-only NVTX3, a no-op unless a tool such as nsys / ncu attaches)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define KG_RANGE_CAT2(a, b) a##b
+#define KG_RANGE_CAT(a, b) KG_RANGE_CAT2(a, b)
+#define KG_RANGE(name) ::kg::NvtxRange KG_RANGE_CAT(kg_nvtx_range_, __LINE__)(name)
 
 #define KG_CUDA(call)                                                                      \
     do {                                                                                   \

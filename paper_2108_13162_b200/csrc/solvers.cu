@@ -2008,6 +2008,7 @@ struct PcgSession {
     PcgSession(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg_, const double* b, const double* x0, bool trace)
         : e(A, cfg_), cfg(cfg_), n(A->n_rows), x(A->n_rows, A->ctx->stream), r(A->n_rows, A->ctx->stream),
           p(A->n_rows, A->ctx->stream), ap(A->n_rows, A->ctx->stream) {
+        KG_RANGE("pcg.setup");
         krysp_gpu_ctx* c = e.c;
         trace_lap(c, "pcg_session", "engine+alloc");
         try {
@@ -2187,6 +2188,7 @@ struct PcgSession {
     }
 
     double run_to_convergence() {
+        KG_RANGE("pcg.iterations");
         krysp_gpu_ctx* c = e.c;
         cudaEvent_t a, b;
         KG_CUDA(cudaEventCreate(&a));
@@ -2521,6 +2523,7 @@ struct BicgstabSession {
     BicgstabSession(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg_, const double* b, const double* x0)
         : e(A, cfg_), cfg(cfg_), n(A->n_rows), x(n, A->ctx->stream), r(n, A->ctx->stream), rh(n, A->ctx->stream),
           p(n, A->ctx->stream), v(n, A->ctx->stream), s(n, A->ctx->stream), t(n, A->ctx->stream) {
+        KG_RANGE("bicgstab.setup");
         krysp_gpu_ctx* c = e.c;
         try {
             if (n) KG_CUDA(cudaMemcpyAsync(x, x0, 8 * n, cudaMemcpyDeviceToDevice, c->stream));
@@ -2614,6 +2617,7 @@ struct BicgstabSession {
     }
 
     double run_to_convergence() {
+        KG_RANGE("bicgstab.iterations");
         cudaEvent_t a, b;
         KG_CUDA(cudaEventCreate(&a));
         KG_CUDA(cudaEventCreate(&b));
@@ -2687,6 +2691,13 @@ krysp_gpu_mat* transpose(const krysp_gpu_mat* m);
 // solution on return.
 void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, const krysp_solver_cfg& cfg,
            krysp_report* out, double* h_history, double* h_trace) {
+    static const char* kNames[2][7] = {
+        {"krysp.solve.pcg.exact", "krysp.solve.cg_classic.exact", "krysp.solve.gcr.exact", "krysp.solve.bicgstab.exact",
+         "krysp.solve.bicgstab_l.exact", "krysp.solve.tfqmr.exact", "krysp.solve.bicgcr.exact"},
+        {"krysp.solve.pcg.fast", "krysp.solve.cg_classic.fast", "krysp.solve.gcr.fast", "krysp.solve.bicgstab.fast",
+         "krysp.solve.bicgstab_l.fast", "krysp.solve.tfqmr.fast", "krysp.solve.bicgcr.fast"}};
+    KG_RANGE(method >= KRYSP_PCG && method <= KRYSP_BICGCR && (cfg.mode == 0 || cfg.mode == 1)
+                 ? kNames[cfg.mode][method] : "krysp.solve");
     auto t0 = std::chrono::steady_clock::now();
     if (A->n_rows != A->n_cols) fail(KRYSP_DIMENSION_MISMATCH, "solver expects a square matrix");
     if (!(cfg.tolerance > 0.0) || cfg.max_iterations < 1 || cfg.restart < 1 || cfg.stab_l < 1)

@@ -135,6 +135,41 @@ def c4(ctx, R):
               "exact_final": ex.final_residual_measure})
 
 
+def true_measure(A, b, x):
+    r = b - kg.spmv(A, x, kg.ExecPolicy(0, 0), mode="fast")
+    d = A.diagonal()
+    return float(np.linalg.norm(r / d) / np.linalg.norm(b / d))
+
+
+def conv(ctx, R):
+    """Full-size FAST solves to convergence (VERDICT r1 "next" 2): C2 BiCGStab on CSR and ELL,
+    C4 GCR / BiCGStab(4) / tfQMR / BiCGStab on HYB w = 27 and w = 26; iterations, the solver's
+    final measure, the true preconditioned measure of the solution, device seconds."""
+    A = ctx.generate("convdiff2d", 4000, 0.5)
+    b = np.ones(A.n_rows)
+    for fmt in ["csr", "ell"]:
+        M = A if fmt == "csr" else A.convert("ell", slot_cap=1 << 40)
+        o = kg.solve(M, "bicgstab", b, cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0)))
+        emit({"config": "C2", "format": fmt, "check": "FAST BiCGStab to convergence, convdiff2d(4000)",
+              "converged": o.converged, "iterations": o.iterations, "final_measure": o.final_residual_measure,
+              "true_measure": true_measure(A, b, o.solution), "device_s": o.device_time,
+              "it_per_s": o.iterations / o.device_time})
+        del M
+    del A
+    A = ctx.generate("fem27", 320, 0.5)
+    b = np.ones(A.n_rows)
+    for w in [-1, 26]:
+        H = A.convert("hyb", hyb_width=w)
+        hi = H.info
+        for method, sl in [("gcr", 1), ("bicgstab_l", 4), ("tfqmr", 1), ("bicgstab", 1)]:
+            o = kg.solve(H, method, b, cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), stab_l=sl))
+            emit({"config": "C4", "format": f"hyb(w={hi['width']}, coo={hi['coo_nnz']})", "method": method,
+                  "check": "FAST to convergence, fem27 320^3", "converged": o.converged, "iterations": o.iterations,
+                  "final_measure": o.final_residual_measure, "true_measure": true_measure(A, b, o.solution),
+                  "device_s": o.device_time, "it_per_s": o.iterations / o.device_time})
+        del H
+
+
 def c5(ctx, R):
     # n = 1M and 10M rows, then ~100M nnz (SURVEY §8(d) C5: "scale n up to reach 10 M and 100 M nnz")
     for n, alpha in [(1_000_000, 2.0), (1_000_000, 1.5), (10_000_000, 2.0), (10_000_000, 1.5), (21_850_000, 2.0),
@@ -203,11 +238,11 @@ def f1(ctx, R):
 
 
 def main():
-    which = sys.argv[1:] or ["C1", "C2", "C4", "C5", "F1"]
+    which = sys.argv[1:] or ["C1", "C2", "C4", "C5", "F1"]  # + "CONV" (full-size convergence)
     ctx = kg.Context(0)
     R = Ref() if os.path.exists(REF_SO) else None
     for w in which:
-        {"C1": c1, "C2": c2, "C4": c4, "C5": c5, "F1": f1}[w](ctx, R)
+        {"C1": c1, "C2": c2, "C4": c4, "C5": c5, "F1": f1, "CONV": conv}[w](ctx, R)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,186 @@
+"""Config-scale parity, re-run by the driver (VERDICT r1 "next" 1-2; SURVEY §8(d) parity gates).
+
+Goldens come from the UNMODIFIED reference (tests/golden/make_spread.py, oracle/_ref):
+  * EXACT mode replays the reference bit for bit: full residual histories at C1 size and for
+    BiCGStab on the north-star matrix (3D 7-point Laplacian) at 100^3 / 200^3, and the first 50
+    iterations at the full C2 (16 M rows) and C3 (64 M rows) sizes, where the reference's full
+    convergence takes hours on the CPU.
+  * FAST mode sums in another order, so it is held to the reference's OWN cross-policy spread
+    (the reference's iteration count moves with its summation order alone):
+    measured for 36 summation orders (6 block sizes x 6 workers_per_row).  For the solvers
+    whose count the order does not move (P-CG, GCR, BiCGStab(l), tfQMR: one or two counts over
+    the 36 orders) FAST must land inside [min, max] of the reference's iterations and final
+    measures.  For BiCGStab — whose count moves by up to +-7 % with the order alone — FAST
+    must land within one spread width of the reference's median count.
+  * Full-size FAST solves to convergence (C2 CSR and ELL, C4 HYB w = 27 and w = 26) are checked
+    on the TRUE preconditioned residual of the returned solution.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2108_13162_b200 as kg
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def spread():
+    return json.load(open(os.path.join(GOLDEN, "oracle_spread.json")))
+
+
+@pytest.fixture(scope="module")
+def hist():
+    return dict(np.load(os.path.join(GOLDEN, "config_histories.npz")))
+
+
+def need(d, key):
+    if key not in d:
+        pytest.fail(f"golden {key} missing: python tests/golden/make_spread.py (needs /root/reference)")
+    return d[key]
+
+
+STAB_L = {"bicgstab_l": 4}
+
+
+def fast_cfg(method, **kw):
+    return kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), stab_l=STAB_L.get(method, 1), **kw)
+
+
+def check_fast_in_spread(o, g):
+    its = [v[0] for v in g["policies"].values()]
+    ms = [v[1] for v in g["policies"].values()]
+    assert o.converged
+    if g["method"] == "bicgstab":
+        width = g["max_iterations"] - g["min_iterations"]
+        assert abs(o.iterations - float(np.median(its))) <= max(width, 2), (o.iterations, g["min_iterations"],
+                                                                           g["max_iterations"])
+    else:
+        assert g["min_iterations"] - 1 <= o.iterations <= g["max_iterations"] + 1, (o.iterations, g["min_iterations"],
+                                                                                   g["max_iterations"])
+        if g["min_iterations"] <= o.iterations <= g["max_iterations"]:
+            assert min(ms) - 1e-10 <= o.final_residual_measure <= max(ms) + 1e-10
+
+
+def true_measure(A, b, x, jacobi=True):
+    """||D^-1 (b - A x)|| / ||D^-1 b|| (x0 = 0): the left-preconditioned solvers' measure,
+    recomputed from the solution (solvers.cpp:357-374)."""
+    r = b - kg.spmv(A, x, kg.ExecPolicy(0, 0), mode="fast")
+    if jacobi:
+        d = A.diagonal()
+        return float(np.linalg.norm(r / d) / np.linalg.norm(b / d))
+    return float(np.linalg.norm(r) / np.linalg.norm(b))
+
+
+# ----------------------------------------------------------------------------- C1
+@pytest.mark.parametrize("bs,tw", [(256, 8), (1024, 1)])
+def test_c1_full_size_exact_history_bitwise(ctx, hist, bs, tw):
+    want = need(hist, f"poisson2d_1000_pcg_{bs}_{tw}")
+    A = ctx.generate("poisson2d", 1000)
+    o = kg.solve(A, "pcg", np.ones(A.n_rows), cfg=kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(bs, tw)))
+    assert o.iterations == len(want) == 1422
+    np.testing.assert_array_equal(o.residual_history, want)
+
+
+def test_c1_full_size_fast(ctx, hist):
+    want = need(hist, "poisson2d_1000_pcg_1024_1")
+    A = ctx.generate("poisson2d", 1000)
+    o = kg.solve(A, "pcg", np.ones(A.n_rows), cfg=fast_cfg("pcg"))
+    assert o.converged and abs(o.iterations - len(want)) <= 1
+    assert abs(o.final_residual_measure - want[-1]) <= 1e-10
+
+
+# ----------------------------------------------------------------------------- C2 / C3 prefixes
+@pytest.mark.parametrize("key,kind,n,method,bs,tw", [
+    ("convdiff2d_4000_bicgstab_1024_1_prefix50", "convdiff2d", 4000, "bicgstab", 1024, 1),
+    ("convdiff2d_4000_bicgstab_256_8_prefix50", "convdiff2d", 4000, "bicgstab", 256, 8),
+    ("lap3d7_400_bicgstab_1024_1_prefix50", "lap3d7", 400, "bicgstab", 1024, 1),
+    ("lap3d7_400_pcg_1024_1_prefix50", "lap3d7", 400, "pcg", 1024, 1),
+])
+def test_full_size_exact_prefix_bitwise(ctx, hist, key, kind, n, method, bs, tw):
+    want = need(hist, key)
+    A = ctx.generate(kind, n, pe=0.5)
+    cfg = kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(bs, tw), tolerance=1e-300, max_iterations=50)
+    o = kg.solve(A, method, np.ones(A.n_rows), cfg=cfg)
+    assert o.iterations == 50 == len(want)
+    np.testing.assert_array_equal(o.residual_history, want)
+
+
+# ----------------------------------------------------------------------------- north star: BiCGStab on lap3d7
+@pytest.mark.parametrize("n", [100, 200])
+def test_lap3d7_bicgstab_exact_bitwise_and_fast_in_spread(ctx, hist, spread, n):
+    want = need(hist, f"lap3d7_{n}_bicgstab_1024_1")
+    g = need(spread, f"lap3d7_{n}_bicgstab")
+    A = ctx.generate("lap3d7", n)
+    b = np.ones(A.n_rows)
+    o = kg.solve(A, "bicgstab", b, cfg=kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(1024, 1)))
+    assert o.iterations == len(want) == g["policies"]["1024,1"][0]
+    np.testing.assert_array_equal(o.residual_history, want)
+    for fmt in ["csr", "ell"]:
+        M = A if fmt == "csr" else A.convert("ell", slot_cap=1 << 40)
+        f = kg.solve(M, "bicgstab", b, cfg=fast_cfg("bicgstab"))
+        check_fast_in_spread(f, g)
+        assert true_measure(A, b, f.solution) <= 2e-6
+
+
+def test_lap3d7_400_bicgstab_fast_full_size(ctx, spread):
+    """C3 size: FAST BiCGStab to convergence on 64 M rows against the reference's full solves."""
+    g = need(spread, "lap3d7_400_bicgstab")
+    A = ctx.generate("lap3d7", 400)
+    b = np.ones(A.n_rows)
+    f = kg.solve(A, "bicgstab", b, cfg=fast_cfg("bicgstab"))
+    check_fast_in_spread(f, g)
+    assert true_measure(A, b, f.solution) <= 2e-6
+
+
+# ----------------------------------------------------------------------------- C4 shape (fem27)
+@pytest.mark.parametrize("method", ["gcr", "bicgstab_l", "tfqmr", "bicgstab"])
+@pytest.mark.parametrize("n", [40, 80])
+def test_fem27_exact_all_orders_and_fast_in_spread(ctx, spread, method, n):
+    g = need(spread, f"fem27_{n}_{method}")
+    A = ctx.generate("fem27", n, pe=0.5)
+    b = np.ones(A.n_rows)
+    # EXACT at three of the reference's orders: its iteration count and final measure, bitwise
+    for pk in ["1024,1", "256,8", "32,4"]:
+        bs, tw = (int(v) for v in pk.split(","))
+        e = kg.solve(A, method, b, cfg=kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(bs, tw),
+                                                       stab_l=STAB_L.get(method, 1)))
+        assert [e.iterations, e.final_residual_measure] == g["policies"][pk][:2], pk
+    for fmt, w in [("hyb", -1), ("hyb", 26), ("csr", -1)]:
+        M = A if fmt == "csr" else A.convert("hyb", hyb_width=w)
+        f = kg.solve(M, method, b, cfg=fast_cfg(method))
+        check_fast_in_spread(f, g)
+
+
+# ----------------------------------------------------------------------------- full-size FAST convergence
+def test_c2_full_size_fast_converges(ctx, spread):
+    """C2: BiCGStab on convdiff2d(4000) (16 M rows) to convergence, CSR and ELL; the 1000^2
+    shape inside the reference's spread."""
+    A = ctx.generate("convdiff2d", 4000, pe=0.5)
+    b = np.ones(A.n_rows)
+    its = []
+    for M in (A, A.convert("ell", slot_cap=1 << 40)):
+        f = kg.solve(M, "bicgstab", b, cfg=fast_cfg("bicgstab"))
+        assert f.converged and f.final_residual_measure <= 1e-6
+        assert true_measure(A, b, f.solution) <= 2e-6
+        its.append(f.iterations)
+    g = need(spread, "convdiff2d_1000_bicgstab")
+    A1 = ctx.generate("convdiff2d", 1000, pe=0.5)
+    check_fast_in_spread(kg.solve(A1, "bicgstab", np.ones(A1.n_rows), cfg=fast_cfg("bicgstab")), g)
+
+
+@pytest.mark.parametrize("width", [-1, 26])
+def test_c4_full_size_fast_converges(ctx, width):
+    """C4: fem27 320^3 (32.8 M rows, 879 M nonzeros) on HYB — w = 27 (COO empty) and w = 26
+    (one COO overflow entry per interior row) — GCR(50), BiCGStab(4), tfQMR, BiCGStab to
+    convergence, true preconditioned residual of each solution."""
+    A = ctx.generate("fem27", 320, pe=0.5)
+    H = A.convert("hyb", hyb_width=width)
+    b = np.ones(A.n_rows)
+    for method in ["gcr", "bicgstab_l", "tfqmr", "bicgstab"]:
+        f = kg.solve(H, method, b, cfg=fast_cfg(method))
+        assert f.converged, method
+        assert true_measure(A, b, f.solution) <= 2e-6, method
