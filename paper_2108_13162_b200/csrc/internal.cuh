@@ -226,6 +226,15 @@ T* dev_alloc_records(int64_t count, cudaStream_t s) {
     return dev_alloc<T>(count, true, s);
 }
 
+// An output array every element of which the caller's kernel writes: no zero fill of the body
+// (a memset of a C4-size CSR is 10 GB of writes), only the kPad tail the vector loads may touch
+template <typename T>
+T* dev_alloc_out(int64_t count, cudaStream_t s) {
+    T* p = dev_alloc<T>((count > 0 ? count : 0) + kPad, false, s);
+    KG_CUDA(cudaMemsetAsync(p + (count > 0 ? count : 0), 0, sizeof(T) * kPad, s));
+    return p;
+}
+
 // RAII owner of one dev_alloc block: setup scratch that must not leak when a call throws
 template <typename T>
 struct DevBuf {
