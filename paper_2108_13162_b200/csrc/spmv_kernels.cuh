@@ -267,7 +267,10 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
 
 // ------------------------------------------------------------------ ELL
 // Thread per row, column-major slab => every slot load is a coalesced 32-lane stream.
-template <class Epi, int KB>
+// kTail: the HYB overflow rows are finished in the same pass (launch_ell_tail); a separate
+// instantiation, so the plain kernels keep their register count (the wide-slab 8-slot store
+// kernel goes from 48 to 64 registers with the tail loop: one CTA per SM fewer, C4 -25 %)
+template <class Epi, int KB, bool kTail = false>
 __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
     pdl_trigger();
     if (!epi.active()) return;
@@ -321,7 +324,7 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
                     if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * ld), __ldg(x + c));
                 }
             }
-            if (E.trp)  // HYB overflow of this row, continuing the sum in column order
+            if (kTail)  // HYB overflow of this row, continuing the sum in column order
                 for (int32_t k = E.trp[r], e = E.trp[r + 1]; k < e; ++k)
                     sum = madd(sum, __ldcs(E.tval + k), __ldg(x + __ldcs(E.tcol + k)));
             epi.row(r, sum);
@@ -455,11 +458,11 @@ inline void launch_ell_tail(const krysp_gpu_mat* m, const double* x, Epi epi, in
     E.tcol = m->co_c;
     E.tval = m->co_v;
     if (epi_is_store<Epi>::value) {
-        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 8><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8, true>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 8, true><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
     } else {
-        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 4><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4, true>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 4, true><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
     }
     KG_LAUNCH(c);
 }

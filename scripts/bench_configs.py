@@ -149,11 +149,15 @@ def conv(ctx, R):
     b = np.ones(A.n_rows)
     for fmt in ["csr", "ell"]:
         M = A if fmt == "csr" else A.convert("ell", slot_cap=1 << 40)
-        o = kg.solve(M, "bicgstab", b, cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0)))
-        emit({"config": "C2", "format": fmt, "check": "FAST BiCGStab to convergence, convdiff2d(4000)",
-              "converged": o.converged, "iterations": o.iterations, "final_measure": o.final_residual_measure,
-              "true_measure": true_measure(A, b, o.solution), "device_s": o.device_time,
-              "it_per_s": o.iterations / o.device_time})
+        try:
+            o = kg.solve(M, "bicgstab", b, cfg=kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0)))
+            emit({"config": "C2", "format": fmt, "check": "FAST BiCGStab to convergence, convdiff2d(4000)",
+                  "converged": o.converged, "iterations": o.iterations, "final_measure": o.final_residual_measure,
+                  "true_measure": true_measure(A, b, o.solution), "device_s": o.device_time,
+                  "it_per_s": o.iterations / o.device_time})
+        except kg.Error as e:  # the residual hump overflows double precision (the reference's too)
+            emit({"config": "C2", "format": fmt, "check": "FAST BiCGStab to convergence, convdiff2d(4000)",
+                  "outcome": type(e).__name__, "message": str(e)})
         del M
     del A
     A = ctx.generate("fem27", 320, 0.5)

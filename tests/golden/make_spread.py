@@ -39,8 +39,9 @@ STAB_L = {"bicgstab_l": 4}
 
 
 def matrix(R, P, kind, n):
-    if kind in ("poisson2d", "convdiff2d"):
-        return R.generate(kind, n, 0.5)          # the reference's own generator
+    """Every config matrix in CSR (the configs' format; the solvers' SpMV order depends on it)."""
+    if kind in ("poisson2d", "convdiff2d"):  # the reference's own generator (COO) -> its coo_to_csr
+        return R.convert(R.generate(kind, n, 0.5), "csr")
     return R.from_csr(P.generate(kind, n, 0.5))  # survey generator, C restatement
 
 
