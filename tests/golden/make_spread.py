@@ -146,6 +146,18 @@ def c2(R, P, spr, hist):
 
 
 @section
+def tfqmr_stall(R, P, spr, hist):
+    """tfQMR on fem27 240^3 (13.8 M rows): the reference's recurrence stagnates (measure
+    0.98988... from iteration 2 on; 320^3 likewise at 0.99060...).  Its first 100 measures."""
+    A = matrix(R, P, "fem27", 240)
+    nr = R.info(A)["n_rows"]
+    t = time.time()
+    r = history(R, A, nr, "tfqmr", 1024, 1, prefix=100)
+    hist["fem27_240_tfqmr_1024_1_prefix100"] = r["residual_history"]
+    print(f"  fem27 240^3 tfqmr prefix 100 ({time.time() - t:.1f} s)", flush=True)
+
+
+@section
 def c2_full(R, P, spr, hist):
     """C2 BiCGStab to the end at 2000^2 and the full 4000^2: the reference's residual hump
     (3e82 at 1000^2, iteration 1499) outgrows double precision, so the reference itself stops
