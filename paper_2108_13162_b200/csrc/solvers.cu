@@ -652,6 +652,79 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
     }
 }
 
+// ---- the direction pass merged into the next SpMV (2 kernels per P-CG iteration)
+// p_new = D^-1 r + beta p_old (solvers.cpp:154-157) is a function of vectors the update kernel
+// has finished, so the SpMV forms it where it gathers it (XDir) instead of a pass writing p
+// first; the epilogue stores p_new for its own rows, applies the previous iteration's deferred
+// x += alpha p_old, and sums <p_new, Ap>.  Same expressions, same roundings as
+// cg_direction_kernel: the iterates are bit-identical to the 3-kernel iteration's.  p is
+// double-buffered (the gathers read p_old while the rows write p_new).
+template <bool kJacobi>
+struct XDir {
+    const double* __restrict__ r;
+    const double* __restrict__ inv;
+    const double* __restrict__ p;
+    const CgState* st;
+    double beta;
+    __device__ __forceinline__ void init() { beta = __ldcg(&st->beta); }
+    __device__ __forceinline__ double operator()(int32_t c) const {
+        const double rc = __ldg(r + c);
+        const double z = kJacobi ? __dmul_rn(rc, __ldg(inv + c)) : rc;
+        return __dadd_rn(__dmul_rn(beta, __ldg(p + c)), z);
+    }
+};
+
+template <bool kJacobi>
+struct EpiCgDir {
+    double* __restrict__ ap;
+    double* __restrict__ p_new;
+    const double* __restrict__ p_old;
+    const double* __restrict__ r;
+    const double* __restrict__ inv;
+    double* __restrict__ x;
+    double* partials;
+    unsigned* counter;
+    CgState* st;
+    double acc;
+    double alpha_prev, beta;
+    bool loaded;
+    __device__ __forceinline__ bool active() const { return *(volatile int*)&st->done == 0; }
+    __device__ __forceinline__ void row(int64_t i, double v) {
+        if (!loaded) {  // read before this block arrives, i.e. before the last block updates alpha
+            alpha_prev = __ldcg(&st->alpha);
+            beta = __ldcg(&st->beta);
+            loaded = true;
+        }
+        const double po = p_old[i], ri = r[i];
+        const double z = kJacobi ? __dmul_rn(ri, inv[i]) : ri;
+        const double pn = __dadd_rn(__dmul_rn(beta, po), z);
+        p_new[i] = pn;
+        x[i] = __dadd_rn(__dmul_rn(alpha_prev, po), x[i]);
+        ap[i] = v;
+        acc = fma(pn, v, acc);
+    }
+    __device__ __forceinline__ void finish() {
+        EpiCgSigma tail{ap, nullptr, partials, counter, st, acc};
+        tail.finish();
+    }
+};
+
+// after the iteration that ended the solve: its x += alpha p (p in the buffer its SpMV
+// wrote, chosen by the parity of the iteration count)
+__global__ void cg_finalize_kernel(int64_t n, double* __restrict__ x, const double* __restrict__ p0,
+                                   const double* __restrict__ p1, CgState* st, unsigned* counter) {
+    if (!*(volatile const int*)&st->done || !*(volatile const int*)&st->x_pending) return;
+    const double alpha = st->alpha;
+    const double* p = (st->iter & 1) ? p1 : p0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+    __syncthreads();
+    if (last_block(counter) && threadIdx.x == 0) {
+        *counter = 0;
+        st->x_pending = 0;
+    }
+}
+
 // generic epilogue pass for formats whose row values are not final inside one kernel
 template <class Epi>
 __global__ void __launch_bounds__(1024) vec_epi_kernel(int64_t n, const double* __restrict__ y, Epi epi) {
@@ -661,13 +734,29 @@ __global__ void __launch_bounds__(1024) vec_epi_kernel(int64_t n, const double* 
     epi.finish();
 }
 
-template <class Epi>
-void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y, Epi epi) {
+// the load-balanced (irregular-row / COO) kernels take x as a plain vector; every other
+// kernel can gather it from an x source (XPtr / XDir)
+bool spmv_irregular(const Engine& e, const krysp_gpu_mat* m) {
+    const bool tail = e.auto_pol && hyb_tail_fusable(m);
+    return e.auto_pol && !tail &&
+           ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) || m->format == KRYSP_FMT_COO ||
+            (m->format == KRYSP_FMT_HYB && m->coo_nnz));
+}
+
+// the kernels spmv_fused_mx reaches with an x source (XDir): tile / vector CSR, ELL, HYB
+// without overflow or with the short overflow the ELL pass finishes
+bool spmv_takes_xsource(const Engine& e, const krysp_gpu_mat* m) {
+    if (e.auto_pol && hyb_tail_fusable(m)) return true;
+    if (spmv_irregular(e, m)) return false;
+    return m->format == KRYSP_FMT_CSR || m->format == KRYSP_FMT_ELL ||
+           (m->format == KRYSP_FMT_HYB && m->coo_nnz == 0);
+}
+
+template <class Epi, class X>
+void spmv_fused_mx(Engine& e, const krysp_gpu_mat* m, X x, double* y, Epi epi) {
     cudaStream_t s = e.c->stream;
     const bool tail = e.auto_pol && hyb_tail_fusable(m);  // HYB overflow finished inside the ELL pass
-    const bool irregular = e.auto_pol && !tail &&
-                           ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) || m->format == KRYSP_FMT_COO ||
-                            (m->format == KRYSP_FMT_HYB && m->coo_nnz));
+    const bool irregular = spmv_irregular(e, m);
     if (tail) {
         if (m->width < 16) {
             launch_ell_tail(m, x, epi, e.pol.block_size, s);
@@ -693,15 +782,31 @@ void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y,
             KG_LAUNCH(e.c);
         }
     } else {
-        spmv_launch(m, x, y, e.launch_pol(), e.mode, s, e.gate);
-        vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y, epi);
-        KG_LAUNCH(e.c);
+        if constexpr (std::is_convertible_v<X, const double*>) {
+            spmv_launch(m, x, y, e.launch_pol(), e.mode, s, e.gate);
+            vec_epi_kernel<Epi><<<grid_for(m->n_rows, 1024, (int64_t)e.c->sm_count * 2), 1024, 0, s>>>(m->n_rows, y,
+                                                                                                       epi);
+            KG_LAUNCH(e.c);
+        } else {
+            fail(KRYSP_ERROR, "internal: an x source on the load-balanced SpMV path");
+        }
     }
 }
 
 template <class Epi>
+void spmv_fused_m(Engine& e, const krysp_gpu_mat* m, const double* x, double* y, Epi epi) {
+    spmv_fused_mx(e, m, x, y, epi);
+}
+
+template <class Epi>
 void spmv_fused(Engine& e, const double* x, double* y, Epi epi) {
-    spmv_fused_m(e, e.A, x, y, epi);
+    spmv_fused_mx(e, e.A, x, y, epi);
+}
+
+// x gathered from an x source (XDir) instead of a vector
+template <class Epi, class XS>
+void spmv_fused_xs(Engine& e, XS xs, double* y, Epi epi) {
+    spmv_fused_mx(e, e.A, xs, y, epi);
 }
 
 // y = D^-1 (A x): the left-Jacobi operator in one pass (spmv_into + copy + scal_elementwise,
@@ -1989,12 +2094,18 @@ struct PcgSession {
     krysp_solver_cfg cfg;
     int64_t n;
     DVec x, r, p, ap;
+    DVec p1;  // merged iteration: the second direction buffer (p_j lives in P[(j + 1) % 2])
     CgState* st = nullptr;
     double* hist = nullptr;
     double* d_trace = nullptr;
     double measure0 = 0.0;
     bool done_at_setup = false;
+    // merged: 2 kernels per iteration (direction pass inside the SpMV, XDir / EpiCgDir);
+    // graphs per starting parity of the direction buffers
+    bool merged = false;
+    int next_parity = 0;
     cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr, exec_prof = nullptr;
+    cudaGraphExec_t exec_chunk1 = nullptr, exec_one1 = nullptr, exec_prof1 = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int kernels_per_iteration = 0;
     // persistent cooperative path (pcg_persistent_kernel) for systems of C1's size class
@@ -2017,8 +2128,17 @@ struct PcgSession {
             e.residual(b, x, r);
             double norm_r0 = e.norm2(r);
             if (norm_r0 == 0.0) norm_r0 = 1.0;
-            e.precond(r, p);  // z, which the first iteration takes as p (swap, no beta term)
-            const double rho = e.dot(r, p);
+            setup_persistent_flag();
+            merged = !persistent && spmv_takes_xsource(e, A) && merged_enabled();
+            double rho;
+            if (merged) {  // z into p1 for rho; P0 = 0, alpha = beta = 0: the first merged
+                p1 = DVec(n, c->stream);  // iteration writes p_0 = z_0 + 0 * 0 = z_0 exactly
+                e.precond(r, p1);
+                rho = e.dot(r, p1);
+            } else {
+                e.precond(r, p);  // z, which the first iteration takes as p (swap, no beta term)
+                rho = e.dot(r, p);
+            }
             measure0 = rho / norm_r0;
             CgState h{};
             h.rho = rho;
@@ -2037,10 +2157,14 @@ struct PcgSession {
             stream_wait(c);
             trace_lap(c, "pcg_session", "setup kernels");
             for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
-            setup_persistent();
-            if (!persistent) {
-                exec_chunk = capture(kChunk, false);
-                exec_one = capture(1, false);
+            if (persistent) setup_persistent();
+            else {
+                exec_chunk = capture(kChunk, false, 0);
+                exec_one = capture(1, false, 0);
+                if (merged) {
+                    exec_chunk1 = capture(kChunk, false, 1);
+                    exec_one1 = capture(1, false, 1);
+                }
                 trace_lap(c, "pcg_session", "graph capture");
             }
         } catch (...) {
@@ -2051,10 +2175,8 @@ struct PcgSession {
     ~PcgSession() { release(); }
 
     void release() {
-        if (exec_chunk) cudaGraphExecDestroy(exec_chunk);
-        if (exec_one) cudaGraphExecDestroy(exec_one);
-        if (exec_prof) cudaGraphExecDestroy(exec_prof);
-        exec_chunk = exec_one = exec_prof = nullptr;
+        for (cudaGraphExec_t* g : {&exec_chunk, &exec_one, &exec_prof, &exec_chunk1, &exec_one1, &exec_prof1})
+            if (*g) cudaGraphExecDestroy(*g), *g = nullptr;
         for (auto& v : ev)
             if (v) cudaEventDestroy(v), v = nullptr;
         dev_free(st);
@@ -2066,8 +2188,28 @@ struct PcgSession {
         hist = d_trace = nullptr;
     }
 
+    // KRYSP_MERGED=1: the 2-kernel iteration (direction pass merged into the SpMV).  Measured
+    // (profiles/r02_merged_pcg.md): C3 575 -> 534 it/s (the SpMV gathering three vectors, r,
+    // D^-1 and p_old, goes from 0.955 to 1.570 ms while the saved direction pass took 0.485 ms),
+    // C1 29.0 -> 28.8 k it/s — so the 3-kernel iteration stays the default
+    static bool merged_enabled() {
+        static const bool v = [] {
+            const char* s = std::getenv("KRYSP_MERGED");
+            return s && s[0] == '1';
+        }();
+        return v;
+    }
+
+    void setup_persistent_flag() {
+        if (!pcg_persistent_eligible(e.A)) return;
+        int coop = 0;
+        KG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, e.c->device));
+        persistent = coop != 0;
+    }
+
     void setup_persistent() {
         krysp_gpu_ctx* c = e.c;
+        persistent = false;
         if (!pcg_persistent_eligible(e.A)) return;
         int coop = 0;
         KG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, c->device));
@@ -2125,7 +2267,7 @@ struct PcgSession {
         ++launches_total;
     }
 
-    void iteration(bool events) {
+    void iteration(bool events, int parity) {
         krysp_gpu_ctx* c = e.c;
         double* part_a = c->d_partials + 2 * kPartialCap;
         double* part_b = c->d_partials + 3 * kPartialCap;
@@ -2133,33 +2275,47 @@ struct PcgSession {
         unsigned* cnt_b = c->d_counters + 3;
         const unsigned g_vec = grid_for(n, kFusedNT, (int64_t)c->sm_count * 8);
         const int64_t before = c->launches;
+        const double* inv = e.jacobi ? (const double*)e.inv : nullptr;
+        double* p_old = parity ? (double*)p1 : (double*)p;
+        double* p_new = parity ? (double*)p : (double*)p1;
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[0], c->stream, cudaEventRecordExternal));
-        EpiCgSigma epi{ap, p, part_a, cnt_a, st, 0.0};
-        spmv_fused(e, p, ap, epi);
+        if (merged) {
+            if (e.jacobi)
+                spmv_fused_xs(e, XDir<true>{r, inv, p_old, st, 0.0},
+                           ap, EpiCgDir<true>{ap, p_new, p_old, r, inv, x, part_a, cnt_a, st, 0.0, 0.0, 0.0, false});
+            else
+                spmv_fused_xs(e, XDir<false>{r, nullptr, p_old, st, 0.0},
+                           ap, EpiCgDir<false>{ap, p_new, p_old, r, nullptr, x, part_a, cnt_a, st, 0.0, 0.0, 0.0, false});
+        } else {
+            EpiCgSigma epi{ap, p, part_a, cnt_a, st, 0.0};
+            spmv_fused(e, (const double*)p, ap, epi);
+        }
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
         // update and direction passes by programmatic dependent launch (the SpMV tile kernel
         // by PDL too was measured: C1 +1.6%, C3 577 -> 491 it/s; not adopted): each grid is resident
         // while its predecessor's tail drains and waits in pdl_wait() for its results
         KG_CUDA(launch_pdl(e.jacobi ? cg_update_kernel<true> : cg_update_kernel<false>, g_vec, kFusedNT, 0, c->stream,
-                           n, (double*)x, (double*)r, (const double*)p, (const double*)ap, (e.jacobi ? (const double*)e.inv : nullptr),
+                           n, (double*)x, (double*)r, (const double*)(merged ? p_new : p), (const double*)ap, inv,
                            st, part_b, cnt_b, hist, d_trace));
         KG_LAUNCH(c);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
-        unsigned* cnt_c = c->d_counters + 5;
-        KG_CUDA(launch_pdl(e.jacobi ? cg_direction_kernel<true> : cg_direction_kernel<false>, g_vec, kFusedNT, 0,
-                           c->stream, n, (double*)p, (const double*)r, (e.jacobi ? (const double*)e.inv : nullptr), (double*)x, st, cnt_c));
-        KG_LAUNCH(c);
+        if (!merged) {
+            unsigned* cnt_c = c->d_counters + 5;
+            KG_CUDA(launch_pdl(e.jacobi ? cg_direction_kernel<true> : cg_direction_kernel<false>, g_vec, kFusedNT, 0,
+                               c->stream, n, (double*)p, (const double*)r, inv, (double*)x, st, cnt_c));
+            KG_LAUNCH(c);
+        }
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[3], c->stream, cudaEventRecordExternal));
         kernels_per_iteration = (int)(c->launches - before);
     }
 
-    cudaGraphExec_t capture(int iters, bool events) {
+    cudaGraphExec_t capture(int iters, bool events, int parity0) {
         krysp_gpu_ctx* c = e.c;
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
         KG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         try {
-            for (int i = 0; i < iters; ++i) iteration(events);
+            for (int i = 0; i < iters; ++i) iteration(events, (parity0 + i) & 1);
         } catch (...) {
             cudaStreamEndCapture(c->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
@@ -2175,8 +2331,22 @@ struct PcgSession {
     void enqueue(int64_t iters) {
         krysp_gpu_ctx* c = e.c;
         if (persistent) return launch_persistent(iters);
-        for (int64_t i = 0; i + kChunk <= iters; i += kChunk) KG_CUDA(cudaGraphLaunch(exec_chunk, c->stream));
-        for (int64_t i = 0; i < iters % kChunk; ++i) KG_CUDA(cudaGraphLaunch(exec_one, c->stream));
+        for (int64_t i = 0; i + kChunk <= iters; i += kChunk)
+            KG_CUDA(cudaGraphLaunch(merged && next_parity ? exec_chunk1 : exec_chunk, c->stream));
+        for (int64_t i = 0; i < iters % kChunk; ++i) {
+            KG_CUDA(cudaGraphLaunch(merged && next_parity ? exec_one1 : exec_one, c->stream));
+            if (merged) next_parity ^= 1;
+        }
+    }
+
+    // merged iteration: the deferred x += alpha p of the iteration that ended the solve (a
+    // later iteration's SpMV epilogue applies it when one is enqueued; this covers the rest)
+    void finalize() {
+        if (!merged) return;
+        krysp_gpu_ctx* c = e.c;
+        cg_finalize_kernel<<<grid_for(n, kFusedNT, (int64_t)c->sm_count * 8), kFusedNT, 0, c->stream>>>(
+            n, x, p, p1, st, c->d_counters + 5);
+        KG_LAUNCH(c);
     }
 
     bool finished() {
@@ -2196,6 +2366,7 @@ struct PcgSession {
         KG_CUDA(cudaEventRecord(a, c->stream));
         if (persistent) launch_persistent(cfg.max_iterations);  // one grid for the whole solve
         else if (!finished()) run_pipelined(c, &st->done, [&] { enqueue(kChunk); });
+        finalize();
         KG_CUDA(cudaEventRecord(b, c->stream));
         KG_CUDA(cudaEventSynchronize(b));
         float ms = 0.f;
@@ -2208,10 +2379,13 @@ struct PcgSession {
     // n single-iteration graphs with event nodes: mean seconds of [spmv, update, direction]
     void profile(int64_t iters, double out[3]) {
         krysp_gpu_ctx* c = e.c;
-        if (!exec_prof) exec_prof = capture(1, true);  // event-node graph, built on first use
+        if (persistent) fail(KRYSP_ERROR, "per-kernel profile: the persistent P-CG grid is one kernel");
+        if (!exec_prof) exec_prof = capture(1, true, 0);  // event-node graphs, built on first use
+        if (merged && !exec_prof1) exec_prof1 = capture(1, true, 1);
         out[0] = out[1] = out[2] = 0.0;
         for (int64_t i = 0; i < iters; ++i) {
-            KG_CUDA(cudaGraphLaunch(exec_prof, c->stream));
+            KG_CUDA(cudaGraphLaunch(merged && next_parity ? exec_prof1 : exec_prof, c->stream));
+            if (merged) next_parity ^= 1;
             KG_CUDA(cudaEventSynchronize(ev[3]));
             for (int k = 0; k < 3; ++k) {
                 float ms = 0.f;
@@ -2932,6 +3106,7 @@ krysp_status krysp_gpu_solver_report(krysp_gpu_solver* h, krysp_report* rep, dou
 krysp_status krysp_gpu_solver_solution(krysp_gpu_solver* h, double* x) {
     return guard([&] {
         if (!h || !x) kg::fail(KRYSP_ERROR, "NULL argument");
+        if (h->pcg) h->pcg->finalize();
         h->visit([&](auto& s) {
             if (s.n) KG_CUDA(cudaMemcpyAsync(x, s.x, 8 * s.n, cudaMemcpyDeviceToDevice, s.e.c->stream));
             KG_CUDA(cudaStreamSynchronize(s.e.c->stream));

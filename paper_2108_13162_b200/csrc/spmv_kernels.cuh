@@ -32,6 +32,21 @@ __device__ __forceinline__ double madd(double acc, double a, double b) {
     return __dadd_rn(acc, __dmul_rn(a, b));
 }
 
+// x sources: where an SpMV kernel gathers x[c] from.  XPtr is a plain vector; a solver may
+// form x on the fly from the vectors it is a function of (XDir in solvers.cu: the P-CG
+// direction p_new = D^-1 r + beta p_old, so the direction pass merges into the SpMV).  init()
+// runs once per thread at kernel start (loads scalars of the running solve).
+struct XPtr {
+    const double* __restrict__ p;
+    __device__ __forceinline__ void init() {}
+    __device__ __forceinline__ double operator()(int32_t c) const { return __ldg(p + c); }
+};
+inline XPtr xs_of(const double* p) { return XPtr{p}; }
+template <class XS>
+inline XS xs_of(XS s) {
+    return s;
+}
+
 struct EpiStore {
     double* __restrict__ y;
     __device__ __forceinline__ bool active() const { return true; }
@@ -65,10 +80,11 @@ struct epi_is_store<EpiStoreGated<G>> : std::true_type {};
 // ------------------------------------------------------------------ CSR vector (paper)
 // One segment of TW lanes per row; virtual blocks of blockDim.x threads cover
 // blockDim.x / TW rows each.  Every lane participates in the shuffles.
-template <int TW, class Epi>
-__global__ void csr_vector_kernel(CsrView A, const double* __restrict__ x, Epi epi, int64_t n_vblocks) {
+template <int TW, class Epi, class XS = XPtr>
+__global__ void csr_vector_kernel(CsrView A, XS x, Epi epi, int64_t n_vblocks) {
     pdl_trigger();
     if (!epi.active()) return;
+    x.init();
     const int lane = threadIdx.x & (TW - 1);
     for (int64_t vb = blockIdx.x; vb < n_vblocks; vb += gridDim.x) {
         const int64_t row = (vb * blockDim.x + threadIdx.x) / TW;
@@ -76,7 +92,7 @@ __global__ void csr_vector_kernel(CsrView A, const double* __restrict__ x, Epi e
         if (row < A.n_rows) {
             const int32_t b = A.row_ptr[row], e = A.row_ptr[row + 1];
 #pragma unroll 4
-            for (int32_t k = b + lane; k < e; k += TW) sum = madd(sum, __ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)));
+            for (int32_t k = b + lane; k < e; k += TW) sum = madd(sum, __ldcs(A.val + k), x(__ldcs(A.col + k)));
         }
 #pragma unroll
         for (int off = TW / 2; off >= 1; off >>= 1) sum = __dadd_rn(sum, __shfl_down_sync(0xffffffffu, sum, off, TW));
@@ -154,11 +170,11 @@ struct epi_staged<E, std::void_t<decltype(E::kStaged)>> {
 // sums entries l, l + TW, ... sequentially from 0.0 and the lanes fold with the shuffle tree
 // of csr_vector_kernel — the reference's tw-lane order (kernels.cpp:175-186), so any policy
 // with a tile that fits the stage runs on the TMA pipeline bit-identically.
-template <int TW, class Epi>
-__global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const double* __restrict__ x, Epi epi,
-                                                            TmaTileLayout L) {
+template <int TW, class Epi, class XS = XPtr>
+__global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, XS x, Epi epi, TmaTileLayout L) {
     pdl_trigger();
     if (!epi.active()) return;
+    x.init();
     constexpr int TR = kTileRows / TW;
     extern __shared__ __align__(128) unsigned char smem_tma[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma);  // 2 mbarriers
@@ -229,7 +245,7 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
                 const int32_t rb = s_rp[tr], re = s_rp[tr + 1];
                 const int av = rb - (k0 & ~1), ac = rb - (k0 & ~3), len = re - rb;
 #pragma unroll 4
-                for (int j = lane; j < len; j += TW) sum = madd(sum, s_val[av + j], __ldg(x + s_col[ac + j]));
+                for (int j = lane; j < len; j += TW) sum = madd(sum, s_val[av + j], x(s_col[ac + j]));
             }
 #pragma unroll
             for (int off = TW / 2; off >= 1; off >>= 1) sum = __dadd_rn(sum, __shfl_down_sync(0xffffffffu, sum, off, TW));
@@ -243,13 +259,13 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
                 double xv[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if (j < len) xv[j] = __ldg(x + s_col[ac + j]);
+                    if (j < len) xv[j] = x(s_col[ac + j]);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     if (j < len) sum = madd(sum, s_val[av + j], xv[j]);
             } else {
 #pragma unroll 8
-                for (int j = 0; j < len; ++j) sum = madd(sum, s_val[av + j], __ldg(x + s_col[ac + j]));
+                for (int j = 0; j < len; ++j) sum = madd(sum, s_val[av + j], x(s_col[ac + j]));
             }
             if constexpr (NS > 0) {
                 double sv[NS > 0 ? NS : 1];
@@ -270,10 +286,11 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, const dou
 // kTail: the HYB overflow rows are finished in the same pass (launch_ell_tail); a separate
 // instantiation, so the plain kernels keep their register count (the wide-slab 8-slot store
 // kernel goes from 48 to 64 registers with the tail loop: one CTA per SM fewer, C4 -25 %)
-template <class Epi, int KB, bool kTail = false>
-__global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
+template <class Epi, int KB, bool kTail = false, class XS = XPtr>
+__global__ void ell_kernel(EllView E, XS x, Epi epi) {
     pdl_trigger();
     if (!epi.active()) return;
+    x.init();
     const int64_t n = E.n_rows, ld = E.ld;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r - threadIdx.x < n;
          r += (int64_t)gridDim.x * blockDim.x) {
@@ -296,7 +313,7 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
                         }
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
+                    for (int j = 0; j < 8; ++j) xv[j] = c[j] != E.n_cols ? x(c[j]) : 0.0;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
                         if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
@@ -314,19 +331,19 @@ __global__ void ell_kernel(EllView E, const double* __restrict__ x, Epi epi) {
                         v[j] = __ldcs(cf + (int64_t)(s + j) * ld);
                     }
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) xv[j] = c[j] != E.n_cols ? __ldg(x + c[j]) : 0.0;
+                    for (int j = 0; j < 4; ++j) xv[j] = c[j] != E.n_cols ? x(c[j]) : 0.0;
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         if (c[j] != E.n_cols) sum = madd(sum, v[j], xv[j]);
                 }
                 for (; s < E.width; ++s) {
                     const int32_t c = __ldcs(jc + (int64_t)s * ld);
-                    if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * ld), __ldg(x + c));
+                    if (c != E.n_cols) sum = madd(sum, __ldcs(cf + (int64_t)s * ld), x(c));
                 }
             }
             if (kTail)  // HYB overflow of this row, continuing the sum in column order
                 for (int32_t k = E.trp[r], e = E.trp[r + 1]; k < e; ++k)
-                    sum = madd(sum, __ldcs(E.tval + k), __ldg(x + __ldcs(E.tcol + k)));
+                    sum = madd(sum, __ldcs(E.tval + k), x(__ldcs(E.tcol + k)));
             epi.row(r, sum);
         }
     }
@@ -368,19 +385,20 @@ inline int64_t bounded_grid(krysp_gpu_ctx* c, int per_sm, int64_t work_blocks) {
     return work_blocks < cap ? work_blocks : cap;
 }
 
-template <int TW, class Epi>
-inline int64_t launch_csr_vector_tw(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
+template <int TW, class Epi, class X>
+inline int64_t launch_csr_vector_tw(const krysp_gpu_mat* m, X x_, Epi epi, int64_t bs, cudaStream_t s) {
     const int64_t nvb = (TW * m->n_rows + bs - 1) / bs;  // grid_spmv_blocks
     if (nvb == 0) return 0;
-    auto k = csr_vector_kernel<TW, Epi>;
+    auto x = xs_of(x_);
+    auto k = csr_vector_kernel<TW, Epi, decltype(x)>;
     const int64_t g = bounded_grid(m->ctx, resident_blocks(k, (int)bs, 0), nvb);
     k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), x, epi, nvb);
     KG_LAUNCH(m->ctx);
     return g;
 }
 
-template <class Epi>
-inline void launch_csr_vector(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, int64_t tw, cudaStream_t s) {
+template <class Epi, class X>
+inline void launch_csr_vector(const krysp_gpu_mat* m, X x, Epi epi, int64_t bs, int64_t tw, cudaStream_t s) {
     switch (tw) {
         case 1: launch_csr_vector_tw<1>(m, x, epi, bs, s); break;
         case 2: launch_csr_vector_tw<2>(m, x, epi, bs, s); break;
@@ -399,8 +417,9 @@ inline int64_t tile_nnz_bound(const krysp_gpu_mat* m, int64_t tw) {
     return tw == 1 ? m->max_tile_nnz : std::min<int64_t>(m->max_tile_nnz, m->max_row * (kTileRows / tw));
 }
 
-template <int TW, class Epi>
-inline int64_t launch_csr_tile_tw(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s) {
+template <int TW, class Epi, class X>
+inline int64_t launch_csr_tile_tw(const krysp_gpu_mat* m, X x_, Epi epi, cudaStream_t s) {
+    auto x = xs_of(x_);
     krysp_gpu_ctx* c = m->ctx;
     constexpr int TR = kTileRows / TW;
     const int64_t tiles = (m->n_rows + TR - 1) / TR;
@@ -409,7 +428,7 @@ inline int64_t launch_csr_tile_tw(const krysp_gpu_mat* m, const double* x, Epi e
     cap = (cap + 3) & ~3;
     const TmaTileLayout L{cap, epi_staged<Epi>::value, TR};
     const int smem = L.total_bytes();
-    auto k = csr_tma_kernel<TW, Epi>;
+    auto k = csr_tma_kernel<TW, Epi, decltype(x)>;
     if (smem > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t g = bounded_grid(c, resident_blocks(k, kTileRows, smem), tiles);
     k<<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, L);
@@ -417,8 +436,8 @@ inline int64_t launch_csr_tile_tw(const krysp_gpu_mat* m, const double* x, Epi e
     return g;
 }
 
-template <class Epi>
-inline int64_t launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi, cudaStream_t s, int64_t tw = 1) {
+template <class Epi, class X>
+inline int64_t launch_csr_tile(const krysp_gpu_mat* m, X x, Epi epi, cudaStream_t s, int64_t tw = 1) {
     switch (tw) {
         case 2: return launch_csr_tile_tw<2>(m, x, epi, s);
         case 4: return launch_csr_tile_tw<4>(m, x, epi, s);
@@ -429,28 +448,32 @@ inline int64_t launch_csr_tile(const krysp_gpu_mat* m, const double* x, Epi epi,
     }
 }
 
-template <class Epi>
-inline void launch_ell(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
+template <class Epi, class X>
+inline void launch_ell(const krysp_gpu_mat* m, X x_, Epi epi, int64_t bs, cudaStream_t s) {
     krysp_gpu_ctx* c = m->ctx;
+    auto x = xs_of(x_);
+    using XS = decltype(x);
     const int64_t nvb = (m->n_rows + bs - 1) / bs;
     if (nvb == 0) return;
     // measured: 8-slot batches lose for the solver epilogues at any width (C2 w = 5, C4
     // w = 27: register-limited occupancy), win for the plain store
     if (epi_is_store<Epi>::value) {
-        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 8><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8, false, XS>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 8, false, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
     } else {
-        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 4><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4, false, XS>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 4, false, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
     }
     KG_LAUNCH(c);
 }
 
 // HYB with short COO overflow rows (hyb_tail_fusable): ELL slots + the row's COO tail in one
 // kernel, one write of y
-template <class Epi>
-inline void launch_ell_tail(const krysp_gpu_mat* m, const double* x, Epi epi, int64_t bs, cudaStream_t s) {
+template <class Epi, class X>
+inline void launch_ell_tail(const krysp_gpu_mat* m, X x_, Epi epi, int64_t bs, cudaStream_t s) {
     krysp_gpu_ctx* c = m->ctx;
+    auto x = xs_of(x_);
+    using XS = decltype(x);
     const int64_t nvb = (m->n_rows + bs - 1) / bs;
     if (nvb == 0) return;
     EllView E = m->ell();
@@ -458,11 +481,11 @@ inline void launch_ell_tail(const krysp_gpu_mat* m, const double* x, Epi epi, in
     E.tcol = m->co_c;
     E.tval = m->co_v;
     if (epi_is_store<Epi>::value) {
-        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8, true>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 8, true><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8, true, XS>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 8, true, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
     } else {
-        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4, true>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 4, true><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
+        const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4, true, XS>, (int)bs, 0), nvb);
+        ell_kernel<Epi, 4, true, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
     }
     KG_LAUNCH(c);
 }
