@@ -74,7 +74,8 @@ __device__ __forceinline__ double strided_row(RowsView A, const double* __restri
 // strided by the whole CTA.
 constexpr int kAdPer = kAdTile / kAdNT;
 
-__global__ void __launch_bounds__(kAdNT, 5) adaptive_kernel(RowsView A, const int32_t* __restrict__ blk, int64_t nblk,
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kAdNT, kMinBlocks) adaptive_kernel(RowsView A, const int32_t* __restrict__ blk, int64_t nblk,
                                                           const int32_t* __restrict__ med, int64_t nmed,
                                                           const int32_t* __restrict__ lng, int64_t nlng,
                                                           const int32_t* __restrict__ chunk, int64_t nchunk,
@@ -325,9 +326,12 @@ void run_plan(krysp_gpu_ctx* c, RowsView A, AdaptivePlan* P, const double* x, do
               cudaStream_t s, const int* gate) {
     const int64_t items = P->nchunk + P->nlng + (P->nmed + kAdNT / 32 - 1) / (kAdNT / 32) + P->nblk;
     if (items) {
-        const int64_t g = bounded_grid(c, resident_blocks(adaptive_kernel, kAdNT, 0), items);
-        adaptive_kernel<<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk,
-                                                      P->nchunk, P->partials, x, y, accumulate ? 1 : 0, gate);
+        // 5 CTAs per SM (48 registers); budgets for 6 / 8 CTAs spill and lose 5-45 % on C5
+        // at 100 M nnz, sliced or not (profiles/r02_c5_occupancy.jsonl)
+        auto k = adaptive_kernel<5>;
+        const int64_t g = bounded_grid(c, resident_blocks(k, kAdNT, 0), items);
+        k<<<(unsigned)g, kAdNT, 0, s>>>(A, P->blk, P->nblk, P->med, P->nmed, P->lng, P->nlng, P->chunk, P->nchunk,
+                                        P->partials, x, y, accumulate ? 1 : 0, gate);
         KG_LAUNCH(c);
     }
     if (P->ngiant) {
