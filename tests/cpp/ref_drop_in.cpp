@@ -111,8 +111,8 @@ CsrMatrix csr_of(const std::vector<Triple>& t, index_t n_rows, index_t n_cols) {
 
 int run() {
     namespace g = krysp::gpu;
-    const CsrMatrix spd = coo_to_csr(poisson2d(40));       // generators.cpp:15-32
-    const CsrMatrix ns = coo_to_csr(convdiff2d(40, 0.5));  // generators.cpp:46-68
+    const CsrMatrix spd = coo_to_csr(poisson2d(24));       // generators.cpp:15-32
+    const CsrMatrix ns = coo_to_csr(convdiff2d(24, 0.5));  // generators.cpp:46-68
     const index_t n = spd.n_rows;
     const std::vector<double> b(n, 1.0), x0(n, 0.0);
     std::vector<ExecPolicy> pols(3);
@@ -253,7 +253,7 @@ int run() {
     // ---- tuner (autotune.hpp:59-60): the reference's TuneResult type, 72 + 0 records
     {
         TimingProtocol proto;
-        const TuneResult t = g::tune_spmv(SparseMatrix(ns), default_policy_grid(), proto, "convdiff2d40");
+        const TuneResult t = g::tune_spmv(SparseMatrix(ns), default_policy_grid(), proto, "convdiff2d24");
         expect(t.table.size() == 72 && t.speedup_vs_default >= 1.0, "tune_spmv table");
         expect(bench_table_csv(t.table).rfind("kernel,matrix,block_size", 0) == 0, "tune table CSV (reference writer)");
     }
