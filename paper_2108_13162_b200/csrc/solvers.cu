@@ -652,6 +652,142 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
     }
 }
 
+// sense-free grid barrier: arrival counter reset by the last arriver, which then bumps the
+// generation the others spin on (counter reset before the bump: no early re-arrival race)
+__device__ __forceinline__ void pc_grid_sync(unsigned* count, unsigned* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = *(volatile unsigned*)gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*(volatile unsigned*)gen == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// every CTA: the grid total of partials[0..gridDim) in one fixed order (warp 0 strided sums,
+// then the warp tree) — bit-identical in all CTAs
+__device__ __forceinline__ double pc_grid_total(const double* partials, double* sh) {
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += __ldcg(partials + i);
+        t = warp_sum(t);
+        if (threadIdx.x == 0) sh[0] = t;
+    }
+    __syncthreads();
+    const double v = sh[0];
+    __syncthreads();
+    return v;
+}
+
+// ---- update and direction in one cooperative grid (C1-size systems)
+// Every thread owns at most kUdRows rows (grid-stride) and keeps their new r and z = D^-1 r in
+// registers across one grid barrier: phase 1 r -= alpha Ap and its <r, z> partial; barrier;
+// every CTA forms rho_new from the same partials in the same order (bit-identical), the lead
+// records history / trace / state; phase 2 x += alpha p, p = z + beta p.  Two kernels per P-CG
+// iteration instead of three, and r, D^-1 are read once instead of twice (V = 8 instead of 10).
+// Same expressions and roundings as cg_update_kernel + cg_direction_kernel; only the rho
+// reduction tree differs (FAST mode).
+constexpr int kUdNT = 256;
+
+template <bool kJacobi, int kUdRows>
+__global__ void __launch_bounds__(kUdNT) cg_update_dir_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                               double* __restrict__ p, const double* __restrict__ ap,
+                                                               const double* __restrict__ inv, CgState* st,
+                                                               double* partials, unsigned* bar, double* history,
+                                                               double* trace) {
+    __shared__ double sh[32];
+    // the state, read by every CTA before the grid barrier (the lead writes it only after)
+    __shared__ int s_done;
+    __shared__ double s_alpha, s_rho, s_beta, s_sigma, s_norm_r0, s_tol;
+    __shared__ long long s_iter, s_max_it;
+    if (threadIdx.x == 0) {
+        s_done = *(volatile int*)&st->done;
+        s_alpha = __ldcg(&st->alpha);
+        s_rho = __ldcg(&st->rho);
+        s_beta = __ldcg(&st->beta);
+        s_sigma = __ldcg(&st->sigma);
+        s_norm_r0 = __ldcg(&st->norm_r0);
+        s_tol = __ldcg(&st->tol);
+        s_iter = __ldcg(&st->iter);
+        s_max_it = __ldcg(&st->max_it);
+    }
+    __syncthreads();
+    if (s_done) return;  // uniform: every CTA read the same flag before anyone could change it
+    const double alpha = s_alpha, malpha = -alpha;
+    const int64_t stride = (int64_t)gridDim.x * kUdNT, i0 = blockIdx.x * (int64_t)kUdNT + threadIdx.x;
+    double rv[kUdRows], zv[kUdRows], av[kUdRows], iv[kUdRows];
+#pragma unroll
+    for (int q = 0; q < kUdRows; ++q) {  // all loads in flight first
+        const int64_t i = i0 + q * stride;
+        if (i < n) rv[q] = r[i], av[q] = ap[i], iv[q] = kJacobi ? inv[i] : 1.0;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kUdRows; ++q) {
+        const int64_t i = i0 + q * stride;
+        if (i < n) {
+            const double ri = __dadd_rn(__dmul_rn(malpha, av[q]), rv[q]);
+            r[i] = ri;
+            const double zi = kJacobi ? __dmul_rn(ri, iv[q]) : ri;
+            rv[q] = ri;
+            zv[q] = zi;
+            acc = fma(ri, zi, acc);
+        }
+    }
+    acc = block_sum<kUdNT>(acc, sh);
+    if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+    pc_grid_sync(bar, bar + 1);
+    const double rho_new = pc_grid_total(partials, sh);
+    const double rho = s_rho;
+    const long long it = s_iter;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    bool stop;
+    double beta = 0.0;
+    if (!isfinite(rho_new)) {
+        stop = true;
+    } else {
+        const double measure = rho_new / s_norm_r0;
+        beta = rho_new / rho;
+        stop = measure <= s_tol || it + 1 >= s_max_it;
+        if (lead) history[it] = measure;
+    }
+    if (lead) {
+        if (trace) {
+            double* t = trace + 4 * it;
+            t[0] = rho;
+            t[1] = s_beta;
+            t[2] = s_sigma;
+            t[3] = alpha;
+        }
+        if (!isfinite(rho_new)) {
+            st->status = kStNonFiniteRho;
+        } else {
+            st->iter = it + 1;
+            st->rho_1 = rho;
+            st->beta = beta;
+            st->rho = rho_new;
+        }
+        if (stop) st->done = 1;  // x += alpha p below, so nothing stays pending
+    }
+#pragma unroll
+    for (int q = 0; q < kUdRows; ++q) {
+        const int64_t i = i0 + q * stride;
+        if (i < n) {
+            const double pi = p[i];
+            x[i] = __dadd_rn(__dmul_rn(alpha, pi), x[i]);
+            if (!stop) p[i] = __dadd_rn(__dmul_rn(beta, pi), zv[q]);
+        }
+    }
+}
+
 // ---- the direction pass merged into the next SpMV (2 kernels per P-CG iteration)
 // p_new = D^-1 r + beta p_old (solvers.cpp:154-157) is a function of vectors the update kernel
 // has finished, so the SpMV forms it where it gathers it (XDir) instead of a pass writing p
@@ -1846,41 +1982,6 @@ void gcr_fast(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x
 // trace as the 3-kernel iteration (cg_update_kernel / cg_direction_kernel), so the two paths
 // share CgState and can alternate.
 
-// sense-free grid barrier: arrival counter reset by the last arriver, which then bumps the
-// generation the others spin on (counter reset before the bump: no early re-arrival race)
-__device__ __forceinline__ void pc_grid_sync(unsigned* count, unsigned* gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned g = *(volatile unsigned*)gen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            atomicExch(count, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (*(volatile unsigned*)gen == g) {
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// every CTA: the grid total of partials[0..gridDim) in one fixed order (warp 0 strided sums,
-// then the warp tree) — bit-identical in all CTAs
-__device__ __forceinline__ double pc_grid_total(const double* partials, double* sh) {
-    if (threadIdx.x < 32) {
-        double t = 0.0;
-        for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += __ldcg(partials + i);
-        t = warp_sum(t);
-        if (threadIdx.x == 0) sh[0] = t;
-    }
-    __syncthreads();
-    const double v = sh[0];
-    __syncthreads();
-    return v;
-}
-
 // kPcNT threads per CTA, kPcRows rows per thread whose loads are issued together, kPcMin CTAs
 // per SM the register budget is sized for
 template <bool kJacobi, int kPcNT, int kPcRows, int kPcMin>
@@ -2104,6 +2205,12 @@ struct PcgSession {
     // graphs per starting parity of the direction buffers
     bool merged = false;
     int next_parity = 0;
+    // cooperative update + direction (cg_update_dir_kernel) when every thread of one resident
+    // grid can hold its rows' r and z in registers
+    bool coop = false;
+    void* ud_kernel = nullptr;
+    unsigned ud_grid = 0;
+    unsigned* ud_bar = nullptr;
     cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr, exec_prof = nullptr;
     cudaGraphExec_t exec_chunk1 = nullptr, exec_one1 = nullptr, exec_prof1 = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -2159,6 +2266,7 @@ struct PcgSession {
             for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
             if (persistent) setup_persistent();
             else {
+                setup_coop();
                 exec_chunk = capture(kChunk, false, 0);
                 exec_one = capture(1, false, 0);
                 if (merged) {
@@ -2183,9 +2291,48 @@ struct PcgSession {
         dev_free(hist);
         dev_free(d_trace);
         dev_free(bar);
+        dev_free(ud_bar);
         st = nullptr;
         bar = nullptr;
+        ud_bar = nullptr;
         hist = d_trace = nullptr;
+    }
+
+    // KRYSP_COOP=0 turns the cooperative update + direction kernel off
+    static bool coop_enabled() {
+        static const bool v = [] {
+            const char* s = std::getenv("KRYSP_COOP");
+            return !(s && s[0] == '0');
+        }();
+        return v;
+    }
+
+    template <int R>
+    static void* ud_pick(bool jacobi) {
+        return jacobi ? (void*)cg_update_dir_kernel<true, R> : (void*)cg_update_dir_kernel<false, R>;
+    }
+
+    void setup_coop() {
+        krysp_gpu_ctx* c = e.c;
+        if (merged || persistent || !coop_enabled() || n == 0) return;
+        int coop_ok = 0;
+        KG_CUDA(cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, c->device));
+        if (!coop_ok) return;
+        void* ks[4] = {ud_pick<1>(e.jacobi), ud_pick<2>(e.jacobi), ud_pick<4>(e.jacobi), ud_pick<8>(e.jacobi)};
+        const int rows[4] = {1, 2, 4, 8};
+        for (int k = 0; k < 4; ++k) {
+            int per_sm = 0;
+            KG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks[k], kUdNT, 0));
+            const int64_t cap = (int64_t)per_sm * c->sm_count;
+            const int64_t need = (n + (int64_t)kUdNT * rows[k] - 1) / ((int64_t)kUdNT * rows[k]);
+            if (per_sm >= 1 && need <= cap && need <= kPartialCap) {
+                ud_kernel = ks[k];
+                ud_grid = (unsigned)need;
+                ud_bar = dev_alloc<unsigned>(2, true, c->stream);
+                coop = true;
+                return;
+            }
+        }
     }
 
     // KRYSP_MERGED=1: the 2-kernel iteration (direction pass merged into the SpMV).  Measured
@@ -2291,6 +2438,33 @@ struct PcgSession {
             spmv_fused(e, (const double*)p, ap, epi);
         }
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
+        if (coop) {  // update + direction in one cooperative grid
+            double* px = x;
+            double* pr = r;
+            double* pp = p;
+            const double* pap = ap;
+            double* d_hist = hist;
+            double* d_tr = d_trace;
+            CgState* pst = st;
+            unsigned* pbar = ud_bar;
+            int64_t nn = n;
+            void* args[] = {&nn, &px, &pr, &pp, &pap, (void*)&inv, &pst, &part_b, &pbar, &d_hist, &d_tr};
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(ud_grid);
+            lc.blockDim = dim3(kUdNT);
+            lc.stream = c->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            KG_CUDA(cudaLaunchKernelExC(&lc, ud_kernel, args));
+            KG_LAUNCH(c);
+            if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
+            if (events) KG_CUDA(cudaEventRecordWithFlags(ev[3], c->stream, cudaEventRecordExternal));
+            kernels_per_iteration = (int)(c->launches - before);
+            return;
+        }
         // update and direction passes by programmatic dependent launch (the SpMV tile kernel
         // by PDL too was measured: C1 +1.6%, C3 577 -> 491 it/s; not adopted): each grid is resident
         // while its predecessor's tail drains and waits in pdl_wait() for its results
