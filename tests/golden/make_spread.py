@@ -146,6 +146,15 @@ def c2(R, P, spr, hist):
 
 
 @section
+def lap3d7_400_pcg(R, P, spr, hist):
+    """The headline config (C3): the reference's full P-CG solve at <1024,1> (733 iterations)."""
+    A = matrix(R, P, "lap3d7", 400)
+    nr = R.info(A)["n_rows"]
+    spr["lap3d7_400_pcg"] = dict(kind="lap3d7", n=400, method="pcg", stab_l=1,
+                                 **spread(R, A, nr, "pcg", [(1024, 1)], "lap3d7 400^3"))
+
+
+@section
 def tfqmr_stall(R, P, spr, hist):
     """tfQMR on fem27 240^3 (13.8 M rows): the reference's recurrence stagnates (measure
     0.98988... from iteration 2 on; 320^3 likewise at 0.99060...).  Its first 100 measures."""

@@ -111,6 +111,16 @@ def test_full_size_exact_prefix_bitwise(ctx, hist, key, kind, n, method, bs, tw)
     np.testing.assert_array_equal(o.residual_history, want)
 
 
+def test_c3_pcg_exact_full_solve(ctx, spread):
+    """The headline config (C3, 64 M rows): EXACT P-CG reproduces the reference's full solve —
+    733 iterations and its final measure, bit for bit."""
+    g = need(spread, "lap3d7_400_pcg")
+    A = ctx.generate("lap3d7", 400)
+    e = kg.solve(A, "pcg", np.ones(A.n_rows), cfg=kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(1024, 1)))
+    assert [e.iterations, e.final_residual_measure] == g["policies"]["1024,1"][:2]
+    assert e.iterations == 733
+
+
 # ----------------------------------------------------------------------------- north star: BiCGStab on lap3d7
 @pytest.mark.parametrize("n", [100, 200])
 def test_lap3d7_bicgstab_exact_bitwise_and_fast_in_spread(ctx, hist, spread, n):
