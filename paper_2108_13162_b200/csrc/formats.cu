@@ -142,6 +142,10 @@ void mat_free_arrays(krysp_gpu_mat* m) {
     adaptive_free(m->ad_csr);
     adaptive_free(m->ad_coo);
     slices_free(m);
+    dev_free(m->long_csr);
+    dev_free(m->long_coo);
+    m->long_csr = m->long_coo = nullptr;
+    m->n_long_csr = m->n_long_coo = -1;
 }
 
 krysp_gpu_mat* mat_new(krysp_gpu_ctx* ctx, int32_t fmt, int64_t n_rows, int64_t n_cols) {

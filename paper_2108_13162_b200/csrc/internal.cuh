@@ -162,6 +162,11 @@ struct krysp_gpu_mat {
     int32_t* coo_rp = nullptr;        // row pointer over the COO entries (FAST COO / HYB)
     int64_t coo_max_row = -1;         // longest COO row segment (with coo_rp)
     kg::ColumnSlices* slices = nullptr;  // FAST irregular CSR with x larger than an L2 slice
+    // EXACT long rows (> kLongRow entries) of the CSR rows / the COO segments (built on first use)
+    int32_t* long_csr = nullptr;
+    int32_t n_long_csr = -1;
+    int32_t* long_coo = nullptr;
+    int32_t n_long_coo = -1;
     bool slices_checked = false;
     int32_t format = KRYSP_FMT_CSR;
     int64_t n_rows = 0, n_cols = 0, nnz = 0;

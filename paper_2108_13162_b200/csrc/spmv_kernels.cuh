@@ -80,8 +80,9 @@ struct epi_is_store<EpiStoreGated<G>> : std::true_type {};
 // ------------------------------------------------------------------ CSR vector (paper)
 // One segment of TW lanes per row; virtual blocks of blockDim.x threads cover
 // blockDim.x / TW rows each.  Every lane participates in the shuffles.
+// skip_long > 0: rows longer than that are left to long_rows_exact_kernel (plain SpMV only)
 template <int TW, class Epi, class XS = XPtr>
-__global__ void csr_vector_kernel(CsrView A, XS x, Epi epi, int64_t n_vblocks) {
+__global__ void csr_vector_kernel(CsrView A, XS x, Epi epi, int64_t n_vblocks, int32_t skip_long = 0) {
     pdl_trigger();
     if (!epi.active()) return;
     x.init();
@@ -89,16 +90,74 @@ __global__ void csr_vector_kernel(CsrView A, XS x, Epi epi, int64_t n_vblocks) {
     for (int64_t vb = blockIdx.x; vb < n_vblocks; vb += gridDim.x) {
         const int64_t row = (vb * blockDim.x + threadIdx.x) / TW;
         double sum = 0.0;
-        if (row < A.n_rows) {
+        bool mine = row < A.n_rows;
+        if (mine) {
             const int32_t b = A.row_ptr[row], e = A.row_ptr[row + 1];
+            if (skip_long && e - b > skip_long) {
+                mine = false;  // the same for every lane of the row
+            } else {
 #pragma unroll 4
-            for (int32_t k = b + lane; k < e; k += TW) sum = madd(sum, __ldcs(A.val + k), x(__ldcs(A.col + k)));
+                for (int32_t k = b + lane; k < e; k += TW) sum = madd(sum, __ldcs(A.val + k), x(__ldcs(A.col + k)));
+            }
         }
 #pragma unroll
         for (int off = TW / 2; off >= 1; off >>= 1) sum = __dadd_rn(sum, __shfl_down_sync(0xffffffffu, sum, off, TW));
-        if (row < A.n_rows && lane == 0) epi.row(row, sum);
+        if (mine && lane == 0) epi.row(row, sum);
     }
     epi.finish();
+}
+
+// ------------------------------------------------------------------ EXACT long rows
+// The reference's row order is sequential per lane (kernels.cpp:175-181), so a power-law row
+// of 10^4-10^5 entries is a dependent add chain whatever the hardware.  What need not be serial
+// are its loads and products: fl(val * x[col]) is formed before the add in madd, so a whole CTA
+// computes a chunk of the row's products into shared memory (coalesced, every gather in flight)
+// and then TW threads — lane l owning entries l, l + TW, ... — add them in order from shared
+// memory, carrying their sums across chunks; the lanes fold with the shuffle tree of
+// csr_vector_kernel.  Bit-identical to the lane order, a chain of ~4 cycles per entry instead of
+// one memory round trip per few entries (C5 EXACT at 10 M rows: one 93 k-entry row).
+constexpr int kLongRow = 512;       // rows longer than this take the long-row path
+constexpr int kLongChunk = 4096;    // products staged per chunk (32 KB)
+constexpr int kLongNT = 256;
+
+// rows: the long rows (any order); acc_from_y: continue from y[row] (coo_accumulate's segments)
+template <int TW>
+__global__ void __launch_bounds__(kLongNT) long_rows_exact_kernel(const int32_t* __restrict__ rp,
+                                                                  const int32_t* __restrict__ col,
+                                                                  const double* __restrict__ val,
+                                                                  const double* __restrict__ x,
+                                                                  const int32_t* __restrict__ rows, int32_t n_long,
+                                                                  double* __restrict__ y, int acc_from_y) {
+    __shared__ double prod[kLongChunk];
+    for (int32_t q = blockIdx.x; q < n_long; q += gridDim.x) {
+        const int32_t r = rows[q], b = rp[r], e = rp[r + 1];
+        double acc = (acc_from_y && threadIdx.x == 0) ? y[r] : 0.0;
+        for (int32_t c0 = b; c0 < e; c0 += kLongChunk) {
+            const int32_t len = min(kLongChunk, e - c0);
+            for (int32_t j = threadIdx.x; j < len; j += kLongNT)
+                prod[j] = __dmul_rn(__ldcs(val + c0 + j), __ldg(x + __ldcs(col + c0 + j)));
+            __syncthreads();
+            if (threadIdx.x < TW) {
+                // lane l's entries k = b + l + m*TW; c0 - b is a multiple of kLongChunk, hence
+                // of TW, so in this chunk they sit at j = l, l + TW, ...
+                int32_t jj = (int32_t)threadIdx.x;
+                for (; jj + 3 * TW < len; jj += 4 * TW) {
+                    const double p0 = prod[jj], p1 = prod[jj + TW], p2 = prod[jj + 2 * TW], p3 = prod[jj + 3 * TW];
+                    acc = __dadd_rn(acc, p0);
+                    acc = __dadd_rn(acc, p1);
+                    acc = __dadd_rn(acc, p2);
+                    acc = __dadd_rn(acc, p3);
+                }
+                for (; jj < len; jj += TW) acc = __dadd_rn(acc, prod[jj]);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x < 32) {
+#pragma unroll
+            for (int off = TW / 2; off >= 1; off >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, off, TW));
+            if (threadIdx.x == 0) y[r] = acc;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ CSR tile (tw == 1 order)
@@ -353,7 +412,9 @@ __global__ void ell_kernel(EllView E, XS x, Epi epi) {
 // ------------------------------------------------------------------ COO accumulate
 // coo_accumulate (kernels.cpp:134-149): each canonical row segment is walked in entry order
 // by the thread that owns its first entry; y[r] continues from its current value.
-__global__ void coo_accumulate_kernel(CooView O, const double* __restrict__ x, double* __restrict__ y);
+// skip_long > 0: segments longer than that are left to long_rows_exact_kernel
+__global__ void coo_accumulate_kernel(CooView O, const double* __restrict__ x, double* __restrict__ y,
+                                      int32_t skip_long = 0);
 
 // Largest shared-memory tile the CSR tile kernel will stage (entries).
 constexpr int kTileCapMax = 8192;
@@ -392,7 +453,7 @@ inline int64_t launch_csr_vector_tw(const krysp_gpu_mat* m, X x_, Epi epi, int64
     auto x = xs_of(x_);
     auto k = csr_vector_kernel<TW, Epi, decltype(x)>;
     const int64_t g = bounded_grid(m->ctx, resident_blocks(k, (int)bs, 0), nvb);
-    k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), x, epi, nvb);
+    k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), x, epi, nvb, 0);
     KG_LAUNCH(m->ctx);
     return g;
 }
@@ -492,5 +553,8 @@ inline void launch_ell_tail(const krysp_gpu_mat* m, X x_, Epi epi, int64_t bs, c
 
 void launch_coo_accumulate(const krysp_gpu_mat* m, const double* x, double* y, cudaStream_t s);
 bool csr_use_tile(const krysp_gpu_mat* m, int64_t tw);
+// EXACT plain SpMV of a CSR with rows longer than kLongRow: the vector kernel skips them and
+// long_rows_exact_kernel computes them (spmv.cu); false when the matrix has none
+bool launch_csr_vector_long(const krysp_gpu_mat* m, const double* x, double* y, int64_t bs, int64_t tw, cudaStream_t s);
 
 }  // namespace kg

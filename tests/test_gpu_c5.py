@@ -66,3 +66,22 @@ def test_slices_off_for_regular_and_small(ctx):
     assert kg.column_slices(ctx.generate("lap3d7", 60)) == 1      # regular rows: the TMA tile kernel
     m = kg.generate_csr("powerlaw", 100_000, alpha=2.0, seed=3)     # x = 0.8 MB: one slice
     assert kg.column_slices(ctx.upload(m)) == 1
+
+
+@pytest.mark.parametrize("alpha", [1.5, 2.0])
+def test_exact_long_rows_bitwise(ctx, port, alpha):
+    """EXACT SpMV on power-law rows (rows > 512 entries take the long-row kernel: products
+    staged by the CTA, lane-ordered sums) is bit-identical to the reference order in CSR for
+    every tw, and in HYB / COO (coo_accumulate's sequential segments)."""
+    from oracle.oracle import Csr
+    m = kg.generate_csr("powerlaw", 60_000, alpha=alpha, seed=11)
+    assert np.max(np.diff(m.row_ptr)) > 512
+    A = ctx.upload(m)
+    o = Csr(m.n_rows, m.n_cols, m.row_ptr, m.col_idx, m.values)
+    x = np.random.default_rng(3).uniform(-1, 1, m.n_cols)
+    for bs, tw in [(256, 1), (256, 8), (64, 32), (1024, 4)]:
+        got = kg.spmv(A, x, kg.ExecPolicy(bs, tw), mode="exact")
+        np.testing.assert_array_equal(got, port.spmv(o, x, "csr", bs, tw), err_msg=f"csr <{bs},{tw}>")
+    for fmt in ["hyb", "coo"]:
+        got = kg.spmv(A.convert(fmt), x, kg.ExecPolicy(256, 1), mode="exact")
+        np.testing.assert_array_equal(got, port.spmv(o, x, fmt, 256, 1), err_msg=fmt)
