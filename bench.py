@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "FP64 CG iterations/sec and SpMV GFLOP/s (+% HBM roofline) at 1/2/4/8 B200"
-GOLDEN_ITERS, GOLDEN_MEASURE = 733, 9.650895609e-07  # SURVEY §6 / §8(a12), oracle at 400^3
+GOLDEN_ITERS, GOLDEN_MEASURE = 733, 9.650895609309785e-07  # the reference solve_pcg at 400^3, <1024,1> (tests/golden/oracle_spread.json)
 TIMED_TOL = 1e-300  # timed steps: no convergence stop (see run_ours)
 STEP_NOTE = ("one full P-CG iteration; the W + K timed iterations run without a convergence stop "
              "(tol 1e-300), the tol-1e-6 solve (733 iterations) is the e2e / parity run")
