@@ -167,6 +167,15 @@ def tfqmr_stall(R, P, spr, hist):
 
 
 @section
+def c2_spread36(R, P, spr, hist):
+    """The C2 shape (convdiff2d 1000^2) under all 36 summation orders (~2 h on 8 cores)."""
+    A = matrix(R, P, "convdiff2d", 1000)
+    nr = R.info(A)["n_rows"]
+    spr["convdiff2d_1000_bicgstab"] = dict(kind="convdiff2d", n=1000, method="bicgstab", stab_l=1,
+                                           **spread(R, A, nr, "bicgstab", ALL36, "convdiff2d 1000^2"))
+
+
+@section
 def c2_full(R, P, spr, hist):
     """C2 BiCGStab to the end at 2000^2 and the full 4000^2: the reference's residual hump
     (3e82 at 1000^2, iteration 1499) outgrows double precision, so the reference itself stops
