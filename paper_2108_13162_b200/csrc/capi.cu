@@ -254,6 +254,7 @@ krysp_status krysp_gpu_gen_csr_rows_host(const char* kind, int64_t n, double pe,
     return guard([&] {
         need(kind, "kind");
         need(rp, "row_ptr");
+        if (ci) need(cv, "values");
         gen_csr_rows_host(kind, n, pe, row_lo, row_hi, rp, ci, cv);
     });
 }

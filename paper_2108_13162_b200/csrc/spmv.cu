@@ -41,15 +41,17 @@ __global__ void find_long_rows(const int32_t* __restrict__ rp, int64_t n, int32_
 
 int32_t long_rows(krysp_gpu_ctx* c, const int32_t* rp, int64_t n, int32_t** list) {
     DevBuf<int32_t> cnt(1, true, c->stream);
-    int32_t* out = dev_alloc<int32_t>(n + 1, false);
+    DevBuf<int32_t> all(n + 1, false);
     if (n) {
-        find_long_rows<<<grid_for(n, 256, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(rp, n, out, cnt);
+        find_long_rows<<<grid_for(n, 256, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(rp, n, all, cnt);
         KG_LAUNCH(c);
     }
     int32_t h = 0;
     KG_CUDA(cudaMemcpyAsync(&h, cnt, 4, cudaMemcpyDeviceToHost, c->stream));
     KG_CUDA(cudaStreamSynchronize(c->stream));
-    *list = out;
+    *list = dev_alloc<int32_t>(h + 1, false);  // the cached list: only the long rows
+    if (h) KG_CUDA(cudaMemcpyAsync(*list, all, 4 * (size_t)h, cudaMemcpyDeviceToDevice, c->stream));
+    KG_CUDA(cudaStreamSynchronize(c->stream));
     return h;
 }
 
