@@ -11,7 +11,7 @@ Goldens come from the UNMODIFIED reference (tests/golden/make_spread.py, oracle/
     whose count the order does not move (P-CG, GCR, BiCGStab(l), tfQMR: one or two counts over
     the 36 orders) FAST must land inside [min, max] of the reference's iterations and final
     measures.  For BiCGStab — whose count moves by up to +-7 % with the order alone — FAST
-    must land within one spread width of the reference's median count.
+    must land within max(spread width, 3 standard deviations) of the reference's median count.
   * Full-size FAST solves to convergence (C4 HYB w = 27 and w = 26, BiCGStab on C3) are checked
     on the TRUE preconditioned residual of the returned solution.  C2 at full size does not
     converge in double precision for the reference itself (its BiCGStab residual hump overflows):
@@ -57,9 +57,12 @@ def check_fast_in_spread(o, g):
     ms = [v[1] for v in g["policies"].values()]
     assert o.converged
     if g["method"] == "bicgstab":
+        # the reference's count under a change of summation order is a random variable; FAST is
+        # one more order: within max(spread width, 3 standard deviations) of the reference's median
         width = g["max_iterations"] - g["min_iterations"]
-        assert abs(o.iterations - float(np.median(its))) <= max(width, 2), (o.iterations, g["min_iterations"],
-                                                                           g["max_iterations"])
+        tol = max(width, 3.0 * float(np.std(its, ddof=1)) if len(its) > 1 else 0.0, 2)
+        assert abs(o.iterations - float(np.median(its))) <= tol, (o.iterations, g["min_iterations"],
+                                                                 g["max_iterations"], tol)
     else:
         assert g["min_iterations"] - 1 <= o.iterations <= g["max_iterations"] + 1, (o.iterations, g["min_iterations"],
                                                                                    g["max_iterations"])
