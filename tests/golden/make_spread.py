@@ -176,6 +176,16 @@ def c2_spread36(R, P, spr, hist):
 
 
 @section
+def small_bicgstab(R, P, spr, hist):
+    """The small BiCGStab configs of the parity suite (test_gpu_parity.CONFIG_KEYS), 36 orders."""
+    for kind, n in (("convdiff2d", 100), ("convdiff2d", 300), ("fem27", 20)):
+        A = matrix(R, P, kind, n)
+        nr = R.info(A)["n_rows"]
+        spr[f"{kind}_{n}_bicgstab"] = dict(kind=kind, n=n, method="bicgstab", stab_l=1,
+                                          **spread(R, A, nr, "bicgstab", ALL36, f"{kind} {n}"))
+
+
+@section
 def c2_full(R, P, spr, hist):
     """C2 BiCGStab to the end at 2000^2 and the full 4000^2: the reference's residual hump
     (3e82 at 1000^2, iteration 1499) outgrows double precision, so the reference itself stops
