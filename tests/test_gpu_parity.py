@@ -5,6 +5,7 @@ solver histories.  FAST mode: SpMV rows still bit-exact; solvers within +-1 iter
 1e-10 absolute on the final measure (SURVEY §8(d) gates), BiCGStab inside the oracle's own
 cross-policy spread (§8(c)).
 """
+import json
 import os
 import subprocess
 
@@ -349,17 +350,29 @@ def test_config_goldens_exact_mode(ctx, golden, key):
     assert o.final_residual_measure == c["final_residual_measure"]
 
 
+@pytest.fixture(scope="module")
+def oracle_spread():
+    with open(os.path.join(ROOT, "tests", "golden", "oracle_spread.json")) as f:
+        return json.load(f)
+
+
 @pytest.mark.parametrize("key", CONFIG_KEYS)
 @pytest.mark.parametrize("fmt", ["csr", "ell", "hyb"])
-def test_config_goldens_fast_mode(ctx, golden, key, fmt):
+def test_config_goldens_fast_mode(ctx, golden, oracle_spread, key, fmt):
     c = golden["configs"][key]
     A = ctx.generate(c["kind"], c["n"], pe=0.5).convert(fmt, slot_cap=1 << 40)
     cfg = kg.SolverConfig(policy=kg.ExecPolicy(0, 0), stab_l=c["stab_l"], mode="fast")
     o = kg.solve(A, c["method"], np.ones(A.n_rows), cfg=cfg)
     assert o.converged
     if c["method"] == "bicgstab":
-        # order-sensitive: inside the oracle's own cross-policy spread
-        assert abs(o.iterations - c["iterations"]) <= max(2, 0.2 * c["iterations"])
+        # order-sensitive: the reference's own count over 36 summation orders
+        # (tests/golden/oracle_spread.json); FAST is one more order — within max(spread width,
+        # 3 sd) of the reference's median
+        g = oracle_spread[f"{c['kind']}_{c['n']}_bicgstab"]
+        its = [v[0] for v in g["policies"].values()]
+        tol = max(g["max_iterations"] - g["min_iterations"], 3.0 * float(np.std(its, ddof=1)), 2)
+        assert abs(o.iterations - float(np.median(its))) <= tol, (o.iterations, g["min_iterations"],
+                                                                 g["max_iterations"])
     else:
         assert abs(o.iterations - c["iterations"]) <= 1
         assert abs(o.final_residual_measure - c["final_residual_measure"]) <= 1e-10
