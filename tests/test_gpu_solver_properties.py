@@ -161,3 +161,22 @@ def test_descent_cg_agrees_with_pcg_on_2x2(ctx, mode):
     assert d.iterations == p.iterations
     assert np.max(np.abs(d.solution - p.solution)) <= 1e-12
     assert abs(p.solution[0] - 1 / 11) < 1e-12 and abs(p.solution[1] - 7 / 11) < 1e-12
+
+
+@pytest.mark.parametrize("kind,n,max_it", [("poisson2d", 200, 80), ("lap3d7", 30, 30000), ("lap3d7", 110, 30000)])
+def test_fast_pcg_stepwise_equals_one_shot(ctx, kind, n, max_it):
+    """The FAST P-CG session driven stepwise (iterate() in uneven chunks, graph replays and the
+    cooperative update kernel of small systems alike) ends bit-identical to one solve call:
+    history, iteration count and solution — the max-iteration stop and the converged stop."""
+    A = ctx.generate(kind, n)
+    b = np.ones(A.n_rows)
+    cfg = kg.SolverConfig(mode="fast", policy=kg.ExecPolicy(0, 0), max_iterations=max_it)
+    one = kg.solve(A, "pcg", b, cfg=cfg)
+    s = kg.PcgSolver(A, ctx.to_device(b), ctx.to_device(np.zeros(A.n_rows)), cfg)
+    for k in (7, 33, 1, 16, 64, 1000):
+        s.iterate(k)
+    rep = s.report()
+    s.close()
+    assert rep.iterations == one.iterations and rep.converged == one.converged
+    np.testing.assert_array_equal(rep.residual_history, one.residual_history)
+    np.testing.assert_array_equal(rep.solution, one.solution)
