@@ -1177,7 +1177,9 @@ krysp_gpu_mat* transpose(const krysp_gpu_mat* m) {
     // csr_transpose formats.cpp:312-334.  Output row c lists the rows r with A(r,c) != 0 in
     // ascending r: a stable sort of the entries by column (CUB radix sort, stable) over the
     // row-major entry order gives exactly that.
-    krysp_gpu_mat* a = convert_to_csr(m);
+    // a CSR input is read in place; other formats go through their CSR first
+    krysp_gpu_mat* owned = m->format == KRYSP_FMT_CSR ? nullptr : convert_to_csr(m);
+    const krysp_gpu_mat* a = owned ? owned : m;
     krysp_gpu_ctx* c = a->ctx;
     int64_t nnz = a->nnz;
     krysp_gpu_mat* t = mat_new(c, KRYSP_FMT_CSR, a->n_cols, a->n_rows);
@@ -1209,9 +1211,9 @@ krysp_gpu_mat* transpose(const krysp_gpu_mat* m) {
         dev_free(d_tmp);
     }
     exclusive_scan(c, cnt, off, a->n_cols);
-    t->rp = dev_alloc<int32_t>(a->n_cols + 1 + kPad, true, c->stream);
-    t->ci = dev_alloc<int32_t>(nnz + kPad, true, c->stream);
-    t->cv = dev_alloc<double>(nnz + kPad, true, c->stream);
+    t->rp = dev_alloc_out<int32_t>(a->n_cols + 1, c->stream);
+    t->ci = dev_alloc_out<int32_t>(nnz, c->stream);
+    t->cv = dev_alloc_out<double>(nnz, c->stream);
     narrow_offsets<<<grid_for(a->n_cols + 1, kNT, cap_grid(c)), kNT, 0, c->stream>>>(off, t->rp, a->n_cols + 1);
     KG_LAUNCH(c);
     if (nnz) {
@@ -1220,8 +1222,10 @@ krysp_gpu_mat* transpose(const krysp_gpu_mat* m) {
     }
     KG_CUDA(cudaStreamSynchronize(c->stream));
     for (void* p : {(void*)rows, (void*)idx, (void*)keys_out, (void*)perm, (void*)cnt, (void*)off}) dev_free(p);
-    mat_free_arrays(a);
-    delete a;
+    if (owned) {
+        mat_free_arrays(owned);
+        delete owned;
+    }
     t->bytes = (t->n_rows + 1) * 4 + nnz * 12;
     mat_row_stats(t);
     return t;
