@@ -33,7 +33,10 @@
 #include "krysp/exec.hpp"
 #include "krysp/formats.hpp"
 #include "krysp/kernels.hpp"
+#include "krysp/matrix_market.hpp"
 #include "krysp/solvers.hpp"
+#include "krysp/stats.hpp"
+#include "krysp/substructure.hpp"
 #include "krysp/types.hpp"
 #include "krysp_gpu.h"
 
@@ -420,6 +423,60 @@ inline TuneResult tune_spmv(const Matrix& m, const std::vector<ExecPolicy>& grid
 inline TuneResult tune_spmv(const SparseMatrix& m, const std::vector<ExecPolicy>& grid, const TimingProtocol& proto,
                             const std::string& matrix_name = "") {
     return tune_spmv(Matrix(m), grid, proto, matrix_name);
+}
+
+// ------------------------------------------------------------------ substructure.hpp:121-127
+// solve_cg_substructured (the paper's hybrid method) with every subdomain on this thread's GPU;
+// EXACT reproduces the reference's report bit for bit
+inline SolveReport solve_cg_substructured(const SparseMatrix& A, std::span<const double> b, std::span<const double> x0,
+                                          const std::vector<index_t>& assignment, const SolverConfig& cfg,
+                                          Mode mode = Mode::Exact, Context& ctx = Context::instance()) {
+    const CsrMatrix c = to_csr(A);
+    if (c.n_rows != c.n_cols) throw DimensionMismatch("solver expects a square matrix");
+    if (b.size() != (size_t)c.n_rows || b.size() != x0.size())
+        throw DimensionMismatch("rhs / initial guess length does not match the matrix");
+    SolveReport r;
+    r.solution.resize(b.size());
+    std::vector<double> hist((size_t)std::max<index_t>(cfg.max_iterations, 1));
+    const krysp_solver_cfg cc = to_c(cfg, mode);
+    krysp_report rep{};
+    check(krysp_gpu_solve_cg_substructured_host(ctx.get(), c.n_rows, c.row_ptr.data(), c.col_idx.data(),
+                                                c.values.data(), b.data(), x0.data(), assignment.data(), 0, &cc,
+                                                &rep, hist.data(), r.solution.data()));
+    r.converged = rep.converged != 0;
+    r.iterations = rep.iterations;
+    r.final_residual_measure = rep.final_residual_measure;
+    r.wall_time = rep.wall_time;
+    r.residual_history.assign(hist.begin(), hist.begin() + std::min<index_t>(rep.iterations, (index_t)hist.size()));
+    return r;
+}
+inline SolveReport solve_cg_substructured(const SparseMatrix& A, std::span<const double> b, std::span<const double> x0,
+                                          index_t n_parts, const SolverConfig& cfg, Mode mode = Mode::Exact) {
+    return solve_cg_substructured(A, b, x0, band_row_assignment(n_rows(A), n_parts), cfg, mode);
+}
+
+// ------------------------------------------------------------------ matrix_market.hpp:13, stats.hpp:23
+// the device parser (same COO, error classes, messages and line numbers as the reference's)
+inline CooMatrix read_matrix_market(const std::string& path, Context& ctx = Context::instance()) {
+    krysp_gpu_mat* o = nullptr;
+    check(krysp_gpu_read_matrix_market(ctx.get(), path.c_str(), KRYSP_FMT_COO, &o));
+    return std::get<CooMatrix>(Matrix(o).download());
+}
+// compute_stats on the device (row-length mean / stddev / max, bandwidth)
+inline MatrixStats compute_stats(const SparseMatrix& m) {
+    Matrix d(m);
+    krysp_stats k{};
+    check(krysp_gpu_mat_stats(d.get(), &k));
+    MatrixStats s;
+    s.h = k.h;
+    s.nz = k.nz;
+    s.density = k.density;
+    s.density_percent = 100.0 * k.density;
+    s.max_row = k.max_row;
+    s.bandwidth = k.bandwidth;
+    s.nz_per_h_mean = k.nz_per_h_mean;
+    s.nz_per_h_stddev = k.nz_per_h_stddev;
+    return s;
 }
 
 }  // namespace krysp::gpu

@@ -19,7 +19,10 @@
 #include "krysp/formats.hpp"
 #include "krysp/generators.hpp"
 #include "krysp/kernels.hpp"
+#include "krysp/matrix_market.hpp"
 #include "krysp/solvers.hpp"
+#include "krysp/stats.hpp"
+#include "krysp/substructure.hpp"
 #include "krysp_gpu_ref.hpp"
 
 using namespace krysp;
@@ -248,6 +251,30 @@ int run() {
                      [&] { g::solve_tfqmr(SparseMatrix(spd), b, x0, bad); }, "config check");
         same_outcome([&] { run_solver("qmr", SparseMatrix(spd), b, x0, cfg, false); },
                      [&] { run_solver("qmr", SparseMatrix(spd), b, x0, cfg, true); }, "unknown method");
+    }
+
+    // ---- the paper's hybrid method (substructure.hpp:121-127), EXACT: the reference's report
+    for (index_t parts : {index_t(2), index_t(5)}) {
+        SolverConfig cfg;
+        same_solve([&] { return solve_cg_substructured(SparseMatrix(spd), b, x0, parts, cfg); },
+                   [&] { return g::solve_cg_substructured(SparseMatrix(spd), b, x0, parts, cfg); },
+                   "solve_cg_substructured " + std::to_string(parts) + " parts");
+    }
+
+    // ---- Matrix Market (matrix_market.hpp:13-18) and stats (stats.hpp:23)
+    {
+        const std::string path = "/tmp/krysp_ref_drop_in.mtx";
+        write_matrix_market(path, csr_to_coo(ns));
+        const CooMatrix h = read_matrix_market(path), d = g::read_matrix_market(path);
+        expect(h.n_rows == d.n_rows && h.row_idx == d.row_idx && h.col_idx == d.col_idx && same_bits(h.values, d.values),
+               "read_matrix_market");
+        const MatrixStats sh = compute_stats(SparseMatrix(ns)), sd = g::compute_stats(SparseMatrix(ns));
+        expect(sh.h == sd.h && sh.nz == sd.nz && sh.max_row == sd.max_row && sh.bandwidth == sd.bandwidth &&
+                   std::abs(sh.nz_per_h_mean - sd.nz_per_h_mean) <= 1e-12 * sh.nz_per_h_mean &&
+                   std::abs(sh.nz_per_h_stddev - sd.nz_per_h_stddev) <= 1e-12 * (1.0 + sh.nz_per_h_stddev),
+               "compute_stats");
+        same_outcome([&] { read_matrix_market(std::string("/tmp/does-not-exist.mtx")); },
+                     [&] { g::read_matrix_market(std::string("/tmp/does-not-exist.mtx")); }, "read_matrix_market missing");
     }
 
     // ---- tuner (autotune.hpp:59-60): the reference's TuneResult type, 72 + 0 records
