@@ -99,7 +99,9 @@ constexpr int kExactWarps = 4;
 
 __global__ void __launch_bounds__(32 * kExactWarps)
     dot_exact_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ y, int bs,
-                     int64_t n_chunks, double* partials, unsigned* counter, double* out) {
+                     int64_t n_chunks, double* partials, unsigned* counter, double* out,
+                     const int* gate = nullptr) {
+    if (gate && *(volatile const int*)gate) return;  // a device-resident solve has finished
     __shared__ double tile[kExactWarps][32][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t c0 = ((int64_t)blockIdx.x * kExactWarps + w) * 32;
@@ -130,6 +132,64 @@ __global__ void __launch_bounds__(32 * kExactWarps)
             *counter = 0;
         }
     }
+}
+
+// Few chunks (C1: 977 chunks of 1024): the lane-per-chunk kernel above has 8 CTAs for the
+// whole vector and runs latency-bound (~110 µs per dot).  Here a CTA of 256 threads owns G
+// chunks (G <= 32, chosen so the grid covers the SMs): all its threads load a tile of tw
+// elements of each chunk (coalesced per chunk row) and store the products into shared memory,
+// then lane q of warp 0 adds chunk q's products in order.  Same per-chunk sequence; the loads
+// of a whole tile in flight at once.
+constexpr int kCtaSmem = 32 * 129;  // doubles of the product tile (>= kFoldTile for the fold)
+
+__global__ void __launch_bounds__(256) dot_exact_cta_kernel(int64_t n, const double* __restrict__ x,
+                                                            const double* __restrict__ y, int bs, int64_t n_chunks,
+                                                            int G, int tw, double* partials, unsigned* counter,
+                                                            double* out, const int* gate) {
+    if (gate && *(volatile const int*)gate) return;
+    __shared__ double tile[kCtaSmem];
+    const int64_t c0 = (int64_t)blockIdx.x * G;
+    const int ld = tw + 1;
+    double acc = 0.0;
+    for (int j0 = 0; j0 < bs; j0 += tw) {
+        for (int k = threadIdx.x; k < G * tw; k += 256) {
+            const int q = k / tw, j = k - q * tw;
+            const int64_t c = c0 + q, i = c * bs + j0 + j;
+            double p = 0.0;  // absent elements add +0.0: a no-op on a sum that starts at +0.0
+            if (c < n_chunks && i < n) p = __dmul_rn(x[i], y[i]);
+            tile[q * ld + j] = p;
+        }
+        __syncthreads();
+        if (threadIdx.x < G) {
+            const double* row = tile + threadIdx.x * ld;
+#pragma unroll 8
+            for (int j = 0; j < tw; ++j) acc = __dadd_rn(acc, row[j]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < G && c0 + threadIdx.x < n_chunks) partials[c0 + threadIdx.x] = acc;
+    if (!out) return;
+    __threadfence();
+    if (last_block(counter)) {
+        const double total = ordered_fold(partials, n_chunks, tile);
+        if (threadIdx.x == 0) {
+            *out = total;
+            *counter = 0;
+        }
+    }
+}
+
+// the CTA kernel while the lane-per-chunk one would leave most SMs idle; its (G, tw, grid)
+inline bool exact_dot_use_cta(krysp_gpu_ctx* c, int64_t n_chunks) {
+    return n_chunks < (int64_t)c->sm_count * 32 * kExactWarps * 4;
+}
+inline void exact_dot_cta_shape(krysp_gpu_ctx* c, int64_t n_chunks, int bs, int* G, int* tw, unsigned* grid) {
+    int g = (int)std::min<int64_t>(32, std::max<int64_t>(1, n_chunks / (2 * (int64_t)c->sm_count)));
+    int t = bs;
+    while (t > 1 && g * (t + 1) > kCtaSmem) t >>= 1;
+    *G = g;
+    *tw = t;
+    *grid = (unsigned)((n_chunks + g - 1) / g);
 }
 
 // ---------------------------------------------------------------- diagonal / Jacobi
@@ -226,8 +286,15 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
             tmp = dev_alloc<double>(n_chunks + per_block, false);
             partials = tmp;
         }
-        dot_exact_kernel<<<(unsigned)blocks, 32 * kExactWarps, 0, c->stream>>>(n, x, y, (int)bs, n_chunks, partials,
-                                                                              c->d_counters + 1, d_out);
+        if (exact_dot_use_cta(c, n_chunks)) {
+            int G, tw;
+            unsigned grid;
+            exact_dot_cta_shape(c, n_chunks, (int)bs, &G, &tw, &grid);
+            dot_exact_cta_kernel<<<grid, 256, 0, c->stream>>>(n, x, y, (int)bs, n_chunks, G, tw, partials,
+                                                              c->d_counters + 1, d_out, nullptr);
+        } else
+            dot_exact_kernel<<<(unsigned)blocks, 32 * kExactWarps, 0, c->stream>>>(n, x, y, (int)bs, n_chunks,
+                                                                                  partials, c->d_counters + 1, d_out);
         KG_LAUNCH(c);
         if (tmp) {
             KG_CUDA(cudaStreamSynchronize(c->stream));
@@ -238,6 +305,30 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
         dot_fast_kernel<kNT><<<g, kNT, 0, c->stream>>>(n, x, y, c->d_partials, c->d_counters, d_out);
         KG_LAUNCH(c);
     }
+}
+
+// EXACT dot into d_out with caller-owned partials (n_chunks + 128 doubles) and its own arrival
+// counter (partials[n_chunks + 128 ...]), gated on a device flag: capturable, no host sync
+void k_dot_exact_into(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, double* partials,
+                      double* d_out, const int* gate) {
+    if (n <= 0) {
+        KG_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), c->stream));
+        return;
+    }
+    if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
+    const int64_t n_chunks = (n + bs - 1) / bs;
+    const int64_t per_block = 32 * kExactWarps;
+    unsigned* counter = reinterpret_cast<unsigned*>(partials + n_chunks + per_block);
+    if (exact_dot_use_cta(c, n_chunks)) {
+        int G, tw;
+        unsigned grid;
+        exact_dot_cta_shape(c, n_chunks, (int)bs, &G, &tw, &grid);
+        dot_exact_cta_kernel<<<grid, 256, 0, c->stream>>>(n, x, y, (int)bs, n_chunks, G, tw, partials, counter,
+                                                          d_out, gate);
+    } else
+        dot_exact_kernel<<<(unsigned)((n_chunks + per_block - 1) / per_block), 32 * kExactWarps, 0, c->stream>>>(
+            n, x, y, (int)bs, n_chunks, partials, counter, d_out, gate);
+    KG_LAUNCH(c);
 }
 
 // the reference's per-chunk partial sums (kernels.cpp:74-78) of n elements, without the fold

@@ -628,6 +628,8 @@ void k_fill(krysp_gpu_ctx* c, int64_t n, double v, double* x);
 void k_scal_elementwise(krysp_gpu_ctx* c, int64_t n, double* a, const double* b);
 void k_mul(krysp_gpu_ctx* c, int64_t n, const double* a, const double* b, double* out);  // out = a*b
 // Device-side dot into d_out (no sync).  EXACT: chunk + fold (policy.block_size).
+void k_dot_exact_into(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, double* partials,
+                      double* d_out, const int* gate);
 void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode,
            double* d_out);
 void k_chunk_partials(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, double* partials);

@@ -652,6 +652,83 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
     }
 }
 
+// ---- EXACT P-CG, device-resident (solve_pcg solvers.cpp:119-187 replayed bit for bit)
+// The host-driven replay waits for every dot on the host (C1: 320 µs per iteration, 10% of
+// FAST).  Here every scalar of the reference stays on the device: the reference-order dots
+// (dot_exact: chunk sums in the policy's block_size + the strict left fold) write into the
+// state, 1-thread kernels replay the reference's scalar algebra and checks in its order, and
+// the vector steps keep its roundings; iterations are graph-captured like FAST's.  z and p
+// swap each iteration (solvers.cpp:154-157), so the graphs come in two parities.
+__global__ void ex_beta_kernel(int64_t n, const double* __restrict__ p, double* __restrict__ z, const CgState* st) {
+    if (*(volatile const int*)&st->done || st->iter == 0) return;  // the first iteration has no beta step
+    const double beta = st->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        z[i] = __dadd_rn(__dmul_rn(beta, p[i]), z[i]);  // daxpy(beta, p, z)
+}
+
+// sigma = <p, Ap> -> checks, alpha (solvers.cpp:160-166)
+__global__ void ex_sigma_kernel(CgState* st, const double* sigma_in) {
+    if (st->done) return;
+    const double sigma = *sigma_in;
+    st->sigma = sigma;
+    if (!isfinite(sigma)) {
+        st->status = kStNonFiniteSigma;
+        st->done = 1;
+    } else if (fabs(sigma) < kBreakdownEps) {
+        st->status = kStBreakdownSigma;
+        st->done = 1;
+    } else {
+        const double alpha = st->rho / sigma;
+        st->alpha = alpha;
+        if (!isfinite(alpha)) {
+            st->status = kStNonFiniteAlpha;
+            st->done = 1;
+        }
+    }
+}
+
+// x += alpha p; r -= alpha Ap (two daxpy, solvers.cpp:167-168); z = D^-1 r (apply_precond :46-52)
+template <bool kJacobi>
+__global__ void ex_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                 const double* __restrict__ p, const double* __restrict__ ap,
+                                 const double* __restrict__ inv, double* __restrict__ z, const CgState* st) {
+    if (*(volatile const int*)&st->done) return;
+    const double alpha = st->alpha, malpha = -alpha;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        const double ri = __dadd_rn(__dmul_rn(malpha, ap[i]), r[i]);
+        r[i] = ri;
+        z[i] = kJacobi ? __dmul_rn(ri, inv[i]) : ri;
+    }
+}
+
+// rho = <r, z> -> check, measure, history, trace, convergence; beta for the next iteration
+// (solvers.cpp:169-181, 152)
+__global__ void ex_rho_kernel(CgState* st, const double* rho_in, double* history, double* trace) {
+    if (st->done) return;
+    const double rho_new = *rho_in, rho = st->rho;
+    const long long it = st->iter;
+    if (trace) {
+        double* t = trace + 4 * it;
+        t[0] = rho;
+        t[1] = it == 0 ? 0.0 : st->beta;
+        t[2] = st->sigma;
+        t[3] = st->alpha;
+    }
+    if (!isfinite(rho_new)) {
+        st->status = kStNonFiniteRho;
+        st->done = 1;
+        return;
+    }
+    const double measure = rho_new / st->norm_r0;
+    history[it] = measure;
+    st->iter = it + 1;
+    st->rho_1 = rho;
+    st->rho = rho_new;
+    st->beta = rho_new / rho;
+    if (measure <= st->tol || it + 1 >= st->max_it) st->done = 1;
+}
+
 // sense-free grid barrier: arrival counter reset by the last arriver, which then bumps the
 // generation the others spin on (counter reset before the bump: no early re-arrival race)
 __device__ __forceinline__ void pc_grid_sync(unsigned* count, unsigned* gen) {
@@ -2204,6 +2281,8 @@ struct PcgSession {
     // merged: 2 kernels per iteration (direction pass inside the SpMV, XDir / EpiCgDir);
     // graphs per starting parity of the direction buffers
     bool merged = false;
+    bool exact = false;  // EXACT mode: the reference's P-CG replayed on the device (ex_* kernels)
+    DVec ex_partials, ex_scal;  // exact dots: chunk partials, and the two dot results
     int next_parity = 0;
     // cooperative update + direction (cg_update_dir_kernel) when every thread of one resident
     // grid can hold its rows' r and z in registers
@@ -2235,8 +2314,9 @@ struct PcgSession {
             e.residual(b, x, r);
             double norm_r0 = e.norm2(r);
             if (norm_r0 == 0.0) norm_r0 = 1.0;
-            setup_persistent_flag();
-            merged = !persistent && spmv_takes_xsource(e, A) && merged_enabled();
+            exact = cfg.mode == KRYSP_MODE_EXACT;
+            if (!exact) setup_persistent_flag();
+            merged = !exact && !persistent && spmv_takes_xsource(e, A) && merged_enabled();
             double rho;
             if (merged) {  // z into p1 for rho; P0 = 0, alpha = beta = 0: the first merged
                 p1 = DVec(n, c->stream);  // iteration writes p_0 = z_0 + 0 * 0 = z_0 exactly
@@ -2264,12 +2344,18 @@ struct PcgSession {
             stream_wait(c);
             trace_lap(c, "pcg_session", "setup kernels");
             for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
+            if (exact) {
+                p1 = DVec(n, c->stream);
+                const int64_t n_chunks = (n + e.pol.block_size - 1) / e.pol.block_size;
+                ex_partials = DVec(n_chunks + 32 * 4 + 64, c->stream);
+                ex_scal = DVec(2, c->stream);
+            }
             if (persistent) setup_persistent();
             else {
-                setup_coop();
+                if (!exact) setup_coop();
                 exec_chunk = capture(kChunk, false, 0);
                 exec_one = capture(1, false, 0);
-                if (merged) {
+                if (merged || exact) {
                     exec_chunk1 = capture(kChunk, false, 1);
                     exec_one1 = capture(1, false, 1);
                 }
@@ -2414,6 +2500,31 @@ struct PcgSession {
         ++launches_total;
     }
 
+    // the EXACT SpMV of spmv_launch (policy kernel and order), gated on the solve's done flag
+    void spmv_exact_gated(const double* xin, double* y) {
+        const krysp_gpu_mat* m = e.A;
+        cudaStream_t s = e.c->stream;
+        EpiStoreGated<FlagGate> epi{y, FlagGate{&st->done}};
+        switch (m->format) {
+            case KRYSP_FMT_CSR:
+                if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, xin, epi, s, e.pol.workers_per_row);
+                else if (!launch_csr_vector_long(m, xin, y, e.pol.block_size, e.pol.workers_per_row, s))
+                    launch_csr_vector(m, xin, epi, e.pol.block_size, e.pol.workers_per_row, s);
+                break;
+            case KRYSP_FMT_ELL: launch_ell(m, xin, epi, e.pol.block_size, s); break;
+            case KRYSP_FMT_HYB:
+                launch_ell(m, xin, epi, e.pol.block_size, s);
+                launch_coo_accumulate(m, xin, y, s);
+                break;
+            default: spmv_launch(m, xin, y, e.pol, KRYSP_MODE_EXACT, s); break;
+        }
+    }
+
+    // the reference-order dot into d_out (device), partials in the session's own buffer
+    void exact_dot(const double* a, const double* b, double* d_out) {
+        k_dot_exact_into(e.c, n, a, b, e.pol.block_size, ex_partials, d_out, &st->done);
+    }
+
     void iteration(bool events, int parity) {
         krysp_gpu_ctx* c = e.c;
         double* part_a = c->d_partials + 2 * kPartialCap;
@@ -2426,6 +2537,30 @@ struct PcgSession {
         double* p_old = parity ? (double*)p1 : (double*)p;
         double* p_new = parity ? (double*)p : (double*)p1;
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[0], c->stream, cudaEventRecordExternal));
+        if (exact) {  // iteration j: z in B[j % 2], the previous p in B[(j + 1) % 2]
+            double* zb = p_old;
+            double* pb = p_new;
+            const unsigned g = grid_for(n, kFusedNT, (int64_t)c->sm_count * 8);
+            ex_beta_kernel<<<g, kFusedNT, 0, c->stream>>>(n, pb, zb, st);  // z += beta p, then swap
+            KG_LAUNCH(c);
+            spmv_exact_gated(zb, ap);                                        // Ap with p = zb
+            exact_dot(zb, ap, ex_scal);
+            ex_sigma_kernel<<<1, 1, 0, c->stream>>>(st, ex_scal);
+            KG_LAUNCH(c);
+            if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
+            if (e.jacobi)
+                ex_update_kernel<true><<<g, kFusedNT, 0, c->stream>>>(n, x, r, zb, ap, inv, pb, st);
+            else
+                ex_update_kernel<false><<<g, kFusedNT, 0, c->stream>>>(n, x, r, zb, ap, nullptr, pb, st);
+            KG_LAUNCH(c);
+            exact_dot(r, pb, (double*)ex_scal + 1);                          // rho = <r, z>
+            ex_rho_kernel<<<1, 1, 0, c->stream>>>(st, (double*)ex_scal + 1, hist, d_trace);
+            KG_LAUNCH(c);
+            if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
+            if (events) KG_CUDA(cudaEventRecordWithFlags(ev[3], c->stream, cudaEventRecordExternal));
+            kernels_per_iteration = (int)(c->launches - before);
+            return;
+        }
         if (merged) {
             if (e.jacobi)
                 spmv_fused_xs(e, XDir<true>{r, inv, p_old, st, 0.0},
@@ -2505,11 +2640,12 @@ struct PcgSession {
     void enqueue(int64_t iters) {
         krysp_gpu_ctx* c = e.c;
         if (persistent) return launch_persistent(iters);
+        const bool two = merged || exact;  // iterations alternate two buffers
         for (int64_t i = 0; i + kChunk <= iters; i += kChunk)
-            KG_CUDA(cudaGraphLaunch(merged && next_parity ? exec_chunk1 : exec_chunk, c->stream));
+            KG_CUDA(cudaGraphLaunch(two && next_parity ? exec_chunk1 : exec_chunk, c->stream));
         for (int64_t i = 0; i < iters % kChunk; ++i) {
-            KG_CUDA(cudaGraphLaunch(merged && next_parity ? exec_one1 : exec_one, c->stream));
-            if (merged) next_parity ^= 1;
+            KG_CUDA(cudaGraphLaunch(two && next_parity ? exec_one1 : exec_one, c->stream));
+            if (two) next_parity ^= 1;
         }
     }
 
@@ -2555,11 +2691,12 @@ struct PcgSession {
         krysp_gpu_ctx* c = e.c;
         if (persistent) fail(KRYSP_ERROR, "per-kernel profile: the persistent P-CG grid is one kernel");
         if (!exec_prof) exec_prof = capture(1, true, 0);  // event-node graphs, built on first use
-        if (merged && !exec_prof1) exec_prof1 = capture(1, true, 1);
+        const bool two = merged || exact;
+        if (two && !exec_prof1) exec_prof1 = capture(1, true, 1);
         out[0] = out[1] = out[2] = 0.0;
         for (int64_t i = 0; i < iters; ++i) {
-            KG_CUDA(cudaGraphLaunch(merged && next_parity ? exec_prof1 : exec_prof, c->stream));
-            if (merged) next_parity ^= 1;
+            KG_CUDA(cudaGraphLaunch(two && next_parity ? exec_prof1 : exec_prof, c->stream));
+            if (two) next_parity ^= 1;
             KG_CUDA(cudaEventSynchronize(ev[3]));
             for (int k = 0; k < 3; ++k) {
                 float ms = 0.f;
@@ -3035,6 +3172,15 @@ void bicgstab_fused(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg, const d
 
 krysp_gpu_mat* transpose(const krysp_gpu_mat* m);
 
+// KRYSP_EXACT_RESIDENT=0: EXACT P-CG on the host-driven replay instead of the device session
+bool exact_resident_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("KRYSP_EXACT_RESIDENT");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 // check_system solvers.cpp:16-28, then dispatch.  x (device, n) holds x0 on entry and the
 // solution on return.
 void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, const krysp_solver_cfg& cfg,
@@ -3060,7 +3206,10 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
         }
     });
     cudaStream_t stream = A->ctx->stream;
-    const bool fused = (method == KRYSP_PCG || method == KRYSP_BICGSTAB) && cfg.mode == KRYSP_MODE_FAST;
+    // FAST P-CG / BiCGStab and EXACT P-CG run device-resident (the EXACT session replays the
+    // reference's sequence bit for bit, its scalars on the device)
+    const bool fused = ((method == KRYSP_PCG || method == KRYSP_BICGSTAB) && cfg.mode == KRYSP_MODE_FAST) ||
+                       (method == KRYSP_PCG && cfg.mode == KRYSP_MODE_EXACT && A->n_rows > 0 && exact_resident_enabled());
     Report rep;
     double dev_s = 0.0;
     std::exception_ptr err;
