@@ -2991,6 +2991,104 @@ __global__ void __launch_bounds__(kBiNT) bi_p_kernel(int64_t n, double* __restri
     }
 }
 
+// ---- EXACT BiCGStab, device-resident (solve_bicgstab solvers.cpp:376-432 bit for bit): the
+// reference's vector steps and roundings, its six dots in reference order (k_dot_exact_into)
+// into the session's scalars, and its scalar algebra and checks in 1-thread kernels, in its
+// order; every kernel gated on the solve's done flag.
+struct EpiScaleGated {  // op(): y = D^-1 (A x), the single rounding fl(sum * inv) of copy + scal
+    double* __restrict__ y;
+    const double* __restrict__ dinv;
+    const int* gate;
+    __device__ __forceinline__ bool active() const { return !*(volatile const int*)gate; }
+    __device__ __forceinline__ void row(int64_t r, double v) { y[r] = dinv ? __dmul_rn(v, dinv[r]) : v; }
+    __device__ __forceinline__ void finish() {}
+};
+
+__global__ void ex_scale_kernel(int64_t n, double* __restrict__ y, const double* __restrict__ inv, const int* gate) {
+    if (*(volatile const int*)gate) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __dmul_rn(y[i], inv[i]);
+}
+
+__global__ void ex_bs_alpha_kernel(BiState* st, const double* denom) {
+    if (st->done) return;
+    FinAlpha()(st, *denom, 0.0);
+}
+
+// s = r; s -= alpha v (copy_vec + daxpy, solvers.cpp:387-388)
+__global__ void ex_bs_s_kernel(int64_t n, double* __restrict__ s, const double* __restrict__ r,
+                               const double* __restrict__ v, const BiState* st) {
+    if (*(volatile const int*)&st->done) return;
+    const double ma = -st->alpha;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s[i] = __dadd_rn(__dmul_rn(ma, v[i]), r[i]);
+}
+
+// measure = norm2(s) / norm_r0 and the half-step test (solvers.cpp:389-397)
+__global__ void ex_bs_half_kernel(BiState* st, const double* ss, double* history) {
+    if (st->done) return;
+    const double measure = sqrt(*ss) / st->norm_r0;
+    if (!isfinite(measure)) return bs_fail(st, kBsNonFiniteMeasure);
+    if (measure <= st->tol) {
+        history[st->iter] = measure;
+        st->iter += 1;
+        st->half = 1;  // x += alpha p still to apply (ex_bs_update_kernel)
+        st->done = 1;
+    }
+}
+
+__global__ void ex_bs_omega_kernel(BiState* st, const double* tt_ts) {
+    if (st->done) return;
+    FinOmega()(st, tt_ts[0], tt_ts[1]);
+}
+
+// x += alpha p; x += omega s; r = s; r -= omega t (solvers.cpp:410-413); after a half-step stop
+// only x += alpha p (:392), once
+__global__ void ex_bs_update_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                    const double* __restrict__ p, const double* __restrict__ s,
+                                    const double* __restrict__ t, BiState* st, unsigned* counter) {
+    const int done = *(volatile const int*)&st->done, half = *(volatile const int*)&st->half;
+    if (done && !half) return;
+    const double alpha = st->alpha, om = st->omega, mom = -om;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (half) {
+            x[i] = __dadd_rn(__dmul_rn(alpha, p[i]), x[i]);
+        } else {
+            const double si = s[i];
+            x[i] = __dadd_rn(__dmul_rn(om, si), __dadd_rn(__dmul_rn(alpha, p[i]), x[i]));
+            r[i] = __dadd_rn(__dmul_rn(mom, t[i]), si);
+        }
+    }
+    if (half) {
+        __syncthreads();
+        if (last_block(counter) && threadIdx.x == 0) {
+            *counter = 0;
+            st->half = 0;
+        }
+    }
+}
+
+// measure = norm2(r) / norm_r0, history, test; rho_new = <r^, r>, beta (solvers.cpp:414-429)
+__global__ void ex_bs_measure_kernel(BiState* st, const double* rr_rho, double* history) {
+    if (st->done) return;
+    const double measure = sqrt(rr_rho[0]) / st->norm_r0;
+    if (!isfinite(measure)) return bs_fail(st, kBsNonFiniteMeasure);
+    const long long it = st->iter;
+    history[it] = measure;
+    st->iter = it + 1;
+    if (measure <= st->tol) {
+        st->done = 1;
+        return;
+    }
+    const double rho_new = rr_rho[1];
+    if (dvanish(rho_new)) return bs_fail(st, kBsBreakdownRho);
+    const double beta = (rho_new / st->rho) * (st->alpha / st->omega);
+    if (!isfinite(beta)) return bs_fail(st, kBsNonFiniteBeta);
+    st->beta = beta;
+    st->rho = rho_new;
+    if (it + 1 >= st->max_it) st->done = 1;
+}
+
 }  // namespace
 
 struct BicgstabSession {
@@ -3004,6 +3102,9 @@ struct BicgstabSession {
     bool done_at_setup = false;
     cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr;
     int kernels_per_iteration = 0;
+    bool exact = false;  // EXACT mode: the reference's BiCGStab replayed on the device (ex_bs_*)
+    DVec ex_partials, ex_scal;
+    DevBuf<unsigned> ex_counter;
 
     BicgstabSession(const krysp_gpu_mat* A, const krysp_solver_cfg& cfg_, const double* b, const double* x0)
         : e(A, cfg_), cfg(cfg_), n(A->n_rows), x(n, A->ctx->stream), r(n, A->ctx->stream), rh(n, A->ctx->stream),
@@ -3032,6 +3133,13 @@ struct BicgstabSession {
             e.gate = &st->done;
             hist = dev_alloc_records<double>(cfg.max_iterations, c->stream);
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+            exact = cfg.mode == KRYSP_MODE_EXACT;
+            if (exact) {
+                const int64_t n_chunks = (n + e.pol.block_size - 1) / e.pol.block_size;
+                ex_partials = DVec(n_chunks + 32 * 4 + 64, c->stream);
+                ex_scal = DVec(8, c->stream);
+                ex_counter.p = dev_alloc<unsigned>(1, true, c->stream);
+            }
             stream_wait(c);
             exec_chunk = capture(kChunk);
             exec_one = capture(1);
@@ -3060,6 +3168,37 @@ struct BicgstabSession {
         const double* dinv = e.jacobi ? (const double*)e.inv : nullptr;
         const unsigned g = grid_for(n, kBiNT, (int64_t)c->sm_count * 8);
         const int64_t before = c->launches;
+        if (exact) {
+            const int* gate = &st->done;
+            double* sc = ex_scal;
+            auto dot = [&](const double* a, const double* b, double* out) {
+                k_dot_exact_into(c, n, a, b, e.pol.block_size, ex_partials, out, gate);
+            };
+            op_exact(p, v);                                  // v = op(p)
+            dot(rh, v, sc);                                  // <r^, v>
+            ex_bs_alpha_kernel<<<1, 1, 0, c->stream>>>(st, sc);
+            KG_LAUNCH(c);
+            ex_bs_s_kernel<<<g, kBiNT, 0, c->stream>>>(n, s, r, v, st);
+            KG_LAUNCH(c);
+            dot(s, s, sc + 1);                               // ||s||^2
+            ex_bs_half_kernel<<<1, 1, 0, c->stream>>>(st, sc + 1, hist);
+            KG_LAUNCH(c);
+            op_exact(s, t);                                  // t = op(s)
+            dot(t, t, sc + 2);
+            dot(t, s, sc + 3);
+            ex_bs_omega_kernel<<<1, 1, 0, c->stream>>>(st, sc + 2);
+            KG_LAUNCH(c);
+            ex_bs_update_kernel<<<g, kBiNT, 0, c->stream>>>(n, x, r, p, s, t, st, ex_counter);
+            KG_LAUNCH(c);
+            dot(r, r, sc + 4);
+            dot(rh, r, sc + 5);
+            ex_bs_measure_kernel<<<1, 1, 0, c->stream>>>(st, sc + 4, hist);
+            KG_LAUNCH(c);
+            bi_p_kernel<<<g, kBiNT, 0, c->stream>>>(n, p, r, v, st);  // p -= omega v; p = r + beta p
+            KG_LAUNCH(c);
+            kernels_per_iteration = (int)(c->launches - before);
+            return;
+        }
         spmv_fused(e, p, v, EpiBi<FinAlpha, 1>{v, dinv, rh, nullptr, st, pa, ca, {0, 0}, {0, 0}});
         bi_s_kernel<<<g, kBiNT, 0, c->stream>>>(n, s, r, v, st, pb, cb, hist);
         KG_LAUNCH(c);
@@ -3069,6 +3208,29 @@ struct BicgstabSession {
         bi_p_kernel<<<g, kBiNT, 0, c->stream>>>(n, p, r, v, st);
         KG_LAUNCH(c);
         kernels_per_iteration = (int)(c->launches - before);
+    }
+
+    // op() of the EXACT replay: the policy's SpMV (spmv_launch's kernel and order), then
+    // fl(y * inv) — fused into the row epilogue for CSR / ELL, a pass for HYB / COO (whose COO
+    // part adds after the ELL rows); gated on the solve's done flag
+    void op_exact(const double* xin, double* y) {
+        const krysp_gpu_mat* m = e.A;
+        krysp_gpu_ctx* c = e.c;
+        const double* dinv = e.jacobi ? (const double*)e.inv : nullptr;
+        EpiScaleGated epi{y, dinv, &st->done};
+        if (m->format == KRYSP_FMT_CSR) {
+            if (csr_use_tile(m, e.pol.workers_per_row)) launch_csr_tile(m, xin, epi, c->stream, e.pol.workers_per_row);
+            else launch_csr_vector(m, xin, epi, e.pol.block_size, e.pol.workers_per_row, c->stream);
+        } else if (m->format == KRYSP_FMT_ELL) {
+            launch_ell(m, xin, epi, e.pol.block_size, c->stream);
+        } else {
+            spmv_launch(m, xin, y, e.pol, KRYSP_MODE_EXACT, c->stream);
+            if (dinv) {
+                ex_scale_kernel<<<grid_for(n, kBiNT, (int64_t)c->sm_count * 8), kBiNT, 0, c->stream>>>(n, y, dinv,
+                                                                                                      &st->done);
+                KG_LAUNCH(c);
+            }
+        }
     }
 
     cudaGraphExec_t capture(int iters) {
@@ -3208,8 +3370,13 @@ void solve(const krysp_gpu_mat* A, int32_t method, const double* b, double* x, c
     cudaStream_t stream = A->ctx->stream;
     // FAST P-CG / BiCGStab and EXACT P-CG run device-resident (the EXACT session replays the
     // reference's sequence bit for bit, its scalars on the device)
+    // (EXACT BiCGStab: not on a CSR with rows beyond the long-row cut, whose EXACT SpMV is the
+    // two-kernel long-row path; those stay host-driven)
+    const bool exact_ok = cfg.mode == KRYSP_MODE_EXACT && A->n_rows > 0 && exact_resident_enabled();
     const bool fused = ((method == KRYSP_PCG || method == KRYSP_BICGSTAB) && cfg.mode == KRYSP_MODE_FAST) ||
-                       (method == KRYSP_PCG && cfg.mode == KRYSP_MODE_EXACT && A->n_rows > 0 && exact_resident_enabled());
+                       (method == KRYSP_PCG && exact_ok) ||
+                       (method == KRYSP_BICGSTAB && exact_ok &&
+                        !(A->format == KRYSP_FMT_CSR && (A->max_row < 0 || A->max_row > kLongRow)));
     Report rep;
     double dev_s = 0.0;
     std::exception_ptr err;
