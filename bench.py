@@ -313,6 +313,13 @@ def run_ours(args, dist):
                    br.final_residual_measure, "reference_iterations": GOLDEN_BICGSTAB_ITERS,
                    "inside_reference_orders": min(GOLDEN_BICGSTAB_ITERS.values()) <= br.iterations
                    <= max(GOLDEN_BICGSTAB_ITERS.values())}
+    # EXACT mode (bit-identical to the reference, the drop-in default) on the same system:
+    # device-resident P-CG and BiCGStab at the reference's tuned <1024,1>
+    exact_rates = {}
+    for meth, its in (("pcg", 30), ("bicgstab", 15)):
+        ecfg = kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(1024, 1), tolerance=1e-300, max_iterations=its)
+        eo = kg.solve(A, meth, np.ones(n), cfg=ecfg)
+        exact_rates[meth] = eo.iterations / eo.device_time
     # the same P-CG on the ELL format (C3 is quoted "CSR (and ELL)")
     ell_rate = None
     if args.format == "csr":
@@ -349,6 +356,9 @@ def run_ours(args, dist):
                                                       / 1e9 / bw_peak},
             "gpu_launches": kpi * args.steps,
             "clocks": ck,
+            "exact_mode": {"pcg": exact_rates["pcg"], "bicgstab": exact_rates["bicgstab"], "unit": "iterations/s",
+                           "what": "EXACT mode (the reference's floating-point sequence at <1024,1>, bit-identical), "
+                                   "device-resident, CUDA events"},
             "pcg_ell": {"value": ell_rate, "unit": "iterations/s",
                         "frac": (B_iter * ell_rate / 1e9 / bw_peak) if ell_rate else None,
                         "what": "same P-CG, ELL format (column-major slab, width 7)"},
