@@ -112,9 +112,10 @@ __global__ void __launch_bounds__(kAdNT, kMinBlocks) adaptive_kernel(RowsView A,
             continue;
         }
         const int64_t q = b - nlng - nmedg;  // stream block of short rows
-        const int32_t r0 = blk[2 * q], r1 = blk[2 * q + 1];
-        const int64_t k0 = A.rp[r0];
-        const int nz = (int)(A.rp[r1] - k0);
+        const int4 bd = reinterpret_cast<const int4*>(blk)[q];  // (r0, r1, rp[r0], rp[r1]): one load
+        const int32_t r0 = bd.x, r1 = bd.y;
+        const int64_t k0 = bd.z;
+        const int nz = bd.w - bd.z;
         int32_t cl[kAdPer];
         double vl[kAdPer];
 #pragma unroll
@@ -176,6 +177,8 @@ void build_plan(krysp_gpu_ctx* c, const int32_t* d_rp, int64_t n, AdaptivePlan& 
         if (cur_rows) {
             blk.push_back((int32_t)cur_r0);
             blk.push_back((int32_t)r);
+            blk.push_back(rp[(size_t)cur_r0]);
+            blk.push_back(rp[(size_t)r]);
         }
         cur_rows = cur_nnz = 0;
     };
@@ -207,7 +210,7 @@ void build_plan(krysp_gpu_ctx* c, const int32_t* d_rp, int64_t n, AdaptivePlan& 
         cur_nnz += len;
     }
     close(n);
-    P.nblk = (int64_t)blk.size() / 2;
+    P.nblk = (int64_t)blk.size() / 4;
     P.nmed = (int64_t)med.size();
     P.nlng = (int64_t)lng.size();
     P.nchunk = (int64_t)chunk.size() / 3;

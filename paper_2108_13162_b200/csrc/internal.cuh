@@ -126,7 +126,7 @@ struct CooView {
 // rows, and rows longer than kAdSplit split into kAdChunk-nnz chunks (partials + fixup).
 namespace kg {
 struct AdaptivePlan {
-    int32_t* blk = nullptr;    // (r0, r1) per stream block of short rows
+    int32_t* blk = nullptr;    // (r0, r1, rp[r0], rp[r1]) per stream block of short rows
     int64_t nblk = 0;
     int32_t* med = nullptr;    // medium rows (a warp each)
     int64_t nmed = 0;

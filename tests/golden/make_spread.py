@@ -30,7 +30,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from oracle.oracle import Port, Ref  # noqa: E402
 
-SPREAD = os.path.join(HERE, "oracle_spread.json")
+SPREAD = os.environ.get("SPREAD_OUT", os.path.join(HERE, "oracle_spread.json"))
 HIST = os.path.join(HERE, "config_histories.npz")
 ALL36 = [(bs, tw) for bs in (32, 64, 128, 256, 512, 1024) for tw in (1, 2, 4, 8, 16, 32)]
 SOME12 = [(bs, tw) for bs in (32, 256, 1024) for tw in (1, 4, 8, 32)]
