@@ -10,6 +10,7 @@
 //   EXACT  partial[c] = sequential sum over chunk c of block_size elements (from 0.0), then
 //          a strict left-to-right fold of the partials (kernels.cpp:66-84) — bit-identical.
 //   FAST   fixed-grid, fixed-tree reduction (deterministic run to run, not bit-equal to CPU).
+#include <cstdlib>
 #include "internal.cuh"
 
 namespace kg {
@@ -231,6 +232,194 @@ __global__ void invert_kernel(int64_t n, double* d, int* zero_row) {
     }
 }
 
+
+// ---------------------------------------------------------------- EXACT dot, streaming fold
+// The reference's left-to-right fold of the chunk partials (kernels.cpp:80-83) is one
+// dependent add chain (C3 at bs 1024: 62.5 k adds, ~0.25 ms) that the kernels above start only
+// after every partial exists.  Here the fold runs WHILE the partials are produced: block 0 is a
+// folder — its warp 1 polls the compute blocks' ready flags (32 at a time, in order), copies
+// each finished prefix of partials into a shared-memory ring and clears the flags; warp 0 lane
+// 0 (and warp 2 lane 0 for a second dot) adds the ring's values in order.  Compute blocks
+// 1..ncb are the CTA kernel's (G chunks each, products staged per tile, one lane per chunk
+// adding in order), then publish their flag.  Two dots share a pass (their folds run on two
+// warps concurrently).  Same chunk sums, same fold order: bit-identical to the kernels above.
+// The folder never blocks a compute block, so any schedule completes.
+constexpr int kStrNT = 256;
+constexpr int kRing = 2048;  // partials per dot in the folder's ring (power of two)
+constexpr int64_t kStreamMinChunks = 4096;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int ND>
+__global__ void __launch_bounds__(kStrNT) dot_exact_stream_kernel(
+    int64_t n, const double* __restrict__ a1, const double* __restrict__ b1, const double* __restrict__ a2,
+    const double* __restrict__ b2, int bs, int64_t n_chunks, int G, int tw, int64_t ncb, double* pa, double* pb,
+    int* flags, double* out1, double* out2, const int* gate) {
+    if (gate && *(volatile const int*)gate) return;
+    extern __shared__ double sm_dot[];  // compute: 2 x ND product tiles; folder: ND rings of kRing
+    __shared__ long long s_avail, s_used[2];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (blockIdx.x == 0) {  // ---- folder
+        double* tile = sm_dot;
+        if (t == 0) {
+            s_avail = 0;
+            s_used[0] = s_used[1] = 0;
+        }
+        __syncthreads();
+        volatile long long* v_avail = &s_avail;
+        volatile long long* v_used = s_used;
+        if (w == 1) {  // loader
+            const int64_t maxk = min(32, kRing / (2 * G));
+            int64_t nb = 0;
+            while (nb < ncb) {
+                const int64_t bb = nb + lane;
+                const int rdy = (lane < maxk && bb < ncb) ? ld_acquire(flags + bb) : 0;
+                const unsigned m = __ballot_sync(0xffffffffu, rdy != 0);
+                const int k = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+                if (k == 0) {
+                    __nanosleep(64);
+                    continue;
+                }
+                const int64_t p0 = nb * G, p1 = min((nb + k) * (int64_t)G, n_chunks);
+                for (;;) {  // ring space: both folders past p1 - kRing
+                    const long long u = ND == 2 ? min(v_used[0], v_used[1]) : v_used[0];
+                    if (p1 - u <= kRing) break;
+                }
+                for (int64_t q0 = p0 + lane; q0 < p1; q0 += 32 * 8) {  // 8 loads per lane in flight
+                    double va[8], vb[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t q = q0 + 32 * u;
+                        if (q < p1) {
+                            va[u] = __ldcg(pa + q);
+                            if (ND == 2) vb[u] = __ldcg(pb + q);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t q = q0 + 32 * u;
+                        if (q < p1) {
+                            tile[q & (kRing - 1)] = va[u];
+                            if (ND == 2) tile[kRing + (q & (kRing - 1))] = vb[u];
+                        }
+                    }
+                }
+                if (lane < k) flags[nb + lane] = 0;  // re-armed for the next launch
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) *v_avail = p1;
+                nb += k;
+            }
+        } else if ((w == 0 || (ND == 2 && w == 2)) && lane == 0) {  // folder of dot 1 / dot 2
+            const int d = w == 0 ? 0 : 1;
+            const double* ring = tile + d * kRing;
+            double total = 0.0;
+            int64_t q = 0;
+            // the add chain is the critical path (one dependent add per partial): batches of 16
+            // from the ring (16-aligned, so a batch never wraps) are read one batch ahead
+            auto batch = [&](int64_t q0, double2* v) {
+                const double2* r2 = reinterpret_cast<const double2*>(ring + (q0 & (kRing - 1)));
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = r2[k];
+            };
+            while (q < n_chunks) {
+                const int64_t a = *v_avail;
+                if (a == q) continue;
+                __threadfence_block();
+                for (; q < a && (q & 15); ++q) total = __dadd_rn(total, ring[q & (kRing - 1)]);
+                if (q + 16 <= a) {
+                    double2 cur[8], nxt[8];
+                    batch(q, cur);
+                    for (; q + 32 <= a; q += 16) {
+                        batch(q + 16, nxt);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            total = __dadd_rn(total, cur[k].x);
+                            total = __dadd_rn(total, cur[k].y);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        total = __dadd_rn(total, cur[k].x);
+                        total = __dadd_rn(total, cur[k].y);
+                    }
+                    q += 16;
+                }
+                for (; q < a; ++q) total = __dadd_rn(total, ring[q & (kRing - 1)]);
+                __threadfence_block();
+                v_used[d] = q;
+            }
+            *(d == 0 ? out1 : out2) = total;
+        }
+        return;
+    }
+    // ---- compute block b: chunks [b G, b G + G), G = kStreamTile / tw.  A tile is tw
+    // consecutive elements of each of the G chunks (rows of >= 2 KB: DRAM-friendly); thread t
+    // owns column t % tw of rows t / tw + 8 u — 8 (ND = 2: 16) independent element pairs in
+    // flight, coalesced.  Iteration jt: every thread issues tile jt's loads, lanes < G of the
+    // first warps add tile jt - 1 (double-buffered) while those loads fly, then the products of
+    // tile jt go to shared memory.  Lane q's sequence is chunk q's elements in order.
+    const int64_t b = blockIdx.x - 1;
+    const int64_t c0 = b * G;
+    const int ld = tw + 1, tsz = G * ld, lg = __ffs(tw) - 1, nt = bs >> lg;
+    const int rows_per_pass = kStrNT >> lg;  // 256 / tw
+    double acc = 0.0;
+    for (int jt = 0; jt <= nt; ++jt) {
+        double xa[8], ya[8], xb[8], yb[8];
+        const int j = t & (tw - 1), q0 = t >> lg;
+        if (jt < nt) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * rows_per_pass;
+                const int64_t i = (c0 + q) * bs + (int64_t)jt * tw + j;
+                const bool in = q < G && c0 + q < n_chunks && i < n;  // absent: +0.0 (dot_exact_kernel)
+                xa[u] = in ? a1[i] : 0.0;
+                ya[u] = in ? b1[i] : 0.0;
+                if (ND == 2) {
+                    xb[u] = in ? a2[i] : 0.0;
+                    yb[u] = in ? b2[i] : 0.0;
+                }
+            }
+        }
+        if (jt > 0 && t < ND * 64) {  // dot d = t / 64 (warps 0-1: dot 1, warps 2-3: dot 2)
+            const int d = t >> 6, q = t & 63;
+            if (q < G) {
+                const double* row = sm_dot + ((jt - 1) & 1) * ND * tsz + d * tsz + q * ld;
+#pragma unroll 8
+                for (int k = 0; k < tw; ++k) acc = __dadd_rn(acc, row[k]);
+            }
+        }
+        if (jt < nt) {
+            double* buf = sm_dot + (jt & 1) * ND * tsz;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q = q0 + u * rows_per_pass;
+                if (q < G) {
+                    buf[q * ld + j] = __dmul_rn(xa[u], ya[u]);
+                    if (ND == 2) buf[tsz + q * ld + j] = __dmul_rn(xb[u], yb[u]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (t < ND * 64) {
+        const int d = t >> 6, q = t & 63;
+        if (q < G && c0 + q < n_chunks) (d == 0 ? pa : pb)[c0 + q] = acc;
+    }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) st_release(flags + b, 1);
+}
+
 }  // namespace
 
 void k_daxpy(krysp_gpu_ctx* c, int64_t n, double a, const double* x, double* y) {
@@ -328,6 +517,65 @@ void k_dot_exact_into(krysp_gpu_ctx* c, int64_t n, const double* x, const double
     } else
         dot_exact_kernel<<<(unsigned)((n_chunks + per_block - 1) / per_block), 32 * kExactWarps, 0, c->stream>>>(
             n, x, y, (int)bs, n_chunks, partials, counter, d_out, gate);
+    KG_LAUNCH(c);
+}
+
+// streaming-fold EXACT dot(s): G chunks per compute block, products tiles for ND dots
+constexpr int kStreamTile = 8 * kStrNT;  // elements per tile and dot: 8 per thread
+static void stream_shape(krysp_gpu_ctx* c, int64_t n_chunks, int bs, int nd, int* G, int* tw, int64_t* ncb,
+                         int* smem) {
+    (void)c;
+    const int t = std::min(bs, kStrNT);  // tile width: a 256-element (2 KB) row per chunk
+    const int g = kStreamTile / t;      // 8 (bs >= 256) .. 64 (bs = 32) chunks per block
+    *G = g;
+    *tw = t;
+    *ncb = (n_chunks + g - 1) / g;
+    *smem = (int)std::max<int64_t>(2LL * nd * g * (t + 1) * 8, (int64_t)nd * kRing * 8);
+}
+
+int64_t exact_dot_stream_scratch(int64_t n, int64_t bs) {
+    const int64_t n_chunks = (n + bs - 1) / bs;
+    // streaming: partials of two dots + one int flag per block; short: k_dot_exact_into's layout
+    return std::max<int64_t>(2 * n_chunks + (n_chunks + 1) / 2 + 16, n_chunks + 32 * kExactWarps + 64);
+}
+
+void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
+                        const double* b2, int64_t bs, double* scratch, double* out1, double* out2, const int* gate) {
+    if (n <= 0) {
+        KG_CUDA(cudaMemsetAsync(out1, 0, sizeof(double), c->stream));
+        if (a2) KG_CUDA(cudaMemsetAsync(out2, 0, sizeof(double), c->stream));
+        return;
+    }
+    if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
+    const int64_t n_chunks = (n + bs - 1) / bs;
+    if (n_chunks < kStreamMinChunks) {  // short fold: the one-pass kernels (C1: 977 chunks)
+        k_dot_exact_into(c, n, a1, b1, bs, scratch, out1, gate);
+        if (a2) k_dot_exact_into(c, n, a2, b2, bs, scratch, out2, gate);
+        return;
+    }
+    const int nd = a2 ? 2 : 1;
+    int G, tw, smem;
+    int64_t ncb;
+    stream_shape(c, n_chunks, (int)bs, nd, &G, &tw, &ncb, &smem);
+    double* pa = scratch;
+    double* pb = scratch + n_chunks;
+    int* flags = reinterpret_cast<int*>(scratch + 2 * n_chunks);
+    static bool attr = [] {
+        KG_CUDA(cudaFuncSetAttribute(dot_exact_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
+        KG_CUDA(cudaFuncSetAttribute(dot_exact_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
+        return true;
+    }();
+    (void)attr;
+    // block 0 folds while blocks 1..ncb produce the partials (one grid: the folder only waits
+    // on blocks of its own launch, which never wait — completes under any schedule, including
+    // a profiler's serialised replay).  A fold kernel on a side stream beside the chunk kernel
+    // measured faster on C2 but hangs when the two kernels do not run concurrently.
+    if (nd == 2)
+        dot_exact_stream_kernel<2><<<(unsigned)(ncb + 1), kStrNT, smem, c->stream>>>(
+            n, a1, b1, a2, b2, (int)bs, n_chunks, G, tw, ncb, pa, pb, flags, out1, out2, gate);
+    else
+        dot_exact_stream_kernel<1><<<(unsigned)(ncb + 1), kStrNT, smem, c->stream>>>(
+            n, a1, b1, nullptr, nullptr, (int)bs, n_chunks, G, tw, ncb, pa, pb, flags, out1, nullptr, gate);
     KG_LAUNCH(c);
 }
 

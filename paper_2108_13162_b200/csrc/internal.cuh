@@ -632,6 +632,11 @@ void k_dot_exact_into(krysp_gpu_ctx* c, int64_t n, const double* x, const double
                       double* d_out, const int* gate);
 void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode,
            double* d_out);
+// EXACT dot(s) with the fold streaming beside the chunk pass (a2 == nullptr: one dot); scratch:
+// exact_dot_stream_scratch(n, bs) doubles, zeroed once (flags re-arm themselves)
+int64_t exact_dot_stream_scratch(int64_t n, int64_t bs);
+void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
+                        const double* b2, int64_t bs, double* scratch, double* out1, double* out2, const int* gate);
 void k_chunk_partials(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, double* partials);
 double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs,
                 int32_t mode);

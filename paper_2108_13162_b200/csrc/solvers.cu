@@ -2346,8 +2346,7 @@ struct PcgSession {
             for (auto& v : ev) KG_CUDA(cudaEventCreate(&v));
             if (exact) {
                 p1 = DVec(n, c->stream);
-                const int64_t n_chunks = (n + e.pol.block_size - 1) / e.pol.block_size;
-                ex_partials = DVec(n_chunks + 32 * 4 + 64, c->stream);
+                ex_partials = DVec(exact_dot_stream_scratch(n, e.pol.block_size), c->stream);
                 ex_scal = DVec(2, c->stream);
             }
             if (persistent) setup_persistent();
@@ -2522,7 +2521,7 @@ struct PcgSession {
 
     // the reference-order dot into d_out (device), partials in the session's own buffer
     void exact_dot(const double* a, const double* b, double* d_out) {
-        k_dot_exact_into(e.c, n, a, b, e.pol.block_size, ex_partials, d_out, &st->done);
+        k_dot_exact_stream(e.c, n, a, b, nullptr, nullptr, e.pol.block_size, ex_partials, d_out, nullptr, &st->done);
     }
 
     void iteration(bool events, int parity) {
@@ -2992,7 +2991,7 @@ __global__ void __launch_bounds__(kBiNT) bi_p_kernel(int64_t n, double* __restri
 }
 
 // ---- EXACT BiCGStab, device-resident (solve_bicgstab solvers.cpp:376-432 bit for bit): the
-// reference's vector steps and roundings, its six dots in reference order (k_dot_exact_into)
+// reference's vector steps and roundings, its six dots in reference order (k_dot_exact_stream)
 // into the session's scalars, and its scalar algebra and checks in 1-thread kernels, in its
 // order; every kernel gated on the solve's done flag.
 struct EpiScaleGated {  // op(): y = D^-1 (A x), the single rounding fl(sum * inv) of copy + scal
@@ -3135,8 +3134,7 @@ struct BicgstabSession {
             KG_CUDA(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
             exact = cfg.mode == KRYSP_MODE_EXACT;
             if (exact) {
-                const int64_t n_chunks = (n + e.pol.block_size - 1) / e.pol.block_size;
-                ex_partials = DVec(n_chunks + 32 * 4 + 64, c->stream);
+                ex_partials = DVec(exact_dot_stream_scratch(n, e.pol.block_size), c->stream);
                 ex_scal = DVec(8, c->stream);
                 ex_counter.p = dev_alloc<unsigned>(1, true, c->stream);
             }
@@ -3171,8 +3169,13 @@ struct BicgstabSession {
         if (exact) {
             const int* gate = &st->done;
             double* sc = ex_scal;
+            // reference-order dots with the fold streaming beside the pass; the independent
+            // pairs (<t,t>, <t,s>) and (<r,r>, <r^,r>) share one pass and fold concurrently
             auto dot = [&](const double* a, const double* b, double* out) {
-                k_dot_exact_into(c, n, a, b, e.pol.block_size, ex_partials, out, gate);
+                k_dot_exact_stream(c, n, a, b, nullptr, nullptr, e.pol.block_size, ex_partials, out, nullptr, gate);
+            };
+            auto dot2 = [&](const double* a1, const double* b1, const double* a2, const double* b2, double* out) {
+                k_dot_exact_stream(c, n, a1, b1, a2, b2, e.pol.block_size, ex_partials, out, out + 1, gate);
             };
             op_exact(p, v);                                  // v = op(p)
             dot(rh, v, sc);                                  // <r^, v>
@@ -3184,14 +3187,12 @@ struct BicgstabSession {
             ex_bs_half_kernel<<<1, 1, 0, c->stream>>>(st, sc + 1, hist);
             KG_LAUNCH(c);
             op_exact(s, t);                                  // t = op(s)
-            dot(t, t, sc + 2);
-            dot(t, s, sc + 3);
+            dot2(t, t, t, s, sc + 2);                        // <t,t>, <t,s>
             ex_bs_omega_kernel<<<1, 1, 0, c->stream>>>(st, sc + 2);
             KG_LAUNCH(c);
             ex_bs_update_kernel<<<g, kBiNT, 0, c->stream>>>(n, x, r, p, s, t, st, ex_counter);
             KG_LAUNCH(c);
-            dot(r, r, sc + 4);
-            dot(rh, r, sc + 5);
+            dot2(r, r, rh, r, sc + 4);                       // <r,r>, <r^,r>
             ex_bs_measure_kernel<<<1, 1, 0, c->stream>>>(st, sc + 4, hist);
             KG_LAUNCH(c);
             bi_p_kernel<<<g, kBiNT, 0, c->stream>>>(n, p, r, v, st);  // p -= omega v; p = r + beta p

@@ -1,0 +1,19 @@
+"""A few EXACT P-CG and BiCGStab iterations on C3 (lap3d7 400^3, <1024,1>) for an ncu launch
+list of the reference-order dots (streaming fold) beside the SpMV and vector passes."""
+import os
+import sys
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import numpy as np  # noqa: E402
+
+import paper_2108_13162_b200 as kg  # noqa: E402
+
+ctx = kg.Context(0)
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 400
+A = ctx.generate("lap3d7", n)
+for method in ("pcg", "bicgstab"):
+    cfg = kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(1024, 1), tolerance=1e-300, max_iterations=3)
+    try:
+        kg.solve(A, method, np.ones(A.n_rows), cfg=cfg)
+    except kg.Error as e:  # timing experiments (KRYSP_DOT_NOFOLD) leave the scalars unset
+        print("stopped:", e)
