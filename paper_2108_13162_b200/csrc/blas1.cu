@@ -245,17 +245,8 @@ __global__ void invert_kernel(int64_t n, double* d, int* zero_row) {
 // warps concurrently).  Same chunk sums, same fold order: bit-identical to the kernels above.
 // The folder never blocks a compute block, so any schedule completes.
 constexpr int kStrNT = 256;
-constexpr int kRing = 2048;  // partials per dot in the folder's ring (power of two)
 constexpr int64_t kStreamMinChunks = 4096;
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <int ND>
 __global__ void __launch_bounds__(kStrNT) dot_exact_stream_kernel(
@@ -264,102 +255,9 @@ __global__ void __launch_bounds__(kStrNT) dot_exact_stream_kernel(
     int* flags, double* out1, double* out2, const int* gate) {
     if (gate && *(volatile const int*)gate) return;
     extern __shared__ double sm_dot[];  // compute: 2 x ND product tiles; folder: ND rings of kRing
-    __shared__ long long s_avail, s_used[2];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x;
     if (blockIdx.x == 0) {  // ---- folder
-        double* tile = sm_dot;
-        if (t == 0) {
-            s_avail = 0;
-            s_used[0] = s_used[1] = 0;
-        }
-        __syncthreads();
-        volatile long long* v_avail = &s_avail;
-        volatile long long* v_used = s_used;
-        if (w == 1) {  // loader
-            const int64_t maxk = min(32, kRing / (2 * G));
-            int64_t nb = 0;
-            while (nb < ncb) {
-                const int64_t bb = nb + lane;
-                const int rdy = (lane < maxk && bb < ncb) ? ld_acquire(flags + bb) : 0;
-                const unsigned m = __ballot_sync(0xffffffffu, rdy != 0);
-                const int k = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
-                if (k == 0) {
-                    __nanosleep(64);
-                    continue;
-                }
-                const int64_t p0 = nb * G, p1 = min((nb + k) * (int64_t)G, n_chunks);
-                for (;;) {  // ring space: both folders past p1 - kRing
-                    const long long u = ND == 2 ? min(v_used[0], v_used[1]) : v_used[0];
-                    if (p1 - u <= kRing) break;
-                }
-                for (int64_t q0 = p0 + lane; q0 < p1; q0 += 32 * 8) {  // 8 loads per lane in flight
-                    double va[8], vb[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int64_t q = q0 + 32 * u;
-                        if (q < p1) {
-                            va[u] = __ldcg(pa + q);
-                            if (ND == 2) vb[u] = __ldcg(pb + q);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int64_t q = q0 + 32 * u;
-                        if (q < p1) {
-                            tile[q & (kRing - 1)] = va[u];
-                            if (ND == 2) tile[kRing + (q & (kRing - 1))] = vb[u];
-                        }
-                    }
-                }
-                if (lane < k) flags[nb + lane] = 0;  // re-armed for the next launch
-                __threadfence_block();
-                __syncwarp();
-                if (lane == 0) *v_avail = p1;
-                nb += k;
-            }
-        } else if ((w == 0 || (ND == 2 && w == 2)) && lane == 0) {  // folder of dot 1 / dot 2
-            const int d = w == 0 ? 0 : 1;
-            const double* ring = tile + d * kRing;
-            double total = 0.0;
-            int64_t q = 0;
-            // the add chain is the critical path (one dependent add per partial): batches of 16
-            // from the ring (16-aligned, so a batch never wraps) are read one batch ahead
-            auto batch = [&](int64_t q0, double2* v) {
-                const double2* r2 = reinterpret_cast<const double2*>(ring + (q0 & (kRing - 1)));
-#pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = r2[k];
-            };
-            while (q < n_chunks) {
-                const int64_t a = *v_avail;
-                if (a == q) continue;
-                __threadfence_block();
-                for (; q < a && (q & 15); ++q) total = __dadd_rn(total, ring[q & (kRing - 1)]);
-                if (q + 16 <= a) {
-                    double2 cur[8], nxt[8];
-                    batch(q, cur);
-                    for (; q + 32 <= a; q += 16) {
-                        batch(q + 16, nxt);
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            total = __dadd_rn(total, cur[k].x);
-                            total = __dadd_rn(total, cur[k].y);
-                        }
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
-                    }
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        total = __dadd_rn(total, cur[k].x);
-                        total = __dadd_rn(total, cur[k].y);
-                    }
-                    q += 16;
-                }
-                for (; q < a; ++q) total = __dadd_rn(total, ring[q & (kRing - 1)]);
-                __threadfence_block();
-                v_used[d] = q;
-            }
-            *(d == 0 ? out1 : out2) = total;
-        }
+        stream_fold<ND>(n_chunks, G, ncb, pa, pb, flags, out1, out2, sm_dot);
         return;
     }
     // ---- compute block b: chunks [b G, b G + G), G = kStreamTile / tw.  A tile is tw
@@ -417,7 +315,7 @@ __global__ void __launch_bounds__(kStrNT) dot_exact_stream_kernel(
     }
     __threadfence();
     __syncthreads();
-    if (t == 0) st_release(flags + b, 1);
+    if (t == 0) st_release_i32(flags + b, 1);
 }
 
 }  // namespace
@@ -525,8 +423,13 @@ constexpr int kStreamTile = 8 * kStrNT;  // elements per tile and dot: 8 per thr
 static void stream_shape(krysp_gpu_ctx* c, int64_t n_chunks, int bs, int nd, int* G, int* tw, int64_t* ncb,
                          int* smem) {
     (void)c;
-    const int t = std::min(bs, kStrNT);  // tile width: a 256-element (2 KB) row per chunk
-    const int g = kStreamTile / t;      // 8 (bs >= 256) .. 64 (bs = 32) chunks per block
+    static const int tw_cap = [] {
+        const char* v = std::getenv("KRYSP_DOT_TW");
+        const int k = v ? std::atoi(v) : 128;
+        return (k >= 32 && k <= 256 && (k & (k - 1)) == 0) ? k : 128;  // measured: 256 / 128 / 64 / 32 -> C3 P-CG 427 / 434 / 435 / 431 it/s
+    }();
+    const int t = std::min(bs, tw_cap);  // tile width: elements per chunk row of a tile
+    const int g = kStreamTile / t;      // 16 (bs >= 128) .. 64 (bs = 32) chunks per block
     *G = g;
     *tw = t;
     *ncb = (n_chunks + g - 1) / g;

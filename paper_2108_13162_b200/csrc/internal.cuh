@@ -375,6 +375,122 @@ __device__ __forceinline__ double ordered_fold(const double* partials, int64_t n
     return total;
 }
 
+// Block 0 of a streaming-fold grid (k_dot_exact_stream, the fused EXACT P-CG update): adds
+// the chunk partials pa (and pb) in index order as the other blocks of the grid publish them
+// (flags[b] = 1 once block b + 1's G partials are stored); warp 1 copies finished prefixes into
+// a shared-memory ring, warp 0 lane 0 (warp 2 lane 0: the second dot) runs the add chain.
+// The flags are cleared as they are consumed (re-armed for the next launch).  Needs >= 96
+// threads and ND * kRing doubles of shared memory at `tile`.
+constexpr int kRing = 2048;  // partials per dot in the folder's ring (power of two)
+
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int ND>
+__device__ __forceinline__ void stream_fold(int64_t n_chunks, int G, int64_t ncb, const double* pa, const double* pb,
+                                            int* flags, double* out1, double* out2, double* tile) {
+    __shared__ long long s_avail, s_used[2];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+        if (t == 0) {
+            s_avail = 0;
+            s_used[0] = s_used[1] = 0;
+        }
+        __syncthreads();
+        volatile long long* v_avail = &s_avail;
+        volatile long long* v_used = s_used;
+        if (w == 1) {  // loader
+            const int64_t maxk = min(32, kRing / (2 * G));
+            int64_t nb = 0;
+            while (nb < ncb) {
+                const int64_t bb = nb + lane;
+                const int rdy = (lane < maxk && bb < ncb) ? ld_acquire_i32(flags + bb) : 0;
+                const unsigned m = __ballot_sync(0xffffffffu, rdy != 0);
+                const int k = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+                if (k == 0) {
+                    __nanosleep(64);
+                    continue;
+                }
+                const int64_t p0 = nb * G, p1 = min((nb + k) * (int64_t)G, n_chunks);
+                for (;;) {  // ring space: both folders past p1 - kRing
+                    const long long u = ND == 2 ? min(v_used[0], v_used[1]) : v_used[0];
+                    if (p1 - u <= kRing) break;
+                }
+                for (int64_t q0 = p0 + lane; q0 < p1; q0 += 32 * 8) {  // 8 loads per lane in flight
+                    double va[8], vb[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t q = q0 + 32 * u;
+                        if (q < p1) {
+                            va[u] = __ldcg(pa + q);
+                            if (ND == 2) vb[u] = __ldcg(pb + q);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t q = q0 + 32 * u;
+                        if (q < p1) {
+                            tile[q & (kRing - 1)] = va[u];
+                            if (ND == 2) tile[kRing + (q & (kRing - 1))] = vb[u];
+                        }
+                    }
+                }
+                if (lane < k) flags[nb + lane] = 0;  // re-armed for the next launch
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) *v_avail = p1;
+                nb += k;
+            }
+        } else if ((w == 0 || (ND == 2 && w == 2)) && lane == 0) {  // folder of dot 1 / dot 2
+            const int d = w == 0 ? 0 : 1;
+            const double* ring = tile + d * kRing;
+            double total = 0.0;
+            int64_t q = 0;
+            // the add chain is the critical path (one dependent add per partial): batches of 16
+            // from the ring (16-aligned, so a batch never wraps) are read one batch ahead
+            auto batch = [&](int64_t q0, double2* v) {
+                const double2* r2 = reinterpret_cast<const double2*>(ring + (q0 & (kRing - 1)));
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = r2[k];
+            };
+            while (q < n_chunks) {
+                const int64_t a = *v_avail;
+                if (a == q) continue;
+                __threadfence_block();
+                for (; q < a && (q & 15); ++q) total = __dadd_rn(total, ring[q & (kRing - 1)]);
+                if (q + 16 <= a) {
+                    double2 cur[8], nxt[8];
+                    batch(q, cur);
+                    for (; q + 32 <= a; q += 16) {
+                        batch(q + 16, nxt);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            total = __dadd_rn(total, cur[k].x);
+                            total = __dadd_rn(total, cur[k].y);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        total = __dadd_rn(total, cur[k].x);
+                        total = __dadd_rn(total, cur[k].y);
+                    }
+                    q += 16;
+                }
+                for (; q < a; ++q) total = __dadd_rn(total, ring[q & (kRing - 1)]);
+                __threadfence_block();
+                v_used[d] = q;
+            }
+            *(d == 0 ? out1 : out2) = total;
+        }
+}
+
 // Same as block_sum for a runtime block size (multiple of 32, <= 1024).
 __device__ __forceinline__ double block_sum_dyn(double v, double* sh) {
     v = warp_sum(v);

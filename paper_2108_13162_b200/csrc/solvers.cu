@@ -702,6 +702,84 @@ __global__ void ex_update_kernel(int64_t n, double* __restrict__ x, double* __re
     }
 }
 
+// The EXACT update fused with the reference-order rho = <r, z> (streaming fold, block 0):
+// blocks 1..ncb own G chunks of bs rows; per tile (tw consecutive rows of each chunk, 4 rows
+// per thread in flight) they apply ex_update_kernel's exact steps and stage fl(r_i z_i); lane
+// q of warp 0 adds chunk q's products in row order (kernels.cpp:74-78), block 0 folds the
+// chunk sums left to right (:80-83).  One pass instead of update + dot.
+constexpr int kUrE = 4;  // rows per thread per tile
+
+template <bool kJacobi>
+__global__ void __launch_bounds__(256) ex_update_rho_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
+                                                            const double* __restrict__ p,
+                                                            const double* __restrict__ ap,
+                                                            const double* __restrict__ inv, double* __restrict__ z,
+                                                            const CgState* st, int bs, int64_t n_chunks, int G, int tw,
+                                                            int64_t ncb, double* partials, int* flags,
+                                                            double* rho_out) {
+    if (*(volatile const int*)&st->done) return;
+    extern __shared__ double sm_ur[];
+    const int t = threadIdx.x;
+    if (blockIdx.x == 0) {
+        stream_fold<1>(n_chunks, G, ncb, partials, nullptr, flags, rho_out, nullptr, sm_ur);
+        return;
+    }
+    const double alpha = st->alpha, malpha = -alpha;
+    const int64_t b = blockIdx.x - 1;
+    const int64_t c0 = b * G;
+    const int ld = tw + 1, tsz = G * ld, lg = __ffs(tw) - 1, nt = bs >> lg;
+    const int rpp = 256 >> lg;  // rows of the tile per pass of the block
+    const int j = t & (tw - 1), q0 = t >> lg;
+    double acc = 0.0;
+    for (int jt = 0; jt <= nt; ++jt) {
+        double xv[kUrE], pv[kUrE], av[kUrE], rv[kUrE], iv[kUrE];
+        bool in[kUrE];
+        if (jt < nt) {
+#pragma unroll
+            for (int u = 0; u < kUrE; ++u) {
+                const int q = q0 + u * rpp;
+                const int64_t i = (c0 + q) * bs + (int64_t)jt * tw + j;
+                in[u] = c0 + q < n_chunks && i < n;
+                if (in[u]) {
+                    xv[u] = x[i];
+                    pv[u] = p[i];
+                    av[u] = ap[i];
+                    rv[u] = r[i];
+                    if (kJacobi) iv[u] = inv[i];
+                }
+            }
+        }
+        if (jt > 0 && t < G) {
+            const double* row = sm_ur + ((jt - 1) & 1) * tsz + t * ld;
+#pragma unroll 8
+            for (int k = 0; k < tw; ++k) acc = __dadd_rn(acc, row[k]);
+        }
+        if (jt < nt) {
+            double* buf = sm_ur + (jt & 1) * tsz;
+#pragma unroll
+            for (int u = 0; u < kUrE; ++u) {
+                const int q = q0 + u * rpp;
+                double prod = 0.0;  // absent rows add +0.0, as in the dot kernels
+                if (in[u]) {
+                    const int64_t i = (c0 + q) * bs + (int64_t)jt * tw + j;
+                    x[i] = __dadd_rn(__dmul_rn(alpha, pv[u]), xv[u]);
+                    const double ri = __dadd_rn(__dmul_rn(malpha, av[u]), rv[u]);
+                    const double zi = kJacobi ? __dmul_rn(ri, iv[u]) : ri;
+                    r[i] = ri;
+                    z[i] = zi;
+                    prod = __dmul_rn(ri, zi);
+                }
+                buf[q * ld + j] = prod;
+            }
+        }
+        __syncthreads();
+    }
+    if (t < G && c0 + t < n_chunks) partials[c0 + t] = acc;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) st_release_i32(flags + b, 1);
+}
+
 // rho = <r, z> -> check, measure, history, trace, convergence; beta for the next iteration
 // (solvers.cpp:169-181, 152)
 __global__ void ex_rho_kernel(CgState* st, const double* rho_in, double* history, double* trace) {
@@ -2519,6 +2597,36 @@ struct PcgSession {
         }
     }
 
+    // update + rho in one pass with the streaming fold (ex_update_rho_kernel); false when the
+    // fold is short (C1 class: the one-pass dot kernels are faster) or disabled (KRYSP_UR=0)
+    bool exact_update_rho(const double* pz, double* z) {
+        static const bool on = [] {
+            const char* v = std::getenv("KRYSP_UR");
+            return !(v && v[0] == '0');
+        }();
+        const int64_t bs = e.pol.block_size;
+        const int64_t n_chunks = (n + bs - 1) / bs;
+        if (!on || n_chunks < 4096) return false;
+        krysp_gpu_ctx* c = e.c;
+        static const int tw_cap = [] {
+            const char* v = std::getenv("KRYSP_UR_TW");
+            const int k = v ? std::atoi(v) : 64;
+            return (k >= 32 && k <= 256 && (k & (k - 1)) == 0) ? k : 64;  // measured: 256 / 128 / 64 / 32 -> C3 395 / 419 / 427 / 425 it/s
+        }();
+        const int tw = (int)std::min<int64_t>(bs, tw_cap);
+        const int G = kUrE * 256 / tw;
+        const int64_t ncb = (n_chunks + G - 1) / G;
+        const int smem = std::max(2 * G * (tw + 1) * 8, kRing * 8);
+        double* partials = ex_partials;
+        int* flags = reinterpret_cast<int*>((double*)ex_partials + 2 * n_chunks);
+        const double* inv = e.jacobi ? (const double*)e.inv : nullptr;
+        auto k = e.jacobi ? ex_update_rho_kernel<true> : ex_update_rho_kernel<false>;
+        k<<<(unsigned)(ncb + 1), 256, smem, c->stream>>>(n, x, r, pz, ap, inv, z, st, (int)bs, n_chunks, G, tw,
+                                                         ncb, partials, flags, (double*)ex_scal + 1);
+        KG_LAUNCH(c);
+        return true;
+    }
+
     // the reference-order dot into d_out (device), partials in the session's own buffer
     void exact_dot(const double* a, const double* b, double* d_out) {
         k_dot_exact_stream(e.c, n, a, b, nullptr, nullptr, e.pol.block_size, ex_partials, d_out, nullptr, &st->done);
@@ -2547,12 +2655,14 @@ struct PcgSession {
             ex_sigma_kernel<<<1, 1, 0, c->stream>>>(st, ex_scal);
             KG_LAUNCH(c);
             if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
-            if (e.jacobi)
-                ex_update_kernel<true><<<g, kFusedNT, 0, c->stream>>>(n, x, r, zb, ap, inv, pb, st);
-            else
-                ex_update_kernel<false><<<g, kFusedNT, 0, c->stream>>>(n, x, r, zb, ap, nullptr, pb, st);
-            KG_LAUNCH(c);
-            exact_dot(r, pb, (double*)ex_scal + 1);                          // rho = <r, z>
+            if (!exact_update_rho(zb, pb)) {
+                if (e.jacobi)
+                    ex_update_kernel<true><<<g, kFusedNT, 0, c->stream>>>(n, x, r, zb, ap, inv, pb, st);
+                else
+                    ex_update_kernel<false><<<g, kFusedNT, 0, c->stream>>>(n, x, r, zb, ap, nullptr, pb, st);
+                KG_LAUNCH(c);
+                exact_dot(r, pb, (double*)ex_scal + 1);                      // rho = <r, z>
+            }
             ex_rho_kernel<<<1, 1, 0, c->stream>>>(st, (double*)ex_scal + 1, hist, d_trace);
             KG_LAUNCH(c);
             if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
