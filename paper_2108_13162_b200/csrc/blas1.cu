@@ -364,6 +364,22 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
     if (mode == KRYSP_MODE_EXACT) {
         if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
         const int64_t n_chunks = (n + bs - 1) / bs;
+        if (n_chunks >= kStreamMinChunks) {  // long fold: streamed beside the chunk pass
+            if (c->dot_scratch_n < 2 * n_chunks || c->dot_flags_n < n_chunks) {
+                KG_CUDA(cudaStreamSynchronize(c->stream));
+                dev_free(c->dot_scratch);
+                dev_free(c->dot_flags);
+                c->dot_scratch = nullptr;
+                c->dot_flags = nullptr;
+                c->dot_scratch_n = c->dot_flags_n = 0;
+                c->dot_scratch = dev_alloc<double>(2 * n_chunks, false, c->stream);
+                c->dot_scratch_n = 2 * n_chunks;
+                c->dot_flags = dev_alloc<int>(n_chunks, true, c->stream);
+                c->dot_flags_n = n_chunks;
+            }
+            k_dot_exact_stream(c, n, x, y, nullptr, nullptr, bs, c->dot_scratch, d_out, nullptr, nullptr, c->dot_flags);
+            return;
+        }
         const int64_t per_block = 32 * kExactWarps;
         const int64_t blocks = (n_chunks + per_block - 1) / per_block;
         // partial storage: use the slot area when it fits, else a temporary
@@ -443,7 +459,8 @@ int64_t exact_dot_stream_scratch(int64_t n, int64_t bs) {
 }
 
 void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
-                        const double* b2, int64_t bs, double* scratch, double* out1, double* out2, const int* gate) {
+                        const double* b2, int64_t bs, double* scratch, double* out1, double* out2, const int* gate,
+                        int* flags_in) {
     if (n <= 0) {
         KG_CUDA(cudaMemsetAsync(out1, 0, sizeof(double), c->stream));
         if (a2) KG_CUDA(cudaMemsetAsync(out2, 0, sizeof(double), c->stream));
@@ -462,7 +479,7 @@ void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const dou
     stream_shape(c, n_chunks, (int)bs, nd, &G, &tw, &ncb, &smem);
     double* pa = scratch;
     double* pb = scratch + n_chunks;
-    int* flags = reinterpret_cast<int*>(scratch + 2 * n_chunks);
+    int* flags = flags_in ? flags_in : reinterpret_cast<int*>(scratch + 2 * n_chunks);
     static bool attr = [] {
         KG_CUDA(cudaFuncSetAttribute(dot_exact_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
         KG_CUDA(cudaFuncSetAttribute(dot_exact_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));

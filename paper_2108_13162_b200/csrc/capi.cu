@@ -104,6 +104,8 @@ krysp_status krysp_gpu_ctx_destroy(krysp_gpu_ctx* c) {
         dev_free(c->d_partials);
         dev_free(c->d_counters);
         dev_free(c->d_scalars);
+        dev_free(c->dot_scratch);
+        dev_free(c->dot_flags);
         if (c->h_pinned) cudaFreeHost(c->h_pinned);
         if (c->sync_ev) cudaEventDestroy(c->sync_ev);
         if (c->own_stream) cudaStreamDestroy(c->own_stream);

@@ -76,6 +76,12 @@ struct krysp_gpu_ctx {
     double* d_scalars = nullptr;
     double* h_pinned = nullptr;
     cudaEvent_t sync_ev = nullptr;  // host waits on solver scalars (spin, see stream_wait)
+    // streaming-fold EXACT dot behind k_dot: partials, and ready flags kept apart (zeroed once,
+    // re-armed by every fold) so a call with another length never sees stale partials as flags
+    double* dot_scratch = nullptr;
+    int64_t dot_scratch_n = 0;
+    int* dot_flags = nullptr;
+    int64_t dot_flags_n = 0;
     // NCCL communicator whose health the host wait loops poll (set while a multi-GPU
     // partition is alive on this context; see comm_poll in dist.cu)
     void* nccl_watch = nullptr;
@@ -752,7 +758,8 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
 // exact_dot_stream_scratch(n, bs) doubles, zeroed once (flags re-arm themselves)
 int64_t exact_dot_stream_scratch(int64_t n, int64_t bs);
 void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
-                        const double* b2, int64_t bs, double* scratch, double* out1, double* out2, const int* gate);
+                        const double* b2, int64_t bs, double* scratch, double* out1, double* out2, const int* gate,
+                        int* flags = nullptr);  // flags: default inside scratch (fixed-length owners)
 void k_chunk_partials(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, double* partials);
 double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs,
                 int32_t mode);
