@@ -11,6 +11,8 @@
 //          a strict left-to-right fold of the partials (kernels.cpp:66-84) — bit-identical.
 //   FAST   fixed-grid, fixed-tree reduction (deterministic run to run, not bit-equal to CPU).
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 #include "internal.cuh"
 
 namespace kg {
@@ -318,6 +320,187 @@ __global__ void __launch_bounds__(kStrNT) dot_exact_stream_kernel(
     if (t == 0) st_release_i32(flags + b, 1);
 }
 
+
+// ---------------------------------------------------------------- EXACT dots sharing an operand
+// <w, v_k> for k < K (K <= kMdK): GCR's classical Gram-Schmidt dots (solvers.cpp:318-320), all
+// against the same w.  Each dot is the reference's (chunk sums of bs elements, left fold);
+// one pass reads w once.  Blocks 1..ncb: 8 chunks x 32-element tiles, products of every dot
+// to shared memory, lane (k, q) adds chunk q of dot k in element order; block 0: the K folds
+// on the lanes of warp 0 (lane k: dot k), in lockstep, fed from a ring as in stream_fold.
+constexpr int kMdK = 16;
+constexpr int kMdG = 8, kMdTw = 32;
+constexpr int kMdRing = 256;  // partials per dot in the folder ring
+
+__global__ void __launch_bounds__(256) dot_exact_shared_kernel(int64_t n, const double* __restrict__ w,
+                                                               const double* const* __restrict__ V, int K, int bs,
+                                                               int64_t n_chunks, int64_t ncb, double* partials,
+                                                               int* flags, double* out) {
+    extern __shared__ double sm_md[];
+    __shared__ long long s_avail, s_used, s_p0, s_p1;
+    __shared__ int s_k;
+    const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+    if (blockIdx.x == 0) {  // ---- folder
+        constexpr int ld = kMdRing + 1;  // padded per-dot ring rows (lanes read different banks)
+        if (t == 0) s_avail = s_used = 0;
+        __syncthreads();
+        volatile long long* v_avail = &s_avail;
+        volatile long long* v_used = &s_used;
+        if (wp >= 1) {  // loaders: warp 1 polls the flags, warps 1-7 copy (named barrier 1)
+            constexpr int64_t maxk = kMdRing / (2 * kMdG);
+            const int lt = t - 32;  // 0..223
+            int64_t nb = 0;
+            for (;;) {
+                if (wp == 1) {
+                    int k = 0;
+                    if (nb < ncb) {
+                        for (;;) {
+                            const int64_t bb = nb + lane;
+                            const int rdy = (lane < maxk && bb < ncb) ? ld_acquire_i32(flags + bb) : 0;
+                            const unsigned m = __ballot_sync(0xffffffffu, rdy != 0);
+                            k = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+                            if (k) break;
+                            __nanosleep(64);
+                        }
+                        const int64_t p1 = min((nb + k) * (int64_t)kMdG, n_chunks);
+                        while (p1 - *v_used > kMdRing) {
+                        }
+                        if (lane == 0) {
+                            s_p0 = nb * kMdG;
+                            s_p1 = p1;
+                        }
+                    }
+                    if (lane == 0) s_k = k;
+                }
+                asm volatile("bar.sync 1, 224;" ::: "memory");
+                const int k = s_k;
+                if (k == 0) break;  // every block folded
+                const int64_t p0 = s_p0;
+                const int cnt = (int)(s_p1 - p0);
+                const int tot = cnt * K;
+                for (int e0 = lt; e0 < tot; e0 += 224 * 4) {  // 4 loads per thread in flight
+                    double v[4];
+                    int dst[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + 224 * u;
+                        if (e < tot) {
+                            const int d = e / cnt, q = e - d * cnt;
+                            v[u] = __ldcg(partials + (int64_t)d * n_chunks + p0 + q);
+                            dst[u] = d * ld + (int)((p0 + q) & (kMdRing - 1));
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (e0 + 224 * u < tot) sm_md[dst[u]] = v[u];
+                }
+                __threadfence_block();
+                asm volatile("bar.sync 1, 224;" ::: "memory");
+                if (wp == 1) {
+                    if (lane < k) flags[nb + lane] = 0;  // re-armed for the next launch
+                    __threadfence_block();
+                    __syncwarp();
+                    if (lane == 0) *v_avail = s_p1;
+                }
+                nb += k;
+            }
+        } else {  // warp 0: lane k folds dot k (lanes >= K idle along)
+            const double* ring = sm_md + (lane < K ? lane : 0) * ld;
+            double total = 0.0;
+            int64_t q = 0;
+            while (q < n_chunks) {
+                const int64_t a = *v_avail;
+                if (a == q) continue;
+                __threadfence_block();
+                for (; q + 8 <= a; q += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = ring[(q + u) & (kMdRing - 1)];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) total = __dadd_rn(total, v[u]);
+                }
+                for (; q < a; ++q) total = __dadd_rn(total, ring[q & (kMdRing - 1)]);
+                __threadfence_block();
+                __syncwarp();
+                if (lane == 0) *v_used = q;
+            }
+            if (lane < K) out[lane] = total;
+        }
+        return;
+    }
+    // ---- compute block b: chunks [b 8, b 8 + 8), tiles of 32 elements of each chunk
+    const int64_t b = blockIdx.x - 1;
+    const int64_t c0 = b * kMdG;
+    constexpr int ld = kMdTw + 1, tsz = kMdG * ld;
+    const int q = t >> 5, j = t & 31;          // this thread's element of the tile
+    const int fk = t >> 3, fq = t & 7;         // this thread's (dot, chunk) chain, t < 8 K
+    const int nt = bs / kMdTw;
+    double acc = 0.0;
+    for (int jt = 0; jt < nt; ++jt) {
+        const int64_t i = (c0 + q) * bs + (int64_t)jt * kMdTw + j;
+        const bool in = c0 + q < n_chunks && i < n;  // absent: +0.0 (dot_exact_kernel)
+        const double wv = in ? w[i] : 0.0;
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = (in && k0 + u < K) ? V[k0 + u][i] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k0 + u < K) sm_md[(k0 + u) * tsz + q * ld + j] = __dmul_rn(wv, v[u]);
+        }
+        __syncthreads();
+        if (fk < K) {
+            const double* row = sm_md + fk * tsz + fq * ld;
+#pragma unroll 8
+            for (int e = 0; e < kMdTw; ++e) acc = __dadd_rn(acc, row[e]);
+        }
+        __syncthreads();
+    }
+    if (fk < K && c0 + fq < n_chunks) partials[(int64_t)fk * n_chunks + c0 + fq] = acc;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) st_release_i32(flags + b, 1);
+}
+
+// GCR's new direction (solvers.cpp:316-322): pn = r, apn = w, then for i = 0..K-1 in order
+// pn -= beta_i p_i, apn -= beta_i Ap_i — each element gets the reference's daxpy sequence
+// (fl(fl(-beta_i x) + y)), one pass instead of 2K
+__global__ void __launch_bounds__(256) gcr_orth_exact_kernel(int64_t n, const double* __restrict__ r,
+                                                             const double* __restrict__ w,
+                                                             const double* const* __restrict__ P,
+                                                             const double* const* __restrict__ Q,
+                                                             const double* __restrict__ beta, int K,
+                                                             double* __restrict__ pn, double* __restrict__ apn) {
+    __shared__ const double* sp[64];
+    __shared__ const double* sq[64];
+    __shared__ double sb[64];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        sp[k] = P[k];
+        sq[k] = Q[k];
+        sb[k] = -beta[k];
+    }
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        double a = r[e], b = w[e];
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            double pv[8], qv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k0 + u < K) {
+                    pv[u] = sp[k0 + u][e];
+                    qv[u] = sq[k0 + u][e];
+                }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k0 + u < K) {
+                    a = __dadd_rn(__dmul_rn(sb[k0 + u], pv[u]), a);
+                    b = __dadd_rn(__dmul_rn(sb[k0 + u], qv[u]), b);
+                }
+        }
+        pn[e] = a;
+        apn[e] = b;
+    }
+}
+
 }  // namespace
 
 void k_daxpy(krysp_gpu_ctx* c, int64_t n, double a, const double* x, double* y) {
@@ -508,6 +691,73 @@ void k_chunk_partials(krysp_gpu_ctx* c, int64_t n, const double* x, const double
     dot_exact_kernel<<<(unsigned)((n_chunks + per_block - 1) / per_block), 32 * kExactWarps, 0, c->stream>>>(
         n, x, y, (int)bs, n_chunks, partials, nullptr, nullptr);
     KG_LAUNCH(c);
+}
+
+
+// EXACT <w, v_k>, k < K, into out_dev (device doubles); groups of kMdK dots per pass
+void k_dots_exact_shared(krysp_gpu_ctx* c, int64_t n, const double* w, const double* const* v_host, int K,
+                         int64_t bs, double* out_dev) {
+    if (K <= 0) return;
+    if (n <= 0) {
+        KG_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * K, c->stream));
+        return;
+    }
+    if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
+    const int64_t n_chunks = (n + bs - 1) / bs;
+    const int64_t ncb = (n_chunks + kMdG - 1) / kMdG;
+    // scratch: kMdK x n_chunks partials + the pointer table; flags apart (zeroed, re-armed)
+    const int64_t need = kMdK * n_chunks + 2 * kMdK;
+    if (c->md_scratch_n < need || c->md_flags_n < ncb) {
+        KG_CUDA(cudaStreamSynchronize(c->stream));
+        dev_free(c->md_scratch);
+        dev_free(c->md_flags);
+        c->md_scratch = nullptr;
+        c->md_flags = nullptr;
+        c->md_scratch_n = c->md_flags_n = 0;
+        c->md_scratch = dev_alloc<double>(need, false, c->stream);
+        c->md_scratch_n = need;
+        c->md_flags = dev_alloc<int>(ncb, true, c->stream);
+        c->md_flags_n = ncb;
+    }
+    static bool attr = [] {
+        KG_CUDA(cudaFuncSetAttribute(dot_exact_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     std::max(kMdK * kMdG * (kMdTw + 1), kMdK * (kMdRing + 1)) * 8));
+        return true;
+    }();
+    (void)attr;
+    const double** table = reinterpret_cast<const double**>(c->md_scratch + kMdK * n_chunks);
+    for (int k0 = 0; k0 < K; k0 += kMdK) {
+        const int kk = std::min(kMdK, K - k0);
+        if (kk == 1) {  // a lone dot: the single-dot kernels (k_dot) are faster
+            k_dot(c, n, w, v_host[k0], bs, KRYSP_MODE_EXACT, out_dev + k0);
+            continue;
+        }
+        KG_CUDA(cudaMemcpyAsync(table, v_host + k0, sizeof(double*) * kk, cudaMemcpyHostToDevice, c->stream));
+        const int smem = std::max(kk * kMdG * (kMdTw + 1), kk * (kMdRing + 1)) * 8;
+        dot_exact_shared_kernel<<<(unsigned)(ncb + 1), 256, smem, c->stream>>>(
+            n, w, table, kk, (int)bs, n_chunks, ncb, c->md_scratch, c->md_flags, out_dev + k0);
+        KG_LAUNCH(c);
+        // the table is re-filled for the next group only after this pass read it
+        if (k0 + kMdK < K) KG_CUDA(cudaStreamSynchronize(c->stream));
+    }
+}
+
+void k_gcr_orth_exact(krysp_gpu_ctx* c, int64_t n, const double* r, const double* w, const double* const* p_host,
+                      const double* const* q_host, const double* beta_host, int K, double* pn, double* apn) {
+    if (K > 64) fail(KRYSP_ERROR, "gcr orthogonalization over %d directions (max 64)", K);
+    if (n <= 0) return;
+    // table: 2 x 64 pointers + 64 betas in the context's small scratch
+    if (!c->orth_table) c->orth_table = dev_alloc<double>(3 * 64, false, c->stream);
+    std::vector<double> h(3 * 64);
+    std::memcpy(h.data(), p_host, sizeof(double*) * K);
+    std::memcpy(h.data() + 64, q_host, sizeof(double*) * K);
+    std::memcpy(h.data() + 128, beta_host, sizeof(double) * K);
+    KG_CUDA(cudaMemcpyAsync(c->orth_table, h.data(), sizeof(double) * 3 * 64, cudaMemcpyHostToDevice, c->stream));
+    const double* const* P = reinterpret_cast<const double* const*>(c->orth_table);
+    const double* const* Q = reinterpret_cast<const double* const*>(c->orth_table + 64);
+    gcr_orth_exact_kernel<<<ew_grid(c, n), 256, 0, c->stream>>>(n, r, w, P, Q, c->orth_table + 128, K, pn, apn);
+    KG_LAUNCH(c);
+    KG_CUDA(cudaStreamSynchronize(c->stream));  // h (pageable) is read by the copy before it leaves scope
 }
 
 double host_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode) {

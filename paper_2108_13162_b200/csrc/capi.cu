@@ -106,6 +106,9 @@ krysp_status krysp_gpu_ctx_destroy(krysp_gpu_ctx* c) {
         dev_free(c->d_scalars);
         dev_free(c->dot_scratch);
         dev_free(c->dot_flags);
+        dev_free(c->md_scratch);
+        dev_free(c->md_flags);
+        dev_free(c->orth_table);
         if (c->h_pinned) cudaFreeHost(c->h_pinned);
         if (c->sync_ev) cudaEventDestroy(c->sync_ev);
         if (c->own_stream) cudaStreamDestroy(c->own_stream);

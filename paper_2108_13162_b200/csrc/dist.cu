@@ -1243,6 +1243,11 @@ __global__ void __launch_bounds__(256) dot_fold_kernel(const double* __restrict_
 
 struct DistEngine : Engine {
     krysp_gpu_dist* d;
+    // distributed dots: GCR keeps the reference's loop over Engine::dot
+    bool gcr_orthogonalize(const double*, const double*, const std::vector<const double*>&,
+                           const std::vector<const double*>&, const std::vector<double>&, double*, double*) override {
+        return false;
+    }
     std::vector<int64_t> off;  // offset of each held band in the engine vectors
     std::vector<DVec> xe;      // per held band: n_local + n_ghost
     // EXACT NCCL dots

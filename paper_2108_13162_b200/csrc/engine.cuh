@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <vector>
 
 #include "descent.cuh"
 #include "internal.cuh"
@@ -98,6 +99,24 @@ struct Engine {
         return v;
     }
     double norm2(const double* x) { return std::sqrt(dot(x, x)); }
+    // GCR's classical Gram-Schmidt step (solvers.cpp:316-322) batched: the dots <w, Ap_i>
+    // (w shared) in one pass, ||Ap_i||^2 from `dd` (the same vectors' dots computed when each
+    // direction was used: identical values), then pn = r, apn = w, minus beta_i p_i / Ap_i in
+    // i order per element.  Returns false when the engine cannot (partitioned engines: their
+    // dots are distributed) — the caller then runs the reference's loop.
+    virtual bool gcr_orthogonalize(const double* r, const double* w, const std::vector<const double*>& p,
+                                   const std::vector<const double*>& ap, const std::vector<double>& dd, double* pn,
+                                   double* apn) {
+        if (mode != KRYSP_MODE_EXACT || p.empty() || p.size() > 64) return false;
+        const int K = (int)p.size();
+        k_dots_exact_shared(c, n, w, ap.data(), K, pol.block_size, c->d_scalars);
+        KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, sizeof(double) * K, cudaMemcpyDeviceToHost, c->stream));
+        stream_wait(c);
+        std::vector<double> beta((size_t)K);
+        for (int i = 0; i < K; ++i) beta[(size_t)i] = c->h_pinned[i] / dd[(size_t)i];
+        k_gcr_orth_exact(c, n, r, w, p.data(), ap.data(), beta.data(), K, pn, apn);
+        return true;
+    }
     void daxpy(double a, const double* x, double* y) { k_daxpy(c, n, a, x, y); }
     void axpby(double a, const double* x, double b, double* y) { k_axpby(c, n, a, x, b, y); }
     void copy(const double* s, double* d) { k_copy(c, n, s, d); }

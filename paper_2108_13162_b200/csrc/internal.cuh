@@ -82,6 +82,12 @@ struct krysp_gpu_ctx {
     int64_t dot_scratch_n = 0;
     int* dot_flags = nullptr;
     int64_t dot_flags_n = 0;
+    // EXACT dots sharing an operand (GCR): partials + pointer table, flags; GCR orthogonalization table
+    double* md_scratch = nullptr;
+    int64_t md_scratch_n = 0;
+    int* md_flags = nullptr;
+    int64_t md_flags_n = 0;
+    double* orth_table = nullptr;
     // NCCL communicator whose health the host wait loops poll (set while a multi-GPU
     // partition is alive on this context; see comm_poll in dist.cu)
     void* nccl_watch = nullptr;
@@ -757,6 +763,13 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
 // EXACT dot(s) with the fold streaming beside the chunk pass (a2 == nullptr: one dot); scratch:
 // exact_dot_stream_scratch(n, bs) doubles, zeroed once (flags re-arm themselves)
 int64_t exact_dot_stream_scratch(int64_t n, int64_t bs);
+// EXACT <w, v_k> for k < K (v_host: host array of device pointers) into out_dev (device), the
+// reference's order per dot; GCR's ordered direction update (pn = r - sum beta_i p_i, apn = w -
+// sum beta_i Ap_i, applied in i order per element)
+void k_dots_exact_shared(krysp_gpu_ctx* c, int64_t n, const double* w, const double* const* v_host, int K,
+                         int64_t bs, double* out_dev);
+void k_gcr_orth_exact(krysp_gpu_ctx* c, int64_t n, const double* r, const double* w, const double* const* p_host,
+                      const double* const* q_host, const double* beta_host, int K, double* pn, double* apn);
 void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
                         const double* b2, int64_t bs, double* scratch, double* out1, double* out2, const int* gate,
                         int* flags = nullptr);  // flags: default inside scratch (fixed-length owners)

@@ -180,6 +180,7 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
         return;
     }
     std::vector<DVec> dirs, op_dirs;
+    std::vector<double> dd;  // <Ap_j, Ap_j> of each direction slot, as computed when it was used
     double measure = 1.0;
     for (rep.mark(e.c->stream); rep.iterations < cfg.max_iterations && !rep.converged;) {
         // the basis storage is reused across restarts (dirs.clear() in the reference)
@@ -195,6 +196,8 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
             double d = e.dot(ap, ap);
             check_finite(d, "direction norm");
             if (vanishes(d)) fail(KRYSP_BREAKDOWN, "gcr: direction norm vanished");
+            if ((int64_t)dd.size() <= j) dd.resize((size_t)j + 1);
+            dd[(size_t)j] = d;
             double alpha = e.dot(r, ap) / d;
             check_finite(alpha, "alpha");
             e.daxpy(alpha, p, x);
@@ -211,12 +214,19 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
             e.op(r, w);
             DVec& pn = slot(dirs, j + 1);
             DVec& apn = slot(op_dirs, j + 1);
-            e.copy(r, pn);
-            e.copy(w, apn);
+            std::vector<const double*> ps, aps;
             for (int64_t i = 0; i <= j; ++i) {
-                double beta = e.dot(w, op_dirs[(size_t)i]) / e.dot(op_dirs[(size_t)i], op_dirs[(size_t)i]);
-                e.daxpy(-beta, dirs[(size_t)i], pn);
-                e.daxpy(-beta, op_dirs[(size_t)i], apn);
+                ps.push_back(dirs[(size_t)i]);
+                aps.push_back(op_dirs[(size_t)i]);
+            }
+            if (!e.gcr_orthogonalize(r, w, ps, aps, dd, pn, apn)) {
+                e.copy(r, pn);
+                e.copy(w, apn);
+                for (int64_t i = 0; i <= j; ++i) {
+                    double beta = e.dot(w, op_dirs[(size_t)i]) / e.dot(op_dirs[(size_t)i], op_dirs[(size_t)i]);
+                    e.daxpy(-beta, dirs[(size_t)i], pn);
+                    e.daxpy(-beta, op_dirs[(size_t)i], apn);
+                }
             }
         }
     }
