@@ -417,17 +417,26 @@ __device__ __forceinline__ void stream_fold(int64_t n_chunks, int G, int64_t ncb
         volatile long long* v_avail = &s_avail;
         volatile long long* v_used = s_used;
         if (w == 1) {  // loader
-            const int64_t maxk = min(32, kRing / (2 * G));
+            // up to 256 blocks per poll (lane l: blocks nb + 8 l .. + 7), then one acquire
+            // fence: one-partial blocks (G = 1) still move 256 partials per round trip
+            const int64_t maxk = min(256, kRing / (2 * G));
             int64_t nb = 0;
             while (nb < ncb) {
-                const int64_t bb = nb + lane;
-                const int rdy = (lane < maxk && bb < ncb) ? ld_acquire_i32(flags + bb) : 0;
-                const unsigned m = __ballot_sync(0xffffffffu, rdy != 0);
-                const int k = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+                int cnt = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t o = 8 * lane + u, bb = nb + o;
+                    const int rdy = (o < maxk && bb < ncb) ? *(volatile const int*)(flags + bb) : 0;
+                    cnt += (cnt == u && rdy) ? 1 : 0;
+                }
+                const unsigned full = __ballot_sync(0xffffffffu, cnt == 8);
+                const int first = (full == 0xffffffffu) ? 32 : __ffs(~full) - 1;
+                const int k = first == 32 ? 256 : 8 * first + __shfl_sync(0xffffffffu, cnt, first);
                 if (k == 0) {
                     __nanosleep(64);
                     continue;
                 }
+                __threadfence();  // acquire: the k blocks' partials are visible from here on
                 const int64_t p0 = nb * G, p1 = min((nb + k) * (int64_t)G, n_chunks);
                 for (;;) {  // ring space: both folders past p1 - kRing
                     const long long u = ND == 2 ? min(v_used[0], v_used[1]) : v_used[0];
@@ -452,7 +461,7 @@ __device__ __forceinline__ void stream_fold(int64_t n_chunks, int G, int64_t ncb
                         }
                     }
                 }
-                if (lane < k) flags[nb + lane] = 0;  // re-armed for the next launch
+                for (int o = lane; o < k; o += 32) flags[nb + o] = 0;  // re-armed for the next launch
                 __threadfence_block();
                 __syncwarp();
                 if (lane == 0) *v_avail = p1;

@@ -712,6 +712,153 @@ __global__ void ex_update_kernel(int64_t n, double* __restrict__ x, double* __re
     }
 }
 
+// EXACT P-CG's SpMV with sigma = <p, Ap> fused (streaming fold): the policy's tile kernel for
+// one lane per row (csr_tma_kernel<1>: same TMA pipeline, same row sums) plus a ninth warp that
+// adds fl(p_r (Ap)_r) in row order into the reference's chunk sums (kernels.cpp:74-78) while
+// the row warps compute the next tile; a CTA takes whole "units" (max(bs, 256) rows: the tiles
+// of one chunk, or the chunks of one tile) so each chunk sum is one CTA's chain.  Block 0 folds
+// the chunk sums left to right (stream_fold) as units complete.
+constexpr int kSgNT = kTileRows + 32;
+
+__global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, const double* __restrict__ xp,
+                                                              double* __restrict__ y, TmaTileLayout L, int bs,
+                                                              int64_t n_chunks, int G, int T_per, int64_t n_units,
+                                                              double* partials, int* flags, double* sigma_out,
+                                                              const int* gate) {
+    if (gate && *(volatile const int*)gate) return;
+    extern __shared__ __align__(128) unsigned char smem_sg[];
+    if (blockIdx.x == 0) {
+        stream_fold<1>(n_chunks, G, n_units, partials, nullptr, flags, sigma_out, nullptr,
+                       reinterpret_cast<double*>(smem_sg + 128));
+        return;
+    }
+    constexpr int TR = kTileRows;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_sg);
+    unsigned char* stage_base = smem_sg + 64;
+    double* sprod = reinterpret_cast<double*>(stage_base + 2 * L.stage_bytes());  // [2][TR]
+    const int64_t n_tiles = ((int64_t)A.n_rows + TR - 1) / TR;
+    const int64_t cta = blockIdx.x - 1, ncta = gridDim.x - 1;
+    const uint64_t pol = evict_first_policy();
+    const int t = threadIdx.x;
+    auto tile_of = [&](int64_t it) -> int64_t { return (cta + (it / T_per) * ncta) * T_per + it % T_per; };
+    auto stage_ptr = [&](int st, int part) -> unsigned char* {
+        unsigned char* b = stage_base + st * L.stage_bytes();
+        return part == 0 ? b : part == 1 ? b + L.val_bytes() : b + L.val_bytes() + L.col_bytes();
+    };
+    auto issue = [&](int64_t tile, int st) {
+        const int64_t r0 = tile * TR;
+        const int64_t r1 = (r0 + TR < A.n_rows) ? r0 + TR : (int64_t)A.n_rows;
+        const int32_t k0 = __ldg(A.row_ptr + r0), k1 = __ldg(A.row_ptr + r1);
+        const int32_t va = k0 & ~1, vb = (k1 + 1) & ~1;
+        const int32_t ca = k0 & ~3, cb = (k1 + 3) & ~3;
+        const uint32_t bv = (uint32_t)(vb - va) * 8u, bc = (uint32_t)(cb - ca) * 4u;
+        const uint32_t brp = (uint32_t)(((r1 - r0 + 1) + 3) & ~3) * 4u;
+        mbar_arrive_expect_tx(&bars[st], bv + bc + brp);
+        bulk_g2s(stage_ptr(st, 2), A.row_ptr + r0, brp, &bars[st], pol);
+        if (bv) bulk_g2s(stage_ptr(st, 0), A.val + va, bv, &bars[st], pol);
+        if (bc) bulk_g2s(stage_ptr(st, 1), A.col + ca, bc, &bars[st], pol);
+    };
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0 && tile_of(0) < n_tiles) issue(tile_of(0), 0);
+    const int lane = t & 31;
+    double acc = 0.0;  // fold warp: lane g's running chunk sum
+    // fold warp: the products of the CTA's it-th tile (buffer it & 1)
+    auto fold = [&](int64_t it) {
+        const double* pr = sprod + (it & 1) * TR;
+        const int64_t tile = tile_of(it);
+        if (G == 1) {  // bs >= TR: lane 0 carries the chunk across its T_per tiles
+            if (lane == 0) {  // the chain reads 8 products ahead (16-byte loads, next batch in flight)
+                const double2* p2 = reinterpret_cast<const double2*>(pr);
+                double2 cur[4], nxt[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) cur[k] = p2[k];
+                for (int j0 = 4; j0 < TR / 2; j0 += 4) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) nxt[k] = p2[j0 + k];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        acc = __dadd_rn(acc, cur[k].x);
+                        acc = __dadd_rn(acc, cur[k].y);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    acc = __dadd_rn(acc, cur[k].x);
+                    acc = __dadd_rn(acc, cur[k].y);
+                }
+            }
+            if (it % T_per == T_per - 1 || tile == n_tiles - 1) {
+                const int64_t unit = tile / T_per;
+                if (lane == 0) {  // st.release orders the partial before the flag (no full fence)
+                    partials[unit] = acc;
+                    acc = 0.0;
+                    st_release_i32(flags + unit, 1);
+                }
+            }
+        } else {  // bs < TR: lane g sums chunk g of the tile
+            if (lane < G) {
+                const double* row = pr + lane * bs;
+                double a = 0.0;
+#pragma unroll 8
+                for (int j = 0; j < bs; ++j) a = __dadd_rn(a, row[j]);
+                if (tile * G + lane < n_chunks) partials[tile * G + lane] = a;
+            }
+            __syncwarp();  // the lanes' partials happen-before lane 0's release (cumulative)
+            if (lane == 0) st_release_i32(flags + tile, 1);
+        }
+    };
+    uint32_t parity = 0;
+    int64_t it = 0;
+    for (;; ++it) {
+        const int64_t tile = tile_of(it);
+        if (tile >= n_tiles) break;
+        const int st = it & 1;
+        if (t < TR) {
+            const int64_t next = tile_of(it + 1);
+            if (t == 0 && next < n_tiles) issue(next, st ^ 1);  // stage st^1 freed last iteration
+            mbar_wait(&bars[st], (parity >> st) & 1u);
+            parity ^= 1u << st;
+            const double* s_val = reinterpret_cast<const double*>(stage_ptr(st, 0));
+            const int32_t* s_col = reinterpret_cast<const int32_t*>(stage_ptr(st, 1));
+            const int32_t* s_rp = reinterpret_cast<const int32_t*>(stage_ptr(st, 2));
+            const int64_t r = tile * TR + t;
+            double prod = 0.0;  // rows past the end add +0.0 (the dot kernels' convention)
+            if (r < A.n_rows) {
+                const int32_t k0 = s_rp[0];
+                const int32_t rb = s_rp[t], re = s_rp[t + 1];
+                const int av = rb - (k0 & ~1), ac = rb - (k0 & ~3), len = re - rb;
+                double sum = 0.0;  // csr_tma_kernel<1>'s row order
+                if (len <= 8) {
+                    double xv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (j < len) xv[j] = __ldg(xp + s_col[ac + j]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (j < len) sum = madd(sum, s_val[av + j], xv[j]);
+                } else {
+#pragma unroll 8
+                    for (int j = 0; j < len; ++j) sum = madd(sum, s_val[av + j], __ldg(xp + s_col[ac + j]));
+                }
+                y[r] = sum;
+                prod = __dmul_rn(__ldg(xp + r), sum);
+            }
+            sprod[st * TR + t] = prod;
+        } else if (it > 0) {
+            fold(it - 1);
+        }
+        __syncthreads();  // stage st re-filled in the next-but-one iteration; sprod[st] folded next
+    }
+    if (t >= TR && it > 0) fold(it - 1);
+}
+
 // The EXACT update fused with the reference-order rho = <r, z> (streaming fold, block 0):
 // blocks 1..ncb own G chunks of bs rows; per tile (tw consecutive rows of each chunk, 4 rows
 // per thread in flight) they apply ex_update_kernel's exact steps and stage fl(r_i z_i); lane
@@ -2607,6 +2754,42 @@ struct PcgSession {
         }
     }
 
+    // Ap and sigma = <p, Ap> in one pass (csr_tma_sigma_kernel); false unless the policy's
+    // SpMV is the one-lane-per-row tile kernel and the fold is long (KRYSP_SIGMA=0: off)
+    bool exact_spmv_sigma(const double* pz, double* y) {
+        static const bool on = [] {
+            const char* v = std::getenv("KRYSP_SIGMA");
+            return !(v && v[0] == '0');
+        }();
+        const krysp_gpu_mat* m = e.A;
+        const int64_t bs = e.pol.block_size;
+        const int64_t n_chunks = (n + bs - 1) / bs;
+        if (!on || m->format != KRYSP_FMT_CSR || e.pol.workers_per_row != 1 || n_chunks < 4096 ||
+            !csr_use_tile(m, 1))
+            return false;
+        krysp_gpu_ctx* c = e.c;
+        const int G = bs >= kTileRows ? 1 : (int)(kTileRows / bs);
+        const int T_per = bs >= kTileRows ? (int)(bs / kTileRows) : 1;
+        const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
+        const int64_t n_units = (n_tiles + T_per - 1) / T_per;
+        int cap = (int)std::min<int64_t>(std::max<int64_t>(tile_nnz_bound(m, 1) + 8, 64), kTileCapMax);
+        cap = (cap + 3) & ~3;
+        const TmaTileLayout L{cap, 0, kTileRows};
+        const int smem = std::max(64 + 2 * L.stage_bytes() + 2 * kTileRows * 8, 128 + kRing * 8);
+        auto k = csr_tma_sigma_kernel;
+        if (smem > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        // persistent compute CTAs + the folder must all be resident at once: a CTA left waiting
+        // for a slot would run its whole share after the others, with the fold waiting on it
+        const int64_t slots = (int64_t)c->sm_count * resident_blocks(k, kSgNT, smem);
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>(n_units, slots - 1));
+        double* partials = ex_partials;
+        int* flags = reinterpret_cast<int*>((double*)ex_partials + 2 * n_chunks);
+        k<<<(unsigned)(g + 1), kSgNT, smem, c->stream>>>(m->csr(), pz, y, L, (int)bs, n_chunks, G, T_per, n_units,
+                                                        partials, flags, ex_scal, &st->done);
+        KG_LAUNCH(c);
+        return true;
+    }
+
     // update + rho in one pass with the streaming fold (ex_update_rho_kernel); false when the
     // fold is short (C1 class: the one-pass dot kernels are faster) or disabled (KRYSP_UR=0)
     bool exact_update_rho(const double* pz, double* z) {
@@ -2660,8 +2843,10 @@ struct PcgSession {
             const unsigned g = grid_for(n, kFusedNT, (int64_t)c->sm_count * 8);
             ex_beta_kernel<<<g, kFusedNT, 0, c->stream>>>(n, pb, zb, st);  // z += beta p, then swap
             KG_LAUNCH(c);
-            spmv_exact_gated(zb, ap);                                        // Ap with p = zb
-            exact_dot(zb, ap, ex_scal);
+            if (!exact_spmv_sigma(zb, ap)) {
+                spmv_exact_gated(zb, ap);                                    // Ap with p = zb
+                exact_dot(zb, ap, ex_scal);
+            }
             ex_sigma_kernel<<<1, 1, 0, c->stream>>>(st, ex_scal);
             KG_LAUNCH(c);
             if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));

@@ -10,7 +10,7 @@ import paper_2108_13162_b200 as kg
 
 pytestmark = pytest.mark.gpu
 
-POLICIES = [(32, 1), (64, 4), (128, 2), (256, 8), (512, 1), (1024, 32)]
+POLICIES = [(32, 1), (64, 1), (128, 1), (64, 4), (128, 2), (256, 8), (512, 1), (1024, 32)]
 
 
 @pytest.fixture(scope="module")
@@ -40,3 +40,17 @@ def test_exact_stream_full_solve_matches_reference(lap100, ref):
         assert o.iterations == want["iterations"]
         assert o.final_residual_measure == want["final_residual_measure"]
         np.testing.assert_array_equal(o.solution, want["solution"])
+
+
+@pytest.mark.parametrize("bs", [256, 512, 1024])
+def test_exact_pcg_fused_sigma_units_bitwise(ctx, port, ref, bs):
+    """lap3d7 200^3 (8 M rows): the SpMV + sigma kernel with one-chunk tiles (bs 256) and
+    chunks of 2 and 4 tiles, against the reference's P-CG history at <bs,1>."""
+    m = port.generate("lap3d7", 200)
+    R = ref.from_csr(m)
+    A = ctx.generate("lap3d7", 200)
+    b = np.ones(m.n_rows)
+    want = ref.solve(R, "pcg", b, tol=1e-300, max_it=30, bs=bs, tw=1)["residual_history"]
+    cfg = kg.SolverConfig(mode="exact", policy=kg.ExecPolicy(bs, 1), tolerance=1e-300, max_iterations=30)
+    o = kg.solve(A, "pcg", b, cfg=cfg)
+    np.testing.assert_array_equal(o.residual_history, want)
