@@ -720,22 +720,28 @@ __global__ void ex_update_kernel(int64_t n, double* __restrict__ x, double* __re
 // the chunk sums left to right (stream_fold) as units complete.
 constexpr int kSgNT = kTileRows + 32;
 
+// ND dots of the row result v_r = (Ax)_r [* inv_r]: dot d multiplies v_r by a_d[r] (a_d NULL:
+// by v_r itself).  EXACT P-CG: ND = 1, a_0 = x (sigma = <p, Ap>); EXACT BiCGStab: ND = 1,
+// a_0 = r^ (<r^, v>) and ND = 2, a_0 = NULL, a_1 = x (<t, t>, <t, s>).
+template <bool kJacobi, int ND>
 __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, const double* __restrict__ xp,
-                                                              double* __restrict__ y, TmaTileLayout L, int bs,
+                                                              double* __restrict__ y,
+                                                              const double* __restrict__ inv,
+                                                              const double* __restrict__ a0,
+                                                              const double* __restrict__ a1, TmaTileLayout L, int bs,
                                                               int64_t n_chunks, int G, int T_per, int64_t n_units,
-                                                              double* partials, int* flags, double* sigma_out,
-                                                              const int* gate) {
+                                                              double* pa, double* pb, int* flags, double* out0,
+                                                              double* out1, const int* gate) {
     if (gate && *(volatile const int*)gate) return;
     extern __shared__ __align__(128) unsigned char smem_sg[];
     if (blockIdx.x == 0) {
-        stream_fold<1>(n_chunks, G, n_units, partials, nullptr, flags, sigma_out, nullptr,
-                       reinterpret_cast<double*>(smem_sg + 128));
+        stream_fold<ND>(n_chunks, G, n_units, pa, pb, flags, out0, out1, reinterpret_cast<double*>(smem_sg + 128));
         return;
     }
     constexpr int TR = kTileRows;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_sg);
     unsigned char* stage_base = smem_sg + 64;
-    double* sprod = reinterpret_cast<double*>(stage_base + 2 * L.stage_bytes());  // [2][TR]
+    double* sprod = reinterpret_cast<double*>(stage_base + 2 * L.stage_bytes());  // [2][ND][TR]
     const int64_t n_tiles = ((int64_t)A.n_rows + TR - 1) / TR;
     const int64_t cta = blockIdx.x - 1, ncta = gridDim.x - 1;
     const uint64_t pol = evict_first_policy();
@@ -766,14 +772,13 @@ __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, cons
     __syncthreads();
     if (t == 0 && tile_of(0) < n_tiles) issue(tile_of(0), 0);
     const int lane = t & 31;
-    double acc = 0.0;  // fold warp: lane g's running chunk sum
+    double acc = 0.0;  // fold warp: lane d's running chunk sum of dot d (G == 1)
     // fold warp: the products of the CTA's it-th tile (buffer it & 1)
     auto fold = [&](int64_t it) {
-        const double* pr = sprod + (it & 1) * TR;
         const int64_t tile = tile_of(it);
-        if (G == 1) {  // bs >= TR: lane 0 carries the chunk across its T_per tiles
-            if (lane == 0) {  // the chain reads 8 products ahead (16-byte loads, next batch in flight)
-                const double2* p2 = reinterpret_cast<const double2*>(pr);
+        if (G == 1) {  // bs >= TR: lane d carries dot d's chunk across its T_per tiles
+            if (lane < ND) {  // the chain reads 8 products ahead (16-byte loads, next batch in flight)
+                const double2* p2 = reinterpret_cast<const double2*>(sprod + ((it & 1) * ND + lane) * TR);
                 double2 cur[4], nxt[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) cur[k] = p2[k];
@@ -796,19 +801,21 @@ __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, cons
             }
             if (it % T_per == T_per - 1 || tile == n_tiles - 1) {
                 const int64_t unit = tile / T_per;
-                if (lane == 0) {  // st.release orders the partial before the flag (no full fence)
-                    partials[unit] = acc;
+                if (lane < ND) {
+                    (lane == 0 ? pa : pb)[unit] = acc;
                     acc = 0.0;
-                    st_release_i32(flags + unit, 1);
                 }
+                __syncwarp();  // both chains' partials happen-before the release (cumulative)
+                if (lane == 0) st_release_i32(flags + unit, 1);
             }
-        } else {  // bs < TR: lane g sums chunk g of the tile
-            if (lane < G) {
-                const double* row = pr + lane * bs;
+        } else {  // bs < TR: lane d G + g sums chunk g of dot d in the tile
+            if (lane < ND * G) {
+                const int d = lane / G, g = lane - d * G;
+                const double* row = sprod + ((it & 1) * ND + d) * TR + g * bs;
                 double a = 0.0;
 #pragma unroll 8
                 for (int j = 0; j < bs; ++j) a = __dadd_rn(a, row[j]);
-                if (tile * G + lane < n_chunks) partials[tile * G + lane] = a;
+                if (tile * G + g < n_chunks) (d == 0 ? pa : pb)[tile * G + g] = a;
             }
             __syncwarp();  // the lanes' partials happen-before lane 0's release (cumulative)
             if (lane == 0) st_release_i32(flags + tile, 1);
@@ -829,7 +836,7 @@ __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, cons
             const int32_t* s_col = reinterpret_cast<const int32_t*>(stage_ptr(st, 1));
             const int32_t* s_rp = reinterpret_cast<const int32_t*>(stage_ptr(st, 2));
             const int64_t r = tile * TR + t;
-            double prod = 0.0;  // rows past the end add +0.0 (the dot kernels' convention)
+            double p0 = 0.0, p1 = 0.0;  // rows past the end add +0.0 (the dot kernels' convention)
             if (r < A.n_rows) {
                 const int32_t k0 = s_rp[0];
                 const int32_t rb = s_rp[t], re = s_rp[t + 1];
@@ -847,10 +854,13 @@ __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, cons
 #pragma unroll 8
                     for (int j = 0; j < len; ++j) sum = madd(sum, s_val[av + j], __ldg(xp + s_col[ac + j]));
                 }
-                y[r] = sum;
-                prod = __dmul_rn(__ldg(xp + r), sum);
+                const double v = kJacobi ? __dmul_rn(sum, __ldg(inv + r)) : sum;  // op(): fl(sum * inv)
+                y[r] = v;
+                p0 = __dmul_rn(a0 ? __ldg(a0 + r) : v, v);
+                if (ND == 2) p1 = __dmul_rn(a1 ? __ldg(a1 + r) : v, v);
             }
-            sprod[st * TR + t] = prod;
+            sprod[(st * ND) * TR + t] = p0;
+            if (ND == 2) sprod[(st * ND + 1) * TR + t] = p1;
         } else if (it > 0) {
             fold(it - 1);
         }
@@ -2501,6 +2511,44 @@ bool pcg_persistent_eligible(const krysp_gpu_mat* m) {
 // Device-resident FAST P-CG session: setup once, then iterations are enqueued as CUDA-graph
 // launches (chunks of kChunk iterations + single-iteration graphs for remainders).  Also
 // backs the krysp_gpu_solver_* C-ABI (bench / profiling / multi-step drivers).
+// the SpMV of an EXACT device-resident session with ND reference-order dots of its rows fused
+// (csr_tma_sigma_kernel); false when not applicable: not CSR, lanes per row > 1, rows too long
+// for the tile kernel, a short fold, or KRYSP_SIGMA=0
+bool exact_spmv_dots(Engine& e, const double* x, double* y, const double* inv, const double* a0, const double* a1,
+                     int nd, double* scratch, double* out0, double* out1, const int* gate) {
+    static const bool on = [] {
+        const char* v = std::getenv("KRYSP_SIGMA");
+        return !(v && v[0] == '0');
+    }();
+    const krysp_gpu_mat* m = e.A;
+    const int64_t n = e.n, bs = e.pol.block_size;
+    const int64_t n_chunks = (n + bs - 1) / bs;
+    if (!on || !m || m->format != KRYSP_FMT_CSR || e.pol.workers_per_row != 1 || n_chunks < 4096 ||
+        !csr_use_tile(m, 1))
+        return false;
+    krysp_gpu_ctx* c = e.c;
+    const int G = bs >= kTileRows ? 1 : (int)(kTileRows / bs);
+    const int T_per = bs >= kTileRows ? (int)(bs / kTileRows) : 1;
+    const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
+    const int64_t n_units = (n_tiles + T_per - 1) / T_per;
+    int cap = (int)std::min<int64_t>(std::max<int64_t>(tile_nnz_bound(m, 1) + 8, 64), kTileCapMax);
+    cap = (cap + 3) & ~3;
+    const TmaTileLayout L{cap, 0, kTileRows};
+    const int smem = std::max(64 + 2 * L.stage_bytes() + 2 * nd * kTileRows * 8, 128 + nd * kRing * 8);
+    auto k = inv ? (nd == 2 ? csr_tma_sigma_kernel<true, 2> : csr_tma_sigma_kernel<true, 1>)
+                 : (nd == 2 ? csr_tma_sigma_kernel<false, 2> : csr_tma_sigma_kernel<false, 1>);
+    if (smem > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // persistent compute CTAs + the folder must all be resident at once: a CTA left waiting
+    // for a slot would run its whole share after the others, with the fold waiting on it
+    const int64_t slots = (int64_t)c->sm_count * resident_blocks(k, kSgNT, smem);
+    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(n_units, slots - 1));
+    int* flags = reinterpret_cast<int*>(scratch + 2 * n_chunks);
+    k<<<(unsigned)(g + 1), kSgNT, smem, c->stream>>>(m->csr(), x, y, inv, a0, a1, L, (int)bs, n_chunks, G, T_per,
+                                                    n_units, scratch, scratch + n_chunks, flags, out0, out1, gate);
+    KG_LAUNCH(c);
+    return true;
+}
+
 struct PcgSession {
     static constexpr int kChunk = 16;
     Engine e;
@@ -2757,37 +2805,7 @@ struct PcgSession {
     // Ap and sigma = <p, Ap> in one pass (csr_tma_sigma_kernel); false unless the policy's
     // SpMV is the one-lane-per-row tile kernel and the fold is long (KRYSP_SIGMA=0: off)
     bool exact_spmv_sigma(const double* pz, double* y) {
-        static const bool on = [] {
-            const char* v = std::getenv("KRYSP_SIGMA");
-            return !(v && v[0] == '0');
-        }();
-        const krysp_gpu_mat* m = e.A;
-        const int64_t bs = e.pol.block_size;
-        const int64_t n_chunks = (n + bs - 1) / bs;
-        if (!on || m->format != KRYSP_FMT_CSR || e.pol.workers_per_row != 1 || n_chunks < 4096 ||
-            !csr_use_tile(m, 1))
-            return false;
-        krysp_gpu_ctx* c = e.c;
-        const int G = bs >= kTileRows ? 1 : (int)(kTileRows / bs);
-        const int T_per = bs >= kTileRows ? (int)(bs / kTileRows) : 1;
-        const int64_t n_tiles = (n + kTileRows - 1) / kTileRows;
-        const int64_t n_units = (n_tiles + T_per - 1) / T_per;
-        int cap = (int)std::min<int64_t>(std::max<int64_t>(tile_nnz_bound(m, 1) + 8, 64), kTileCapMax);
-        cap = (cap + 3) & ~3;
-        const TmaTileLayout L{cap, 0, kTileRows};
-        const int smem = std::max(64 + 2 * L.stage_bytes() + 2 * kTileRows * 8, 128 + kRing * 8);
-        auto k = csr_tma_sigma_kernel;
-        if (smem > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        // persistent compute CTAs + the folder must all be resident at once: a CTA left waiting
-        // for a slot would run its whole share after the others, with the fold waiting on it
-        const int64_t slots = (int64_t)c->sm_count * resident_blocks(k, kSgNT, smem);
-        const int64_t g = std::max<int64_t>(1, std::min<int64_t>(n_units, slots - 1));
-        double* partials = ex_partials;
-        int* flags = reinterpret_cast<int*>((double*)ex_partials + 2 * n_chunks);
-        k<<<(unsigned)(g + 1), kSgNT, smem, c->stream>>>(m->csr(), pz, y, L, (int)bs, n_chunks, G, T_per, n_units,
-                                                        partials, flags, ex_scal, &st->done);
-        KG_LAUNCH(c);
-        return true;
+        return exact_spmv_dots(e, pz, y, nullptr, pz, nullptr, 1, ex_partials, ex_scal, nullptr, &st->done);
     }
 
     // update + rho in one pass with the streaming fold (ex_update_rho_kernel); false when the
@@ -3482,8 +3500,10 @@ struct BicgstabSession {
             auto dot2 = [&](const double* a1, const double* b1, const double* a2, const double* b2, double* out) {
                 k_dot_exact_stream(c, n, a1, b1, a2, b2, e.pol.block_size, ex_partials, out, out + 1, gate);
             };
-            op_exact(p, v);                                  // v = op(p)
-            dot(rh, v, sc);                                  // <r^, v>
+            if (!exact_spmv_dots(e, p, v, dinv, rh, nullptr, 1, ex_partials, sc, nullptr, gate)) {
+                op_exact(p, v);                              // v = op(p)
+                dot(rh, v, sc);                              // <r^, v>
+            }
             ex_bs_alpha_kernel<<<1, 1, 0, c->stream>>>(st, sc);
             KG_LAUNCH(c);
             ex_bs_s_kernel<<<g, kBiNT, 0, c->stream>>>(n, s, r, v, st);
@@ -3491,8 +3511,10 @@ struct BicgstabSession {
             dot(s, s, sc + 1);                               // ||s||^2
             ex_bs_half_kernel<<<1, 1, 0, c->stream>>>(st, sc + 1, hist);
             KG_LAUNCH(c);
-            op_exact(s, t);                                  // t = op(s)
-            dot2(t, t, t, s, sc + 2);                        // <t,t>, <t,s>
+            if (!exact_spmv_dots(e, s, t, dinv, nullptr, s, 2, ex_partials, sc + 2, sc + 3, gate)) {
+                op_exact(s, t);                              // t = op(s)
+                dot2(t, t, t, s, sc + 2);                    // <t,t>, <t,s>
+            }
             ex_bs_omega_kernel<<<1, 1, 0, c->stream>>>(st, sc + 2);
             KG_LAUNCH(c);
             ex_bs_update_kernel<<<g, kBiNT, 0, c->stream>>>(n, x, r, p, s, t, st, ex_counter);
