@@ -539,6 +539,32 @@ void k_mul(krysp_gpu_ctx* c, int64_t n, const double* a, const double* b, double
     KG_LAUNCH(c);
 }
 
+// the context's streaming-dot partials (two dots) and ready flags, grown on demand
+static void ensure_dot_scratch(krysp_gpu_ctx* c, int64_t n_chunks) {
+    if (c->dot_scratch_n >= 2 * n_chunks && c->dot_flags_n >= n_chunks) return;
+    KG_CUDA(cudaStreamSynchronize(c->stream));
+    dev_free(c->dot_scratch);
+    dev_free(c->dot_flags);
+    c->dot_scratch = nullptr;
+    c->dot_flags = nullptr;
+    c->dot_scratch_n = c->dot_flags_n = 0;
+    c->dot_scratch = dev_alloc<double>(2 * n_chunks, false, c->stream);
+    c->dot_scratch_n = 2 * n_chunks;
+    c->dot_flags = dev_alloc<int>(n_chunks, true, c->stream);
+    c->dot_flags_n = n_chunks;
+}
+
+// two EXACT dots in one pass (streaming fold, two chains) into out[0], out[1]; false when
+// the folds are short (the caller takes the one-dot path)
+bool k_dot2_exact(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
+                  const double* b2, int64_t bs, double* out) {
+    const int64_t n_chunks = (n + bs - 1) / bs;
+    if (n <= 0 || n_chunks < kStreamMinChunks) return false;
+    ensure_dot_scratch(c, n_chunks);
+    k_dot_exact_stream(c, n, a1, b1, a2, b2, bs, c->dot_scratch, out, out + 1, nullptr, c->dot_flags);
+    return true;
+}
+
 void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_t bs, int32_t mode, double* d_out) {
     if (n <= 0) {
         KG_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), c->stream));
@@ -548,18 +574,7 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
         if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
         const int64_t n_chunks = (n + bs - 1) / bs;
         if (n_chunks >= kStreamMinChunks) {  // long fold: streamed beside the chunk pass
-            if (c->dot_scratch_n < 2 * n_chunks || c->dot_flags_n < n_chunks) {
-                KG_CUDA(cudaStreamSynchronize(c->stream));
-                dev_free(c->dot_scratch);
-                dev_free(c->dot_flags);
-                c->dot_scratch = nullptr;
-                c->dot_flags = nullptr;
-                c->dot_scratch_n = c->dot_flags_n = 0;
-                c->dot_scratch = dev_alloc<double>(2 * n_chunks, false, c->stream);
-                c->dot_scratch_n = 2 * n_chunks;
-                c->dot_flags = dev_alloc<int>(n_chunks, true, c->stream);
-                c->dot_flags_n = n_chunks;
-            }
+            ensure_dot_scratch(c, n_chunks);
             k_dot_exact_stream(c, n, x, y, nullptr, nullptr, bs, c->dot_scratch, d_out, nullptr, nullptr, c->dot_flags);
             return;
         }

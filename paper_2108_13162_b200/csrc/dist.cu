@@ -1243,6 +1243,11 @@ __global__ void __launch_bounds__(256) dot_fold_kernel(const double* __restrict_
 
 struct DistEngine : Engine {
     krysp_gpu_dist* d;
+    void dot_pair(const double* a1, const double* b1, const double* a2, const double* b2, double& d1,
+                  double& d2) override {
+        d1 = dot(a1, b1);
+        d2 = dot(a2, b2);
+    }
     // distributed dots: GCR keeps the reference's loop over Engine::dot
     bool gcr_orthogonalize(const double*, const double*, const std::vector<const double*>&,
                            const std::vector<const double*>&, const std::vector<double>&, double*, double*) override {

@@ -99,6 +99,20 @@ struct Engine {
         return v;
     }
     double norm2(const double* x) { return std::sqrt(dot(x, x)); }
+    // two independent dots of the reference's recurrence, one pass when the folds are long
+    // (EXACT: each value bit-identical to its own dot); partitioned engines: two dots
+    virtual void dot_pair(const double* a1, const double* b1, const double* a2, const double* b2, double& d1,
+                          double& d2) {
+        if (mode == KRYSP_MODE_EXACT && k_dot2_exact(c, n, a1, b1, a2, b2, pol.block_size, c->d_scalars)) {
+            KG_CUDA(cudaMemcpyAsync(c->h_pinned, c->d_scalars, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            stream_wait(c);
+            d1 = c->h_pinned[0];
+            d2 = c->h_pinned[1];
+            return;
+        }
+        d1 = dot(a1, b1);
+        d2 = dot(a2, b2);
+    }
     // GCR's classical Gram-Schmidt step (solvers.cpp:316-322) batched: the dots <w, Ap_i>
     // (w shared) in one pass, ||Ap_i||^2 from `dd` (the same vectors' dots computed when each
     // direction was used: identical values), then pn = r, apn = w, minus beta_i p_i / Ap_i in

@@ -772,6 +772,8 @@ void k_dot(krysp_gpu_ctx* c, int64_t n, const double* x, const double* y, int64_
 // EXACT dot(s) with the fold streaming beside the chunk pass (a2 == nullptr: one dot); scratch:
 // exact_dot_stream_scratch(n, bs) doubles, zeroed once (flags re-arm themselves)
 int64_t exact_dot_stream_scratch(int64_t n, int64_t bs);
+bool k_dot2_exact(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
+                  const double* b2, int64_t bs, double* out);
 // EXACT <w, v_k> for k < K (v_host: host array of device pointers) into out_dev (device), the
 // reference's order per dot; GCR's ordered direction update (pn = r - sum beta_i p_i, apn = w -
 // sum beta_i Ap_i, applied in i order per element)

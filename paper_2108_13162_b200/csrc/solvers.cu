@@ -193,12 +193,13 @@ void gcr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, Rep
         for (int64_t j = 0; j < m; ++j) {
             const double* p = dirs[(size_t)j];
             const double* ap = op_dirs[(size_t)j];
-            double d = e.dot(ap, ap);
+            double d, r_ap;  // <Ap, Ap> and <r, Ap> (independent): one pass
+            e.dot_pair(ap, ap, r, ap, d, r_ap);
             check_finite(d, "direction norm");
             if (vanishes(d)) fail(KRYSP_BREAKDOWN, "gcr: direction norm vanished");
             if ((int64_t)dd.size() <= j) dd.resize((size_t)j + 1);
             dd[(size_t)j] = d;
-            double alpha = e.dot(r, ap) / d;
+            double alpha = r_ap / d;
             check_finite(alpha, "alpha");
             e.daxpy(alpha, p, x);
             e.daxpy(-alpha, ap, r);
@@ -420,7 +421,14 @@ void tfqmr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, R
         double scale = (theta * theta * eta) / alpha;
         check_finite(scale, "direction scale");
         e.axpby(1.0, u, scale, d);
-        theta = e.norm2(w) / tau;
+        double w_r0 = 0.0;  // odd steps: <w, r_shadow> with ||w||^2 in one pass (w is final here)
+        if (even) {
+            theta = e.norm2(w) / tau;
+        } else {
+            double ww;
+            e.dot_pair(w, w, w, r0, ww, w_r0);
+            theta = std::sqrt(ww) / tau;
+        }
         double cc = 1.0 / std::sqrt(1.0 + theta * theta);
         tau = tau * theta * cc;
         eta = cc * cc * alpha;
@@ -436,7 +444,7 @@ void tfqmr(Engine& e, const krysp_solver_cfg& cfg, const double* b, double* x, R
             }
         }
         if (!even) {
-            double rho_new = e.dot(w, r0);
+            double rho_new = w_r0;
             if (vanishes(rho_new)) fail(KRYSP_BREAKDOWN, "tfqmr: rho vanished");
             double beta = rho_new / rho;
             check_finite(beta, "beta");
