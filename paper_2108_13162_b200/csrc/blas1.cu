@@ -650,10 +650,13 @@ static void stream_shape(krysp_gpu_ctx* c, int64_t n_chunks, int bs, int nd, int
     *smem = (int)std::max<int64_t>(2LL * nd * g * (t + 1) * 8, (int64_t)nd * kRing * 8);
 }
 
+static int64_t stream_region(int64_t n_chunks) { return 2 * n_chunks + (n_chunks + 1) / 2 + 16; }
+
 int64_t exact_dot_stream_scratch(int64_t n, int64_t bs) {
     const int64_t n_chunks = (n + bs - 1) / bs;
-    // streaming: partials of two dots + one int flag per block; short: k_dot_exact_into's layout
-    return std::max<int64_t>(2 * n_chunks + (n_chunks + 1) / 2 + 16, n_chunks + 32 * kExactWarps + 64);
+    // [two dots' partials | one int flag per block | the one-pass kernels' partials + counter]:
+    // disjoint, so the streaming, fused and one-pass dots of one session never share a word
+    return stream_region(n_chunks) + n_chunks + 32 * kExactWarps + 64;
 }
 
 void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const double* b1, const double* a2,
@@ -667,8 +670,9 @@ void k_dot_exact_stream(krysp_gpu_ctx* c, int64_t n, const double* a1, const dou
     if (bs < 32 || bs > 1024 || (bs & (bs - 1))) fail(KRYSP_ERROR, "block_size %lld not in {32..1024}", (long long)bs);
     const int64_t n_chunks = (n + bs - 1) / bs;
     if (n_chunks < kStreamMinChunks) {  // short fold: the one-pass kernels (C1: 977 chunks)
-        k_dot_exact_into(c, n, a1, b1, bs, scratch, out1, gate);
-        if (a2) k_dot_exact_into(c, n, a2, b2, bs, scratch, out2, gate);
+        double* one = scratch + stream_region(n_chunks);
+        k_dot_exact_into(c, n, a1, b1, bs, one, out1, gate);
+        if (a2) k_dot_exact_into(c, n, a2, b2, bs, one, out2, gate);
         return;
     }
     const int nd = a2 ? 2 : 1;

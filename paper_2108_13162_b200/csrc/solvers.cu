@@ -2519,6 +2519,14 @@ bool pcg_persistent_eligible(const krysp_gpu_mat* m) {
 // Device-resident FAST P-CG session: setup once, then iterations are enqueued as CUDA-graph
 // launches (chunks of kChunk iterations + single-iteration graphs for remainders).  Also
 // backs the krysp_gpu_solver_* C-ABI (bench / profiling / multi-step drivers).
+// smallest chunk count for the fused EXACT passes (SpMV + dots, update + rho); measured at
+// 1 M rows (977 chunks): C1 EXACT P-CG 13.5 k -> 14.7 k it/s, convdiff2d 1000^2 BiCGStab
+// 5.5 k -> 6.4 k; KRYSP_FUSED_MIN overrides
+int fused_min_chunks() {
+    static const int v = std::getenv("KRYSP_FUSED_MIN") ? std::atoi(std::getenv("KRYSP_FUSED_MIN")) : 32;
+    return v;
+}
+
 // the SpMV of an EXACT device-resident session with ND reference-order dots of its rows fused
 // (csr_tma_sigma_kernel); false when not applicable: not CSR, lanes per row > 1, rows too long
 // for the tile kernel, a short fold, or KRYSP_SIGMA=0
@@ -2531,7 +2539,7 @@ bool exact_spmv_dots(Engine& e, const double* x, double* y, const double* inv, c
     const krysp_gpu_mat* m = e.A;
     const int64_t n = e.n, bs = e.pol.block_size;
     const int64_t n_chunks = (n + bs - 1) / bs;
-    if (!on || !m || m->format != KRYSP_FMT_CSR || e.pol.workers_per_row != 1 || n_chunks < 4096 ||
+    if (!on || !m || m->format != KRYSP_FMT_CSR || e.pol.workers_per_row != 1 || n_chunks < fused_min_chunks() ||
         !csr_use_tile(m, 1))
         return false;
     krysp_gpu_ctx* c = e.c;
@@ -2825,7 +2833,7 @@ struct PcgSession {
         }();
         const int64_t bs = e.pol.block_size;
         const int64_t n_chunks = (n + bs - 1) / bs;
-        if (!on || n_chunks < 4096) return false;
+        if (!on || n_chunks < fused_min_chunks()) return false;
         krysp_gpu_ctx* c = e.c;
         static const int tw_cap = [] {
             const char* v = std::getenv("KRYSP_UR_TW");
