@@ -685,9 +685,7 @@ __global__ void ex_beta_kernel(int64_t n, const double* __restrict__ p, double* 
 }
 
 // sigma = <p, Ap> -> checks, alpha (solvers.cpp:160-166)
-__global__ void ex_sigma_kernel(CgState* st, const double* sigma_in) {
-    if (st->done) return;
-    const double sigma = *sigma_in;
+__device__ __forceinline__ void ex_sigma_apply(CgState* st, double sigma) {
     st->sigma = sigma;
     if (!isfinite(sigma)) {
         st->status = kStNonFiniteSigma;
@@ -703,6 +701,10 @@ __global__ void ex_sigma_kernel(CgState* st, const double* sigma_in) {
             st->done = 1;
         }
     }
+}
+__global__ void ex_sigma_kernel(CgState* st, const double* sigma_in) {
+    if (st->done) return;
+    ex_sigma_apply(st, *sigma_in);
 }
 
 // x += alpha p; r -= alpha Ap (two daxpy, solvers.cpp:167-168); z = D^-1 r (apply_precond :46-52)
@@ -720,6 +722,52 @@ __global__ void ex_update_kernel(int64_t n, double* __restrict__ x, double* __re
     }
 }
 
+// rho = <r, z> -> check, measure, history, trace, convergence; beta for the next iteration
+// (solvers.cpp:169-181, 152)
+__device__ __forceinline__ void ex_rho_apply(CgState* st, double rho_new, double* history, double* trace) {
+    const double rho = st->rho;
+    const long long it = st->iter;
+    if (trace) {
+        double* t = trace + 4 * it;
+        t[0] = rho;
+        t[1] = it == 0 ? 0.0 : st->beta;
+        t[2] = st->sigma;
+        t[3] = st->alpha;
+    }
+    if (!isfinite(rho_new)) {
+        st->status = kStNonFiniteRho;
+        st->done = 1;
+        return;
+    }
+    const double measure = rho_new / st->norm_r0;
+    history[it] = measure;
+    st->iter = it + 1;
+    st->rho_1 = rho;
+    st->rho = rho_new;
+    st->beta = rho_new / rho;
+    if (measure <= st->tol || it + 1 >= st->max_it) st->done = 1;
+}
+__global__ void ex_rho_kernel(CgState* st, const double* rho_in, double* history, double* trace) {
+    if (st->done) return;
+    ex_rho_apply(st, *rho_in, history, trace);
+}
+
+// what the folder block does with the folded dot(s) once the fold ends — the 1-thread scalar
+// kernel of the unfused path, run in place (one launch fewer per dot)
+struct FinNone {
+    __device__ __forceinline__ void operator()(double, double) const {}
+};
+struct FinSigma {
+    CgState* st;
+    __device__ __forceinline__ void operator()(double v, double) const { ex_sigma_apply(st, v); }
+};
+struct FinRho {
+    CgState* st;
+    double* hist;
+    double* trace;
+    __device__ __forceinline__ void operator()(double v, double) const { ex_rho_apply(st, v, hist, trace); }
+};
+
 // EXACT P-CG's SpMV with sigma = <p, Ap> fused (streaming fold): the policy's tile kernel for
 // one lane per row (csr_tma_kernel<1>: same TMA pipeline, same row sums) plus a ninth warp that
 // adds fl(p_r (Ap)_r) in row order into the reference's chunk sums (kernels.cpp:74-78) while
@@ -731,7 +779,7 @@ constexpr int kSgNT = kTileRows + 32;
 // ND dots of the row result v_r = (Ax)_r [* inv_r]: dot d multiplies v_r by a_d[r] (a_d NULL:
 // by v_r itself).  EXACT P-CG: ND = 1, a_0 = x (sigma = <p, Ap>); EXACT BiCGStab: ND = 1,
 // a_0 = r^ (<r^, v>) and ND = 2, a_0 = NULL, a_1 = x (<t, t>, <t, s>).
-template <bool kJacobi, int ND>
+template <bool kJacobi, int ND, class Fin>
 __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, const double* __restrict__ xp,
                                                               double* __restrict__ y,
                                                               const double* __restrict__ inv,
@@ -739,11 +787,13 @@ __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, cons
                                                               const double* __restrict__ a1, TmaTileLayout L, int bs,
                                                               int64_t n_chunks, int G, int T_per, int64_t n_units,
                                                               double* pa, double* pb, int* flags, double* out0,
-                                                              double* out1, const int* gate) {
+                                                              double* out1, const int* gate, Fin fin) {
     if (gate && *(volatile const int*)gate) return;
     extern __shared__ __align__(128) unsigned char smem_sg[];
     if (blockIdx.x == 0) {
         stream_fold<ND>(n_chunks, G, n_units, pa, pb, flags, out0, out1, reinterpret_cast<double*>(smem_sg + 128));
+        __syncthreads();  // the folded values (written by the folder lanes) are visible block-wide
+        if (threadIdx.x == 0) fin(*(volatile double*)out0, ND == 2 ? *(volatile double*)out1 : 0.0);
         return;
     }
     constexpr int TR = kTileRows;
@@ -884,19 +934,21 @@ __global__ void __launch_bounds__(kSgNT, 4) csr_tma_sigma_kernel(CsrView A, cons
 // chunk sums left to right (:80-83).  One pass instead of update + dot.
 constexpr int kUrE = 4;  // rows per thread per tile
 
-template <bool kJacobi>
+template <bool kJacobi, class Fin>
 __global__ void __launch_bounds__(256) ex_update_rho_kernel(int64_t n, double* __restrict__ x, double* __restrict__ r,
                                                             const double* __restrict__ p,
                                                             const double* __restrict__ ap,
                                                             const double* __restrict__ inv, double* __restrict__ z,
                                                             const CgState* st, int bs, int64_t n_chunks, int G, int tw,
                                                             int64_t ncb, double* partials, int* flags,
-                                                            double* rho_out) {
+                                                            double* rho_out, Fin fin) {
     if (*(volatile const int*)&st->done) return;
     extern __shared__ double sm_ur[];
     const int t = threadIdx.x;
     if (blockIdx.x == 0) {
         stream_fold<1>(n_chunks, G, ncb, partials, nullptr, flags, rho_out, nullptr, sm_ur);
+        __syncthreads();
+        if (t == 0) fin(*(volatile double*)rho_out, 0.0);
         return;
     }
     const double alpha = st->alpha, malpha = -alpha;
@@ -955,32 +1007,6 @@ __global__ void __launch_bounds__(256) ex_update_rho_kernel(int64_t n, double* _
     if (t == 0) st_release_i32(flags + b, 1);
 }
 
-// rho = <r, z> -> check, measure, history, trace, convergence; beta for the next iteration
-// (solvers.cpp:169-181, 152)
-__global__ void ex_rho_kernel(CgState* st, const double* rho_in, double* history, double* trace) {
-    if (st->done) return;
-    const double rho_new = *rho_in, rho = st->rho;
-    const long long it = st->iter;
-    if (trace) {
-        double* t = trace + 4 * it;
-        t[0] = rho;
-        t[1] = it == 0 ? 0.0 : st->beta;
-        t[2] = st->sigma;
-        t[3] = st->alpha;
-    }
-    if (!isfinite(rho_new)) {
-        st->status = kStNonFiniteRho;
-        st->done = 1;
-        return;
-    }
-    const double measure = rho_new / st->norm_r0;
-    history[it] = measure;
-    st->iter = it + 1;
-    st->rho_1 = rho;
-    st->rho = rho_new;
-    st->beta = rho_new / rho;
-    if (measure <= st->tol || it + 1 >= st->max_it) st->done = 1;
-}
 
 // sense-free grid barrier: arrival counter reset by the last arriver, which then bumps the
 // generation the others spin on (counter reset before the bump: no early re-arrival race)
@@ -2530,8 +2556,9 @@ int fused_min_chunks() {
 // the SpMV of an EXACT device-resident session with ND reference-order dots of its rows fused
 // (csr_tma_sigma_kernel); false when not applicable: not CSR, lanes per row > 1, rows too long
 // for the tile kernel, a short fold, or KRYSP_SIGMA=0
+template <class Fin = FinNone>
 bool exact_spmv_dots(Engine& e, const double* x, double* y, const double* inv, const double* a0, const double* a1,
-                     int nd, double* scratch, double* out0, double* out1, const int* gate) {
+                     int nd, double* scratch, double* out0, double* out1, const int* gate, Fin fin = Fin{}) {
     static const bool on = [] {
         const char* v = std::getenv("KRYSP_SIGMA");
         return !(v && v[0] == '0');
@@ -2551,8 +2578,8 @@ bool exact_spmv_dots(Engine& e, const double* x, double* y, const double* inv, c
     cap = (cap + 3) & ~3;
     const TmaTileLayout L{cap, 0, kTileRows};
     const int smem = std::max(64 + 2 * L.stage_bytes() + 2 * nd * kTileRows * 8, 128 + nd * kRing * 8);
-    auto k = inv ? (nd == 2 ? csr_tma_sigma_kernel<true, 2> : csr_tma_sigma_kernel<true, 1>)
-                 : (nd == 2 ? csr_tma_sigma_kernel<false, 2> : csr_tma_sigma_kernel<false, 1>);
+    auto k = inv ? (nd == 2 ? csr_tma_sigma_kernel<true, 2, Fin> : csr_tma_sigma_kernel<true, 1, Fin>)
+                 : (nd == 2 ? csr_tma_sigma_kernel<false, 2, Fin> : csr_tma_sigma_kernel<false, 1, Fin>);
     if (smem > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     // persistent compute CTAs + the folder must all be resident at once: a CTA left waiting
     // for a slot would run its whole share after the others, with the fold waiting on it
@@ -2560,7 +2587,8 @@ bool exact_spmv_dots(Engine& e, const double* x, double* y, const double* inv, c
     const int64_t g = std::max<int64_t>(1, std::min<int64_t>(n_units, slots - 1));
     int* flags = reinterpret_cast<int*>(scratch + 2 * n_chunks);
     k<<<(unsigned)(g + 1), kSgNT, smem, c->stream>>>(m->csr(), x, y, inv, a0, a1, L, (int)bs, n_chunks, G, T_per,
-                                                    n_units, scratch, scratch + n_chunks, flags, out0, out1, gate);
+                                                    n_units, scratch, scratch + n_chunks, flags, out0, out1, gate,
+                                                    fin);
     KG_LAUNCH(c);
     return true;
 }
@@ -2820,8 +2848,9 @@ struct PcgSession {
 
     // Ap and sigma = <p, Ap> in one pass (csr_tma_sigma_kernel); false unless the policy's
     // SpMV is the one-lane-per-row tile kernel and the fold is long (KRYSP_SIGMA=0: off)
-    bool exact_spmv_sigma(const double* pz, double* y) {
-        return exact_spmv_dots(e, pz, y, nullptr, pz, nullptr, 1, ex_partials, ex_scal, nullptr, &st->done);
+    bool exact_spmv_sigma(const double* pz, double* y) {  // sigma's checks and alpha run in the folder
+        return exact_spmv_dots(e, pz, y, nullptr, pz, nullptr, 1, ex_partials, ex_scal, nullptr, &st->done,
+                               FinSigma{st});
     }
 
     // update + rho in one pass with the streaming fold (ex_update_rho_kernel); false when the
@@ -2847,9 +2876,10 @@ struct PcgSession {
         double* partials = ex_partials;
         int* flags = reinterpret_cast<int*>((double*)ex_partials + 2 * n_chunks);
         const double* inv = e.jacobi ? (const double*)e.inv : nullptr;
-        auto k = e.jacobi ? ex_update_rho_kernel<true> : ex_update_rho_kernel<false>;
+        auto k = e.jacobi ? ex_update_rho_kernel<true, FinRho> : ex_update_rho_kernel<false, FinRho>;
         k<<<(unsigned)(ncb + 1), 256, smem, c->stream>>>(n, x, r, pz, ap, inv, z, st, (int)bs, n_chunks, G, tw,
-                                                         ncb, partials, flags, (double*)ex_scal + 1);
+                                                         ncb, partials, flags, (double*)ex_scal + 1,
+                                                         FinRho{st, hist, d_trace});
         KG_LAUNCH(c);
         return true;
     }
@@ -2880,9 +2910,9 @@ struct PcgSession {
             if (!exact_spmv_sigma(zb, ap)) {
                 spmv_exact_gated(zb, ap);                                    // Ap with p = zb
                 exact_dot(zb, ap, ex_scal);
+                ex_sigma_kernel<<<1, 1, 0, c->stream>>>(st, ex_scal);
+                KG_LAUNCH(c);
             }
-            ex_sigma_kernel<<<1, 1, 0, c->stream>>>(st, ex_scal);
-            KG_LAUNCH(c);
             if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
             if (!exact_update_rho(zb, pb)) {
                 if (e.jacobi)
@@ -2891,9 +2921,9 @@ struct PcgSession {
                     ex_update_kernel<false><<<g, kFusedNT, 0, c->stream>>>(n, x, r, zb, ap, nullptr, pb, st);
                 KG_LAUNCH(c);
                 exact_dot(r, pb, (double*)ex_scal + 1);                      // rho = <r, z>
+                ex_rho_kernel<<<1, 1, 0, c->stream>>>(st, (double*)ex_scal + 1, hist, d_trace);
+                KG_LAUNCH(c);
             }
-            ex_rho_kernel<<<1, 1, 0, c->stream>>>(st, (double*)ex_scal + 1, hist, d_trace);
-            KG_LAUNCH(c);
             if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
             if (events) KG_CUDA(cudaEventRecordWithFlags(ev[3], c->stream, cudaEventRecordExternal));
             kernels_per_iteration = (int)(c->launches - before);
