@@ -3378,6 +3378,16 @@ __global__ void ex_scale_kernel(int64_t n, double* __restrict__ y, const double*
         y[i] = __dmul_rn(y[i], inv[i]);
 }
 
+// the same steps run by the fused SpMV's folder block (csr_tma_sigma_kernel's Fin)
+struct FinBsAlpha {
+    BiState* st;
+    __device__ __forceinline__ void operator()(double denom, double) const { FinAlpha()(st, denom, 0.0); }
+};
+struct FinBsOmega {
+    BiState* st;
+    __device__ __forceinline__ void operator()(double tt, double ts) const { FinOmega()(st, tt, ts); }
+};
+
 __global__ void ex_bs_alpha_kernel(BiState* st, const double* denom) {
     if (st->done) return;
     FinAlpha()(st, *denom, 0.0);
@@ -3546,23 +3556,24 @@ struct BicgstabSession {
             auto dot2 = [&](const double* a1, const double* b1, const double* a2, const double* b2, double* out) {
                 k_dot_exact_stream(c, n, a1, b1, a2, b2, e.pol.block_size, ex_partials, out, out + 1, gate);
             };
-            if (!exact_spmv_dots(e, p, v, dinv, rh, nullptr, 1, ex_partials, sc, nullptr, gate)) {
+            // fused: the folder block runs alpha's step (FinBsAlpha) after its fold
+            if (!exact_spmv_dots(e, p, v, dinv, rh, nullptr, 1, ex_partials, sc, nullptr, gate, FinBsAlpha{st})) {
                 op_exact(p, v);                              // v = op(p)
                 dot(rh, v, sc);                              // <r^, v>
+                ex_bs_alpha_kernel<<<1, 1, 0, c->stream>>>(st, sc);
+                KG_LAUNCH(c);
             }
-            ex_bs_alpha_kernel<<<1, 1, 0, c->stream>>>(st, sc);
-            KG_LAUNCH(c);
             ex_bs_s_kernel<<<g, kBiNT, 0, c->stream>>>(n, s, r, v, st);
             KG_LAUNCH(c);
             dot(s, s, sc + 1);                               // ||s||^2
             ex_bs_half_kernel<<<1, 1, 0, c->stream>>>(st, sc + 1, hist);
             KG_LAUNCH(c);
-            if (!exact_spmv_dots(e, s, t, dinv, nullptr, s, 2, ex_partials, sc + 2, sc + 3, gate)) {
+            if (!exact_spmv_dots(e, s, t, dinv, nullptr, s, 2, ex_partials, sc + 2, sc + 3, gate, FinBsOmega{st})) {
                 op_exact(s, t);                              // t = op(s)
                 dot2(t, t, t, s, sc + 2);                    // <t,t>, <t,s>
+                ex_bs_omega_kernel<<<1, 1, 0, c->stream>>>(st, sc + 2);
+                KG_LAUNCH(c);
             }
-            ex_bs_omega_kernel<<<1, 1, 0, c->stream>>>(st, sc + 2);
-            KG_LAUNCH(c);
             ex_bs_update_kernel<<<g, kBiNT, 0, c->stream>>>(n, x, r, p, s, t, st, ex_counter);
             KG_LAUNCH(c);
             dot2(r, r, rh, r, sc + 4);                       // <r,r>, <r^,r>
