@@ -283,7 +283,7 @@ int64_t slice_bytes() {
     return v;
 }
 
-void build_slices(krysp_gpu_mat* m) {
+void build_slices(krysp_gpu_mat* m, RowsView src) {
     krysp_gpu_ctx* c = m->ctx;
     cudaStream_t s = c->stream;
     const int64_t n = m->n_rows, cols_per = std::max<int64_t>(slice_bytes() / 8, 1024);
@@ -293,7 +293,7 @@ void build_slices(krysp_gpu_mat* m) {
     S->s.resize((size_t)K);
     DevBuf<int32_t> cnt((int64_t)K * n + 1, false);
     const unsigned g = grid_for(n, 256, (int64_t)c->sm_count * 16);
-    slice_count_kernel<<<g, 256, 0, s>>>(m->rp, m->ci, n, S->slice_cols, K, cnt);
+    slice_count_kernel<<<g, 256, 0, s>>>(src.rp, src.col, n, S->slice_cols, K, cnt);
     KG_LAUNCH(c);
     std::vector<int32_t*> rps((size_t)K), cis((size_t)K);
     std::vector<double*> cvs((size_t)K);
@@ -319,7 +319,7 @@ void build_slices(krysp_gpu_mat* m) {
     KG_CUDA(cudaMemcpyAsync(d_rps.p, rps.data(), 8 * (size_t)K, cudaMemcpyHostToDevice, s));
     KG_CUDA(cudaMemcpyAsync(d_cis.p, cis.data(), 8 * (size_t)K, cudaMemcpyHostToDevice, s));
     KG_CUDA(cudaMemcpyAsync(d_cvs.p, cvs.data(), 8 * (size_t)K, cudaMemcpyHostToDevice, s));
-    slice_copy_kernel<<<g, 256, 0, s>>>(m->rp, m->ci, m->cv, n, K, d_rps, d_cis, d_cvs);
+    slice_copy_kernel<<<g, 256, 0, s>>>(src.rp, src.col, src.val, n, K, d_rps, d_cis, d_cvs);
     KG_LAUNCH(c);
     for (auto& q : S->s) build_plan(c, q.rp, n, q.plan);  // synchronises the stream
     m->slices = S;
@@ -382,6 +382,13 @@ int32_t* ensure_coo_rp(const krysp_gpu_mat* cm) {
 // measured (C4 fem27 320^3, w = 26, one overflow entry per row): finishing the overflow in
 // the ELL kernel beats the separate load-balanced COO pass; rows with longer overflow
 // segments (C5's power-law tails) keep the load-balanced kernel
+// a HYB whose overflow rows are long (power-law): the whole-matrix sliced path applies
+bool hyb_irregular(const krysp_gpu_mat* m) {
+    if (m->format != KRYSP_FMT_HYB || m->coo_nnz == 0) return false;
+    ensure_coo_rp(m);
+    return m->coo_max_row > 4;
+}
+
 bool hyb_tail_fusable(const krysp_gpu_mat* m) {
     if (m->format != KRYSP_FMT_HYB || m->coo_nnz == 0) return false;
     ensure_coo_rp(m);
@@ -407,7 +414,25 @@ int64_t csr_column_slices(const krysp_gpu_mat* cm) {
     if (!m->slices_checked) {
         m->slices_checked = true;
         const int64_t sb = slice_bytes();
-        if (m->format == KRYSP_FMT_CSR && sb > 0 && 8 * m->n_cols > sb && m->nnz > 0) build_slices(m);
+        if (sb > 0 && 8 * m->n_cols > sb && m->nnz > 0) {
+            if (m->format == KRYSP_FMT_CSR) build_slices(m, RowsView{m->rp, m->ci, m->cv});
+            else if (m->format == KRYSP_FMT_COO)  // canonical COO: its row pointer makes it a CSR view
+                build_slices(m, RowsView{ensure_coo_rp(m), m->co_c, m->co_v});
+            else if (m->format == KRYSP_FMT_HYB && hyb_irregular(m)) {
+                // power-law HYB (long overflow rows): FAST runs it as one sliced CSR of all its
+                // entries (any row order is FAST's; the EXACT kernels keep the ELL + COO order)
+                krysp_gpu_mat* tmp = convert_to_csr(m);
+                try {
+                    build_slices(m, RowsView{tmp->rp, tmp->ci, tmp->cv});
+                } catch (...) {
+                    mat_free_arrays(tmp);
+                    delete tmp;
+                    throw;
+                }
+                mat_free_arrays(tmp);
+                delete tmp;
+            }
+        }
     }
     return m->slices ? (int64_t)m->slices->s.size() : 1;
 }
@@ -426,7 +451,9 @@ void launch_adaptive(const krysp_gpu_mat* cm, bool coo_part, const double* x, do
         A = {m->rp, m->ci, m->cv};
         P = &m->ad_csr;
     }
-    if (!coo_part && csr_column_slices(m) > 1) {  // slice by slice, y accumulating
+    // slice by slice, y accumulating (CSR, the COO format, a power-law HYB as a whole: coo_part
+    // false); a HYB's overflow part alone is never sliced
+    if ((m->format != KRYSP_FMT_HYB || !coo_part) && csr_column_slices(m) > 1) {
         bool acc = accumulate;
         for (auto& q : m->slices->s) {
             run_plan(c, RowsView{q.rp, q.ci, q.cv}, &q.plan, x, y, acc, s, gate);

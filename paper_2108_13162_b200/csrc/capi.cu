@@ -525,7 +525,10 @@ krysp_status krysp_gpu_mat_column_slices(const krysp_gpu_mat* m, int64_t* n_slic
         need(m, "mat");
         need(n_slices, "n_slices");
         set_dev(m->ctx);
-        *n_slices = (m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) ? csr_column_slices(m) : 1;
+        *n_slices = ((m->format == KRYSP_FMT_CSR && csr_is_irregular(m)) || m->format == KRYSP_FMT_COO ||
+                     hyb_irregular(m))
+                        ? csr_column_slices(m)
+                        : 1;
     });
 }
 

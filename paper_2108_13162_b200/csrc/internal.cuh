@@ -736,6 +736,7 @@ int32_t* ensure_coo_rp(const krysp_gpu_mat* m);
 bool hyb_tail_fusable(const krysp_gpu_mat* m);
 // number of column slices the FAST irregular CSR SpMV of m runs (1: unsliced); builds them
 int64_t csr_column_slices(const krysp_gpu_mat* m);
+bool hyb_irregular(const krysp_gpu_mat* m);
 
 // spmv.cu
 enum SpmvVariant : int32_t {

@@ -138,6 +138,10 @@ int32_t spmv_launch(const krysp_gpu_mat* m, const double* x, double* y, const kr
             launch_adaptive(m, false, x, y, false, s, gate);
             return kVarCsrAdaptive;
         }
+        if (hyb_irregular(m) && csr_column_slices(m) > 1) {  // power-law HYB beyond L2: sliced as a whole
+            launch_adaptive(m, false, x, y, false, s, gate);
+            return kVarHybAdaptive;
+        }
         if (hyb_tail_fusable(m)) {
             launch_ell_tail(m, x, EpiStoreGated<FlagGate>{y, FlagGate{gate}}, pol.block_size, s);
             return kVarHybTail;

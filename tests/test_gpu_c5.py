@@ -50,6 +50,18 @@ for alpha, n in ((2.0, 300_000), (1.5, 200_000)):
     # the conversions and EXACT rows never see the slices
     H = A.convert("hyb")
     assert np.array_equal(kg.spmv(H, x, kg.ExecPolicy(256, 1), mode="exact"), want)
+    # a power-law HYB (long overflow rows) runs FAST as one sliced matrix
+    assert kg.column_slices(H) == k, (kg.column_slices(H), k)
+    yh = kg.spmv(H, x, kg.ExecPolicy(0, 0), mode="fast")
+    assert float(np.max(np.abs(yh - want) / (1 + np.abs(want)))) <= 1e-13
+    assert np.array_equal(yh, kg.spmv(H, x, kg.ExecPolicy(0, 0), mode="fast"))
+    # the COO format is sliced through its row pointer the same way
+    C = A.convert("coo")
+    assert kg.column_slices(C) == k, (kg.column_slices(C), k)
+    yc = kg.spmv(C, x, kg.ExecPolicy(0, 0), mode="fast")
+    wc = kg.spmv(C, x, kg.ExecPolicy(256, 1), mode="exact")
+    assert float(np.max(np.abs(yc - wc) / (1 + np.abs(wc)))) <= 1e-13
+    assert np.array_equal(yc, kg.spmv(C, x, kg.ExecPolicy(0, 0), mode="fast"))
 print("slices ok")
 """
 
@@ -66,6 +78,7 @@ def test_slices_off_for_regular_and_small(ctx):
     assert kg.column_slices(ctx.generate("lap3d7", 60)) == 1      # regular rows: the TMA tile kernel
     m = kg.generate_csr("powerlaw", 100_000, alpha=2.0, seed=3)     # x = 0.8 MB: one slice
     assert kg.column_slices(ctx.upload(m)) == 1
+    assert kg.column_slices(ctx.upload(m).convert("coo")) == 1
 
 
 @pytest.mark.parametrize("alpha", [1.5, 2.0])
