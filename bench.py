@@ -144,15 +144,19 @@ def spmv_bytes(n_rows, n_cols, nnz):
     return 12 * nnz + 4 * (n_rows + 1) + 8 * n_cols + 8 * n_rows
 
 
-PCG_V = 10  # vector streams per P-CG iteration as implemented (below)
+# vector streams per P-CG iteration as implemented (below): 9.5 with the paired x updates
+# (KRYSP_XPAIR, default on), 10 without
+PCG_V = 10.0 if os.environ.get("KRYSP_XPAIR", "1").startswith("0") else 9.5
 
 
 def iter_bytes(n_rows, n_cols, nnz, v=PCG_V):
     """P-CG: k_spmv = 1 plus V vector streams.  SURVEY §8(d) counts V = 11 (update: x, p, r, Ap,
     D^-1 -> x, r; direction: r, D^-1, p -> p); the FAST kernels defer x += alpha p into the
     direction pass, which reads p anyway (update: r, Ap, D^-1 -> r; direction: x, p, r, D^-1 ->
-    x, p), so the algorithmic minimum of this schedule is V = 10."""
-    return spmv_bytes(n_rows, n_cols, nnz) + 8 * n_rows * v
+    x, p), so this schedule moves V = 10; pairing the x updates of two iterations (two p
+    buffers: the even direction pass leaves x alone, the odd one applies both terms) takes it to
+    V = 4 (update) + (4 + 7) / 2 (direction, even / odd) = 9.5."""
+    return spmv_bytes(n_rows, n_cols, nnz) + int(8 * n_rows * v)
 
 
 def ncu_traffic():
@@ -493,7 +497,7 @@ def run_ours_dist(args, dist):
     D.close()
     nnz_total = 7 * N - 6 * args.n ** 2
     bw_peak, peak_kind = peaks()
-    B_iter_gpu = iter_bytes(N, N, nnz_total) / dist.world
+    B_iter_gpu = iter_bytes(N, N, nnz_total, 10) / dist.world  # the partitioned kernels: V = 10
     t_it = t_max / args.steps
     line = {"metric": METRIC, "value": args.steps / t_max, "unit": "iterations/s", "n_gpus": dist.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_it, "higher_is_better": True,

@@ -524,6 +524,7 @@ struct CgState {
     long long iter, max_it;
     int done, status;
     int x_pending;  // the last iteration's x += alpha p still to apply (deferred update)
+    double alpha_prev;  // paired x updates (cg_direction_pair_kernel): the even iteration's alpha
 };
 
 enum : int { kStRunning = 0, kStBreakdownSigma = 1, kStNonFiniteSigma = 2, kStNonFiniteAlpha = 3, kStNonFiniteRho = 4 };
@@ -665,6 +666,60 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
                 x[i] = __dadd_rn(__dmul_rn(alpha, pv[q]), xv[q]);
                 const double zi = kJacobi ? __dmul_rn(rv[q], iv[q]) : rv[q];
                 p[i] = __dadd_rn(__dmul_rn(beta, pv[q]), zi);
+            }
+        }
+    }
+}
+
+// FAST P-CG with the x updates of two iterations paired (KRYSP_XPAIR, default on for the
+// 3-kernel iteration): p alternates between two buffers, so an even iteration's direction pass
+// leaves x alone (reads r, D^-1, p_k; writes p_{k+1}) and keeps p_k, and the odd one applies
+// x = (x + alpha_{k-1} p_{k-1}) + alpha_k p_k while forming p_{k+2} over p_{k-1} — 5.5 vector
+// streams per iteration instead of 6.  The iteration that ends the solve flushes what is
+// pending (x_pending: one term after an even iteration, both after an odd one).
+template <bool kJacobi, bool kOdd>
+__global__ void __launch_bounds__(kFusedNT) cg_direction_pair_kernel(int64_t n, const double* __restrict__ pc,
+                                                                      double* __restrict__ po,
+                                                                      const double* __restrict__ r,
+                                                                      const double* __restrict__ inv,
+                                                                      double* __restrict__ x, CgState* st,
+                                                                      unsigned* counter) {
+    pdl_wait();
+    const int done = *(volatile const int*)&st->done;
+    if (done && !*(volatile const int*)&st->x_pending) return;
+    const double alpha = st->alpha, beta = st->beta, aprev = kOdd ? st->alpha_prev : 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kFusedNT;
+    if (done) {  // flush the pending x terms of the iteration that ended the solve
+        for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += stride) {
+            double xi = x[i];
+            if (kOdd) xi = __dadd_rn(__dmul_rn(aprev, po[i]), xi);
+            x[i] = __dadd_rn(__dmul_rn(alpha, pc[i]), xi);
+        }
+        __syncthreads();
+        if (last_block(counter) && threadIdx.x == 0) {
+            *counter = 0;
+            st->x_pending = 0;
+        }
+        return;
+    }
+    if (!kOdd && blockIdx.x == 0 && threadIdx.x == 0) st->alpha_prev = alpha;  // read by the odd pass only
+    for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double pv[kVu], ov[kVu], xv[kVu], rv[kVu], iv[kVu];  // loads of kVu rows before any store
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                pv[q] = pc[i], rv[q] = r[i], iv[q] = kJacobi ? inv[i] : 1.0;
+                if (kOdd) ov[q] = po[i], xv[q] = x[i];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kVu; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i < n) {
+                if (kOdd) x[i] = __dadd_rn(__dmul_rn(alpha, pv[q]), __dadd_rn(__dmul_rn(aprev, ov[q]), xv[q]));
+                const double zi = kJacobi ? __dmul_rn(rv[q], iv[q]) : rv[q];
+                po[i] = __dadd_rn(__dmul_rn(beta, pv[q]), zi);
             }
         }
     }
@@ -2608,6 +2663,7 @@ struct PcgSession {
     // merged: 2 kernels per iteration (direction pass inside the SpMV, XDir / EpiCgDir);
     // graphs per starting parity of the direction buffers
     bool merged = false;
+    bool xpair = false;  // 3-kernel FAST iteration with paired x updates (two p buffers)
     bool exact = false;  // EXACT mode: the reference's P-CG replayed on the device (ex_* kernels)
     DVec ex_partials, ex_scal;  // exact dots: chunk partials, and the two dot results
     int next_parity = 0;
@@ -2679,9 +2735,11 @@ struct PcgSession {
             if (persistent) setup_persistent();
             else {
                 if (!exact) setup_coop();
+                xpair = !exact && !merged && !coop && xpair_enabled();
+                if (xpair) p1 = DVec(n, c->stream);
                 exec_chunk = capture(kChunk, false, 0);
                 exec_one = capture(1, false, 0);
-                if (merged || exact) {
+                if (merged || exact || xpair) {
                     exec_chunk1 = capture(kChunk, false, 1);
                     exec_one1 = capture(1, false, 1);
                 }
@@ -2745,6 +2803,14 @@ struct PcgSession {
                 return;
             }
         }
+    }
+
+    static bool xpair_enabled() {
+        static const bool v = [] {
+            const char* s = std::getenv("KRYSP_XPAIR");
+            return !(s && s[0] == '0');
+        }();
+        return v;
     }
 
     // KRYSP_MERGED=1: the 2-kernel iteration (direction pass merged into the SpMV).  Measured
@@ -2937,8 +3003,9 @@ struct PcgSession {
                 spmv_fused_xs(e, XDir<false>{r, nullptr, p_old, st, 0.0},
                            ap, EpiCgDir<false>{ap, p_new, p_old, r, nullptr, x, part_a, cnt_a, st, 0.0, 0.0, 0.0, false});
         } else {
-            EpiCgSigma epi{ap, p, part_a, cnt_a, st, 0.0};
-            spmv_fused(e, (const double*)p, ap, epi);
+            double* pcur = xpair ? p_old : (double*)p;  // xpair: p_k alternates between p and p1
+            EpiCgSigma epi{ap, pcur, part_a, cnt_a, st, 0.0};
+            spmv_fused(e, (const double*)pcur, ap, epi);
         }
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[1], c->stream, cudaEventRecordExternal));
         if (coop) {  // update + direction in one cooperative grid
@@ -2976,7 +3043,14 @@ struct PcgSession {
                            st, part_b, cnt_b, hist, d_trace));
         KG_LAUNCH(c);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
-        if (!merged) {
+        if (!merged && xpair) {
+            unsigned* cnt_c = c->d_counters + 5;
+            auto k = parity ? (e.jacobi ? cg_direction_pair_kernel<true, true> : cg_direction_pair_kernel<false, true>)
+                            : (e.jacobi ? cg_direction_pair_kernel<true, false> : cg_direction_pair_kernel<false, false>);
+            KG_CUDA(launch_pdl(k, g_vec, kFusedNT, 0, c->stream, n, (const double*)p_old, p_new, (const double*)r, inv,
+                               (double*)x, st, cnt_c));
+            KG_LAUNCH(c);
+        } else if (!merged) {
             unsigned* cnt_c = c->d_counters + 5;
             KG_CUDA(launch_pdl(e.jacobi ? cg_direction_kernel<true> : cg_direction_kernel<false>, g_vec, kFusedNT, 0,
                                c->stream, n, (double*)p, (const double*)r, inv, (double*)x, st, cnt_c));
@@ -3008,7 +3082,7 @@ struct PcgSession {
     void enqueue(int64_t iters) {
         krysp_gpu_ctx* c = e.c;
         if (persistent) return launch_persistent(iters);
-        const bool two = merged || exact;  // iterations alternate two buffers
+        const bool two = merged || exact || xpair;  // iterations alternate two buffers
         for (int64_t i = 0; i + kChunk <= iters; i += kChunk)
             KG_CUDA(cudaGraphLaunch(two && next_parity ? exec_chunk1 : exec_chunk, c->stream));
         for (int64_t i = 0; i < iters % kChunk; ++i) {
@@ -3059,7 +3133,7 @@ struct PcgSession {
         krysp_gpu_ctx* c = e.c;
         if (persistent) fail(KRYSP_ERROR, "per-kernel profile: the persistent P-CG grid is one kernel");
         if (!exec_prof) exec_prof = capture(1, true, 0);  // event-node graphs, built on first use
-        const bool two = merged || exact;
+        const bool two = merged || exact || xpair;
         if (two && !exec_prof1) exec_prof1 = capture(1, true, 1);
         out[0] = out[1] = out[2] = 0.0;
         for (int64_t i = 0; i < iters; ++i) {
