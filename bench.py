@@ -144,18 +144,19 @@ def spmv_bytes(n_rows, n_cols, nnz):
     return 12 * nnz + 4 * (n_rows + 1) + 8 * n_cols + 8 * n_rows
 
 
-# vector streams per P-CG iteration as implemented (below): 9.5 with the paired x updates
-# (KRYSP_XPAIR, default on), 10 without
-PCG_V = 10.0 if os.environ.get("KRYSP_XPAIR", "1").startswith("0") else 9.5
+# vector streams per P-CG iteration as implemented (below): 9 + 1/G with the x updates of G
+# iterations grouped (KRYSP_XGROUP, default 4; KRYSP_XPAIR=0 -> G = 1, V = 10)
+_XG = 1 if os.environ.get("KRYSP_XPAIR", "1").startswith("0") else int(os.environ.get("KRYSP_XGROUP", "4"))
+PCG_V = 9.0 + 1.0 / (_XG if _XG in (1, 2, 4, 8) else 4)
 
 
 def iter_bytes(n_rows, n_cols, nnz, v=PCG_V):
     """P-CG: k_spmv = 1 plus V vector streams.  SURVEY §8(d) counts V = 11 (update: x, p, r, Ap,
     D^-1 -> x, r; direction: r, D^-1, p -> p); the FAST kernels defer x += alpha p into the
     direction pass, which reads p anyway (update: r, Ap, D^-1 -> r; direction: x, p, r, D^-1 ->
-    x, p), so this schedule moves V = 10; pairing the x updates of two iterations (two p
-    buffers: the even direction pass leaves x alone, the odd one applies both terms) takes it to
-    V = 4 (update) + (4 + 7) / 2 (direction, even / odd) = 9.5."""
+    x, p), so this schedule moves V = 10; grouping the x updates of G iterations (G p buffers:
+    the first G - 1 direction passes leave x alone, 4 streams; the last applies all G terms,
+    G + 5 streams) takes it to V = 4 + (4 (G - 1) + G + 5) / G = 9 + 1/G."""
     return spmv_bytes(n_rows, n_cols, nnz) + int(8 * n_rows * v)
 
 

@@ -524,7 +524,7 @@ struct CgState {
     long long iter, max_it;
     int done, status;
     int x_pending;  // the last iteration's x += alpha p still to apply (deferred update)
-    double alpha_prev;  // paired x updates (cg_direction_pair_kernel): the even iteration's alpha
+    double ahist[8];  // grouped x updates (cg_direction_group_kernel): the group's earlier alphas
 };
 
 enum : int { kStRunning = 0, kStBreakdownSigma = 1, kStNonFiniteSigma = 2, kStNonFiniteAlpha = 3, kStNonFiniteRho = 4 };
@@ -671,28 +671,39 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
     }
 }
 
-// FAST P-CG with the x updates of two iterations paired (KRYSP_XPAIR, default on for the
-// 3-kernel iteration): p alternates between two buffers, so an even iteration's direction pass
-// leaves x alone (reads r, D^-1, p_k; writes p_{k+1}) and keeps p_k, and the odd one applies
-// x = (x + alpha_{k-1} p_{k-1}) + alpha_k p_k while forming p_{k+2} over p_{k-1} — 5.5 vector
-// streams per iteration instead of 6.  The iteration that ends the solve flushes what is
-// pending (x_pending: one term after an even iteration, both after an odd one).
-template <bool kJacobi, bool kOdd>
-__global__ void __launch_bounds__(kFusedNT) cg_direction_pair_kernel(int64_t n, const double* __restrict__ pc,
-                                                                      double* __restrict__ po,
-                                                                      const double* __restrict__ r,
-                                                                      const double* __restrict__ inv,
-                                                                      double* __restrict__ x, CgState* st,
-                                                                      unsigned* counter) {
+// FAST P-CG with the x updates of G consecutive iterations grouped (KRYSP_XGROUP, default 4;
+// 1 = every iteration): p cycles through G buffers, so a direction pass at phase q < G - 1
+// leaves x alone (reads r, D^-1, p_k; writes p_{k+1}) and keeps p_k, and the last phase applies
+// x = (((x + a_0 P_0) + a_1 P_1) + ...) + alpha_k p_k while forming the next p over P_0:
+// V = 9 + 1/G vector streams per iteration instead of 10.  The iteration that ends the solve
+// flushes the group's pending terms (x_pending).
+constexpr int kXgMax = 8;
+struct XBufs {
+    double* b[kXgMax];
+};
+
+template <bool kJacobi, int G>
+__global__ void __launch_bounds__(kFusedNT) cg_direction_group_kernel(int64_t n, XBufs P, int q,
+                                                                       const double* __restrict__ r,
+                                                                       const double* __restrict__ inv,
+                                                                       double* __restrict__ x, CgState* st,
+                                                                       unsigned* counter) {
     pdl_wait();
     const int done = *(volatile const int*)&st->done;
     if (done && !*(volatile const int*)&st->x_pending) return;
-    const double alpha = st->alpha, beta = st->beta, aprev = kOdd ? st->alpha_prev : 0.0;
+    const double alpha = st->alpha, beta = st->beta;
+    double ah[G > 1 ? G - 1 : 1];
+#pragma unroll
+    for (int j = 0; j < G - 1; ++j) ah[j] = st->ahist[j];
+    const double* __restrict__ pc = P.b[q];
+    double* __restrict__ pn = P.b[q + 1 < G ? q + 1 : 0];
     const int64_t stride = (int64_t)gridDim.x * kFusedNT;
-    if (done) {  // flush the pending x terms of the iteration that ended the solve
+    if (done) {  // flush the pending x terms of the group, in order
         for (int64_t i = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i < n; i += stride) {
             double xi = x[i];
-            if (kOdd) xi = __dadd_rn(__dmul_rn(aprev, po[i]), xi);
+#pragma unroll
+            for (int j = 0; j < G - 1; ++j)
+                if (j < q) xi = __dadd_rn(__dmul_rn(ah[j], P.b[j][i]), xi);
             x[i] = __dadd_rn(__dmul_rn(alpha, pc[i]), xi);
         }
         __syncthreads();
@@ -702,24 +713,43 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_pair_kernel(int64_t n, 
         }
         return;
     }
-    if (!kOdd && blockIdx.x == 0 && threadIdx.x == 0) st->alpha_prev = alpha;  // read by the odd pass only
-    for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
-        double pv[kVu], ov[kVu], xv[kVu], rv[kVu], iv[kVu];  // loads of kVu rows before any store
+    if (q < G - 1) {  // keep this alpha for the group's last phase; x untouched
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->ahist[q] = alpha;
+        for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+            double pv[kVu], rv[kVu], iv[kVu];
 #pragma unroll
-        for (int q = 0; q < kVu; ++q) {
-            const int64_t i = i0 + q * stride;
+            for (int u = 0; u < kVu; ++u) {
+                const int64_t i = i0 + u * stride;
+                if (i < n) pv[u] = pc[i], rv[u] = r[i], iv[u] = kJacobi ? inv[i] : 1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kVu; ++u) {
+                const int64_t i = i0 + u * stride;
+                if (i < n) pn[i] = __dadd_rn(__dmul_rn(beta, pv[u]), kJacobi ? __dmul_rn(rv[u], iv[u]) : rv[u]);
+            }
+        }
+        return;
+    }
+    for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
+        double pv[kVu], xv[kVu], rv[kVu], iv[kVu], ov[kVu][G > 1 ? G - 1 : 1];  // all loads before any store
+#pragma unroll
+        for (int u = 0; u < kVu; ++u) {
+            const int64_t i = i0 + u * stride;
             if (i < n) {
-                pv[q] = pc[i], rv[q] = r[i], iv[q] = kJacobi ? inv[i] : 1.0;
-                if (kOdd) ov[q] = po[i], xv[q] = x[i];
+                pv[u] = pc[i], xv[u] = x[i], rv[u] = r[i], iv[u] = kJacobi ? inv[i] : 1.0;
+#pragma unroll
+                for (int j = 0; j < G - 1; ++j) ov[u][j] = P.b[j][i];
             }
         }
 #pragma unroll
-        for (int q = 0; q < kVu; ++q) {
-            const int64_t i = i0 + q * stride;
+        for (int u = 0; u < kVu; ++u) {
+            const int64_t i = i0 + u * stride;
             if (i < n) {
-                if (kOdd) x[i] = __dadd_rn(__dmul_rn(alpha, pv[q]), __dadd_rn(__dmul_rn(aprev, ov[q]), xv[q]));
-                const double zi = kJacobi ? __dmul_rn(rv[q], iv[q]) : rv[q];
-                po[i] = __dadd_rn(__dmul_rn(beta, pv[q]), zi);
+                double xi = xv[u];
+#pragma unroll
+                for (int j = 0; j < G - 1; ++j) xi = __dadd_rn(__dmul_rn(ah[j], ov[u][j]), xi);
+                x[i] = __dadd_rn(__dmul_rn(alpha, pv[u]), xi);
+                pn[i] = __dadd_rn(__dmul_rn(beta, pv[u]), kJacobi ? __dmul_rn(rv[u], iv[u]) : rv[u]);
             }
         }
     }
@@ -2663,18 +2693,19 @@ struct PcgSession {
     // merged: 2 kernels per iteration (direction pass inside the SpMV, XDir / EpiCgDir);
     // graphs per starting parity of the direction buffers
     bool merged = false;
-    bool xpair = false;  // 3-kernel FAST iteration with paired x updates (two p buffers)
+    int xgroup = 1;  // 3-kernel FAST iteration: x updates grouped over xgroup iterations (p buffers)
+    std::vector<DVec> xbuf;  // the group's p buffers beyond p
+    int nph = 1;  // phases of the captured graphs (1; 2: merged / EXACT buffer swap; xgroup)
     bool exact = false;  // EXACT mode: the reference's P-CG replayed on the device (ex_* kernels)
     DVec ex_partials, ex_scal;  // exact dots: chunk partials, and the two dot results
-    int next_parity = 0;
+    int next_parity = 0;  // phase of the next iteration (0 .. nph - 1)
     // cooperative update + direction (cg_update_dir_kernel) when every thread of one resident
     // grid can hold its rows' r and z in registers
     bool coop = false;
     void* ud_kernel = nullptr;
     unsigned ud_grid = 0;
     unsigned* ud_bar = nullptr;
-    cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr, exec_prof = nullptr;
-    cudaGraphExec_t exec_chunk1 = nullptr, exec_one1 = nullptr, exec_prof1 = nullptr;
+    cudaGraphExec_t exec_chunk[kXgMax] = {}, exec_one[kXgMax] = {}, exec_prof[kXgMax] = {};  // per starting phase
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int kernels_per_iteration = 0;
     // persistent cooperative path (pcg_persistent_kernel) for systems of C1's size class
@@ -2735,13 +2766,12 @@ struct PcgSession {
             if (persistent) setup_persistent();
             else {
                 if (!exact) setup_coop();
-                xpair = !exact && !merged && !coop && xpair_enabled();
-                if (xpair) p1 = DVec(n, c->stream);
-                exec_chunk = capture(kChunk, false, 0);
-                exec_one = capture(1, false, 0);
-                if (merged || exact || xpair) {
-                    exec_chunk1 = capture(kChunk, false, 1);
-                    exec_one1 = capture(1, false, 1);
+                xgroup = (!exact && !merged && !coop) ? xgroup_size() : 1;
+                for (int j = 1; j < xgroup; ++j) xbuf.emplace_back(n, c->stream);
+                nph = xgroup > 1 ? xgroup : (merged || exact) ? 2 : 1;
+                for (int ph = 0; ph < nph; ++ph) {
+                    exec_chunk[ph] = capture(kChunk, false, ph);
+                    exec_one[ph] = capture(1, false, ph);
                 }
                 trace_lap(c, "pcg_session", "graph capture");
             }
@@ -2753,8 +2783,9 @@ struct PcgSession {
     ~PcgSession() { release(); }
 
     void release() {
-        for (cudaGraphExec_t* g : {&exec_chunk, &exec_one, &exec_prof, &exec_chunk1, &exec_one1, &exec_prof1})
-            if (*g) cudaGraphExecDestroy(*g), *g = nullptr;
+        for (cudaGraphExec_t* arr : {exec_chunk, exec_one, exec_prof})
+            for (int ph = 0; ph < kXgMax; ++ph)
+                if (arr[ph]) cudaGraphExecDestroy(arr[ph]), arr[ph] = nullptr;
         for (auto& v : ev)
             if (v) cudaEventDestroy(v), v = nullptr;
         dev_free(st);
@@ -2805,10 +2836,20 @@ struct PcgSession {
         }
     }
 
-    static bool xpair_enabled() {
-        static const bool v = [] {
-            const char* s = std::getenv("KRYSP_XPAIR");
-            return !(s && s[0] == '0');
+    XBufs xbufs() {
+        XBufs b{};
+        b.b[0] = p;
+        for (int j = 1; j < xgroup; ++j) b.b[j] = xbuf[(size_t)j - 1];
+        return b;
+    }
+
+    static int xgroup_size() {  // KRYSP_XGROUP: 1, 2, 4 or 8 (default 4); KRYSP_XPAIR=0 -> 1
+        static const int v = [] {
+            const char* off = std::getenv("KRYSP_XPAIR");
+            if (off && off[0] == '0') return 1;
+            const char* s = std::getenv("KRYSP_XGROUP");
+            const int k = s ? std::atoi(s) : 4;
+            return (k == 1 || k == 2 || k == 4 || k == 8) ? k : 4;
         }();
         return v;
     }
@@ -3003,7 +3044,7 @@ struct PcgSession {
                 spmv_fused_xs(e, XDir<false>{r, nullptr, p_old, st, 0.0},
                            ap, EpiCgDir<false>{ap, p_new, p_old, r, nullptr, x, part_a, cnt_a, st, 0.0, 0.0, 0.0, false});
         } else {
-            double* pcur = xpair ? p_old : (double*)p;  // xpair: p_k alternates between p and p1
+            double* pcur = xgroup > 1 ? xbufs().b[parity] : (double*)p;  // grouped x: p_k cycles
             EpiCgSigma epi{ap, pcur, part_a, cnt_a, st, 0.0};
             spmv_fused(e, (const double*)pcur, ap, epi);
         }
@@ -3043,12 +3084,14 @@ struct PcgSession {
                            st, part_b, cnt_b, hist, d_trace));
         KG_LAUNCH(c);
         if (events) KG_CUDA(cudaEventRecordWithFlags(ev[2], c->stream, cudaEventRecordExternal));
-        if (!merged && xpair) {
+        if (!merged && xgroup > 1) {
             unsigned* cnt_c = c->d_counters + 5;
-            auto k = parity ? (e.jacobi ? cg_direction_pair_kernel<true, true> : cg_direction_pair_kernel<false, true>)
-                            : (e.jacobi ? cg_direction_pair_kernel<true, false> : cg_direction_pair_kernel<false, false>);
-            KG_CUDA(launch_pdl(k, g_vec, kFusedNT, 0, c->stream, n, (const double*)p_old, p_new, (const double*)r, inv,
-                               (double*)x, st, cnt_c));
+            auto pick = [&](auto kt, auto kf) { return e.jacobi ? kt : kf; };
+            auto k = xgroup == 2 ? pick(cg_direction_group_kernel<true, 2>, cg_direction_group_kernel<false, 2>)
+                     : xgroup == 4 ? pick(cg_direction_group_kernel<true, 4>, cg_direction_group_kernel<false, 4>)
+                                   : pick(cg_direction_group_kernel<true, 8>, cg_direction_group_kernel<false, 8>);
+            KG_CUDA(launch_pdl(k, g_vec, kFusedNT, 0, c->stream, n, xbufs(), parity, (const double*)r, inv, (double*)x,
+                               st, cnt_c));
             KG_LAUNCH(c);
         } else if (!merged) {
             unsigned* cnt_c = c->d_counters + 5;
@@ -3066,7 +3109,7 @@ struct PcgSession {
         cudaGraphExec_t exec = nullptr;
         KG_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         try {
-            for (int i = 0; i < iters; ++i) iteration(events, (parity0 + i) & 1);
+            for (int i = 0; i < iters; ++i) iteration(events, (parity0 + i) % nph);
         } catch (...) {
             cudaStreamEndCapture(c->stream, &graph);
             if (graph) cudaGraphDestroy(graph);
@@ -3082,12 +3125,11 @@ struct PcgSession {
     void enqueue(int64_t iters) {
         krysp_gpu_ctx* c = e.c;
         if (persistent) return launch_persistent(iters);
-        const bool two = merged || exact || xpair;  // iterations alternate two buffers
-        for (int64_t i = 0; i + kChunk <= iters; i += kChunk)
-            KG_CUDA(cudaGraphLaunch(two && next_parity ? exec_chunk1 : exec_chunk, c->stream));
+        // graphs per starting phase (kChunk is a multiple of every phase count: a chunk keeps it)
+        for (int64_t i = 0; i + kChunk <= iters; i += kChunk) KG_CUDA(cudaGraphLaunch(exec_chunk[next_parity], c->stream));
         for (int64_t i = 0; i < iters % kChunk; ++i) {
-            KG_CUDA(cudaGraphLaunch(two && next_parity ? exec_one1 : exec_one, c->stream));
-            if (two) next_parity ^= 1;
+            KG_CUDA(cudaGraphLaunch(exec_one[next_parity], c->stream));
+            next_parity = (next_parity + 1) % nph;
         }
     }
 
@@ -3132,13 +3174,12 @@ struct PcgSession {
     void profile(int64_t iters, double out[3]) {
         krysp_gpu_ctx* c = e.c;
         if (persistent) fail(KRYSP_ERROR, "per-kernel profile: the persistent P-CG grid is one kernel");
-        if (!exec_prof) exec_prof = capture(1, true, 0);  // event-node graphs, built on first use
-        const bool two = merged || exact || xpair;
-        if (two && !exec_prof1) exec_prof1 = capture(1, true, 1);
+        for (int ph = 0; ph < nph; ++ph)  // event-node graphs, built on first use
+            if (!exec_prof[ph]) exec_prof[ph] = capture(1, true, ph);
         out[0] = out[1] = out[2] = 0.0;
         for (int64_t i = 0; i < iters; ++i) {
-            KG_CUDA(cudaGraphLaunch(two && next_parity ? exec_prof1 : exec_prof, c->stream));
-            if (two) next_parity ^= 1;
+            KG_CUDA(cudaGraphLaunch(exec_prof[next_parity], c->stream));
+            next_parity = (next_parity + 1) % nph;
             KG_CUDA(cudaEventSynchronize(ev[3]));
             for (int k = 0; k < 3; ++k) {
                 float ms = 0.f;
