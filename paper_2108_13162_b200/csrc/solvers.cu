@@ -678,6 +678,8 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_kernel(int64_t n, doubl
 // V = 9 + 1/G vector streams per iteration instead of 10.  The iteration that ends the solve
 // flushes the group's pending terms (x_pending).
 constexpr int kXgMax = 8;
+template <int G>
+constexpr int kGroupRows = G >= 8 ? 1 : kVu;  // rows per thread in flight (G = 8: registers)
 struct XBufs {
     double* b[kXgMax];
 };
@@ -689,6 +691,7 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_group_kernel(int64_t n,
                                                                        double* __restrict__ x, CgState* st,
                                                                        unsigned* counter) {
     pdl_wait();
+    constexpr int kGu = kGroupRows<G>;
     const int done = *(volatile const int*)&st->done;
     if (done && !*(volatile const int*)&st->x_pending) return;
     const double alpha = st->alpha, beta = st->beta;
@@ -715,25 +718,25 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_group_kernel(int64_t n,
     }
     if (q < G - 1) {  // keep this alpha for the group's last phase; x untouched
         if (blockIdx.x == 0 && threadIdx.x == 0) st->ahist[q] = alpha;
-        for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
-            double pv[kVu], rv[kVu], iv[kVu];
+        for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kGu * stride) {
+            double pv[kGu], rv[kGu], iv[kGu];
 #pragma unroll
-            for (int u = 0; u < kVu; ++u) {
+            for (int u = 0; u < kGu; ++u) {
                 const int64_t i = i0 + u * stride;
                 if (i < n) pv[u] = pc[i], rv[u] = r[i], iv[u] = kJacobi ? inv[i] : 1.0;
             }
 #pragma unroll
-            for (int u = 0; u < kVu; ++u) {
+            for (int u = 0; u < kGu; ++u) {
                 const int64_t i = i0 + u * stride;
                 if (i < n) pn[i] = __dadd_rn(__dmul_rn(beta, pv[u]), kJacobi ? __dmul_rn(rv[u], iv[u]) : rv[u]);
             }
         }
         return;
     }
-    for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kVu * stride) {
-        double pv[kVu], xv[kVu], rv[kVu], iv[kVu], ov[kVu][G > 1 ? G - 1 : 1];  // all loads before any store
+    for (int64_t i0 = blockIdx.x * (int64_t)kFusedNT + threadIdx.x; i0 < n; i0 += kGu * stride) {
+        double pv[kGu], xv[kGu], rv[kGu], iv[kGu], ov[kGu][G > 1 ? G - 1 : 1];  // all loads before any store
 #pragma unroll
-        for (int u = 0; u < kVu; ++u) {
+        for (int u = 0; u < kGu; ++u) {
             const int64_t i = i0 + u * stride;
             if (i < n) {
                 pv[u] = pc[i], xv[u] = x[i], rv[u] = r[i], iv[u] = kJacobi ? inv[i] : 1.0;
@@ -742,7 +745,7 @@ __global__ void __launch_bounds__(kFusedNT) cg_direction_group_kernel(int64_t n,
             }
         }
 #pragma unroll
-        for (int u = 0; u < kVu; ++u) {
+        for (int u = 0; u < kGu; ++u) {
             const int64_t i = i0 + u * stride;
             if (i < n) {
                 double xi = xv[u];
