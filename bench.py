@@ -498,7 +498,7 @@ def run_ours_dist(args, dist):
     D.close()
     nnz_total = 7 * N - 6 * args.n ** 2
     bw_peak, peak_kind = peaks()
-    B_iter_gpu = iter_bytes(N, N, nnz_total, 10) / dist.world  # the partitioned kernels: V = 10
+    B_iter_gpu = iter_bytes(N, N, nnz_total) / dist.world  # the partitioned kernels group x updates too
     t_it = t_max / args.steps
     line = {"metric": METRIC, "value": args.steps / t_max, "unit": "iterations/s", "n_gpus": dist.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_it, "higher_is_better": True,

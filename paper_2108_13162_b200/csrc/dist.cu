@@ -62,6 +62,7 @@ struct DistCgState {
     double omega;
     double red_loc[4], red[4];  // (sum, compensation) pairs
     int half;
+    double ahist[8];  // P-CG grouped x updates: the group's earlier alphas (dist_direction_group_kernel)
 };
 enum : int {
     kDsBreakdownSigma = 1, kDsNonFiniteSigma = 2, kDsNonFiniteAlpha = 3, kDsNonFiniteRho = 4,
@@ -86,6 +87,8 @@ struct DistPart {
     // solver state (P-CG: x r p ap inv; BiCGStab adds rh, sx (s, with ghost tail), t; v = ap)
     DVec x, r, p, ap, inv;  // p has n_local + n_ghost entries
     DVec rh, sx, t;
+    std::vector<DVec> pg;  // P-CG grouped x updates: p buffers 1 .. G-1 (n_local + n_ghost each)
+    double* pbuf(int j) { return j == 0 ? (double*)p : (double*)pg[(size_t)j - 1]; }
     DistCgState* st = nullptr;
     double* hist = nullptr;
     double* part_slot = nullptr;  // 3 x kPartialCap partials (interior, lower, upper boundary)
@@ -264,6 +267,61 @@ __global__ void __launch_bounds__(kNT) dist_direction_kernel(int64_t n, double* 
     }
     if (last_block(counter) && threadIdx.x == 0) {
         *counter = 0;
+        if (bad) {
+            st->status = kDsNonFiniteRho;
+            st->done = 1;
+            return;
+        }
+        if (history) history[it] = measure;
+        st->iter = it + 1;
+        st->rho_1 = rho;
+        st->beta = beta;
+        st->rho = rho_new;
+        if (stop) st->done = 1;
+    }
+}
+
+// dist_direction_kernel with the x updates of G iterations grouped (as the single-GPU
+// cg_direction_group_kernel): p cycles through G band buffers; phases < G - 1 leave x alone and
+// keep alpha, the last applies all G terms; a stop flushes the group's pending terms.
+struct DBufs {
+    double* b[8];
+};
+template <bool kJacobi, int G>
+__global__ void __launch_bounds__(kNT) dist_direction_group_kernel(int64_t n, DBufs P, int q,
+                                                                    const double* __restrict__ r,
+                                                                    const double* __restrict__ inv,
+                                                                    double* __restrict__ x, DistCgState* st,
+                                                                    double* history, unsigned* counter) {
+    if (*(volatile const int*)&st->done) return;
+    const double rho_new = st->rho_new, rho = st->rho, alpha = st->alpha;
+    const long long it = st->iter;
+    const double measure = rho_new / st->norm_r0, beta = rho_new / rho;
+    const bool bad = !isfinite(rho_new);
+    const bool stop = bad || measure <= st->tol || it + 1 >= st->max_it;
+    double ah[G > 1 ? G - 1 : 1];
+#pragma unroll
+    for (int j = 0; j < G - 1; ++j) ah[j] = st->ahist[j];
+    const double* __restrict__ pc = P.b[q];
+    double* __restrict__ pn = P.b[q + 1 < G ? q + 1 : 0];
+    const int64_t stride = (int64_t)gridDim.x * kNT;
+    if (stop || q == G - 1) {  // the reference updated x before its rho test: apply the group's terms
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += stride) {
+            const double pi = pc[i];
+            double xi = x[i];
+#pragma unroll
+            for (int j = 0; j < G - 1; ++j)
+                if (j < q) xi = __dadd_rn(__dmul_rn(ah[j], P.b[j][i]), xi);
+            x[i] = __dadd_rn(__dmul_rn(alpha, pi), xi);
+            if (!stop) pn[i] = __dadd_rn(__dmul_rn(beta, pi), kJacobi ? __dmul_rn(r[i], inv[i]) : r[i]);
+        }
+    } else {  // x untouched; keep alpha for the group's last phase
+        for (int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x; i < n; i += stride)
+            pn[i] = __dadd_rn(__dmul_rn(beta, pc[i]), kJacobi ? __dmul_rn(r[i], inv[i]) : r[i]);
+    }
+    if (last_block(counter) && threadIdx.x == 0) {
+        *counter = 0;
+        if (!stop && q < G - 1) st->ahist[q] = alpha;
         if (bad) {
             st->status = kDsNonFiniteRho;
             st->done = 1;
@@ -551,7 +609,8 @@ struct krysp_gpu_dist {
     int method = KRYSP_PCG;
     krysp_solver_cfg cfg{};
     kg::DistCgState** d_sts = nullptr;
-    cudaGraphExec_t exec_chunk = nullptr, exec_one = nullptr;
+    cudaGraphExec_t exec_chunk[8] = {}, exec_one[8] = {};  // per starting phase (P-CG x groups)
+    int xg = 1, next_phase = 0;  // P-CG: iterations per x update, and the next iteration's phase
     int kernels_per_iteration = 0;
     double measure0 = 0.0;
     bool done_at_setup = false;
@@ -915,12 +974,12 @@ void dist_iteration_bicg(krysp_gpu_dist* d) {
 }
 
 // one distributed P-CG iteration (all held parts), enqueued on ctx->stream
-void dist_iteration(krysp_gpu_dist* d, cudaEvent_t ev_spmv_done = nullptr) {
+void dist_iteration(krysp_gpu_dist* d, int q, cudaEvent_t ev_spmv_done = nullptr) {
     krysp_gpu_ctx* c = d->ctx;
     cudaStream_t s = c->stream;
     const int64_t before = c->launches;
     std::vector<double*> ps;
-    for (auto& P : d->parts) ps.push_back(P.p);
+    for (auto& P : d->parts) ps.push_back(P.pbuf(q));  // phase q's p (grouped x updates)
     const bool overlap = !d->emulated();
     if (overlap) {
         KG_CUDA(cudaEventRecord(d->ev_fork, s));
@@ -934,17 +993,19 @@ void dist_iteration(krysp_gpu_dist* d, cudaEvent_t ev_spmv_done = nullptr) {
     for (size_t i = 0; i < d->parts.size(); ++i) {  // interior rows (no ghosts): overlap the halo
         DistPart& P = d->parts[i];
         krysp_gpu_mat v = row_view(P.A, P.clean_a, P.clean_b);
-        EpiDotPartial e{P.ap + P.clean_a, P.p + P.clean_a, P.part_slot, P.st, 0.0};
-        ga[i] = launch_rows(v, P.p, e, s);
+        double* pq = P.pbuf(q);
+        EpiDotPartial e{P.ap + P.clean_a, pq + P.clean_a, P.part_slot, P.st, 0.0};
+        ga[i] = launch_rows(v, pq, e, s);
     }
     if (overlap) KG_CUDA(cudaStreamWaitEvent(s, d->ev_halo, 0));
     for (size_t i = 0; i < d->parts.size(); ++i) {  // boundary rows
         DistPart& P = d->parts[i];
         krysp_gpu_mat lo_v = row_view(P.A, 0, P.clean_a), hi_v = row_view(P.A, P.clean_b, P.n_local);
-        EpiDotPartial e1{P.ap, P.p, P.part_slot + kPartialCap, P.st, 0.0};
-        EpiDotPartial e2{P.ap + P.clean_b, P.p + P.clean_b, P.part_slot + 2 * kPartialCap, P.st, 0.0};
-        gb[i] = launch_rows(lo_v, P.p, e1, s);
-        gc[i] = launch_rows(hi_v, P.p, e2, s);
+        double* pq = P.pbuf(q);
+        EpiDotPartial e1{P.ap, pq, P.part_slot + kPartialCap, P.st, 0.0};
+        EpiDotPartial e2{P.ap + P.clean_b, pq + P.clean_b, P.part_slot + 2 * kPartialCap, P.st, 0.0};
+        gb[i] = launch_rows(lo_v, pq, e1, s);
+        gc[i] = launch_rows(hi_v, pq, e2, s);
         sum_partials<<<1, kNT, 0, s>>>(P.st, P.part_slot, (int)ga[i], P.part_slot + kPartialCap, (int)gb[i],
                                        P.part_slot + 2 * kPartialCap, (int)gc[i]);
         KG_LAUNCH(c);
@@ -962,14 +1023,24 @@ void dist_iteration(krysp_gpu_dist* d, cudaEvent_t ev_spmv_done = nullptr) {
     for (size_t i = 0; i < d->parts.size(); ++i) {
         DistPart& P = d->parts[i];
         const unsigned g = grid_for(P.n_local, kNT, (int64_t)c->sm_count * 8);
-        dist_direction_kernel<<<g, kNT, 0, s>>>(P.n_local, P.p, P.r, d->cfg.preconditioner ? (const double*)P.inv : nullptr,
-                                                 P.x, P.st, P.hist, c->d_counters + 4 + (i % 4));
+        const double* inv = d->cfg.preconditioner ? (const double*)P.inv : nullptr;
+        unsigned* cnt = c->d_counters + 4 + (i % 4);
+        if (d->xg > 1) {
+            DBufs B{};
+            for (int j = 0; j < d->xg; ++j) B.b[j] = P.pbuf(j);
+            auto k = d->xg == 2 ? (inv ? dist_direction_group_kernel<true, 2> : dist_direction_group_kernel<false, 2>)
+                     : d->xg == 4 ? (inv ? dist_direction_group_kernel<true, 4> : dist_direction_group_kernel<false, 4>)
+                                  : (inv ? dist_direction_group_kernel<true, 8> : dist_direction_group_kernel<false, 8>);
+            k<<<g, kNT, 0, s>>>(P.n_local, B, q, P.r, inv, P.x, P.st, P.hist, cnt);
+        } else {
+            dist_direction_kernel<<<g, kNT, 0, s>>>(P.n_local, P.p, P.r, inv, P.x, P.st, P.hist, cnt);
+        }
         KG_LAUNCH(c);
     }
     d->kernels_per_iteration = (int)(c->launches - before);
 }
 
-cudaGraphExec_t capture(krysp_gpu_dist* d, int iters) {
+cudaGraphExec_t capture(krysp_gpu_dist* d, int iters, int phase0 = 0) {
     krysp_gpu_ctx* c = d->ctx;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -977,7 +1048,7 @@ cudaGraphExec_t capture(krysp_gpu_dist* d, int iters) {
     try {
         for (int i = 0; i < iters; ++i) {
             if (d->method == KRYSP_BICGSTAB) dist_iteration_bicg(d);
-            else dist_iteration(d);
+            else dist_iteration(d, (phase0 + i) % d->xg);
         }
     } catch (...) {
         cudaStreamEndCapture(c->stream, &graph);
@@ -991,9 +1062,13 @@ cudaGraphExec_t capture(krysp_gpu_dist* d, int iters) {
 }
 
 void pcg_release(krysp_gpu_dist* d) {
-    if (d->exec_chunk) cudaGraphExecDestroy(d->exec_chunk);
-    if (d->exec_one) cudaGraphExecDestroy(d->exec_one);
-    d->exec_chunk = d->exec_one = nullptr;
+    for (int ph = 0; ph < 8; ++ph) {
+        if (d->exec_chunk[ph]) cudaGraphExecDestroy(d->exec_chunk[ph]);
+        if (d->exec_one[ph]) cudaGraphExecDestroy(d->exec_one[ph]);
+        d->exec_chunk[ph] = d->exec_one[ph] = nullptr;
+    }
+    d->xg = 1;
+    d->next_phase = 0;
     dev_free(d->d_sts);
     d->d_sts = nullptr;
     for (auto& P : d->parts) {
@@ -1005,6 +1080,7 @@ void pcg_release(krysp_gpu_dist* d) {
         P.x = DVec();
         P.r = DVec();
         P.p = DVec();
+        P.pg.clear();
         P.ap = DVec();
         P.inv = DVec();
         P.rh = DVec();
@@ -1132,16 +1208,35 @@ void krylov_create(krysp_gpu_dist* d, int method, const double* const* bs, const
     d->d_sts = reinterpret_cast<DistCgState**>(dev_alloc<char>(8 * (int64_t)sts.size(), false));
     KG_CUDA(cudaMemcpyAsync(d->d_sts, sts.data(), 8 * sts.size(), cudaMemcpyHostToDevice, s));
     kg::wait_stream(c, s);
-    d->exec_chunk = capture(d, krysp_gpu_dist::kChunk);
-    d->exec_one = capture(d, 1);
+    // P-CG: the x updates of xg iterations grouped over xg p buffers (KRYSP_XGROUP, as the
+    // single-GPU session; BiCGStab: 1)
+    d->xg = 1;
+    if (method == KRYSP_PCG) {
+        const char* off = std::getenv("KRYSP_XPAIR");
+        const char* gs = std::getenv("KRYSP_XGROUP");
+        const int k = (off && off[0] == '0') ? 1 : gs ? std::atoi(gs) : 4;
+        d->xg = (k == 1 || k == 2 || k == 4 || k == 8) ? k : 4;
+        for (auto& P : d->parts)
+            for (int j = 1; j < d->xg; ++j) P.pg.emplace_back(P.n_local + P.n_ghost, s);
+        kg::wait_stream(c, s);
+    }
+    d->next_phase = 0;
+    for (int ph = 0; ph < d->xg; ++ph) {
+        d->exec_chunk[ph] = capture(d, krysp_gpu_dist::kChunk, ph);
+        d->exec_one[ph] = capture(d, 1, ph);
+    }
     d->pcg = true;
 }
 
 void pcg_enqueue(krysp_gpu_dist* d, int64_t n) {
     if (!d->pcg) fail(KRYSP_ERROR, "no distributed solver (krysp_gpu_dist_pcg_create)");
     cudaStream_t s = d->ctx->stream;
-    for (int64_t i = 0; i + krysp_gpu_dist::kChunk <= n; i += krysp_gpu_dist::kChunk) KG_CUDA(cudaGraphLaunch(d->exec_chunk, s));
-    for (int64_t i = 0; i < n % krysp_gpu_dist::kChunk; ++i) KG_CUDA(cudaGraphLaunch(d->exec_one, s));
+    for (int64_t i = 0; i + krysp_gpu_dist::kChunk <= n; i += krysp_gpu_dist::kChunk)
+        KG_CUDA(cudaGraphLaunch(d->exec_chunk[d->next_phase], s));
+    for (int64_t i = 0; i < n % krysp_gpu_dist::kChunk; ++i) {
+        KG_CUDA(cudaGraphLaunch(d->exec_one[d->next_phase], s));
+        d->next_phase = (d->next_phase + 1) % d->xg;
+    }
 }
 
 bool pcg_done(krysp_gpu_dist* d) {
@@ -1699,7 +1794,8 @@ krysp_status krysp_gpu_dist_pcg_profile(krysp_gpu_dist* d, int64_t n, double* sp
         try {
             for (int64_t i = 0; i < n; ++i) {
                 KG_CUDA(cudaEventRecord(e[0], s));
-                kg::dist_iteration(d, e[1]);
+                kg::dist_iteration(d, d->next_phase, e[1]);
+                d->next_phase = (d->next_phase + 1) % d->xg;
                 KG_CUDA(cudaEventRecord(e[2], s));
                 kg::wait_event(d->ctx, e[2]);
                 float a = 0.f, b = 0.f;
