@@ -75,7 +75,7 @@ bool launch_csr_vector_long(const krysp_gpu_mat* cm, const double* x, double* y,
     EpiStore epi{y};
     auto vec = [&](auto k) {
         const int64_t g = bounded_grid(c, resident_blocks(k, (int)bs, 0), nvb);
-        k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), XPtr{x}, epi, nvb, (int32_t)kLongRow);
+        k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), XPtr{x}, epi, nvb, (int32_t)kLongRow, x);
         KG_LAUNCH(c);
     };
     switch (tw) {

@@ -42,6 +42,14 @@ struct XPtr {
     __device__ __forceinline__ double operator()(int32_t c) const { return __ldg(p + c); }
 };
 inline XPtr xs_of(const double* p) { return XPtr{p}; }
+// the plain vector of an XPtr, for kernels that take it as a __restrict__ parameter of their
+// own: through the struct member nvcc loses the no-alias fact and schedules the gathers after
+// the previous row's y store (C4's tail ELL kernel: 1.78 -> 2.11 ms)
+inline const double* xraw_of(const XPtr& x) { return x.p; }
+template <class XS>
+inline const double* xraw_of(const XS&) {
+    return nullptr;
+}
 template <class XS>
 inline XS xs_of(XS s) {
     return s;
@@ -82,10 +90,15 @@ struct epi_is_store<EpiStoreGated<G>> : std::true_type {};
 // blockDim.x / TW rows each.  Every lane participates in the shuffles.
 // skip_long > 0: rows longer than that are left to long_rows_exact_kernel (plain SpMV only)
 template <int TW, class Epi, class XS = XPtr>
-__global__ void csr_vector_kernel(CsrView A, XS x, Epi epi, int64_t n_vblocks, int32_t skip_long = 0) {
+__global__ void csr_vector_kernel(CsrView A, XS xs, Epi epi, int64_t n_vblocks, int32_t skip_long,
+                                  const double* __restrict__ xr) {
     pdl_trigger();
     if (!epi.active()) return;
-    x.init();
+    xs.init();
+    auto x = [&](int32_t c) -> double {  // XPtr: through the __restrict__ parameter (xraw_of)
+        if constexpr (std::is_same_v<XS, XPtr>) return __ldg(xr + c);
+        else return xs(c);
+    };
     const int lane = threadIdx.x & (TW - 1);
     for (int64_t vb = blockIdx.x; vb < n_vblocks; vb += gridDim.x) {
         const int64_t row = (vb * blockDim.x + threadIdx.x) / TW;
@@ -230,10 +243,15 @@ struct epi_staged<E, std::void_t<decltype(E::kStaged)>> {
 // of csr_vector_kernel — the reference's tw-lane order (kernels.cpp:175-186), so any policy
 // with a tile that fits the stage runs on the TMA pipeline bit-identically.
 template <int TW, class Epi, class XS = XPtr>
-__global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, XS x, Epi epi, TmaTileLayout L) {
+__global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, XS xs, Epi epi, TmaTileLayout L,
+                                                            const double* __restrict__ xr) {
     pdl_trigger();
     if (!epi.active()) return;
-    x.init();
+    xs.init();
+    auto x = [&](int32_t c) -> double {  // XPtr: through the __restrict__ parameter (xraw_of)
+        if constexpr (std::is_same_v<XS, XPtr>) return __ldg(xr + c);
+        else return xs(c);
+    };
     constexpr int TR = kTileRows / TW;
     extern __shared__ __align__(128) unsigned char smem_tma[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma);  // 2 mbarriers
@@ -346,10 +364,14 @@ __global__ void __launch_bounds__(kTileRows) csr_tma_kernel(CsrView A, XS x, Epi
 // instantiation, so the plain kernels keep their register count (the wide-slab 8-slot store
 // kernel goes from 48 to 64 registers with the tail loop: one CTA per SM fewer, C4 -25 %)
 template <class Epi, int KB, bool kTail = false, class XS = XPtr>
-__global__ void ell_kernel(EllView E, XS x, Epi epi) {
+__global__ void ell_kernel(EllView E, XS xs, Epi epi, const double* __restrict__ xr) {
     pdl_trigger();
     if (!epi.active()) return;
-    x.init();
+    xs.init();
+    auto x = [&](int32_t c) -> double {
+        if constexpr (std::is_same_v<XS, XPtr>) return __ldg(xr + c);
+        else return xs(c);
+    };
     const int64_t n = E.n_rows, ld = E.ld;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r - threadIdx.x < n;
          r += (int64_t)gridDim.x * blockDim.x) {
@@ -453,7 +475,7 @@ inline int64_t launch_csr_vector_tw(const krysp_gpu_mat* m, X x_, Epi epi, int64
     auto x = xs_of(x_);
     auto k = csr_vector_kernel<TW, Epi, decltype(x)>;
     const int64_t g = bounded_grid(m->ctx, resident_blocks(k, (int)bs, 0), nvb);
-    k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), x, epi, nvb, 0);
+    k<<<(unsigned)g, (unsigned)bs, 0, s>>>(m->csr(), x, epi, nvb, 0, xraw_of(x));
     KG_LAUNCH(m->ctx);
     return g;
 }
@@ -492,7 +514,7 @@ inline int64_t launch_csr_tile_tw(const krysp_gpu_mat* m, X x_, Epi epi, cudaStr
     auto k = csr_tma_kernel<TW, Epi, decltype(x)>;
     if (smem > 48 * 1024) KG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int64_t g = bounded_grid(c, resident_blocks(k, kTileRows, smem), tiles);
-    k<<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, L);
+    k<<<(unsigned)g, kTileRows, smem, s>>>(m->csr(), x, epi, L, xraw_of(x));
     KG_LAUNCH(c);
     return g;
 }
@@ -520,10 +542,10 @@ inline void launch_ell(const krysp_gpu_mat* m, X x_, Epi epi, int64_t bs, cudaSt
     // w = 27: register-limited occupancy), win for the plain store
     if (epi_is_store<Epi>::value) {
         const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8, false, XS>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 8, false, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+        ell_kernel<Epi, 8, false, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi, xraw_of(x));
     } else {
         const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4, false, XS>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 4, false, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi);
+        ell_kernel<Epi, 4, false, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(m->ell(), x, epi, xraw_of(x));
     }
     KG_LAUNCH(c);
 }
@@ -543,10 +565,10 @@ inline void launch_ell_tail(const krysp_gpu_mat* m, X x_, Epi epi, int64_t bs, c
     E.tval = m->co_v;
     if (epi_is_store<Epi>::value) {
         const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 8, true, XS>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 8, true, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
+        ell_kernel<Epi, 8, true, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi, xraw_of(x));
     } else {
         const int64_t g = bounded_grid(c, resident_blocks(ell_kernel<Epi, 4, true, XS>, (int)bs, 0), nvb);
-        ell_kernel<Epi, 4, true, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi);
+        ell_kernel<Epi, 4, true, XS><<<(unsigned)g, (unsigned)bs, 0, s>>>(E, x, epi, xraw_of(x));
     }
     KG_LAUNCH(c);
 }
